@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark of the FP64 mEVP hot path (BASELINE.json metric: element-updates/s and % of HBM roofline).
+
+One *step* = one outer step over the whole hot path: DG advection of A, H
+(nxsdg_advect), outer-step prep (BEGIN_STEP) and n_sub = 100 fused mEVP subcycles
+(nxsdg_mevp_substeps), on the BASELINE config C4 (4096 x 4096 CG2/DG2) by default.
+value = N_e * n_sub * steps / (max over ranks of the device time), element-updates/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+N > 1 runs under torchrun (one rank per GPU, row strips, NCCL halo exchange) and
+reports strong scaling on C4 (weak on C5).  --impl reference times the oracle (the
+plain FP64 CPU implementation) on the host cores, on a bounded window of the same
+workload.  Inputs are seeded synthetic fields of the config's shape
+and larger than L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2402_00466_b200 import inputs  # noqa: E402
+
+KERNEL = "k_subcycle<2>"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (recipe in B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0])); mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic_per_launch():
+    """dram__bytes_read.sum + dram__bytes_write.sum of the fused kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("k_subcycle", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def rank_window(cfg, rank, nranks):
+    from paper_2402_00466_b200 import nxsdg
+    r0, er, n0, nr = nxsdg.partition(cfg.ny, cfg.p, nranks, rank)
+    return r0, er, n0, nr
+
+
+def gen_rank_state(cfg, rank, nranks):
+    r0, er, n0, nr = rank_window(cfg, rank, nranks)
+    st = inputs.make_config_case(cfg, window=(0, r0, cfg.nx, er))
+    for k in ("vx", "vy", "ox", "oy", "ax", "ay"):
+        st[k] = np.ascontiguousarray(st[k][:nr])
+    return st
+
+
+# ------------------------------------------------------------------ oracle (reference arm / cpu baseline)
+def oracle_sample(cfg, nsub, win=160):
+    """The oracle as it stands on a bounded window of the workload (same resolution, global coordinates):
+    advection (if the config advects) + prep + n_sub subcycles."""
+    import oracle
+    w = min(win, cfg.nx), min(win, cfg.ny)
+    ix0, iy0 = (cfg.nx - w[0]) // 2, (cfg.ny - w[1]) // 2
+    st = inputs.make_config_case(cfg, window=(ix0, iy0, w[0], w[1]))
+    hx, hy = cfg.lx / cfg.nx, cfg.ly / cfg.ny
+    m = oracle.Mesh(w[0], w[1], lx=w[0] * hx, ly=w[1] * hy, p=cfg.p, ns=cfg.ns, na=cfg.na)
+    o = oracle.Oracle()
+    t0 = time.perf_counter()
+    o.outer_step(m, oracle.Params(), nsub, st, do_advect=True)
+    dt = time.perf_counter() - t0
+    return {"value": w[0] * w[1] * nsub / dt, "seconds": dt, "cores": o.threads,
+            "sample": f"{w[0]}x{w[1]} window of {cfg.name} ({cfg.nx}x{cfg.ny}) at the same resolution, "
+                      f"advect + prep + {nsub} subcycles, oracle (plain C FP64, OpenMP)"}
+
+
+def run_reference(args, cfg):
+    rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return 0
+    samples = []
+    for _ in range(args.warmup):
+        oracle_sample(cfg, min(cfg.nsub, 10), win=64)
+    for _ in range(args.steps):
+        samples.append(oracle_sample(cfg, cfg.nsub, win=args.ref_window))
+    vals = [s["value"] for s in samples]
+    secs = sum(s["seconds"] for s in samples)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": "FP64 mEVP element-updates/s", "value": v, "unit": "element-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / max(1, args.steps), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} CG{cfg.p}/DG{cfg.p} (n_S={cfg.ns}), outer step = advect + {cfg.nsub} mEVP subcycles",
+                       "sample": samples[0]["sample"]},
+            "cpu_baseline": {"value": v, "unit": "element-updates/s", "cores": samples[0]["cores"], "kind": "oracle",
+                             "sample": samples[0]["sample"]},
+            "e2e": {"value": v, "unit": "element-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=None, help="C2|C3|C4|C5 (default C4, C5 when --weak)")
+    ap.add_argument("--weak", action="store_true", help="C5: 8192^2 per GPU (weak scaling)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nsub", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-window", type=int, default=160)
+    args = ap.parse_args()
+    cname = args.config or ("C5" if args.weak else "C4")
+    cfg = inputs.CONFIGS[cname]
+    world = _env_int("WORLD_SIZE", 1)
+    if cname == "C5":   # 8192^2 per GPU: Ly = P * 512 km
+        cfg = inputs.Config("C5", cfg.nx, cfg.ny * world, cfg.p, cfg.ns, cfg.na, cfg.nsub, cfg.lx, cfg.ly * world,
+                            cfg.kind, cfg.advect)
+    if args.nsub:
+        cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, args.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2402_00466_b200 import nxsdg
+
+    rank, local = _env_int("RANK", 0), _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nxsdg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+    prm = nxsdg.PhysParams()
+    st = gen_rank_state(cfg, rank, world)
+    kw = dict(rank=rank, nranks=world, transport=nxsdg.TRANSPORT_NCCL, nccl_id=nid) if world > 1 else {}
+    m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, device=local, **kw)
+    m.load(st)
+    stream = torch.cuda.ExternalStream(m.stream)
+    n_el = cfg.nx * cfg.ny   # whole job
+    n_el_rank = m.elem_rows * cfg.nx
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def step(ev=None):
+        if ev: ev[0].record(stream)
+        m.advect(prm.dt)
+        if ev: ev[1].record(stream)
+        m.mevp_substeps(0, begin_step=True)
+        if ev: ev[2].record(stream)
+        m.mevp_substeps(cfg.nsub, begin_step=False)
+        if ev: ev[3].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    l0 = m.kernel_launches
+    with Clocks(local) as clk:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t1.record(stream)
+        barrier()
+    launches = m.kernel_launches - l0
+    ms = t0.elapsed_time(t1)
+    adv = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    prep = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    sub = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))
+    if world > 1:
+        t = torch.tensor([ms, adv, prep, sub], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, adv, prep, sub = t.tolist()
+    ms_step = ms / args.steps
+    value = n_el * cfg.nsub * args.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (the fused subcycle kernel): algorithmic bytes per launch
+    bpe = m.bytes_per_element_subcycle
+    kernel_ms = sub / cfg.nsub
+    achieved = bpe * n_el_rank / (kernel_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+    traffic = ncu_traffic_per_launch()
+
+    # e2e: the same metric through the C ABI with pinned HOST buffers, copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        pinned = {k: torch.from_numpy(v).pin_memory() for k, v in st.items()}
+        outv = {k: torch.empty(pinned[k].shape, dtype=torch.float64).pin_memory() for k in ("vx", "vy")}
+        h2d = sum(v.numel() * 8 for v in pinned.values())
+        d2h = sum(v.numel() * 8 for v in outv.values())
+        barrier()
+        te = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            m.load(pinned)
+            step()
+            for k in ("vx", "vy"):
+                m.read_state(k, outv[k])
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": n_el * cfg.nsub * args.e2e_steps / (ems * 1e-3), "unit": "element-updates/s",
+               "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
+               "steps": args.e2e_steps, "wall_s": time.perf_counter() - te}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            s = oracle_sample(cfg, cfg.nsub, win=args.ref_window)
+            cpu = {"value": s["value"], "unit": "element-updates/s", "cores": s["cores"], "kind": "oracle",
+                   "sample": s["sample"], "seconds": s["seconds"]}
+        except Exception as ex:  # the oracle is a reported baseline, never the product
+            cpu = {"value": None, "error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": "FP64 mEVP element-updates/s", "value": value, "unit": "element-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak" if cname == "C5" else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} CG{cfg.p}/DG{cfg.p} (n_S={cfg.ns}, n_A={cfg.na}) warm box + "
+                                   f"cyclone forcing; step = advect + prep + {cfg.nsub} fused mEVP subcycles",
+                       "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el,
+                       "parallelism": f"row strips x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},
+            "breakdown_ms": {"advect": adv, "prep": prep, "subcycles": sub, "per_subcycle": kernel_ms},
+            "roofline": {"bound": "hbm", "kernel": KERNEL, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": bpe * n_el_rank, "bytes_per_element_subcycle": bpe},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    m.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

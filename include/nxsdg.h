@@ -1,0 +1,196 @@
+/*
+ * nxsdg.h — C ABI of the B200-native neXtSIM-DG mEVP hot path (libnxsdg.so).
+ *
+ * What it computes (PAPER.md = arXiv 2402.00466; "P:n" = PAPER.md line n;
+ * "R#n" = reading n in DESIGN.md §3):
+ *   - Eq. (1): upwind DG advection of ice concentration A and
+ *     thickness H with the CG velocity, explicit SSP Runge-Kutta.
+ *   - Eq. (2)-(3): the mEVP pseudo-time iteration of the momentum
+ *     equation with the viscous-plastic rheology, subcycled within one outer
+ *     (advection) step.  One subcycle = strain (Table 1) ->
+ *     stress update (Listing 1/2) -> stress divergence
+ *      -> velocity update.
+ *   Discretisation: structured quadrilateral box mesh, CG velocity
+ *   of degree p (Q1|Q2), DG stress with n_S coefficients (3|6), DG tracers
+ *   with n_A coefficients (1|3|6), Gauss rule NGP from Listing 2 line 462.
+ *
+ * Layouts at the ABI (logical, independent of the device layout):
+ *   DG field : (owned element rows) x nx x n doubles, row-major, one element's
+ *              n coefficients contiguous, element e = iy*nx + ix.
+ *   CG field : (owned node rows) x (p*nx+1) doubles, row-major,
+ *              node = J*(p*nx+1) + I (R#8).
+ *   With nranks == 1 the owned rows are all rows: N_e = nx*ny elements,
+ *   (p*ny+1)*(p*nx+1) nodes.  With nranks > 1 rank r owns element rows
+ *   [r0, r1) (nxsdg_get_partition) and node rows [p*r0, p*r1), the top rank
+ *   also node row p*ny.
+ *
+ * Ownership: the context owns all device memory.  Caller pointers are
+ * borrowed for the duration of the call only (data is copied).  DEVICE
+ * pointers must be on the context's device.
+ *
+ * Asynchrony: all work is ordered on the context stream.  HOST-memory reads
+ * and writes are synchronous with respect to the host buffer; DEVICE-memory
+ * reads and writes and all compute calls are asynchronous (stream-ordered);
+ * nxsdg_synchronize waits.
+ *
+ * Errors: every call returns nxsdg_status; nothing throws across the ABI.
+ * Invalid arguments never mutate state.  A CUDA or NCCL failure poisons the
+ * context: every later call except nxsdg_destroy / nxsdg_last_error returns
+ * NXSDG_ERR_STATE.  No CUDA device -> NXSDG_ERR_CUDA: there is no CPU
+ * fallback.  A context is not thread-safe; several contexts per process are
+ * allowed (used by the loopback row-strip tests).
+ */
+#ifndef NXSDG_ABI_INCLUDED_H_
+#define NXSDG_ABI_INCLUDED_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NXSDG_ABI_VERSION 1
+
+typedef struct nxsdg_ctx nxsdg_ctx;
+
+typedef enum {
+    NXSDG_OK = 0,
+    NXSDG_ERR_INVALID_ARG = 1, /* null pointer, bad size/count, bad enum            */
+    NXSDG_ERR_UNSUPPORTED = 2, /* degree combination or mode not implemented         */
+    NXSDG_ERR_STATE = 3,       /* wrong call order, or context poisoned              */
+    NXSDG_ERR_CUDA = 4,        /* CUDA error or no device                            */
+    NXSDG_ERR_NCCL = 5,        /* NCCL error or NCCL not loadable                    */
+    NXSDG_ERR_OOM = 6          /* device allocation failed                           */
+} nxsdg_status;
+
+typedef enum { NXSDG_MEM_HOST = 0, NXSDG_MEM_DEVICE = 1 } nxsdg_mem;
+
+typedef enum {
+    NXSDG_BC_CLOSED = 0,   /* v = 0 on the box boundary, zero advective boundary flux (R#16)   */
+    NXSDG_BC_PERIODIC = 1  /* advection only (tests); nxsdg_mevp_substeps -> UNSUPPORTED       */
+} nxsdg_bc;
+
+typedef enum {
+    NXSDG_VX = 0, NXSDG_VY = 1,                   /* CG nodes                                  */
+    NXSDG_S11 = 2, NXSDG_S12 = 3, NXSDG_S22 = 4,  /* DG n_S: stress (mEVP state)        */
+    NXSDG_A = 5, NXSDG_H = 6,                     /* DG n_A: concentration, thickness  */
+    NXSDG_E11 = 7, NXSDG_E12 = 8, NXSDG_E22 = 9,  /* DG n_S: strain rate, debug steps only     */
+    NXSDG_FX = 10, NXSDG_FY = 11,                 /* CG: assembled -(sigma, grad phi), debug   */
+    NXSDG_NFIELDS = 12
+} nxsdg_field;
+
+/* nxsdg_mevp_substeps flags */
+enum {
+    NXSDG_BEGIN_STEP = 1u, /* start an outer step: v^n <- v, nodal H/A, node constants, P at Gauss points */
+    NXSDG_UNFUSED = 2u     /* run the 4 unfused step kernels instead of the fused subcycle kernel        */
+};
+
+/* single debug steps (nxsdg_run_step) */
+typedef enum {
+    NXSDG_STEP_STRAIN = 0,     /* E <- Pi_DG sym grad v                      (R#9)          */
+    NXSDG_STEP_STRESS = 1,     /* S <- Listing 2 update with stored E, H, A           */
+    NXSDG_STEP_DIVERGENCE = 2, /* F <- -(sigma, grad phi_j) assembled        (R#10)         */
+    NXSDG_STEP_VELOCITY = 3    /* v <- mEVP velocity update with stored F    (R#11)     */
+} nxsdg_step;
+
+typedef enum {
+    NXSDG_TRANSPORT_NONE = 0,     /* nranks == 1                                                  */
+    NXSDG_TRANSPORT_NCCL = 1,     /* one process per GPU, ncclSend/ncclRecv halo rows              */
+    NXSDG_TRANSPORT_LOOPBACK = 2  /* all ranks' contexts in one process (tests), cudaMemcpyAsync  */
+} nxsdg_transport;
+
+typedef struct {
+    int32_t nx, ny;       /* global elements per direction, >= 1                                  */
+    double lx, ly;        /* box extents [m], > 0; hx = lx/nx, hy = ly/ny                         */
+    int32_t cg_degree;    /* p: 1 | 2                                                             */
+    int32_t n_stress;     /* n_S: 3 with p = 1, 6 with p = 2 (R#6)                                */
+    int32_t n_adv;        /* n_A: 1 | 3 (p = 1), 1 | 3 | 6 (p = 2) (R#7)                          */
+    int32_t bc;           /* nxsdg_bc                                                             */
+    int32_t rank, nranks; /* row-strip partition, 1 <= nranks <= ny                               */
+    int32_t transport;    /* nxsdg_transport                                                      */
+    const void* nccl_id;  /* 128-byte ncclUniqueId (NCCL transport), else NULL                    */
+    int32_t device;       /* CUDA ordinal                                                         */
+    void* stream;         /* cudaStream_t to run on; NULL -> library-owned stream                 */
+} nxsdg_mesh_desc;
+
+typedef struct {
+    double rho_ice, rho_atm, rho_ocean; /* densities [kg m^-3] (values R#12)                 */
+    double C_atm, C_ocean;              /* drag coefficients (R#11, R#12)                           */
+    double f_c;                         /* Coriolis parameter [s^-1]                                */
+    double Pstar, DeltaMin;             /* ice strength [N m^-2], minimal deformation [s^-1] */
+    double C_conc;                      /* concentration exponent, the literal 20 of P:183          */
+    double alpha, beta;                 /* mEVP, code form fac = 1 - 1/alpha (R#1); > 1, > 0 */
+    double dt;                          /* outer step [s] (R#14)                                    */
+    int32_t replacement_pressure;       /* 0: -P/2 as Listing 1/2; 1: -P_r/2, P_r = P Draw/Delta (R#4) */
+} nxsdg_params;
+
+/* ---- lifecycle ----------------------------------------------------------- */
+/* Validate, pick the device, partition, allocate padded SoA buffers, run the
+ * element-matrix precompute kernel (K0).  State starts at zero; forcing unset.
+ * Errors: INVALID_ARG (null, nx/ny < 1, extents <= 0, alpha <= 1, bad rank),
+ * UNSUPPORTED (degree combination, periodic with nranks > 1), CUDA, NCCL, OOM. */
+nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* desc, const nxsdg_params* params, nxsdg_ctx** out);
+nxsdg_status nxsdg_destroy(nxsdg_ctx* ctx);
+const char* nxsdg_last_error(const nxsdg_ctx* ctx);
+int32_t nxsdg_abi_version(void);
+
+/* Replace the physical parameters (takes effect at the next BEGIN_STEP for the
+ * node constants; alpha/beta/DeltaMin/Pstar immediately). */
+nxsdg_status nxsdg_set_params(nxsdg_ctx* ctx, const nxsdg_params* params);
+
+/* Row-strip partition of this rank: element rows [elem_row0, elem_row0+elem_rows),
+ * node rows [node_row0, node_row0+node_rows).  Pure host arithmetic. */
+nxsdg_status nxsdg_get_partition(const nxsdg_ctx* ctx, int64_t* elem_row0, int32_t* elem_rows,
+                                 int64_t* node_row0, int32_t* node_rows);
+/* Same arithmetic without a context (host only, no GPU needed). */
+nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int32_t rank,
+                             int64_t* elem_row0, int32_t* elem_rows, int64_t* node_row0, int32_t* node_rows);
+
+/* ---- state ----------------------------------------------------------------- */
+/* count = number of doubles of this rank's owned part in the ABI layout.
+ * Writing invalidates the outer-step constants (next substep call needs BEGIN_STEP). */
+nxsdg_status nxsdg_write_state(nxsdg_ctx* ctx, nxsdg_field field, const double* src, int64_t count, nxsdg_mem mem);
+nxsdg_status nxsdg_read_state(nxsdg_ctx* ctx, nxsdg_field field, double* dst, int64_t count, nxsdg_mem mem);
+
+/* Forcing on the CG nodes (owned rows): ocean current o and wind a [m/s] ("F"). */
+nxsdg_status nxsdg_set_forcing(nxsdg_ctx* ctx, const double* ox, const double* oy,
+                               const double* ax, const double* ay, int64_t count, nxsdg_mem mem);
+
+/* ---- compute ----------------------------------------------------------------- */
+/* n_sub mEVP subcycles.  flags: NXSDG_BEGIN_STEP, NXSDG_UNFUSED.
+ * STATE if forcing unset, or if no BEGIN_STEP happened since the last state write. */
+nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* ctx, int32_t n_sub, uint32_t flags);
+
+/* One advection step of A and H over dt with the current v (Eq. 1, P:121 order: call before
+ * the outer step's substeps).  Invalidates the outer-step constants. */
+nxsdg_status nxsdg_advect(nxsdg_ctx* ctx, double dt);
+
+/* Debug: one unfused step on the current state (needs BEGIN_STEP for STRESS/VELOCITY). */
+nxsdg_status nxsdg_run_step(nxsdg_ctx* ctx, nxsdg_step step);
+
+nxsdg_status nxsdg_synchronize(nxsdg_ctx* ctx);
+
+/* ---- multi-rank plumbing ------------------------------------------------------- */
+/* Fill 128 bytes with a fresh ncclUniqueId (rank 0; broadcast it to the others). */
+nxsdg_status nxsdg_nccl_unique_id(void* out128);
+/* Link the contexts of a loopback partition (ctxs[r] has rank r), all in this process,
+ * all on one device and one stream.  INVALID_ARG otherwise. */
+nxsdg_status nxsdg_loopback_connect(nxsdg_ctx** ctxs, int32_t n);
+/* Loopback partitions step in lockstep: the same semantics as nxsdg_mevp_substeps /
+ * nxsdg_advect on every rank, with the halo rows copied between the contexts
+ * (cudaMemcpyAsync) where the NCCL transport would send/recv them. */
+nxsdg_status nxsdg_group_mevp_substeps(nxsdg_ctx** ctxs, int32_t n, int32_t n_sub, uint32_t flags);
+nxsdg_status nxsdg_group_advect(nxsdg_ctx** ctxs, int32_t n, double dt);
+
+/* ---- introspection ------------------------------------------------------------- */
+/* Number of kernels this context has launched (for the bench's gpu_launches claim). */
+int64_t nxsdg_kernel_launches(const nxsdg_ctx* ctx);
+/* Algorithmic HBM bytes per element-subcycle of the fused kernel. */
+double nxsdg_bytes_per_element_subcycle(const nxsdg_ctx* ctx);
+/* cudaStream_t the context runs on. */
+void* nxsdg_stream(const nxsdg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NXSDG_ABI_INCLUDED_H_ */

@@ -1,0 +1,899 @@
+// libnxsdg.so — host runtime and C ABI (include/nxsdg.h).
+//
+// Owns: the context (partition, padded SoA device buffers, stream), the
+// element-matrix precompute (K0), outer-step prep (K0p), the fused subcycle
+// kernel and its CUDA-graph replay, the unfused debug steps, DG advection, the
+// AoS<->SoA conversion at the ABI, and the row-strip halo exchange (NCCL
+// send/recv, or a loopback transport between contexts of one process).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <string>
+#include <vector>
+
+#include "../../include/nxsdg.h"
+#include "kernels.cuh"
+
+using namespace nxk;
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int kNcclFloat64 = 8;
+
+struct NcclApi {
+    bool loaded = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (api.loaded) return api;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+    api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.loaded = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+                 api.GroupStart && api.GroupEnd;
+    return api;
+}
+}  // namespace
+
+// ---------------------------------------------------------------- context
+struct nxsdg_ctx {
+    nxsdg_mesh_desc d{};
+    nxsdg_params prm{};
+    int P = 2, NS = 6, NA = 6, NG = 9;
+    // partition
+    int64_t r0 = 0, r1 = 0;
+    int glo = 0, ghi = 0, nown = 0, erows_local = 0, nrows_local = 0;
+    int64_t eplane = 0, npitch = 0;
+    // device buffers
+    double* S[2] = {nullptr, nullptr};
+    double* Pg = nullptr;
+    double* A = nullptr; double* H = nullptr;
+    double* Asc[2] = {nullptr, nullptr}; double* Hsc[2] = {nullptr, nullptr};
+    double* E = nullptr; double* Fx = nullptr; double* Fy = nullptr;
+    double* vx[2] = {nullptr, nullptr}; double* vy[2] = {nullptr, nullptr};
+    double *ox = nullptr, *oy = nullptr, *ax = nullptr, *ay = nullptr;
+    double *c1 = nullptr, *rx0 = nullptr, *ry0 = nullptr, *cafo = nullptr;
+    double* staging = nullptr; size_t staging_bytes = 0;
+    int cv = 0, cs = 0; // ping-pong index of v and of S
+    // state flags
+    bool forcing_set = false, prepped = false, poisoned = false;
+    cudaStream_t stream = nullptr; bool own_stream = false;
+    std::string err;
+    int64_t launches = 0;
+    int ty = 32;       // fused kernel chunk rows
+    // transport
+    ncclComm_t comm = nullptr;
+    std::vector<nxsdg_ctx*> peers;   // loopback: all ranks' contexts
+    // graphs: key = (n_sub, cv, cs)
+    std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+};
+
+static nxsdg_status fail(nxsdg_ctx* c, nxsdg_status s, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap; va_start(ap, fmt); vsnprintf(buf, sizeof buf, fmt, ap); va_end(ap);
+        c->err = buf;
+        if (s == NXSDG_ERR_CUDA || s == NXSDG_ERR_NCCL) c->poisoned = true;
+    }
+    return s;
+}
+
+#define CU(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LAUNCHED()                                                                            \
+    do {                                                                                      \
+        ++c->launches;                                                                        \
+        cudaError_t e_ = cudaGetLastError();                                                  \
+        if (e_ != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "launch: %s", cudaGetErrorString(e_)); \
+    } while (0)
+
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+extern "C" nxsdg_status nxsdg_partition(int32_t ny, int32_t p, int32_t nranks, int32_t rank, int64_t* er0,
+                                        int32_t* erows, int64_t* nr0, int32_t* nrows) {
+    if (ny < 1 || nranks < 1 || nranks > ny || rank < 0 || rank >= nranks || (p != 1 && p != 2))
+        return NXSDG_ERR_INVALID_ARG;
+    int64_t base = ny / nranks, rem = ny % nranks;
+    int64_t r0 = rank * base + std::min<int64_t>(rank, rem);
+    int64_t n = base + (rank < rem ? 1 : 0);
+    if (er0) *er0 = r0;
+    if (erows) *erows = (int32_t)n;
+    if (nr0) *nr0 = p * r0;
+    if (nrows) *nrows = (int32_t)(p * n + (rank == nranks - 1 ? 1 : 0));
+    return NXSDG_OK;
+}
+
+extern "C" int32_t nxsdg_abi_version(void) { return NXSDG_ABI_VERSION; }
+
+static nxsdg_status check_params(nxsdg_ctx* c, const nxsdg_params* p) {
+    if (!p) return fail(c, NXSDG_ERR_INVALID_ARG, "params is NULL");
+    if (!(p->alpha > 1.0) || !(p->beta > 0.0) || !(p->dt > 0.0) || !(p->rho_ice > 0.0) || !(p->DeltaMin > 0.0) ||
+        p->Pstar < 0.0)
+        return fail(c, NXSDG_ERR_INVALID_ARG, "params out of range (alpha>1, beta>0, dt>0, rho_ice>0, DeltaMin>0, Pstar>=0)");
+    return NXSDG_OK;
+}
+
+static nxsdg_status alloc(nxsdg_ctx* c, double** p, size_t n) {
+    cudaError_t e = cudaMalloc((void**)p, n * sizeof(double));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, e == cudaErrorMemoryAllocation ? NXSDG_ERR_OOM : NXSDG_ERR_CUDA, "cudaMalloc(%zu doubles): %s", n,
+                    cudaGetErrorString(e));
+    }
+    e = cudaMemsetAsync(*p, 0, n * sizeof(double), c->stream);
+    if (e != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "cudaMemset: %s", cudaGetErrorString(e));
+    return NXSDG_OK;
+}
+
+static void free_all(nxsdg_ctx* c) {
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    double** bufs[] = {&c->S[0], &c->S[1], &c->Pg, &c->A, &c->H, &c->Asc[0], &c->Asc[1], &c->Hsc[0], &c->Hsc[1],
+                       &c->E, &c->Fx, &c->Fy, &c->vx[0], &c->vx[1], &c->vy[0], &c->vy[1], &c->ox, &c->oy,
+                       &c->ax, &c->ay, &c->c1, &c->rx0, &c->ry0, &c->cafo, &c->staging};
+    for (auto b : bufs)
+        if (*b) { cudaFree(*b); *b = nullptr; }
+}
+
+extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_params* prm, nxsdg_ctx** out) {
+    if (!d || !prm || !out) return NXSDG_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (d->nx < 1 || d->ny < 1 || !(d->lx > 0) || !(d->ly > 0)) return NXSDG_ERR_INVALID_ARG;
+    if (d->nranks < 1 || d->nranks > d->ny || d->rank < 0 || d->rank >= d->nranks) return NXSDG_ERR_INVALID_ARG;
+    if (d->bc != NXSDG_BC_CLOSED && d->bc != NXSDG_BC_PERIODIC) return NXSDG_ERR_INVALID_ARG;
+    bool ok_deg = (d->cg_degree == 1 && d->n_stress == 3 && (d->n_adv == 1 || d->n_adv == 3)) ||
+                  (d->cg_degree == 2 && d->n_stress == 6 && (d->n_adv == 1 || d->n_adv == 3 || d->n_adv == 6));
+    if (!ok_deg) return NXSDG_ERR_UNSUPPORTED;
+    if (d->bc == NXSDG_BC_PERIODIC && d->nranks > 1) return NXSDG_ERR_UNSUPPORTED;
+    if (d->nranks > 1 && d->transport != NXSDG_TRANSPORT_NCCL && d->transport != NXSDG_TRANSPORT_LOOPBACK)
+        return NXSDG_ERR_INVALID_ARG;
+    if (d->transport == NXSDG_TRANSPORT_NCCL && d->nranks > 1 && !d->nccl_id) return NXSDG_ERR_INVALID_ARG;
+    if (!(prm->alpha > 1.0) || !(prm->beta > 0.0) || !(prm->dt > 0.0) || !(prm->rho_ice > 0.0) ||
+        !(prm->DeltaMin > 0.0) || prm->Pstar < 0.0)
+        return NXSDG_ERR_INVALID_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { cudaGetLastError(); return NXSDG_ERR_CUDA; }
+    if (d->device < 0 || d->device >= ndev) return NXSDG_ERR_INVALID_ARG;
+
+    nxsdg_ctx* c = new nxsdg_ctx();
+    c->d = *d; c->prm = *prm;
+    c->P = d->cg_degree; c->NS = d->n_stress; c->NA = d->n_adv; c->NG = (c->P + 1) * (c->P + 1);
+    int32_t erows = 0;
+    nxsdg_partition(d->ny, c->P, d->nranks, d->rank, &c->r0, &erows, nullptr, nullptr);
+    c->r1 = c->r0 + erows;
+    c->nown = erows;
+    c->glo = c->r0 > 0 ? 1 : 0;
+    c->ghi = c->r1 < d->ny ? 1 : 0;
+    c->erows_local = c->glo + c->nown + c->ghi;
+    c->nrows_local = c->P * (c->glo + c->nown) + 1;
+    c->eplane = round_up((int64_t)c->erows_local * d->nx, 32);
+    c->npitch = round_up((int64_t)c->P * d->nx + 2, 32);
+    auto bail = [&](nxsdg_status s) { nxsdg_status r = s; free_all(c); if (c->own_stream) cudaStreamDestroy(c->stream); delete c; return r; };
+    if (cudaSetDevice(d->device) != cudaSuccess) { cudaGetLastError(); return bail(NXSDG_ERR_CUDA); }
+    if (d->stream) c->stream = (cudaStream_t)d->stream;
+    else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(NXSDG_ERR_CUDA);
+        c->own_stream = true;
+    }
+    const size_t ne = (size_t)c->eplane, nn = (size_t)c->npitch * c->nrows_local;
+    nxsdg_status s;
+#define AL(ptr, n) if ((s = alloc(c, &(ptr), (n))) != NXSDG_OK) return bail(s)
+    AL(c->S[0], 3 * c->NS * ne); AL(c->S[1], 3 * c->NS * ne);
+    AL(c->Pg, c->NG * ne);
+    AL(c->A, c->NA * ne); AL(c->H, c->NA * ne);
+    AL(c->Asc[0], c->NA * ne); AL(c->Asc[1], c->NA * ne); AL(c->Hsc[0], c->NA * ne); AL(c->Hsc[1], c->NA * ne);
+    AL(c->vx[0], nn); AL(c->vx[1], nn); AL(c->vy[0], nn); AL(c->vy[1], nn);
+    AL(c->ox, nn); AL(c->oy, nn); AL(c->ax, nn); AL(c->ay, nn);
+    AL(c->c1, nn); AL(c->rx0, nn); AL(c->ry0, nn); AL(c->cafo, nn);
+#undef AL
+    // K0: reference-element tables into __constant__ (both degrees; tiny)
+    {
+        RefTab* dtab = nullptr;
+        if (cudaMalloc(&dtab, sizeof(RefTab)) != cudaSuccess) return bail(NXSDG_ERR_OOM);
+        for (int p = 1; p <= 2; ++p) {
+            k_build_tables<<<1, 32, 0, c->stream>>>(dtab, p);
+            ++c->launches;
+            if (cudaMemcpyToSymbolAsync(c_tab, dtab, sizeof(RefTab), (p - 1) * sizeof(RefTab),
+                                        cudaMemcpyDeviceToDevice, c->stream) != cudaSuccess) {
+                cudaFree(dtab); return bail(NXSDG_ERR_CUDA);
+            }
+        }
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        cudaFree(dtab);
+        if (e != cudaSuccess) return bail(NXSDG_ERR_CUDA);
+    }
+    if (d->nranks > 1 && d->transport == NXSDG_TRANSPORT_NCCL) {
+        NcclApi& api = nccl();
+        if (!api.loaded) return bail(NXSDG_ERR_NCCL);
+        ncclUniqueId id; memcpy(&id, d->nccl_id, sizeof id);
+        if (api.CommInitRank(&c->comm, d->nranks, id, d->rank) != 0) return bail(NXSDG_ERR_NCCL);
+    }
+    *out = c;
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_destroy(nxsdg_ctx* c) {
+    if (!c) return NXSDG_ERR_INVALID_ARG;
+    cudaSetDevice(c->d.device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) { nccl().CommDestroy(c->comm); c->comm = nullptr; }
+    free_all(c);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return NXSDG_OK;
+}
+
+extern "C" const char* nxsdg_last_error(const nxsdg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+extern "C" int64_t nxsdg_kernel_launches(const nxsdg_ctx* c) { return c ? c->launches : -1; }
+extern "C" void* nxsdg_stream(const nxsdg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+extern "C" double nxsdg_bytes_per_element_subcycle(const nxsdg_ctx* c) {
+    if (!c) return 0.0;
+    // one fused pass: v gather P^2*2, S read+write 2*3NS, P_g NG,
+    // per node (P^2 per element): 6 constants + v write 2
+    const double p2 = (double)c->P * c->P;
+    return 8.0 * (2 * p2 + 6.0 * c->NS + c->NG + 8.0 * p2);
+}
+
+extern "C" nxsdg_status nxsdg_get_partition(const nxsdg_ctx* c, int64_t* er0, int32_t* erows, int64_t* nr0,
+                                            int32_t* nrows) {
+    if (!c) return NXSDG_ERR_INVALID_ARG;
+    return nxsdg_partition(c->d.ny, c->P, c->d.nranks, c->d.rank, er0, erows, nr0, nrows);
+}
+
+#define GUARD(c)                                                                   \
+    do {                                                                           \
+        if (!(c)) return NXSDG_ERR_INVALID_ARG;                                    \
+        if ((c)->poisoned) return NXSDG_ERR_STATE;                                 \
+        if (cudaSetDevice((c)->d.device) != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "cudaSetDevice"); \
+    } while (0)
+
+extern "C" nxsdg_status nxsdg_set_params(nxsdg_ctx* c, const nxsdg_params* p) {
+    GUARD(c);
+    nxsdg_status s = check_params(c, p);
+    if (s) return s;
+    c->prm = *p;
+    c->prepped = false;
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);   // captured launch arguments are stale
+    c->graphs.clear();
+    return NXSDG_OK;
+}
+
+// ---------------------------------------------------------------- state I/O
+static bool is_dg(nxsdg_field f) {
+    return f == NXSDG_S11 || f == NXSDG_S12 || f == NXSDG_S22 || f == NXSDG_A || f == NXSDG_H || f == NXSDG_E11 ||
+           f == NXSDG_E12 || f == NXSDG_E22;
+}
+
+static int64_t owned_node_rows(const nxsdg_ctx* c) {
+    return (int64_t)c->P * c->nown + (c->r1 == c->d.ny ? 1 : 0);
+}
+
+// device pointer of plane 0 of a DG field and its coefficient count
+static double* dg_base(nxsdg_ctx* c, nxsdg_field f, int* n) {
+    switch (f) {
+        case NXSDG_S11: *n = c->NS; return c->S[c->cs];
+        case NXSDG_S12: *n = c->NS; return c->S[c->cs] + (size_t)c->NS * c->eplane;
+        case NXSDG_S22: *n = c->NS; return c->S[c->cs] + (size_t)2 * c->NS * c->eplane;
+        case NXSDG_A: *n = c->NA; return c->A;
+        case NXSDG_H: *n = c->NA; return c->H;
+        case NXSDG_E11: *n = c->NS; return c->E;
+        case NXSDG_E12: *n = c->NS; return c->E ? c->E + (size_t)c->NS * c->eplane : nullptr;
+        case NXSDG_E22: *n = c->NS; return c->E ? c->E + (size_t)2 * c->NS * c->eplane : nullptr;
+        default: *n = 0; return nullptr;
+    }
+}
+static double* cg_base(nxsdg_ctx* c, nxsdg_field f) {
+    switch (f) {
+        case NXSDG_VX: return c->vx[c->cv];
+        case NXSDG_VY: return c->vy[c->cv];
+        case NXSDG_FX: return c->Fx;
+        case NXSDG_FY: return c->Fy;
+        default: return nullptr;
+    }
+}
+
+static nxsdg_status ensure_staging(nxsdg_ctx* c, size_t bytes) {
+    if (c->staging_bytes >= bytes) return NXSDG_OK;
+    if (c->staging) { cudaFree(c->staging); c->staging = nullptr; c->staging_bytes = 0; }
+    cudaError_t e = cudaMalloc((void**)&c->staging, bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(c, NXSDG_ERR_OOM, "staging alloc %zu B", bytes); }
+    c->staging_bytes = bytes;
+    return NXSDG_OK;
+}
+
+static nxsdg_status ensure_debug_buffers(nxsdg_ctx* c) {
+    nxsdg_status s;
+    const size_t nn = (size_t)c->npitch * c->nrows_local;
+    if (!c->E && (s = alloc(c, &c->E, 3 * (size_t)c->NS * c->eplane))) return s;
+    if (!c->Fx && (s = alloc(c, &c->Fx, nn))) return s;
+    if (!c->Fy && (s = alloc(c, &c->Fy, nn))) return s;
+    return NXSDG_OK;
+}
+
+static nxsdg_status copy_in_nodes(nxsdg_ctx* c, double* dst, const double* src, int64_t count, nxsdg_mem mem) {
+    const int64_t rows = owned_node_rows(c), cols = (int64_t)c->P * c->d.nx + 1;
+    if (count != rows * cols) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld nodes", (long long)count, (long long)(rows * cols));
+    double* d0 = dst + (size_t)c->P * c->glo * c->npitch;
+    CU(cudaMemcpy2DAsync(d0, c->npitch * sizeof(double), src, cols * sizeof(double), cols * sizeof(double), rows,
+                         mem == NXSDG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream));
+    if (mem == NXSDG_MEM_HOST) CU(cudaStreamSynchronize(c->stream));
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_write_state(nxsdg_ctx* c, nxsdg_field f, const double* src, int64_t count, nxsdg_mem mem) {
+    GUARD(c);
+    if (!src || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE) || f < 0 || f >= NXSDG_NFIELDS)
+        return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
+    if (f == NXSDG_FX || f == NXSDG_FY || f == NXSDG_E11 || f == NXSDG_E12 || f == NXSDG_E22) {
+        nxsdg_status s = ensure_debug_buffers(c);
+        if (s) return s;
+    }
+    if (is_dg(f)) {
+        int n = 0;
+        double* base = dg_base(c, f, &n);
+        const int64_t ne = (int64_t)c->nown * c->d.nx;
+        if (count != ne * n) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)(ne * n));
+        const double* dsrc = src;
+        if (mem == NXSDG_MEM_HOST) {
+            nxsdg_status s = ensure_staging(c, count * sizeof(double));
+            if (s) return s;
+            CU(cudaMemcpyAsync(c->staging, src, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            dsrc = c->staging;
+        }
+        const int64_t tot = ne * n;
+        k_aos_to_soa<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(dsrc, base, ne, n, c->eplane,
+                                                                         (int64_t)c->glo * c->d.nx);
+        LAUNCHED();
+        if (mem == NXSDG_MEM_HOST) CU(cudaStreamSynchronize(c->stream));
+    } else {
+        nxsdg_status s = copy_in_nodes(c, cg_base(c, f), src, count, mem);
+        if (s) return s;
+    }
+    c->prepped = false;
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_read_state(nxsdg_ctx* c, nxsdg_field f, double* dst, int64_t count, nxsdg_mem mem) {
+    GUARD(c);
+    if (!dst || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE) || f < 0 || f >= NXSDG_NFIELDS)
+        return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
+    if (is_dg(f)) {
+        int n = 0;
+        double* base = dg_base(c, f, &n);
+        if (!base) return fail(c, NXSDG_ERR_STATE, "field not computed yet");
+        const int64_t ne = (int64_t)c->nown * c->d.nx;
+        if (count != ne * n) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)(ne * n));
+        double* ddst = dst;
+        if (mem == NXSDG_MEM_HOST) {
+            nxsdg_status s = ensure_staging(c, count * sizeof(double));
+            if (s) return s;
+            ddst = c->staging;
+        }
+        const int64_t tot = ne * n;
+        k_soa_to_aos<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(base, ddst, ne, n, c->eplane,
+                                                                          (int64_t)c->glo * c->d.nx);
+        LAUNCHED();
+        if (mem == NXSDG_MEM_HOST) {
+            CU(cudaMemcpyAsync(dst, c->staging, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaStreamSynchronize(c->stream));
+        }
+    } else {
+        double* base = cg_base(c, f);
+        if (!base) return fail(c, NXSDG_ERR_STATE, "field not computed yet");
+        const int64_t rows = owned_node_rows(c), cols = (int64_t)c->P * c->d.nx + 1;
+        if (count != rows * cols) return fail(c, NXSDG_ERR_INVALID_ARG, "count mismatch");
+        CU(cudaMemcpy2DAsync(dst, cols * sizeof(double), base + (size_t)c->P * c->glo * c->npitch,
+                             c->npitch * sizeof(double), cols * sizeof(double), rows,
+                             mem == NXSDG_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream));
+        if (mem == NXSDG_MEM_HOST) CU(cudaStreamSynchronize(c->stream));
+    }
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_set_forcing(nxsdg_ctx* c, const double* ox, const double* oy, const double* ax,
+                                          const double* ay, int64_t count, nxsdg_mem mem) {
+    GUARD(c);
+    if (!ox || !oy || !ax || !ay || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE))
+        return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
+    const int64_t need = owned_node_rows(c) * ((int64_t)c->P * c->d.nx + 1);
+    if (count != need) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)need);
+    nxsdg_status s;
+    if ((s = copy_in_nodes(c, c->ox, ox, count, mem))) return s;
+    if ((s = copy_in_nodes(c, c->oy, oy, count, mem))) return s;
+    if ((s = copy_in_nodes(c, c->ax, ax, count, mem))) return s;
+    if ((s = copy_in_nodes(c, c->ay, ay, count, mem))) return s;
+    c->forcing_set = true;
+    c->prepped = false;
+    return NXSDG_OK;
+}
+
+// ---------------------------------------------------------------- halo exchange
+// Rows that cross a rank boundary:
+//   up   (r -> r+1): top owned element row of element fields; top P owned node rows of node fields
+//   down (r -> r-1): bottom owned node row of node fields; bottom owned element row (advection only)
+enum HaloWhat { HALO_V = 1, HALO_S = 2, HALO_AH = 4, HALO_AH_SCR0 = 8, HALO_AH_SCR1 = 16 };
+
+struct Seg { double* src; double* dst; size_t n; int peer; };
+
+static void element_row_segs(nxsdg_ctx* c, nxsdg_ctx* nb, double* base_me, double* base_nb, int nplanes,
+                             int my_row, int nb_row, int peer, std::vector<Seg>& out) {
+    for (int k = 0; k < nplanes; ++k)
+        out.push_back({base_me + (size_t)k * c->eplane + (size_t)my_row * c->d.nx,
+                       base_nb ? base_nb + (size_t)k * nb->eplane + (size_t)nb_row * nb->d.nx : nullptr,
+                       (size_t)c->d.nx, peer});
+}
+
+// Build the list of (send) segments of this rank for `what`; for loopback the
+// destination pointers are filled from the neighbour context.
+static void halo_segments(nxsdg_ctx* c, int what, std::vector<Seg>& sends, std::vector<Seg>& recvs) {
+    const int rank = c->d.rank, nr = c->d.nranks;
+    const bool up = rank + 1 < nr, down = rank > 0;
+    nxsdg_ctx* nup = (up && !c->peers.empty()) ? c->peers[rank + 1] : nullptr;
+    nxsdg_ctx* ndn = (down && !c->peers.empty()) ? c->peers[rank - 1] : nullptr;
+    const int top_row = c->glo + c->nown - 1, bot_row = c->glo;
+    const size_t prow = (size_t)c->npitch;
+    auto node_rows = [&](double* base_me, double* base_nb_up, double* base_nb_dn, double* recv_lo, double* recv_hi) {
+        if (up) {
+            sends.push_back({base_me + (size_t)c->P * top_row * prow, base_nb_up, prow * c->P, rank + 1});
+            recvs.push_back({nullptr, recv_hi, prow, rank + 1});
+        }
+        if (down) {
+            sends.push_back({base_me + (size_t)c->P * bot_row * prow,
+                             base_nb_dn ? base_nb_dn + (size_t)c->P * (ndn->glo + ndn->nown) * prow : nullptr, prow,
+                             rank - 1});
+            recvs.push_back({nullptr, recv_lo, prow * c->P, rank - 1});
+        }
+    };
+    if (what & HALO_V) {
+        for (int comp = 0; comp < 2; ++comp) {
+            double* me = comp ? c->vy[c->cv] : c->vx[c->cv];
+            double* u = nup ? (comp ? nup->vy[nup->cv] : nup->vx[nup->cv]) : nullptr;
+            double* dn = ndn ? (comp ? ndn->vy[ndn->cv] : ndn->vx[ndn->cv]) : nullptr;
+            node_rows(me, u, dn, me, me + (size_t)c->P * (c->glo + c->nown) * prow);
+        }
+    }
+    auto elem_field = [&](double* me, double* u, double* dn, int nplanes, bool both) {
+        if (up) {
+            element_row_segs(c, nup, me, u, nplanes, top_row, 0, rank + 1, sends);
+            if (both) element_row_segs(c, nup, me, nullptr, nplanes, c->glo + c->nown, 0, rank + 1, recvs);
+        }
+        if (down) {
+            if (both) element_row_segs(c, ndn, me, dn, nplanes, bot_row, ndn ? ndn->glo + ndn->nown : 0, rank - 1, sends);
+            element_row_segs(c, ndn, me, nullptr, nplanes, 0, 0, rank - 1, recvs);
+        }
+    };
+    if (what & HALO_S) elem_field(c->S[c->cs], nup ? nup->S[nup->cs] : nullptr, ndn ? ndn->S[ndn->cs] : nullptr, 3 * c->NS, false);
+    if (what & HALO_AH) {
+        elem_field(c->A, nup ? nup->A : nullptr, ndn ? ndn->A : nullptr, c->NA, true);
+        elem_field(c->H, nup ? nup->H : nullptr, ndn ? ndn->H : nullptr, c->NA, true);
+    }
+    if (what & (HALO_AH_SCR0 | HALO_AH_SCR1)) {
+        int b = (what & HALO_AH_SCR0) ? 0 : 1;
+        elem_field(c->Asc[b], nup ? nup->Asc[b] : nullptr, ndn ? ndn->Asc[b] : nullptr, c->NA, true);
+        elem_field(c->Hsc[b], nup ? nup->Hsc[b] : nullptr, ndn ? ndn->Hsc[b] : nullptr, c->NA, true);
+    }
+    // recv segments for the element "both" case were generated with src = my ghost rows; turn them into dsts
+    for (auto& r : recvs)
+        if (!r.dst) { r.dst = r.src; r.src = nullptr; }
+}
+
+static nxsdg_status halo_nccl(nxsdg_ctx* c, int what) {
+    std::vector<Seg> sends, recvs;
+    halo_segments(c, what, sends, recvs);
+    NcclApi& api = nccl();
+    if (api.GroupStart() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupStart");
+    for (auto& s : sends)
+        if (api.Send(s.src, s.n, kNcclFloat64, s.peer, c->comm, c->stream) != 0) { api.GroupEnd(); return fail(c, NXSDG_ERR_NCCL, "ncclSend"); }
+    for (auto& r : recvs)
+        if (api.Recv(r.dst, r.n, kNcclFloat64, r.peer, c->comm, c->stream) != 0) { api.GroupEnd(); return fail(c, NXSDG_ERR_NCCL, "ncclRecv"); }
+    if (api.GroupEnd() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupEnd");
+    return NXSDG_OK;
+}
+
+// Loopback: every context pushes its send segments straight into its neighbours'
+// ghost rows (all contexts share one stream, so ordering is the stream order).
+static nxsdg_status halo_loopback_all(std::vector<nxsdg_ctx*>& ctxs, int what) {
+    for (nxsdg_ctx* c : ctxs) {
+        std::vector<Seg> sends, recvs;
+        halo_segments(c, what, sends, recvs);
+        for (auto& s : sends)
+            CU(cudaMemcpyAsync(s.dst, s.src, s.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return NXSDG_OK;
+}
+
+static nxsdg_status halo(nxsdg_ctx* c, int what) {
+    if (c->d.nranks == 1) return NXSDG_OK;
+    if (c->d.transport == NXSDG_TRANSPORT_NCCL) return halo_nccl(c, what);
+    return NXSDG_OK;   // loopback exchanges are driven by the group calls
+}
+
+// ---------------------------------------------------------------- launches
+static PrepArgs prep_args(nxsdg_ctx* c) {
+    PrepArgs a{};
+    a.H = c->H; a.A = c->A; a.vx = c->vx[c->cv]; a.vy = c->vy[c->cv];
+    a.ox = c->ox; a.oy = c->oy; a.ax = c->ax; a.ay = c->ay;
+    a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.Pg = c->Pg;
+    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx; a.erows_local = c->erows_local;
+    a.node_row_begin = c->P * c->glo;
+    a.node_row_end = (int)(c->P * c->glo + owned_node_rows(c));
+    a.elem_rows_with_nodes = c->glo + c->nown;
+    a.rho_ice = c->prm.rho_ice; a.Fa = c->prm.rho_atm * c->prm.C_atm; a.Fo = c->prm.rho_ocean * c->prm.C_ocean;
+    a.f_c = c->prm.f_c; a.dt = c->prm.dt; a.Pstar = c->prm.Pstar; a.C_conc = c->prm.C_conc;
+    return a;
+}
+
+template <int P, int NA>
+static nxsdg_status launch_prep(nxsdg_ctx* c) {
+    PrepArgs a = prep_args(c);
+    dim3 bn(128), gn((unsigned)((P * c->d.nx + 1 + 127) / 128), (unsigned)(a.node_row_end - a.node_row_begin));
+    k_prep_nodes<P, NA><<<gn, bn, 0, c->stream>>>(a);
+    LAUNCHED();
+    dim3 be(128), ge((unsigned)((c->d.nx + 127) / 128), (unsigned)c->erows_local);
+    k_prep_elems<P, NA><<<ge, be, 0, c->stream>>>(a);
+    LAUNCHED();
+    return NXSDG_OK;
+}
+
+static nxsdg_status dispatch_prep(nxsdg_ctx* c) {
+    if (c->P == 1) return c->NA == 1 ? launch_prep<1, 1>(c) : launch_prep<1, 3>(c);
+    if (c->NA == 1) return launch_prep<2, 1>(c);
+    if (c->NA == 3) return launch_prep<2, 3>(c);
+    return launch_prep<2, 6>(c);
+}
+
+static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
+    SubArgs a{};
+    a.S_in = c->S[cs]; a.S_out = c->S[cs ^ 1]; a.Pg = c->Pg;
+    a.vx_in = c->vx[cv]; a.vy_in = c->vy[cv]; a.vx_out = c->vx[cv ^ 1]; a.vy_out = c->vy[cv ^ 1];
+    a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.ox = c->ox; a.oy = c->oy;
+    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx;
+    a.nstrips = (c->d.nx + 1 + 30) / 31;
+    a.ty = c->ty;
+    a.erow_begin = c->glo; a.erow_end = c->glo + c->nown;
+    a.bottom_boundary = c->r0 == 0;
+    a.top_boundary = c->r1 == c->d.ny;
+    const double hx = c->d.lx / c->d.nx, hy = c->d.ly / c->d.ny;
+    a.ihx = 1.0 / hx; a.ihy = 1.0 / hy;
+    a.ainv = 1.0 / c->prm.alpha; a.fac = 1.0 - a.ainv;
+    a.dmin2 = c->prm.DeltaMin * c->prm.DeltaMin;
+    a.beta = c->prm.beta; a.b1 = 1.0 + c->prm.beta; a.kc = c->prm.dt * c->prm.f_c;
+    a.repl = c->prm.replacement_pressure;
+    return a;
+}
+
+static nxsdg_status launch_subcycle(nxsdg_ctx* c) {
+    SubArgs a = sub_args(c, c->cv, c->cs);
+    const int nchunks = (c->nown + a.ty - 1) / a.ty;
+    const int64_t warps = (int64_t)a.nstrips * nchunks;
+    const unsigned blocks = (unsigned)((warps + 3) / 4);
+    if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
+    else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
+    LAUNCHED();
+    c->cv ^= 1; c->cs ^= 1;
+    return NXSDG_OK;
+}
+
+static StepArgs step_args(nxsdg_ctx* c) {
+    StepArgs a{};
+    a.vx_in = c->vx[c->cv]; a.vy_in = c->vy[c->cv]; a.vx_out = c->vx[c->cv ^ 1]; a.vy_out = c->vy[c->cv ^ 1];
+    a.S = c->S[c->cs]; a.E = c->E; a.Fx = c->Fx; a.Fy = c->Fy; a.H = c->H; a.A = c->A;
+    a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.ox = c->ox; a.oy = c->oy;
+    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx;
+    a.erow_begin = c->glo; a.erow_end = c->glo + c->nown; a.elem_rows_with_nodes = c->glo + c->nown;
+    a.node_row_begin = c->P * c->glo; a.node_row_end = (int)(c->P * c->glo + owned_node_rows(c));
+    a.node_row_global0 = (int)(c->P * (c->r0 - c->glo));
+    a.node_rows_global = c->P * c->d.ny + 1;
+    const double hx = c->d.lx / c->d.nx, hy = c->d.ly / c->d.ny;
+    a.ihx = 1.0 / hx; a.ihy = 1.0 / hy; a.area = hx * hy;
+    a.ainv = 1.0 / c->prm.alpha; a.fac = 1.0 - a.ainv;
+    a.dmin2 = c->prm.DeltaMin * c->prm.DeltaMin;
+    a.beta = c->prm.beta; a.b1 = 1.0 + c->prm.beta; a.kc = c->prm.dt * c->prm.f_c;
+    a.Pstar = c->prm.Pstar; a.C_conc = c->prm.C_conc; a.repl = c->prm.replacement_pressure;
+    return a;
+}
+
+template <int P, int NA>
+static nxsdg_status launch_step_t(nxsdg_ctx* c, nxsdg_step st) {
+    StepArgs a = step_args(c);
+    dim3 be(128), ge((unsigned)((c->d.nx + 127) / 128), (unsigned)c->nown);
+    dim3 bn(128), gn((unsigned)((P * c->d.nx + 1 + 127) / 128), (unsigned)(a.node_row_end - a.node_row_begin));
+    switch (st) {
+        case NXSDG_STEP_STRAIN: k_strain<P><<<ge, be, 0, c->stream>>>(a); break;
+        case NXSDG_STEP_STRESS: k_stress<P, NA><<<ge, be, 0, c->stream>>>(a); break;
+        case NXSDG_STEP_DIVERGENCE: k_divergence<P><<<gn, bn, 0, c->stream>>>(a); break;
+        case NXSDG_STEP_VELOCITY: k_velocity<P><<<gn, bn, 0, c->stream>>>(a); break;
+    }
+    LAUNCHED();
+    if (st == NXSDG_STEP_VELOCITY) c->cv ^= 1;   // S is updated in place, v ping-pongs
+    return NXSDG_OK;
+}
+
+static nxsdg_status launch_step(nxsdg_ctx* c, nxsdg_step st) {
+    if (c->P == 1) return c->NA == 1 ? launch_step_t<1, 1>(c, st) : launch_step_t<1, 3>(c, st);
+    if (c->NA == 1) return launch_step_t<2, 1>(c, st);
+    if (c->NA == 3) return launch_step_t<2, 3>(c, st);
+    return launch_step_t<2, 6>(c, st);
+}
+
+// ---------------------------------------------------------------- compute API
+static nxsdg_status begin_step(nxsdg_ctx* c) {
+    if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
+    nxsdg_status s;
+    if ((s = halo(c, HALO_V | HALO_S | HALO_AH))) return s;
+    if ((s = dispatch_prep(c))) return s;
+    c->prepped = true;
+    return NXSDG_OK;
+}
+
+static nxsdg_status check_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
+    if (n < 0 || (flags & ~(uint32_t)(NXSDG_BEGIN_STEP | NXSDG_UNFUSED))) return fail(c, NXSDG_ERR_INVALID_ARG, "bad n/flags");
+    if (c->d.bc != NXSDG_BC_CLOSED) return fail(c, NXSDG_ERR_UNSUPPORTED, "mEVP substeps need the closed box");
+    if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
+    if (!(flags & NXSDG_BEGIN_STEP) && !c->prepped) return fail(c, NXSDG_ERR_STATE, "first call of an outer step needs NXSDG_BEGIN_STEP");
+    return NXSDG_OK;
+}
+
+static nxsdg_status one_subcycle(nxsdg_ctx* c, bool unfused) {
+    nxsdg_status s;
+    if (!unfused) {
+        if ((s = launch_subcycle(c))) return s;
+        return halo(c, HALO_V | HALO_S);
+    }
+    if ((s = ensure_debug_buffers(c))) return s;
+    if ((s = launch_step(c, NXSDG_STEP_STRAIN))) return s;
+    if ((s = launch_step(c, NXSDG_STEP_STRESS))) return s;
+    if ((s = halo(c, HALO_S))) return s;
+    if ((s = launch_step(c, NXSDG_STEP_DIVERGENCE))) return s;
+    if ((s = launch_step(c, NXSDG_STEP_VELOCITY))) return s;
+    return halo(c, HALO_V);
+}
+
+// Capture n fused subcycles into a CUDA graph (nranks == 1) and replay it.
+static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
+    auto key = std::make_tuple(n, c->cv, c->cs);
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        cudaGraph_t g;
+        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        int cv = c->cv, cs = c->cs;
+        for (int i = 0; i < n; ++i) {
+            SubArgs a = sub_args(c, cv, cs);
+            const int nchunks = (c->nown + a.ty - 1) / a.ty;
+            const unsigned blocks = (unsigned)(((int64_t)a.nstrips * nchunks + 3) / 4);
+            if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
+            else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
+            cv ^= 1; cs ^= 1;
+        }
+        cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (e != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        cudaGraphExec_t ge;
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+        it = c->graphs.emplace(key, ge).first;
+    }
+    CU(cudaGraphLaunch(it->second, c->stream));
+    c->launches += n;
+    if (n & 1) { c->cv ^= 1; c->cs ^= 1; }
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
+    GUARD(c);
+    nxsdg_status s = check_substeps(c, n, flags);
+    if (s) return s;
+    if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_LOOPBACK)
+        return fail(c, NXSDG_ERR_STATE, "loopback ranks step through nxsdg_group_mevp_substeps");
+    if ((flags & NXSDG_BEGIN_STEP) && (s = begin_step(c))) return s;
+    const bool unfused = flags & NXSDG_UNFUSED;
+    if (!unfused && c->d.nranks == 1 && n > 0) return run_graph(c, n);
+    for (int i = 0; i < n; ++i)
+        if ((s = one_subcycle(c, unfused))) return s;
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_run_step(nxsdg_ctx* c, nxsdg_step st) {
+    GUARD(c);
+    if (st < NXSDG_STEP_STRAIN || st > NXSDG_STEP_VELOCITY) return fail(c, NXSDG_ERR_INVALID_ARG, "bad step");
+    if ((st == NXSDG_STEP_STRESS || st == NXSDG_STEP_VELOCITY) && !c->prepped)
+        return fail(c, NXSDG_ERR_STATE, "needs a BEGIN_STEP (nxsdg_mevp_substeps(ctx, 0, NXSDG_BEGIN_STEP))");
+    if (c->d.nranks > 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "debug steps are single-rank");
+    nxsdg_status s = ensure_debug_buffers(c);
+    if (s) return s;
+    return launch_step(c, st);
+}
+
+// ---------------------------------------------------------------- advection
+template <int P, int NA>
+static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const double* Hin, double* Aout,
+                                        double* Hout, double dt, double a0, double a1) {
+    AdvArgs a{};
+    a.Ain = Ain; a.Hin = Hin; a.A0 = c->A; a.H0 = c->H; a.Aout = Aout; a.Hout = Hout;
+    a.vx = c->vx[c->cv]; a.vy = c->vy[c->cv];
+    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx;
+    a.erow_begin = c->glo; a.erow_end = c->glo + c->nown;
+    a.has_south = c->glo; a.has_north = c->ghi;
+    a.periodic = c->d.bc == NXSDG_BC_PERIODIC; a.erows_local = c->erows_local;
+    a.ihx = c->d.nx / c->d.lx; a.ihy = c->d.ny / c->d.ly;
+    a.ihx = 1.0 / (c->d.lx / c->d.nx); a.ihy = 1.0 / (c->d.ly / c->d.ny);
+    a.dt = dt; a.a0 = a0; a.a1 = a1;
+    dim3 b(32, 8), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + 7) / 8));
+    k_advect<P, NA><<<g, b, 0, c->stream>>>(a);
+    LAUNCHED();
+    return NXSDG_OK;
+}
+
+template <int P, int NA>
+static nxsdg_status advect_t(nxsdg_ctx* c, double dt, int stage) {
+    // stage-by-stage so the loopback group driver can exchange between stages
+    switch (NA) {
+        case 1:
+            return launch_advect_stage<P, NA>(c, c->A, c->H, c->Asc[0], c->Hsc[0], dt, 0.0, 1.0);
+        case 3:
+            if (stage == 0) return launch_advect_stage<P, NA>(c, c->A, c->H, c->Asc[0], c->Hsc[0], dt, 0.0, 1.0);
+            return launch_advect_stage<P, NA>(c, c->Asc[0], c->Hsc[0], c->Asc[1], c->Hsc[1], dt, 0.5, 0.5);
+        default:
+            if (stage == 0) return launch_advect_stage<P, NA>(c, c->A, c->H, c->Asc[0], c->Hsc[0], dt, 0.0, 1.0);
+            if (stage == 1) return launch_advect_stage<P, NA>(c, c->Asc[0], c->Hsc[0], c->Asc[1], c->Hsc[1], dt, 0.75, 0.25);
+            return launch_advect_stage<P, NA>(c, c->Asc[1], c->Hsc[1], c->Asc[0], c->Hsc[0], dt, 1.0 / 3.0, 2.0 / 3.0);
+    }
+}
+
+static int n_stages(const nxsdg_ctx* c) { return c->NA == 1 ? 1 : (c->NA == 3 ? 2 : 3); }
+static int stage_out_buf(const nxsdg_ctx* c, int stage) {
+    if (c->NA == 3) return stage;           // 0 -> scr0, 1 -> scr1
+    if (c->NA == 6) return stage == 1 ? 1 : 0;
+    return 0;
+}
+
+static nxsdg_status advect_stage(nxsdg_ctx* c, double dt, int stage) {
+    if (c->P == 1) return c->NA == 1 ? advect_t<1, 1>(c, dt, stage) : advect_t<1, 3>(c, dt, stage);
+    if (c->NA == 1) return advect_t<2, 1>(c, dt, stage);
+    if (c->NA == 3) return advect_t<2, 3>(c, dt, stage);
+    return advect_t<2, 6>(c, dt, stage);
+}
+
+// copy the final stage buffer back into A, H (owned rows)
+static nxsdg_status advect_finish(nxsdg_ctx* c) {
+    const int last = stage_out_buf(c, n_stages(c) - 1);
+    const size_t off = (size_t)c->glo * c->d.nx, n = (size_t)c->nown * c->d.nx;
+    for (int k = 0; k < c->NA; ++k) {
+        CU(cudaMemcpyAsync(c->A + k * c->eplane + off, c->Asc[last] + k * c->eplane + off, n * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->H + k * c->eplane + off, c->Hsc[last] + k * c->eplane + off, n * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c->stream));
+    }
+    c->prepped = false;
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
+    GUARD(c);
+    if (!(dt >= 0.0)) return fail(c, NXSDG_ERR_INVALID_ARG, "dt < 0");
+    if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_LOOPBACK)
+        return fail(c, NXSDG_ERR_STATE, "loopback ranks advect through nxsdg_group_advect");
+    nxsdg_status s;
+    if ((s = halo(c, HALO_V | HALO_AH))) return s;
+    for (int st = 0; st < n_stages(c); ++st) {
+        if ((s = advect_stage(c, dt, st))) return s;
+        if (st + 1 < n_stages(c) && (s = halo(c, stage_out_buf(c, st) == 0 ? HALO_AH_SCR0 : HALO_AH_SCR1))) return s;
+    }
+    return advect_finish(c);
+}
+
+extern "C" nxsdg_status nxsdg_synchronize(nxsdg_ctx* c) {
+    GUARD(c);
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaGetLastError());
+    return NXSDG_OK;
+}
+
+// ---------------------------------------------------------------- multi-rank plumbing
+extern "C" nxsdg_status nxsdg_nccl_unique_id(void* out128) {
+    if (!out128) return NXSDG_ERR_INVALID_ARG;
+    NcclApi& api = nccl();
+    if (!api.loaded) return NXSDG_ERR_NCCL;
+    ncclUniqueId id;
+    if (api.GetUniqueId(&id) != 0) return NXSDG_ERR_NCCL;
+    memcpy(out128, &id, sizeof id);
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_loopback_connect(nxsdg_ctx** ctxs, int32_t n) {
+    if (!ctxs || n < 1) return NXSDG_ERR_INVALID_ARG;
+    for (int i = 0; i < n; ++i) {
+        if (!ctxs[i] || ctxs[i]->d.rank != i || ctxs[i]->d.nranks != n || ctxs[i]->d.transport != NXSDG_TRANSPORT_LOOPBACK)
+            return NXSDG_ERR_INVALID_ARG;
+        if (ctxs[i]->stream != ctxs[0]->stream || ctxs[i]->d.device != ctxs[0]->d.device) return NXSDG_ERR_INVALID_ARG;
+    }
+    std::vector<nxsdg_ctx*> v(ctxs, ctxs + n);
+    for (int i = 0; i < n; ++i) ctxs[i]->peers = v;
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_group_mevp_substeps(nxsdg_ctx** ctxs, int32_t nr, int32_t n, uint32_t flags) {
+    if (!ctxs || nr < 1) return NXSDG_ERR_INVALID_ARG;
+    std::vector<nxsdg_ctx*> v(ctxs, ctxs + nr);
+    nxsdg_status s;
+    for (nxsdg_ctx* c : v) {
+        GUARD(c);
+        if (c->peers.size() != (size_t)nr && nr > 1) return fail(c, NXSDG_ERR_STATE, "not loopback-connected");
+        if ((s = check_substeps(c, n, flags))) return s;
+    }
+    const bool unfused = flags & NXSDG_UNFUSED;
+    if (flags & NXSDG_BEGIN_STEP) {
+        if ((s = halo_loopback_all(v, HALO_V | HALO_S | HALO_AH))) return s;
+        for (nxsdg_ctx* c : v) {
+            cudaSetDevice(c->d.device);
+            if ((s = dispatch_prep(c))) return s;
+            c->prepped = true;
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        if (!unfused) {
+            for (nxsdg_ctx* c : v) if ((s = launch_subcycle(c))) return s;
+            if ((s = halo_loopback_all(v, HALO_V | HALO_S))) return s;
+        } else {
+            for (nxsdg_ctx* c : v) {
+                if ((s = ensure_debug_buffers(c))) return s;
+                if ((s = launch_step(c, NXSDG_STEP_STRAIN))) return s;
+                if ((s = launch_step(c, NXSDG_STEP_STRESS))) return s;
+            }
+            if ((s = halo_loopback_all(v, HALO_S))) return s;
+            for (nxsdg_ctx* c : v) {
+                if ((s = launch_step(c, NXSDG_STEP_DIVERGENCE))) return s;
+                if ((s = launch_step(c, NXSDG_STEP_VELOCITY))) return s;
+            }
+            if ((s = halo_loopback_all(v, HALO_V))) return s;
+        }
+    }
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_group_advect(nxsdg_ctx** ctxs, int32_t nr, double dt) {
+    if (!ctxs || nr < 1) return NXSDG_ERR_INVALID_ARG;
+    std::vector<nxsdg_ctx*> v(ctxs, ctxs + nr);
+    nxsdg_status s;
+    for (nxsdg_ctx* c : v) GUARD(c);
+    if ((s = halo_loopback_all(v, HALO_V | HALO_AH))) return s;
+    const int ns = n_stages(v[0]);
+    for (int st = 0; st < ns; ++st) {
+        for (nxsdg_ctx* c : v) if ((s = advect_stage(c, dt, st))) return s;
+        if (st + 1 < ns && (s = halo_loopback_all(v, stage_out_buf(v[0], st) == 0 ? HALO_AH_SCR0 : HALO_AH_SCR1))) return s;
+    }
+    for (nxsdg_ctx* c : v) if ((s = advect_finish(c))) return s;
+    return NXSDG_OK;
+}

@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle, element by element,
+on identical seeded inputs.  Bar (BASELINE.json north_star):
+group-normalised relative max error <= 1e-12 after one subcycle and <= 1e-10
+after the config's full subcycle count, on the fields and on their increments."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2402_00466_b200 import inputs
+from tests.parity import case, ora_mesh, ora_params, parity
+
+pytestmark = pytest.mark.gpu
+
+TOL1, TOLN = 1e-12, 1e-10
+
+
+@pytest.fixture(scope="module")
+def nx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2402_00466_b200 import build
+    build.build()
+    from paper_2402_00466_b200 import nxsdg
+    return nxsdg
+
+
+@pytest.fixture(scope="module")
+def ora():
+    return oracle.Oracle()
+
+
+def _gpu_run(nx, st, nxe, nye, p, ns, na, nsub, lx=512e3, ly=512e3, unfused=False, advect_dt=None, params=None):
+    params = params or nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly, p, ns, na, params=params) as m:
+        m.load(st)
+        if advect_dt is not None:
+            m.advect(advect_dt)
+        m.mevp_substeps(nsub, begin_step=True, unfused=unfused)
+        return m.state()
+
+
+def _check(got, ref, init, tol, groups=("S", "v")):
+    e = parity(got, ref, init, groups)
+    bad = {k: v for k, v in e.items() if not v <= tol}
+    assert not bad, f"parity {e} > {tol}"
+    return e
+
+
+# (nx, ny, p, ns, na, kind, lx, ly): ragged sizes spanning several 31-wide warp
+# strips and 32-row chunks, plus degenerate shapes
+CASES = [
+    (16, 16, 1, 3, 3, "random", 512e3, 512e3),     # C1
+    (37, 29, 2, 6, 6, "warm", 512e3, 512e3),
+    (70, 75, 2, 6, 6, "warm", 140e3, 150e3),       # 3 strips x 3 chunks, ragged
+    (64, 66, 1, 3, 1, "random", 64e3, 66e3),
+    (45, 40, 2, 6, 3, "random", 45e3, 40e3),
+    (1, 5, 2, 6, 6, "random", 1e3, 5e3),
+    (6, 1, 2, 6, 1, "random", 6e3, 1e3),
+    (2, 2, 1, 3, 3, "random", 2e3, 2e3),
+]
+
+
+@pytest.mark.parametrize("unfused", [False, True])
+@pytest.mark.parametrize("c", CASES, ids=[f"{c[0]}x{c[1]}p{c[2]}na{c[4]}{c[5]}" for c in CASES])
+def test_one_subcycle(nx, ora, c, unfused):
+    nxe, nye, p, ns, na, kind, lx, ly = c
+    st = case(nxe, nye, p, ns, na, kind, lx, ly)
+    got = _gpu_run(nx, st, nxe, nye, p, ns, na, 1, lx, ly, unfused=unfused)
+    ref = ora.subcycles(ora_mesh(nxe, nye, p, ns, na, lx, ly), ora_params(nx.PhysParams()), 1, st)
+    _check(got, ref, st, TOL1)
+
+
+@pytest.mark.parametrize("c,nsub", [(CASES[0], 10), (CASES[1], 100), (CASES[2], 30), (CASES[3], 20)],
+                         ids=["C1x10", "37x29x100", "70x75x30", "64x66p1x20"])
+def test_full_subcycle_count(nx, ora, c, nsub):
+    nxe, nye, p, ns, na, kind, lx, ly = c
+    st = case(nxe, nye, p, ns, na, kind, lx, ly)
+    got = _gpu_run(nx, st, nxe, nye, p, ns, na, nsub, lx, ly)
+    ref = ora.subcycles(ora_mesh(nxe, nye, p, ns, na, lx, ly), ora_params(nx.PhysParams()), nsub, st)
+    _check(got, ref, st, TOLN)
+
+
+def test_c2_full_config(nx, ora):
+    """C2: 256x256 CG2/DG2 warm box + cyclone, 100 subcycles (oracle ~1 min on 8 cores)."""
+    cfg = inputs.CONFIGS["C2"]
+    st = inputs.make_config_case(cfg)
+    got = _gpu_run(nx, st, cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, cfg.nsub)
+    ref = ora.subcycles(ora_mesh(cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na), ora_params(nx.PhysParams()), cfg.nsub, st)
+    _check(got, ref, st, TOLN)
+
+
+@pytest.mark.parametrize("na", [1, 3, 6])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_advection(nx, ora, na, bc):
+    p, ns = 2, 6
+    nxe, nye, lx, ly = 45, 38, 45e3, 38e3
+    st = case(nxe, nye, p, ns, na, "random", lx, ly)
+    if bc == 1:   # periodic nodal velocity
+        for k in ("vx", "vy"):
+            st[k] = np.random.default_rng(3).uniform(-0.1, 0.1, st[k].shape)
+            st[k][-1, :] = st[k][0, :]; st[k][:, -1] = st[k][:, 0]
+    dt = 600.0
+    with nx.Mesh(nxe, nye, lx, ly, p, ns, na, bc=bc) as m:
+        m.load(st)
+        m.advect(dt)
+        got = m.state(("A", "H"))
+    A, H = ora.advect(ora_mesh(nxe, nye, p, ns, na, lx, ly, bc=bc), dt, st["vx"], st["vy"], st["A"], st["H"])
+    _check(got, {"A": A, "H": H}, st, 1e-12, groups=("A", "H"))
+    if bc == 1:
+        assert abs(got["A"][:, 0].sum() - st["A"][:, 0].sum()) < 1e-12 * abs(st["A"][:, 0]).sum()
+
+
+def test_outer_step_c3_shape(nx, ora):
+    """Paper order: advect, then subcycles; 96x80 CG2/DG2 at C3 resolution (250 m)."""
+    nxe, nye = 96, 80
+    lx, ly = nxe * 250.0, nye * 250.0
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    prm = nx.PhysParams()
+    got = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 20, lx, ly, advect_dt=prm.dt)
+    ref = ora.outer_step(ora_mesh(nxe, nye, 2, 6, 6, lx, ly), ora_params(prm), 20, st, do_advect=True)
+    _check(got, ref, st, TOLN, groups=("S", "v", "A", "H"))
+
+
+def test_debug_steps_each_against_oracle(nx, ora):
+    """Each Table 1 step alone (unfused kernels via nxsdg_run_step) against the oracle's step."""
+    nxe, nye, p, ns, na = 33, 35, 2, 6, 6
+    lx, ly = 33e3, 35e3
+    st = case(nxe, nye, p, ns, na, "random", lx, ly)
+    om = ora_mesh(nxe, nye, p, ns, na, lx, ly)
+    prm = nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly, p, ns, na) as m:
+        m.load(st)
+        m.mevp_substeps(0, begin_step=True)
+        m.run_step("strain")
+        E = {k: m.read_state(k) for k in ("E11", "E12", "E22")}
+        rE = dict(zip(("E11", "E12", "E22"), ora.strain(om, st["vx"], st["vy"])))
+        from tests.parity import group_err
+        assert group_err(E, rE, ("E11", "E12", "E22")) < 1e-13
+        m.run_step("stress")
+        S = m.state(("S11", "S12", "S22"))
+        rS = dict(zip(("S11", "S12", "S22"), ora.stress(om, ora_params(prm), rE["E11"], rE["E12"], rE["E22"],
+                                                       st["H"], st["A"], st["S11"], st["S12"], st["S22"])))
+        assert group_err(S, rS, ("S11", "S12", "S22")) < 1e-12
+        m.run_step("divergence")
+        F = {"Fx": m.read_state("Fx"), "Fy": m.read_state("Fy")}
+        rF = dict(zip(("Fx", "Fy"), ora.divergence(om, rS["S11"], rS["S12"], rS["S22"])))
+        assert group_err(F, rF, ("Fx", "Fy")) < 1e-12
+        m.run_step("velocity")
+        v = m.state(("vx", "vy"))
+        Hn, An = ora.prep(om, st["H"], st["A"])
+        rv = ora.velocity(om, ora_params(prm), rF["Fx"], rF["Fy"], ora.lumped_mass(om), Hn, An, st["vx"], st["vy"],
+                          st["ox"], st["oy"], st["ax"], st["ay"], st["vx"], st["vy"])
+        assert group_err(v, {"vx": rv[0], "vy": rv[1]}, ("vx", "vy")) < 1e-12
+
+
+def test_bitwise_run_to_run(nx):
+    nxe, nye = 70, 75
+    st = case(nxe, nye, 2, 6, 6, "warm", 140e3, 150e3)
+    a = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 7, 140e3, 150e3)
+    b = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 7, 140e3, 150e3)
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_graph_replay_matches_eager_chunks(nx):
+    """n subcycles in one call (CUDA graph) == the same n split over several calls."""
+    nxe, nye = 40, 41
+    st = case(nxe, nye, 2, 6, 6, "warm", 40e3, 41e3)
+    a = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 9, 40e3, 41e3)
+    with nx.Mesh(nxe, nye, 40e3, 41e3) as m:
+        m.load(st)
+        m.mevp_substeps(4, begin_step=True)
+        m.mevp_substeps(3, begin_step=False)
+        m.mevp_substeps(2, begin_step=False)
+        b = m.state()
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+def test_loopback_strips_bitwise_equal_single(nx, nranks):
+    """Row strips with halo exchange give bitwise the single-GPU result (fused + advection)."""
+    nxe, nye, lx, ly = 50, 47, 50e3, 47e3
+    st = case(nxe, nye, 2, 6, 6, "random", lx, ly)
+    prm = nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly) as m:
+        m.load(st)
+        m.advect(prm.dt)
+        m.mevp_substeps(6, begin_step=True)
+        ref = m.state()
+    import torch
+    s = torch.cuda.Stream()
+    ms = [nx.Mesh(nxe, nye, lx, ly, rank=r, nranks=nranks, transport=nx.TRANSPORT_LOOPBACK,
+                  stream=s.cuda_stream) for r in range(nranks)]
+    nx.loopback_connect(ms)
+    for m in ms:
+        er0, ern = m.elem_row0, m.elem_rows
+        nr0, nrn = m.node_row0, m.node_rows
+        loc = {k: st[k][nr0:nr0 + nrn].copy() for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
+        for k in ("S11", "S12", "S22", "A", "H"):
+            loc[k] = st[k][er0 * nxe:(er0 + ern) * nxe].copy()
+        m.load(loc)
+    nx.group_advect(ms, prm.dt)
+    nx.group_mevp_substeps(ms, 6, begin_step=True)
+    got = {k: np.concatenate([m.read_state(k) for m in ms]) for k in ref}
+    for m in ms:
+        m.destroy()
+    for k in ref:
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+
+
+def test_state_roundtrip_and_errors(nx):
+    with nx.Mesh(9, 7, 9e3, 7e3) as m:
+        st = case(9, 7, 2, 6, 6, "random", 9e3, 7e3)
+        m.load(st)
+        for k, v in m.state().items():
+            np.testing.assert_array_equal(v, st[k])
+        with pytest.raises(nx.NxsdgError) as e:
+            m.write_state("vx", np.zeros(5))
+        assert e.value.status == nx.ERR_INVALID_ARG
+    with nx.Mesh(9, 7, 9e3, 7e3) as m:
+        with pytest.raises(nx.NxsdgError) as e:
+            m.mevp_substeps(1)
+        assert e.value.status == nx.ERR_STATE   # forcing unset
+        m.load(case(9, 7, 2, 6, 6, "random", 9e3, 7e3))
+        with pytest.raises(nx.NxsdgError) as e:
+            m.mevp_substeps(1, begin_step=False)
+        assert e.value.status == nx.ERR_STATE   # first call needs BEGIN_STEP
+
+
+def test_device_pointers_roundtrip(nx):
+    import torch
+    st = case(12, 10, 2, 6, 6, "warm", 12e3, 10e3)
+    with nx.Mesh(12, 10, 12e3, 10e3) as m:
+        m.load({k: torch.from_numpy(v).cuda() for k, v in st.items()})
+        out = torch.empty(st["S11"].shape, dtype=torch.float64, device="cuda")
+        m.mevp_substeps(2)
+        m.read_state("S11", out)
+        m.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), m.read_state("S11"))
