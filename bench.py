@@ -132,7 +132,7 @@ def oracle_sample(cfg, nsub, win=160):
     m = oracle.Mesh(w[0], w[1], lx=w[0] * hx, ly=w[1] * hy, p=cfg.p, ns=cfg.ns, na=cfg.na)
     o = oracle.Oracle()
     t0 = time.perf_counter()
-    o.outer_step(m, oracle.Params(), nsub, st, do_advect=True)
+    o.outer_step(m, oracle.Params(alpha=cfg.alpha, beta=cfg.alpha), nsub, st, do_advect=True)
     dt = time.perf_counter() - t0
     return {"value": w[0] * w[1] * nsub / dt, "seconds": dt, "cores": o.threads,
             "sample": f"{w[0]}x{w[1]} window of {cfg.name} ({cfg.nx}x{cfg.ny}) at the same resolution, "
@@ -183,9 +183,10 @@ def main():
     world = _env_int("WORLD_SIZE", 1)
     if cname == "C5":   # 8192^2 per GPU: Ly = P * 512 km
         cfg = inputs.Config("C5", cfg.nx, cfg.ny * world, cfg.p, cfg.ns, cfg.na, cfg.nsub, cfg.lx, cfg.ly * world,
-                            cfg.kind, cfg.advect)
+                            cfg.kind, cfg.advect, cfg.alpha)
     if args.nsub:
-        cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, args.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect)
+        cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, args.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect,
+                            cfg.alpha)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -202,7 +203,7 @@ def main():
             idt.copy_(torch.frombuffer(bytearray(nxsdg.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nid = bytes(idt.cpu().numpy().tobytes())
-    prm = nxsdg.PhysParams()
+    prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
     st = gen_rank_state(cfg, rank, world)
     kw = dict(rank=rank, nranks=world, transport=nxsdg.TRANSPORT_NCCL, nccl_id=nid) if world > 1 else {}
     m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, device=local, **kw)
@@ -301,7 +302,7 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} CG{cfg.p}/DG{cfg.p} (n_S={cfg.ns}, n_A={cfg.na}) warm box + "
                                    f"cyclone forcing; step = advect + prep + {cfg.nsub} fused mEVP subcycles",
-                       "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el,
+                       "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el, "alpha": cfg.alpha, "beta": cfg.alpha,
                        "parallelism": f"row strips x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},
             "breakdown_ms": {"advect": adv, "prep": prep, "subcycles": sub, "per_subcycle": kernel_ms},

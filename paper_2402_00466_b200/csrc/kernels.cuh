@@ -197,6 +197,22 @@ __global__ void __launch_bounds__(128) k_subcycle(SubArgs a) {
         //      + stress update per Gauss point (Listing 2) accumulated into S
 #pragma unroll
         for (int k = 0; k < NS; ++k) { s11[k] *= a.fac; s12[k] *= a.fac; s22[k] *= a.fac; }
+        // velocities relative to one node of the element: the strain rows sum to zero, so this
+        // is exact in real arithmetic and removes the cancellation of sum_j K_j v_j (the VP law
+        // amplifies strain roundoff by P/Delta near rigid ice)
+        double dvx[NCG], dvy[NCG];
+        {
+            const double rx_ = vx[P / 2][P / 2 < P ? P / 2 : 0], ry_ = vy[P / 2][P / 2 < P ? P / 2 : 0];
+#pragma unroll
+            for (int jy = 0; jy <= P; ++jy)
+#pragma unroll
+                for (int jx = 0; jx <= P; ++jx) {
+                    const double ux = (jx < P) ? vx[jy][jx < P ? jx : 0] : vxe[jy];
+                    const double uy = (jx < P) ? vy[jy][jx < P ? jx : 0] : vye[jy];
+                    dvx[jy * (P + 1) + jx] = ux - rx_;
+                    dvy[jy * (P + 1) + jx] = uy - ry_;
+                }
+        }
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
             double dxs = 0.0, dxt = 0.0, dys = 0.0, dyt = 0.0;
@@ -205,8 +221,7 @@ __global__ void __launch_bounds__(128) k_subcycle(SubArgs a) {
 #pragma unroll
                 for (int jx = 0; jx <= P; ++jx) {
                     const int j = jy * (P + 1) + jx;
-                    const double ux = (jx < P) ? vx[jy][jx < P ? jx : 0] : vxe[jy];
-                    const double uy = (jx < P) ? vy[jy][jx < P ? jx : 0] : vye[jy];
+                    const double ux = dvx[j], uy = dvy[j];
                     dxs = fma(T.Ks[g][j], ux, dxs);
                     dxt = fma(T.Kt[g][j], ux, dxt);
                     dys = fma(T.Ks[g][j], uy, dys);
@@ -340,10 +355,12 @@ __global__ void k_strain(StepArgs a) {
     int lr = a.erow_begin + blockIdx.y;
     if (ix >= a.nx || lr >= a.erow_end) return;
     double ux[P + 1][P + 1], uy[P + 1][P + 1];
+    const int64_t nref = (int64_t)(P * lr + P / 2) * a.npitch + P * ix + P / 2;
+    const double rx_ = a.vx_in[nref], ry_ = a.vy_in[nref];   // reference node (see k_subcycle)
     for (int jy = 0; jy <= P; ++jy)
         for (int jx = 0; jx <= P; ++jx) {
             int64_t n = (int64_t)(P * lr + jy) * a.npitch + P * ix + jx;
-            ux[jy][jx] = a.vx_in[n]; uy[jy][jx] = a.vy_in[n];
+            ux[jy][jx] = a.vx_in[n] - rx_; uy[jy][jx] = a.vy_in[n] - ry_;
         }
     double E11[NS] = {}, E12[NS] = {}, E22[NS] = {};
     for (int g = 0; g < NG; ++g) {

@@ -38,15 +38,16 @@ class Config:
     ly: float = 512e3
     kind: str = "warm"
     advect: bool = False
+    alpha: float = 1500.0   # = beta; R#13: raised with resolution (mEVP needs alpha*beta >> gamma ~ 1/dx^2)
 
 
 # BASELINE.json configs (C5 is per GPU: Ly = P * 512 km)
 CONFIGS = {
     "C1": Config("C1", 16, 16, 1, 3, 3, 10, kind="random"),
     "C2": Config("C2", 256, 256, 2, 6, 6, 100),
-    "C3": Config("C3", 2048, 2048, 2, 6, 6, 100, advect=True),
-    "C4": Config("C4", 4096, 4096, 2, 6, 6, 100),
-    "C5": Config("C5", 8192, 8192, 2, 6, 6, 100, advect=True),
+    "C3": Config("C3", 2048, 2048, 2, 6, 6, 100, advect=True, alpha=25000.0),
+    "C4": Config("C4", 4096, 4096, 2, 6, 6, 100, advect=True, alpha=25000.0),
+    "C5": Config("C5", 8192, 8192, 2, 6, 6, 100, advect=True, alpha=25000.0),
 }
 
 

@@ -1,0 +1,89 @@
+"""Full-size parity at BASELINE.json's bench configuration (C4: 4096 x 4096 CG2/DG2,
+one outer step = advection + BEGIN_STEP prep + 100 fused subcycles, exactly the launch
+configuration bench.py times), checked against the oracle on windows.
+
+Light cone: one subcycle moves information by at most one element
+(node v -> adjacent elements' strain/stress -> their nodes), each RK stage of the
+advection by one element, the prep's nodal means by one.  So the oracle run on a
+window padded by a ring of n_sub + 3 + 2 elements, with the window's own (wrong)
+boundary conditions on the ring's outside, reproduces the global solution exactly
+in the window's centre.  Windows: the four domain corners (the true boundary is
+inside them), the cyclone centre, and seeded random positions."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2402_00466_b200 import inputs
+from tests.parity import group_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c4_result():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2402_00466_b200 import build
+    build.build()
+    from paper_2402_00466_b200 import nxsdg
+    cfg = inputs.CONFIGS["C4"]
+    st = inputs.make_config_case(cfg)
+    prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
+    with nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm) as m:
+        m.load(st)
+        m.advect(prm.dt)
+        m.mevp_substeps(cfg.nsub, begin_step=True)
+        got = m.state()
+    return cfg, st, got
+
+
+def _cut(cfg, arrs, ix0, iy0, w, h):
+    p, nx, ny = cfg.p, cfg.nx, cfg.ny
+    out = {}
+    for k, a in arrs.items():
+        if a.ndim == 2 and a.shape == (p * ny + 1, p * nx + 1):
+            out[k] = np.ascontiguousarray(a[p * iy0:p * (iy0 + h) + 1, p * ix0:p * (ix0 + w) + 1])
+        else:
+            n = a.shape[1]
+            out[k] = np.ascontiguousarray(a.reshape(ny, nx, n)[iy0:iy0 + h, ix0:ix0 + w].reshape(-1, n))
+    return out
+
+
+def _windows(cfg, core=12):
+    rng = np.random.default_rng(inputs.SEED_BASE + 4)
+    nx, ny = cfg.nx, cfg.ny
+    ws = [(0, 0), (nx - core, 0), (0, ny - core), (nx - core, ny - core), (nx // 2 - core // 2, ny // 2 - core // 2)]
+    ws += [(int(rng.integers(0, nx - core)), int(rng.integers(0, ny - core))) for _ in range(3)]
+    return ws
+
+
+@pytest.mark.parametrize("wi", range(8))
+def test_c4_window_parity(c4_result, wi):
+    cfg, st, got = c4_result
+    core = 12
+    ring = cfg.nsub + 3 + 2
+    cx, cy = _windows(cfg, core)[wi]
+    ix0, iy0 = max(0, cx - ring), max(0, cy - ring)
+    ix1, iy1 = min(cfg.nx, cx + core + ring), min(cfg.ny, cy + core + ring)
+    w, h = ix1 - ix0, iy1 - iy0
+    hx, hy = cfg.lx / cfg.nx, cfg.ly / cfg.ny
+    sub = _cut(cfg, st, ix0, iy0, w, h)
+    mesh = oracle.Mesh(w, h, lx=w * hx, ly=h * hy, p=cfg.p, ns=cfg.ns, na=cfg.na)
+    ref = oracle.Oracle().outer_step(mesh, oracle.Params(alpha=cfg.alpha, beta=cfg.alpha), cfg.nsub, sub, do_advect=True)
+    # compare the core cells: elements [cx, cx+core) x [cy, cy+core), and their nodes
+    g = _cut(cfg, got, cx, cy, core, core)
+    loc = {k: v for k, v in ref.items() if k in got}
+    p = cfg.p
+    rc = {}
+    for k, a in loc.items():
+        if a.ndim == 2 and a.shape == (p * h + 1, p * w + 1):
+            rc[k] = a[p * (cy - iy0):p * (cy - iy0 + core) + 1, p * (cx - ix0):p * (cx - ix0 + core) + 1]
+        else:
+            n = a.shape[1]
+            rc[k] = a.reshape(h, w, n)[cy - iy0:cy - iy0 + core, cx - ix0:cx - ix0 + core].reshape(-1, n)
+    init = _cut(cfg, st, cx, cy, core, core)
+    for grp in (("S11", "S12", "S22"), ("vx", "vy"), ("A",), ("H",)):
+        e = group_err(g, rc, grp)
+        de = group_err({k: g[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp)
+        assert e <= 1e-10 and de <= 1e-10, (grp, e, de, (cx, cy))

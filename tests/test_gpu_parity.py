@@ -116,8 +116,8 @@ def test_outer_step_c3_shape(nx, ora):
     nxe, nye = 96, 80
     lx, ly = nxe * 250.0, nye * 250.0
     st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
-    prm = nx.PhysParams()
-    got = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 20, lx, ly, advect_dt=prm.dt)
+    prm = nx.PhysParams(alpha=25000.0, beta=25000.0)   # R#13: C3 resolution needs alpha*beta >> gamma
+    got = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 20, lx, ly, advect_dt=prm.dt, params=prm)
     ref = ora.outer_step(ora_mesh(nxe, nye, 2, 6, 6, lx, ly), ora_params(prm), 20, st, do_advect=True)
     _check(got, ref, st, TOLN, groups=("S", "v", "A", "H"))
 
