@@ -146,6 +146,15 @@ nxsdg_status nxsdg_get_partition(const nxsdg_ctx* ctx, int64_t* elem_row0, int32
 nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int32_t rank,
                              int64_t* elem_row0, int32_t* elem_rows, int64_t* node_row0, int32_t* node_rows);
 
+/* Tuning / A-B options (take effect at the next compute call):
+ *   NXSDG_OPT_FUSED_KERNEL  0 (default): TMA-staged structured kernel for p = 2 (table-driven for p = 1);
+ *                           1: table-driven register kernel k_subcycle<p> (reference-table variant)
+ *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (default 32; one ring row each)
+ *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy)
+ * INVALID_ARG for an unknown option or value. */
+enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2 };
+nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
+
 /* ---- state ----------------------------------------------------------------- */
 /* count = number of doubles of this rank's owned part in the ABI layout.
  * Writing invalidates the outer-step constants (next substep call needs BEGIN_STEP). */

@@ -31,7 +31,7 @@ struct PrepArgs {
     const double* ox; const double* oy; const double* ax; const double* ay;
     double* c1; double* rx0; double* ry0; double* cafo;
     double* Pg;                                // NG planes
-    int64_t eplane, npitch;
+    int64_t eplane, npitch, epitch;            // plane stride, node row pitch, element row pitch
     int nx, erows_local;                       // stored element rows (incl. ghosts)
     int node_row_begin, node_row_end;          // owned local node rows [begin, end)
     int elem_rows_with_nodes;                  // element rows that touch stored nodes (excl. upper ghost)
@@ -56,7 +56,7 @@ __global__ void k_prep_nodes(PrepArgs a) {
             if (ex < 0 || ex >= a.nx || ey < 0 || ey >= a.elem_rows_with_nodes) continue;
             if (jx < 0 || jx > P || jy < 0 || jy > P) continue;
             int j = jy * (P + 1) + jx;
-            int64_t e = (int64_t)ey * a.nx + ex;
+            int64_t e = (int64_t)ey * a.epitch + ex;
             double hv = 0.0, av = 0.0;
 #pragma unroll
             for (int k = 0; k < NA; ++k) {
@@ -86,7 +86,7 @@ __global__ void k_prep_elems(PrepArgs a) {
     int ix = blockIdx.x * blockDim.x + threadIdx.x;
     int lr = blockIdx.y;
     if (ix >= a.nx || lr >= a.erows_local) return;
-    int64_t e = (int64_t)lr * a.nx + ix;
+    int64_t e = (int64_t)lr * a.epitch + ix;
     double h[NA], c[NA];
 #pragma unroll
     for (int k = 0; k < NA; ++k) { h[k] = a.H[k * a.eplane + e]; c[k] = a.A[k * a.eplane + e]; }
@@ -121,7 +121,7 @@ struct SubArgs {
     double* __restrict__ vx_out; double* __restrict__ vy_out;
     const double* __restrict__ c1; const double* __restrict__ rx0; const double* __restrict__ ry0;
     const double* __restrict__ cafo; const double* __restrict__ ox; const double* __restrict__ oy;
-    int64_t eplane, npitch;
+    int64_t eplane, npitch, epitch;
     int nx, nstrips, ty;
     int erow_begin, erow_end;       // owned local element rows
     int bottom_boundary;            // local element row erow_begin touches global node row 0
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(128) k_subcycle(SubArgs a) {
     for (; lr < lr1; ++lr) {
 #pragma unroll
         for (int r = 1; r <= P; ++r) load_row(P * lr + r, vx[r], vy[r], vxe[r], vye[r]);
-        const int64_t e = (int64_t)lr * a.nx + ix;
+        const int64_t e = (int64_t)lr * a.epitch + ix;
         double s11[NS], s12[NS], s22[NS], pg[NG];
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
@@ -336,7 +336,7 @@ struct StepArgs {
     double* S;  double* E;  double* Fx; double* Fy;  const double* H; const double* A;
     const double* c1; const double* rx0; const double* ry0; const double* cafo;
     const double* ox; const double* oy;
-    int64_t eplane, npitch;
+    int64_t eplane, npitch, epitch;
     int nx, erow_begin, erow_end, elem_rows_with_nodes;
     int node_row_begin, node_row_end;
     int node_row_global0;          // global index of local node row 0
@@ -376,7 +376,7 @@ __global__ void k_strain(StepArgs a) {
             E11[k] += T.R[k][g] * e11; E12[k] += T.R[k][g] * e12; E22[k] += T.R[k][g] * e22;
         }
     }
-    int64_t e = (int64_t)lr * a.nx + ix;
+    int64_t e = (int64_t)lr * a.epitch + ix;
     for (int k = 0; k < NS; ++k) {
         a.E[(0 * NS + k) * a.eplane + e] = E11[k];
         a.E[(1 * NS + k) * a.eplane + e] = E12[k];
@@ -393,7 +393,7 @@ __global__ void k_stress(StepArgs a) {
     int ix = blockIdx.x * blockDim.x + threadIdx.x;
     int lr = a.erow_begin + blockIdx.y;
     if (ix >= a.nx || lr >= a.erow_end) return;
-    int64_t e = (int64_t)lr * a.nx + ix;
+    int64_t e = (int64_t)lr * a.epitch + ix;
     double r11[NG], r12[NG], r22[NG];
     for (int g = 0; g < NG; ++g) {
         double hv = 0, av = 0, e11 = 0, e12 = 0, e22 = 0;
@@ -439,7 +439,7 @@ __global__ void k_divergence(StepArgs a) {
             if (ex < 0 || ex >= a.nx || ey < 0 || ey >= a.elem_rows_with_nodes) continue;
             if (jx < 0 || jx > P || jy < 0 || jy > P) continue;
             int j = jy * (P + 1) + jx;
-            int64_t e = (int64_t)ey * a.nx + ex;
+            int64_t e = (int64_t)ey * a.epitch + ex;
             double ax = 0, bx = 0, ay = 0, by = 0;
             for (int k = 0; k < NS; ++k) {
                 double s11 = a.S[(0 * NS + k) * a.eplane + e], s12 = a.S[(1 * NS + k) * a.eplane + e];
@@ -492,7 +492,7 @@ struct AdvArgs {
     const double* A0; const double* H0;
     double* Aout; double* Hout;
     const double* vx; const double* vy;
-    int64_t eplane, npitch;
+    int64_t eplane, npitch, epitch;
     int nx, erow_begin, erow_end;             // owned local rows
     int has_south, has_north;                 // ghost rows exist below/above (multi-rank)
     int periodic, erows_local;
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(256) k_advect(AdvArgs a) {
     const int lr = a.erow_begin + blockIdx.y * 8 + ty;
     const bool valid = ix < a.nx && lr < a.erow_end;
     const int ixc = valid ? ix : 0, lrc = valid ? lr : a.erow_begin;
-    const int64_t e = (int64_t)lrc * a.nx + ixc;
+    const int64_t e = (int64_t)lrc * a.epitch + ixc;
     Cf<NA> me; load_coef<P, NA>(a, e, me);
     // node velocities of this element
     double ux[P + 1][P + 1], uy[P + 1][P + 1];
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(256) k_advect(AdvArgs a) {
         if (ex < 0 || ex >= a.nx) { if (!a.periodic) { open = false; return e; } ex = (ex + a.nx) % a.nx; }
         if (ey < a.erow_begin && !a.has_south) { if (!a.periodic) { open = false; return e; } ey = a.erow_end - 1; }
         if (ey >= a.erow_end && !a.has_north) { if (!a.periodic) { open = false; return e; } ey = a.erow_begin; }
-        return (int64_t)ey * a.nx + ex;
+        return (int64_t)ey * a.epitch + ex;
     };
     // east edge (this element = lo)
     double FeA[NGP], FeH[NGP], FnA[NGP], FnH[NGP], FwA[NGP], FwH[NGP], FsA[NGP], FsH[NGP];
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) k_advect(AdvArgs a) {
                    + wqy * (FnH[q] * T.psiedge[2][k][q] - FsH[q] * T.psiedge[3][k][q]);
         }
     }
-    const int64_t eo = (int64_t)lr * a.nx + ix;
+    const int64_t eo = (int64_t)lr * a.epitch + ix;
 #pragma unroll
     for (int k = 0; k < NA; ++k) {
         const double la = LA[k] / T.mref[k], lh = LH[k] / T.mref[k];
@@ -661,17 +661,20 @@ __global__ void __launch_bounds__(256) k_advect(AdvArgs a) {
 // --------------------------------------------------------------------------
 // ABI layout conversion: AoS rows (n per element) <-> SoA planes.
 // --------------------------------------------------------------------------
-__global__ void k_aos_to_soa(const double* src, double* dst, int64_t nelem, int n, int64_t eplane, int64_t dst_off) {
+// compact ABI element e = row*nx + col  <->  device (row + row_off)*epitch + col
+__global__ void k_aos_to_soa(const double* src, double* dst, int64_t nelem, int n, int64_t eplane, int64_t row_off,
+                             int nx, int64_t epitch) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nelem * n) return;
     int64_t e = i / n; int k = (int)(i % n);
-    dst[k * eplane + dst_off + e] = src[i];
+    dst[k * eplane + (e / nx + row_off) * epitch + e % nx] = src[i];
 }
-__global__ void k_soa_to_aos(const double* src, double* dst, int64_t nelem, int n, int64_t eplane, int64_t src_off) {
+__global__ void k_soa_to_aos(const double* src, double* dst, int64_t nelem, int n, int64_t eplane, int64_t row_off,
+                             int nx, int64_t epitch) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nelem * n) return;
     int64_t e = i / n; int k = (int)(i % n);
-    dst[i] = src[k * eplane + src_off + e];
+    dst[i] = src[k * eplane + (e / nx + row_off) * epitch + e % nx];
 }
 
 }  // namespace nxk

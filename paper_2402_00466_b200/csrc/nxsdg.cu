@@ -17,8 +17,11 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/nxsdg.h"
 #include "kernels.cuh"
+#include "subcycle_tma.cuh"
 
 using namespace nxk;
 
@@ -70,7 +73,7 @@ struct nxsdg_ctx {
     // partition
     int64_t r0 = 0, r1 = 0;
     int glo = 0, ghi = 0, nown = 0, erows_local = 0, nrows_local = 0;
-    int64_t eplane = 0, npitch = 0;
+    int64_t eplane = 0, npitch = 0, epitch = 0;
     // device buffers
     double* S[2] = {nullptr, nullptr};
     double* Pg = nullptr;
@@ -80,6 +83,8 @@ struct nxsdg_ctx {
     double* vx[2] = {nullptr, nullptr}; double* vy[2] = {nullptr, nullptr};
     double *ox = nullptr, *oy = nullptr, *ax = nullptr, *ay = nullptr;
     double *c1 = nullptr, *rx0 = nullptr, *ry0 = nullptr, *cafo = nullptr;
+    double* nodec = nullptr;   // one allocation: c1, rx0, ry0, cafo, ox, oy (6 x node grid; one TMA tensor)
+    int64_t nn = 0;            // doubles per node grid
     double* staging = nullptr; size_t staging_bytes = 0;
     int cv = 0, cs = 0; // ping-pong index of v and of S
     // state flags
@@ -88,6 +93,10 @@ struct nxsdg_ctx {
     std::string err;
     int64_t launches = 0;
     int ty = 32;       // fused kernel chunk rows
+    int variant = 0;   // fused kernel: 0 = TMA-staged structured (p = 2), 1 = table-driven k_subcycle<P>
+    int ctas_per_sm = 0;
+    K2Maps maps[2][2]; // [cv][cs]
+    bool maps_ok = false;
     // transport
     ncclComm_t comm = nullptr;
     std::vector<nxsdg_ctx*> peers;   // loopback: all ranks' contexts
@@ -160,10 +169,11 @@ static void free_all(nxsdg_ctx* c) {
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
     double** bufs[] = {&c->S[0], &c->S[1], &c->Pg, &c->A, &c->H, &c->Asc[0], &c->Asc[1], &c->Hsc[0], &c->Hsc[1],
-                       &c->E, &c->Fx, &c->Fy, &c->vx[0], &c->vx[1], &c->vy[0], &c->vy[1], &c->ox, &c->oy,
-                       &c->ax, &c->ay, &c->c1, &c->rx0, &c->ry0, &c->cafo, &c->staging};
+                       &c->E, &c->Fx, &c->Fy, &c->vx[0], &c->vx[1], &c->vy[0], &c->vy[1],
+                       &c->ax, &c->ay, &c->nodec, &c->staging};
     for (auto b : bufs)
         if (*b) { cudaFree(*b); *b = nullptr; }
+    c->c1 = c->rx0 = c->ry0 = c->cafo = c->ox = c->oy = nullptr;
 }
 
 extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_params* prm, nxsdg_ctx** out) {
@@ -197,7 +207,8 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     c->ghi = c->r1 < d->ny ? 1 : 0;
     c->erows_local = c->glo + c->nown + c->ghi;
     c->nrows_local = c->P * (c->glo + c->nown) + 1;
-    c->eplane = round_up((int64_t)c->erows_local * d->nx, 32);
+    c->epitch = round_up(d->nx, 4);     // element row pitch: 32-B aligned rows (TMA strides)
+    c->eplane = round_up((int64_t)c->erows_local * c->epitch, 32);
     c->npitch = round_up((int64_t)c->P * d->nx + 2, 32);
     auto bail = [&](nxsdg_status s) { nxsdg_status r = s; free_all(c); if (c->own_stream) cudaStreamDestroy(c->stream); delete c; return r; };
     if (cudaSetDevice(d->device) != cudaSuccess) { cudaGetLastError(); return bail(NXSDG_ERR_CUDA); }
@@ -214,8 +225,11 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     AL(c->A, c->NA * ne); AL(c->H, c->NA * ne);
     AL(c->Asc[0], c->NA * ne); AL(c->Asc[1], c->NA * ne); AL(c->Hsc[0], c->NA * ne); AL(c->Hsc[1], c->NA * ne);
     AL(c->vx[0], nn); AL(c->vx[1], nn); AL(c->vy[0], nn); AL(c->vy[1], nn);
-    AL(c->ox, nn); AL(c->oy, nn); AL(c->ax, nn); AL(c->ay, nn);
-    AL(c->c1, nn); AL(c->rx0, nn); AL(c->ry0, nn); AL(c->cafo, nn);
+    AL(c->ax, nn); AL(c->ay, nn);
+    AL(c->nodec, 6 * nn);
+    c->nn = (int64_t)nn;
+    c->c1 = c->nodec; c->rx0 = c->nodec + nn; c->ry0 = c->nodec + 2 * nn; c->cafo = c->nodec + 3 * nn;
+    c->ox = c->nodec + 4 * nn; c->oy = c->nodec + 5 * nn;
 #undef AL
     // K0: reference-element tables into __constant__ (both degrees; tiny)
     {
@@ -286,6 +300,25 @@ extern "C" nxsdg_status nxsdg_set_params(nxsdg_ctx* c, const nxsdg_params* p) {
     c->prm = *p;
     c->prepped = false;
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);   // captured launch arguments are stale
+    c->graphs.clear();
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t value) {
+    GUARD(c);
+    switch (opt) {
+        case NXSDG_OPT_FUSED_KERNEL:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "fused kernel variant 0|1");
+            c->variant = (int)value; break;
+        case NXSDG_OPT_CHUNK_ROWS:
+            if (value < 1 || value > (1 << 20)) return fail(c, NXSDG_ERR_INVALID_ARG, "chunk rows >= 1");
+            c->ty = (int)value; break;
+        case NXSDG_OPT_CTAS_PER_SM:
+            if (value < 0 || value > 32) return fail(c, NXSDG_ERR_INVALID_ARG, "ctas per SM 0..32");
+            c->ctas_per_sm = (int)value; break;
+        default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
+    }
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
     return NXSDG_OK;
 }
@@ -374,7 +407,7 @@ extern "C" nxsdg_status nxsdg_write_state(nxsdg_ctx* c, nxsdg_field f, const dou
         }
         const int64_t tot = ne * n;
         k_aos_to_soa<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(dsrc, base, ne, n, c->eplane,
-                                                                         (int64_t)c->glo * c->d.nx);
+                                                                         (int64_t)c->glo, c->d.nx, c->epitch);
         LAUNCHED();
         if (mem == NXSDG_MEM_HOST) CU(cudaStreamSynchronize(c->stream));
     } else {
@@ -403,7 +436,7 @@ extern "C" nxsdg_status nxsdg_read_state(nxsdg_ctx* c, nxsdg_field f, double* ds
         }
         const int64_t tot = ne * n;
         k_soa_to_aos<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(base, ddst, ne, n, c->eplane,
-                                                                          (int64_t)c->glo * c->d.nx);
+                                                                          (int64_t)c->glo, c->d.nx, c->epitch);
         LAUNCHED();
         if (mem == NXSDG_MEM_HOST) {
             CU(cudaMemcpyAsync(dst, c->staging, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -450,8 +483,8 @@ struct Seg { double* src; double* dst; size_t n; int peer; };
 static void element_row_segs(nxsdg_ctx* c, nxsdg_ctx* nb, double* base_me, double* base_nb, int nplanes,
                              int my_row, int nb_row, int peer, std::vector<Seg>& out) {
     for (int k = 0; k < nplanes; ++k)
-        out.push_back({base_me + (size_t)k * c->eplane + (size_t)my_row * c->d.nx,
-                       base_nb ? base_nb + (size_t)k * nb->eplane + (size_t)nb_row * nb->d.nx : nullptr,
+        out.push_back({base_me + (size_t)k * c->eplane + (size_t)my_row * c->epitch,
+                       base_nb ? base_nb + (size_t)k * nb->eplane + (size_t)nb_row * nb->epitch : nullptr,
                        (size_t)c->d.nx, peer});
 }
 
@@ -546,7 +579,7 @@ static PrepArgs prep_args(nxsdg_ctx* c) {
     a.H = c->H; a.A = c->A; a.vx = c->vx[c->cv]; a.vy = c->vy[c->cv];
     a.ox = c->ox; a.oy = c->oy; a.ax = c->ax; a.ay = c->ay;
     a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.Pg = c->Pg;
-    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx; a.erows_local = c->erows_local;
+    a.eplane = c->eplane; a.npitch = c->npitch; a.epitch = c->epitch; a.nx = c->d.nx; a.erows_local = c->erows_local;
     a.node_row_begin = c->P * c->glo;
     a.node_row_end = (int)(c->P * c->glo + owned_node_rows(c));
     a.elem_rows_with_nodes = c->glo + c->nown;
@@ -579,7 +612,7 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     a.S_in = c->S[cs]; a.S_out = c->S[cs ^ 1]; a.Pg = c->Pg;
     a.vx_in = c->vx[cv]; a.vy_in = c->vy[cv]; a.vx_out = c->vx[cv ^ 1]; a.vy_out = c->vy[cv ^ 1];
     a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.ox = c->ox; a.oy = c->oy;
-    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx;
+    a.eplane = c->eplane; a.npitch = c->npitch; a.epitch = c->epitch; a.nx = c->d.nx;
     a.nstrips = (c->d.nx + 1 + 30) / 31;
     a.ty = c->ty;
     a.erow_begin = c->glo; a.erow_end = c->glo + c->nown;
@@ -594,13 +627,84 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     return a;
 }
 
-static nxsdg_status launch_subcycle(nxsdg_ctx* c) {
-    SubArgs a = sub_args(c, c->cv, c->cs);
+// ---------------------------------------------------------------- TMA descriptors
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+static bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static nxsdg_status build_maps(nxsdg_ctx* c) {
+    if (c->maps_ok) return NXSDG_OK;
+    const cuuint64_t nx = c->d.nx, er = c->erows_local, ncols = 2 * (cuuint64_t)c->d.nx + 1, nr = c->nrows_local;
+    const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 8, (cuuint64_t)c->eplane * 8};
+    const cuuint64_t ns[2] = {(cuuint64_t)c->npitch * 8, (cuuint64_t)c->nn * 8};
+    const cuuint64_t dS[3] = {nx, er, 18}, dP[3] = {nx, er, 9}, dV[2] = {ncols, nr}, dC[3] = {ncols, nr, 6};
+    const cuuint32_t bS[3] = {K2_ECOLS, 1, 18}, bP[3] = {K2_ECOLS, 1, 9}, bV[2] = {K2_VCOLS, 3}, bC[3] = {K2_CCOLS, 2, 6};
+    for (int v = 0; v < 2; ++v)
+        for (int s = 0; s < 2; ++s) {
+            K2Maps& M = c->maps[v][s];
+            bool ok = encode(&M.S, c->S[s], 3, dS, es, bS) && encode(&M.Pg, c->Pg, 3, dP, es, bP) &&
+                      encode(&M.vx, c->vx[v], 2, dV, ns, bV) && encode(&M.vy, c->vy[v], 2, dV, ns, bV) &&
+                      encode(&M.C, c->nodec, 3, dC, ns, bC);
+            if (!ok) return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        }
+    c->maps_ok = true;
+    return NXSDG_OK;
+}
+
+static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0; }
+
+static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs) {
+    nxsdg_status st = build_maps(c);
+    if (st) return st;
+    SubArgs a = sub_args(c, cv, cs);
+    const size_t smem = (size_t)K2_WARPS * K2_STAGES * (sizeof(K2Stage) + sizeof(uint64_t));
+    static bool attr = false;
+    if (!attr) {
+        CU(cudaFuncSetAttribute(k_subcycle_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    int dev = c->d.device, nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma, 32 * K2_WARPS, smem));
+    if (c->ctas_per_sm > 0) occ = std::min(occ, c->ctas_per_sm);
     const int nchunks = (c->nown + a.ty - 1) / a.ty;
-    const int64_t warps = (int64_t)a.nstrips * nchunks;
-    const unsigned blocks = (unsigned)((warps + 3) / 4);
-    if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
-    else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
+    const int64_t units = (int64_t)a.nstrips * nchunks;
+    const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
+    k_subcycle_tma<<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->maps[cv][cs], a);
+    return NXSDG_OK;
+}
+
+static nxsdg_status launch_subcycle(nxsdg_ctx* c) {
+    if (use_tma(c)) {
+        nxsdg_status st = launch_tma(c, c->cv, c->cs);
+        if (st) return st;
+    } else {
+        SubArgs a = sub_args(c, c->cv, c->cs);
+        const int nchunks = (c->nown + a.ty - 1) / a.ty;
+        const int64_t warps = (int64_t)a.nstrips * nchunks;
+        const unsigned blocks = (unsigned)((warps + 3) / 4);
+        if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
+        else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
+    }
     LAUNCHED();
     c->cv ^= 1; c->cs ^= 1;
     return NXSDG_OK;
@@ -611,7 +715,7 @@ static StepArgs step_args(nxsdg_ctx* c) {
     a.vx_in = c->vx[c->cv]; a.vy_in = c->vy[c->cv]; a.vx_out = c->vx[c->cv ^ 1]; a.vy_out = c->vy[c->cv ^ 1];
     a.S = c->S[c->cs]; a.E = c->E; a.Fx = c->Fx; a.Fy = c->Fy; a.H = c->H; a.A = c->A;
     a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.ox = c->ox; a.oy = c->oy;
-    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx;
+    a.eplane = c->eplane; a.npitch = c->npitch; a.epitch = c->epitch; a.nx = c->d.nx;
     a.erow_begin = c->glo; a.erow_end = c->glo + c->nown; a.elem_rows_with_nodes = c->glo + c->nown;
     a.node_row_begin = c->P * c->glo; a.node_row_end = (int)(c->P * c->glo + owned_node_rows(c));
     a.node_row_global0 = (int)(c->P * (c->r0 - c->glo));
@@ -689,12 +793,21 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
         cudaGraph_t g;
         CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         int cv = c->cv, cs = c->cs;
+        if (use_tma(c)) {
+            nxsdg_status st = build_maps(c);   // descriptors are encoded outside the capture
+            if (st) { cudaGraph_t junk; cudaStreamEndCapture(c->stream, &junk); if (junk) cudaGraphDestroy(junk); return st; }
+        }
         for (int i = 0; i < n; ++i) {
-            SubArgs a = sub_args(c, cv, cs);
-            const int nchunks = (c->nown + a.ty - 1) / a.ty;
-            const unsigned blocks = (unsigned)(((int64_t)a.nstrips * nchunks + 3) / 4);
-            if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
-            else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
+            if (use_tma(c)) {
+                nxsdg_status st = launch_tma(c, cv, cs);
+                if (st) { cudaGraph_t junk; cudaStreamEndCapture(c->stream, &junk); if (junk) cudaGraphDestroy(junk); return st; }
+            } else {
+                SubArgs a = sub_args(c, cv, cs);
+                const int nchunks = (c->nown + a.ty - 1) / a.ty;
+                const unsigned blocks = (unsigned)(((int64_t)a.nstrips * nchunks + 3) / 4);
+                if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
+                else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
+            }
             cv ^= 1; cs ^= 1;
         }
         cudaError_t e = cudaStreamEndCapture(c->stream, &g);
@@ -743,11 +856,10 @@ static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const d
     AdvArgs a{};
     a.Ain = Ain; a.Hin = Hin; a.A0 = c->A; a.H0 = c->H; a.Aout = Aout; a.Hout = Hout;
     a.vx = c->vx[c->cv]; a.vy = c->vy[c->cv];
-    a.eplane = c->eplane; a.npitch = c->npitch; a.nx = c->d.nx;
+    a.eplane = c->eplane; a.npitch = c->npitch; a.epitch = c->epitch; a.nx = c->d.nx;
     a.erow_begin = c->glo; a.erow_end = c->glo + c->nown;
     a.has_south = c->glo; a.has_north = c->ghi;
     a.periodic = c->d.bc == NXSDG_BC_PERIODIC; a.erows_local = c->erows_local;
-    a.ihx = c->d.nx / c->d.lx; a.ihy = c->d.ny / c->d.ly;
     a.ihx = 1.0 / (c->d.lx / c->d.nx); a.ihy = 1.0 / (c->d.ly / c->d.ny);
     a.dt = dt; a.a0 = a0; a.a1 = a1;
     dim3 b(32, 8), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + 7) / 8));
@@ -789,7 +901,7 @@ static nxsdg_status advect_stage(nxsdg_ctx* c, double dt, int stage) {
 // copy the final stage buffer back into A, H (owned rows)
 static nxsdg_status advect_finish(nxsdg_ctx* c) {
     const int last = stage_out_buf(c, n_stages(c) - 1);
-    const size_t off = (size_t)c->glo * c->d.nx, n = (size_t)c->nown * c->d.nx;
+    const size_t off = (size_t)c->glo * c->epitch, n = (size_t)c->nown * c->epitch;
     for (int k = 0; k < c->NA; ++k) {
         CU(cudaMemcpyAsync(c->A + k * c->eplane + off, c->Asc[last] + k * c->eplane + off, n * sizeof(double),
                            cudaMemcpyDeviceToDevice, c->stream));

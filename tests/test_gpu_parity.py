@@ -30,9 +30,12 @@ def ora():
     return oracle.Oracle()
 
 
-def _gpu_run(nx, st, nxe, nye, p, ns, na, nsub, lx=512e3, ly=512e3, unfused=False, advect_dt=None, params=None):
+def _gpu_run(nx, st, nxe, nye, p, ns, na, nsub, lx=512e3, ly=512e3, unfused=False, advect_dt=None, params=None,
+             options=None):
     params = params or nx.PhysParams()
     with nx.Mesh(nxe, nye, lx, ly, p, ns, na, params=params) as m:
+        for k, v in (options or {}).items():
+            m.set_option(k, v)
         m.load(st)
         if advect_dt is not None:
             m.advect(advect_dt)
@@ -79,6 +82,30 @@ def test_full_subcycle_count(nx, ora, c, nsub):
     got = _gpu_run(nx, st, nxe, nye, p, ns, na, nsub, lx, ly)
     ref = ora.subcycles(ora_mesh(nxe, nye, p, ns, na, lx, ly), ora_params(nx.PhysParams()), nsub, st)
     _check(got, ref, st, TOLN)
+
+
+@pytest.mark.parametrize("variant,ty,ctas", [(1, 32, 0), (0, 7, 0), (0, 64, 1), (0, 1, 2)])
+def test_fused_variants_and_tuning(nx, ora, variant, ty, ctas):
+    """Both fused kernels (TMA-staged structured, table-driven) and several chunk heights /
+    persistent grid sizes give the oracle's result (ragged 70x75 CG2 box, 5 subcycles)."""
+    c = CASES[2]
+    nxe, nye, p, ns, na, kind, lx, ly = c
+    st = case(nxe, nye, p, ns, na, kind, lx, ly)
+    opts = {nx.OPT_FUSED_KERNEL: variant, nx.OPT_CHUNK_ROWS: ty, nx.OPT_CTAS_PER_SM: ctas}
+    got = _gpu_run(nx, st, nxe, nye, p, ns, na, 5, lx, ly, options=opts)
+    ref = ora.subcycles(ora_mesh(nxe, nye, p, ns, na, lx, ly), ora_params(nx.PhysParams()), 5, st)
+    _check(got, ref, st, 1e-11)
+
+
+def test_fused_variants_agree(nx):
+    """TMA structured kernel vs table-driven kernel (tables from the K0 kernel): same result
+    to rounding after 3 subcycles."""
+    nxe, nye, lx, ly = 64, 40, 64e3, 40e3
+    st = case(nxe, nye, 2, 6, 6, "random", lx, ly)
+    a = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 3, lx, ly, options={nx.OPT_FUSED_KERNEL: 0})
+    b = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 3, lx, ly, options={nx.OPT_FUSED_KERNEL: 1})
+    e = parity(a, b, st)
+    assert max(e.values()) < 1e-12, e
 
 
 def test_c2_full_config(nx, ora):
