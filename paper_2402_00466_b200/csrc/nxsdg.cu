@@ -94,7 +94,8 @@ struct nxsdg_ctx {
     int64_t launches = 0;
     int ty = 32;       // fused kernel chunk rows
     int variant = 0;   // fused kernel: 0 = TMA-staged structured (p = 2), 1 = table-driven k_subcycle<P>
-    int ctas_per_sm = 0;
+    int ctas_per_sm = 2;   // tuned on C4: 4 warps/SM beat the occupancy maximum
+    int stages = 2;        // TMA pipeline depth 2..4
     K2Maps maps[2][2]; // [cv][cs]
     bool maps_ok = false;
     // transport
@@ -316,6 +317,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_CTAS_PER_SM:
             if (value < 0 || value > 32) return fail(c, NXSDG_ERR_INVALID_ARG, "ctas per SM 0..32");
             c->ctas_per_sm = (int)value; break;
+        case NXSDG_OPT_STAGES:
+            if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
+            c->stages = (int)value; break;
         default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
     }
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
@@ -671,26 +675,38 @@ static nxsdg_status build_maps(nxsdg_ctx* c) {
 
 static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0; }
 
-static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs) {
-    nxsdg_status st = build_maps(c);
-    if (st) return st;
-    SubArgs a = sub_args(c, cv, cs);
-    const size_t smem = (size_t)K2_WARPS * K2_STAGES * (sizeof(K2Stage) + sizeof(uint64_t));
+template <bool R, int ST>
+static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage) + sizeof(uint64_t));
     static bool attr = false;
     if (!attr) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    int dev = c->d.device, nsm = 148, occ = 1;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma, 32 * K2_WARPS, smem));
+    int nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST>, 32 * K2_WARPS, smem));
     if (c->ctas_per_sm > 0) occ = std::min(occ, c->ctas_per_sm);
     const int nchunks = (c->nown + a.ty - 1) / a.ty;
     const int64_t units = (int64_t)a.nstrips * nchunks;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
-    k_subcycle_tma<<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->maps[cv][cs], a);
+    k_subcycle_tma<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->maps[cv][cs], a);
     return NXSDG_OK;
+}
+
+static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs) {
+    nxsdg_status st = build_maps(c);
+    if (st) return st;
+    SubArgs a = sub_args(c, cv, cs);
+    switch (c->stages * 2 + (a.repl ? 1 : 0)) {
+        case 4: return launch_tma_t<false, 2>(c, cv, cs, a);
+        case 5: return launch_tma_t<true, 2>(c, cv, cs, a);
+        case 6: return launch_tma_t<false, 3>(c, cv, cs, a);
+        case 7: return launch_tma_t<true, 3>(c, cv, cs, a);
+        case 8: return launch_tma_t<false, 4>(c, cv, cs, a);
+        default: return launch_tma_t<true, 4>(c, cv, cs, a);
+    }
 }
 
 static nxsdg_status launch_subcycle(nxsdg_ctx* c) {

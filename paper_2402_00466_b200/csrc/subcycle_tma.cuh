@@ -31,7 +31,7 @@
 namespace nxk {
 
 constexpr int K2_WARPS = 2;          // warps per CTA (independent work lists)
-constexpr int K2_STAGES = 2;
+constexpr int K2_MAX_STAGES = 4;     // pipeline depth is a template parameter (2..4)
 constexpr int K2_VCOLS = 66;         // node columns per v box: 2*32 + 2
 constexpr int K2_CCOLS = 62;         // owned node columns per const box: 2*31
 constexpr int K2_ECOLS = 34;         // element columns per S / P_g box: the TMA start column must be even
@@ -87,6 +87,23 @@ __device__ __forceinline__ void tma2(void* dst, const CUtensorMap* m, uint64_t* 
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
         ::"r"(su32(dst)), "l"((uint64_t)m), "r"(x), "r"(y), "r"(su32(bar)) : "memory");
+}
+
+// Branch-free FP64 reciprocal / reciprocal square root: the MUFU seed (~20 bits) plus one
+// third-order correction (error ~ seed^3 ~ 2^-60, i.e. <= 1 ulp after rounding).  Valid for
+// positive normal arguments, which is all this kernel feeds them (Delta^2 >= DeltaMin^2 > 0,
+// c1 (1 + beta) + cAFo w > 0); no slow-path branches, unlike the IEEE-exact library calls.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-(x * r), r, 1.0);          // 1 - x r^2
+    return fma(r * e, fma(0.375, e, 0.5), r);        // r (1 + e/2 + 3 e^2/8)
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);                // 1 - x r
+    return fma(r, fma(e, e, e), r);                  // r (1 + e + e^2)
 }
 
 // ---------------------------------------------------------------- element math (Q2/P2)
@@ -190,11 +207,12 @@ __device__ __forceinline__ void div_t(const double S[6], double h, double r[3][3
 }
 
 // ---------------------------------------------------------------- the kernel
-__global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
+template <bool REPL, int STAGES>
+__global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
     extern __shared__ __align__(1024) unsigned char k2_smem[];   // no static smem: base stays 1024-B aligned
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    K2Stage* stg = reinterpret_cast<K2Stage*>(k2_smem) + wib * K2_STAGES;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * K2_STAGES * sizeof(K2Stage)) + wib * K2_STAGES;
+    K2Stage* stg = reinterpret_cast<K2Stage*>(k2_smem) + wib * STAGES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * STAGES * sizeof(K2Stage)) + wib * STAGES;
     if ((su32(k2_smem) & 127u) != 0u) {                          // TMA destinations need 128-B alignment
         printf("nxsdg: dynamic smem misaligned %u\n", su32(k2_smem));
         __trap();
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_
     const int nunits = a.nstrips * nchunks;
     if (gw >= nunits) return;
     if (lane == 0) {
-        for (int s = 0; s < K2_STAGES; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -237,15 +255,23 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_
 
     const double ihx = a.ihx, ihy = a.ihy, fac = a.fac, hA = 0.5 * a.ainv;
     const int64_t npitch = a.npitch, eplane = a.eplane;
-    Cur cur, nxt;
+    // prologue: jobs 0 .. STAGES-2 in flight; job j lives in stage j % STAGES
+    Cur cur, pre;
     start_unit(gw, cur);
-    if (lane == 0) issue(cur, 0);
-    nxt = cur; advance(nxt);
-    uint32_t phase = 0;     // bit s = parity of stage s
+    pre = cur;
+    if (lane == 0) issue(pre, 0);
+#pragma unroll
+    for (int k = 1; k < STAGES - 1; ++k) {
+        advance(pre);
+        if (pre.ok && lane == 0) issue(pre, k);
+    }
+    advance(pre);          // pre = job (current + STAGES - 1)
+    uint32_t phase = 0;    // bit s = parity of stage s
     int s = 0;
     double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
     while (cur.ok) {
-        if (nxt.ok && lane == 0) issue(nxt, s ^ 1);
+        const int sp = (s + STAGES - 1) % STAGES;
+        if (pre.ok && lane == 0) issue(pre, sp);
         mbar_wait(&bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
         const K2Stage& t = stg[s];
@@ -288,10 +314,11 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_
         for (int g = 0; g < 9; ++g) {
             const double x = e11[g], y = e22[g], z = e12[g];
             const double draw2 = fma(z, z, fma(1.5 * x, y, 1.25 * fma(x, x, y * y)));
-            const double rD = rsqrt(draw2 + a.dmin2);
+            const double rD = rsqrt_nr(draw2 + a.dmin2);
             const double ph = t.Pg[g][eo + lane] * hA;
             const double pr = ph * rD;
-            const double sub = a.repl ? pr * sqrt(draw2) : ph;
+            // replacement pressure (R#4): P_r/2 = (P/2) Draw/Delta, Draw = draw2 * rsqrt(draw2)
+            const double sub = REPL ? pr * (draw2 > 0.0 ? draw2 * rsqrt_nr(draw2) : 0.0) : ph;
             e11[g] = fma(pr, fma(1.25, x, 0.75 * y), -sub);
             e22[g] = fma(pr, fma(1.25, y, 0.75 * x), -sub);
             e12[g] = pr * z;
@@ -322,9 +349,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_
             for (int j = 0; j < 3; ++j) { rX[i][j] = 0.0; rY[i][j] = 0.0; }
         div_s(S11, ihx, rX); div_t(S12, ihy, rX);
         div_s(S12, ihx, rY); div_t(S22, ihy, rY);
-        // ---- per-node gather (row below, W, E) + velocity update (R#11)
-        const bool nvalid = lane >= 1 && ix >= 0 && ix <= a.nx;
-        const double invm[2][2] = {{-9.0, -4.5}, {-4.5, -2.25}};   // -1 / lumped-mass factor [q][jy]
+        // ---- per-node gather (row below, W, E) + velocity update (R#11), branch-free:
+        //      all four owned nodes are updated, boundary nodes select 0, stores are predicated
+        const bool nvalid = lane >= 1 && ix >= 0 && ix <= a.nx && !cur.ring;
+        double sumx[2][2], sumy[2][2];                 // [jy][q]
 #pragma unroll
         for (int jy = 0; jy < 3; ++jy) {
             const double wx = __shfl_up_sync(0xffffffffu, rX[2][jy], 1);
@@ -335,27 +363,43 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_
                 if (q == 0) { sx = wx + sx; sy = wy + sy; }
                 if (jy == 2) { carx[q] = sx; cary[q] = sy; continue; }
                 if (jy == 0) { sx = carx[q] + sx; sy = cary[q] + sy; }
-                const int I = 2 * ix + q;
-                if (cur.ring || !nvalid || I > 2 * a.nx) continue;
-                const int64_t n = (int64_t)(2 * lr + jy) * npitch + I;
-                const bool bnd = (I == 0) || (I == 2 * a.nx) || (jy == 0 && lr == a.erow_begin && a.bottom_boundary);
-                double nvx = 0.0, nvy = 0.0;
-                if (!bnd) {
+                sumx[jy][q] = sx; sumy[jy][q] = sy;
+            }
+        }
+        if (nvalid) {
+            const double invm[2][2] = {{-9.0, -4.5}, {-4.5, -2.25}};   // -1 / lumped-mass factor [jy][q]
+            const bool brow0 = lr == a.erow_begin && a.bottom_boundary;
+#pragma unroll
+            for (int jy = 0; jy < 2; ++jy) {
+                double nvx[2], nvy[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int I = 2 * ix + q;
                     const int cc = 2 * lane - 2 + q;
-                    const double fx = sx * invm[q][jy], fy = sy * invm[q][jy];
+                    const double fx = sumx[jy][q] * invm[jy][q], fy = sumy[jy][q] * invm[jy][q];
                     const double vxo = Vx[jy][q], vyo = Vy[jy][q];
                     const double c1 = t.C[0][jy][cc], r0x = t.C[1][jy][cc], r0y = t.C[2][jy][cc];
                     const double cf = t.C[3][jy][cc], oxv = t.C[4][jy][cc], oyv = t.C[5][jy][cc];
                     const double dx = oxv - vxo, dy = oyv - vyo;
-                    const double w = sqrt(fma(dx, dx, dy * dy));
+                    const double w2 = fma(dx, dx, dy * dy);
+                    const double w = w2 > 0.0 ? w2 * rsqrt_nr(w2) : 0.0;   // |o - v|
                     const double cw = cf * w;
-                    const double rden = 1.0 / fma(c1, a.b1, cw);
+                    const double rden = rcp_nr(fma(c1, a.b1, cw));
                     const double cb = c1 * a.beta, ck = c1 * a.kc;
-                    nvx = (fma(cb, vxo, r0x) + fma(cw, oxv, fma(ck, vyo, fx))) * rden;
-                    nvy = (fma(cb, vyo, r0y) + fma(cw, oyv, fma(-ck, vxo, fy))) * rden;
+                    const double ux = (fma(cb, vxo, r0x) + fma(cw, oxv, fma(ck, vyo, fx))) * rden;
+                    const double uy = (fma(cb, vyo, r0y) + fma(cw, oyv, fma(-ck, vxo, fy))) * rden;
+                    const bool bnd = (I == 0) || (I == 2 * a.nx) || (jy == 0 && brow0);
+                    nvx[q] = bnd ? 0.0 : ux;
+                    nvy[q] = bnd ? 0.0 : uy;
                 }
-                a.vx_out[n] = nvx;
-                a.vy_out[n] = nvy;
+                const int64_t n = (int64_t)(2 * lr + jy) * npitch + 2 * ix;
+                if (ix < a.nx) {
+                    *reinterpret_cast<double2*>(a.vx_out + n) = make_double2(nvx[0], nvx[1]);
+                    *reinterpret_cast<double2*>(a.vy_out + n) = make_double2(nvy[0], nvy[1]);
+                } else {                                  // ix == nx: only the boundary column 2 nx
+                    a.vx_out[n] = 0.0;
+                    a.vy_out[n] = 0.0;
+                }
             }
         }
         // global top boundary row (Dirichlet) after the last owned element row
@@ -369,8 +413,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 3) k_subcycle_tma(const __grid_
             }
         }
         __syncwarp();
-        cur = nxt; advance(nxt);
-        s ^= 1;
+        advance(cur); advance(pre);
+        s = (s + 1) % STAGES;
     }
 }
 
