@@ -192,6 +192,24 @@ nxsdg_status nxsdg_loopback_connect(nxsdg_ctx** ctxs, int32_t n);
 nxsdg_status nxsdg_group_mevp_substeps(nxsdg_ctx** ctxs, int32_t n, int32_t n_sub, uint32_t flags);
 nxsdg_status nxsdg_group_advect(nxsdg_ctx** ctxs, int32_t n, double dt);
 
+/* Halo-exchange plan (pure host arithmetic; what the NCCL and loopback transports execute).
+ * For rank `rank` of a row-strip partition: an ordered list of segments, each a contiguous run of
+ * `count` doubles at `offset` doubles from the base of buffer `field` in this rank's local layout
+ * (nxsdg_local_geometry).  dir 0 = send to `peer`, 1 = receive from `peer`.  Rank r's k-th send to q
+ * pairs with q's k-th receive from r (ncclSend/ncclRecv matching).  With out == NULL only *n_out is
+ * set.  INVALID_ARG for a bad partition or max < the plan length. */
+typedef enum { NXSDG_HALO_V = 1, NXSDG_HALO_S = 2, NXSDG_HALO_AH = 4, NXSDG_HALO_AH_SCR0 = 8, NXSDG_HALO_AH_SCR1 = 16 } nxsdg_halo_what;
+typedef enum { NXSDG_HF_VX = 0, NXSDG_HF_VY = 1, NXSDG_HF_S = 2, NXSDG_HF_A = 3, NXSDG_HF_H = 4, NXSDG_HF_A_SCR0 = 5,
+               NXSDG_HF_H_SCR0 = 6, NXSDG_HF_A_SCR1 = 7, NXSDG_HF_H_SCR1 = 8 } nxsdg_halo_field;
+typedef struct { int32_t dir, field, peer, plane; int64_t offset, count; } nxsdg_halo_seg;
+nxsdg_status nxsdg_halo_plan(int32_t nx, int32_t ny, int32_t cg_degree, int32_t n_stress, int32_t n_adv, int32_t nranks,
+                             int32_t rank, uint32_t what, nxsdg_halo_seg* out, int32_t max, int32_t* n_out);
+/* Local layout of a rank: out8 = {elem_row0, owned elem rows, ghost rows below (0|1), stored element rows,
+ * stored node rows, element row pitch, element plane stride, node row pitch} (element rows and node rows
+ * in local numbering start at the ghost row below). */
+nxsdg_status nxsdg_local_geometry(int32_t nx, int32_t ny, int32_t cg_degree, int32_t n_stress, int32_t n_adv,
+                                  int32_t nranks, int32_t rank, int64_t* out8);
+
 /* ---- introspection ------------------------------------------------------------- */
 /* Number of kernels this context has launched (for the bench's gpu_launches claim). */
 int64_t nxsdg_kernel_launches(const nxsdg_ctx* ctx);

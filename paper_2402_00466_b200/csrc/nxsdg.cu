@@ -66,11 +66,21 @@ NcclApi& nccl() {
 }  // namespace
 
 // ---------------------------------------------------------------- context
+// Local geometry of one rank's row strip.
+struct Geom {
+    int nx, ny, P, NS, NA, nranks, rank;
+    int64_t r0, r1;
+    int glo, ghi, nown, erows_local, nrows_local;
+    int64_t epitch, eplane, npitch, nn;
+};
+static Geom make_geom(int nx, int ny, int p, int ns, int na, int nranks, int rank);
+
 struct nxsdg_ctx {
     nxsdg_mesh_desc d{};
     nxsdg_params prm{};
     int P = 2, NS = 6, NA = 6, NG = 9;
     // partition
+    Geom geom{};
     int64_t r0 = 0, r1 = 0;
     int glo = 0, ghi = 0, nown = 0, erows_local = 0, nrows_local = 0;
     int64_t eplane = 0, npitch = 0, epitch = 0;
@@ -200,17 +210,11 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     nxsdg_ctx* c = new nxsdg_ctx();
     c->d = *d; c->prm = *prm;
     c->P = d->cg_degree; c->NS = d->n_stress; c->NA = d->n_adv; c->NG = (c->P + 1) * (c->P + 1);
-    int32_t erows = 0;
-    nxsdg_partition(d->ny, c->P, d->nranks, d->rank, &c->r0, &erows, nullptr, nullptr);
-    c->r1 = c->r0 + erows;
-    c->nown = erows;
-    c->glo = c->r0 > 0 ? 1 : 0;
-    c->ghi = c->r1 < d->ny ? 1 : 0;
-    c->erows_local = c->glo + c->nown + c->ghi;
-    c->nrows_local = c->P * (c->glo + c->nown) + 1;
-    c->epitch = round_up(d->nx, 4);     // element row pitch: 32-B aligned rows (TMA strides)
-    c->eplane = round_up((int64_t)c->erows_local * c->epitch, 32);
-    c->npitch = round_up((int64_t)c->P * d->nx + 2, 32);
+    c->geom = make_geom(d->nx, d->ny, c->P, c->NS, c->NA, d->nranks, d->rank);
+    c->r0 = c->geom.r0; c->r1 = c->geom.r1; c->nown = c->geom.nown;
+    c->glo = c->geom.glo; c->ghi = c->geom.ghi;
+    c->erows_local = c->geom.erows_local; c->nrows_local = c->geom.nrows_local;
+    c->epitch = c->geom.epitch; c->eplane = c->geom.eplane; c->npitch = c->geom.npitch;
     auto bail = [&](nxsdg_status s) { nxsdg_status r = s; free_all(c); if (c->own_stream) cudaStreamDestroy(c->stream); delete c; return r; };
     if (cudaSetDevice(d->device) != cudaSuccess) { cudaGetLastError(); return bail(NXSDG_ERR_CUDA); }
     if (d->stream) c->stream = (cudaStream_t)d->stream;
@@ -479,99 +483,143 @@ extern "C" nxsdg_status nxsdg_set_forcing(nxsdg_ctx* c, const double* ox, const 
 // ---------------------------------------------------------------- halo exchange
 // Rows that cross a rank boundary:
 //   up   (r -> r+1): top owned element row of element fields; top P owned node rows of node fields
-//   down (r -> r-1): bottom owned node row of node fields; bottom owned element row (advection only)
-enum HaloWhat { HALO_V = 1, HALO_S = 2, HALO_AH = 4, HALO_AH_SCR0 = 8, HALO_AH_SCR1 = 16 };
+//   down (r -> r-1): bottom owned node row of node fields; bottom owned element row (A/H only)
+// The plan is pure host arithmetic on the local geometry (nxsdg_halo_plan exports it).  Every
+// rank emits the fields in the same order and, per field, [send up, recv up, send down,
+// recv down], so rank r's k-th send to q pairs with q's k-th recv from r - the matching rule
+// of ncclSend/ncclRecv, and the rule the loopback transport applies explicitly.
 
-struct Seg { double* src; double* dst; size_t n; int peer; };
-
-static void element_row_segs(nxsdg_ctx* c, nxsdg_ctx* nb, double* base_me, double* base_nb, int nplanes,
-                             int my_row, int nb_row, int peer, std::vector<Seg>& out) {
-    for (int k = 0; k < nplanes; ++k)
-        out.push_back({base_me + (size_t)k * c->eplane + (size_t)my_row * c->epitch,
-                       base_nb ? base_nb + (size_t)k * nb->eplane + (size_t)nb_row * nb->epitch : nullptr,
-                       (size_t)c->d.nx, peer});
+static Geom make_geom(int nx, int ny, int p, int ns, int na, int nranks, int rank) {
+    Geom g{};
+    g.nx = nx; g.ny = ny; g.P = p; g.NS = ns; g.NA = na; g.nranks = nranks; g.rank = rank;
+    int32_t erows = 0;
+    nxsdg_partition(ny, p, nranks, rank, &g.r0, &erows, nullptr, nullptr);
+    g.r1 = g.r0 + erows; g.nown = erows;
+    g.glo = g.r0 > 0 ? 1 : 0;
+    g.ghi = g.r1 < ny ? 1 : 0;
+    g.erows_local = g.glo + g.nown + g.ghi;
+    g.nrows_local = p * (g.glo + g.nown) + 1;
+    g.epitch = round_up(nx, 4);     // element row pitch: 32-B aligned rows (TMA strides)
+    g.eplane = round_up((int64_t)g.erows_local * g.epitch, 32);
+    g.npitch = round_up((int64_t)p * nx + 2, 32);
+    g.nn = g.npitch * g.nrows_local;
+    return g;
 }
 
-// Build the list of (send) segments of this rank for `what`; for loopback the
-// destination pointers are filled from the neighbour context.
-static void halo_segments(nxsdg_ctx* c, int what, std::vector<Seg>& sends, std::vector<Seg>& recvs) {
-    const int rank = c->d.rank, nr = c->d.nranks;
-    const bool up = rank + 1 < nr, down = rank > 0;
-    nxsdg_ctx* nup = (up && !c->peers.empty()) ? c->peers[rank + 1] : nullptr;
-    nxsdg_ctx* ndn = (down && !c->peers.empty()) ? c->peers[rank - 1] : nullptr;
-    const int top_row = c->glo + c->nown - 1, bot_row = c->glo;
-    const size_t prow = (size_t)c->npitch;
-    auto node_rows = [&](double* base_me, double* base_nb_up, double* base_nb_dn, double* recv_lo, double* recv_hi) {
+static void halo_plan(const Geom& g, uint32_t what, std::vector<nxsdg_halo_seg>& out) {
+    const bool up = g.rank + 1 < g.nranks, down = g.rank > 0;
+    const int64_t top = g.glo + g.nown - 1, bot = g.glo, ghost_hi = g.glo + g.nown;
+    auto seg = [&](int dir, int field, int peer, int plane, int64_t off, int64_t cnt) {
+        out.push_back(nxsdg_halo_seg{dir, field, peer, plane, off, cnt});
+    };
+    auto node_field = [&](int f) {
         if (up) {
-            sends.push_back({base_me + (size_t)c->P * top_row * prow, base_nb_up, prow * c->P, rank + 1});
-            recvs.push_back({nullptr, recv_hi, prow, rank + 1});
+            seg(0, f, g.rank + 1, 0, g.P * top * g.npitch, g.P * g.npitch);       // top P owned rows
+            seg(1, f, g.rank + 1, 0, g.P * ghost_hi * g.npitch, g.npitch);        // top ghost row
         }
         if (down) {
-            sends.push_back({base_me + (size_t)c->P * bot_row * prow,
-                             base_nb_dn ? base_nb_dn + (size_t)c->P * (ndn->glo + ndn->nown) * prow : nullptr, prow,
-                             rank - 1});
-            recvs.push_back({nullptr, recv_lo, prow * c->P, rank - 1});
+            seg(0, f, g.rank - 1, 0, g.P * bot * g.npitch, g.npitch);              // bottom owned row
+            seg(1, f, g.rank - 1, 0, 0, g.P * g.npitch);                           // P bottom ghost rows
         }
     };
-    if (what & HALO_V) {
-        for (int comp = 0; comp < 2; ++comp) {
-            double* me = comp ? c->vy[c->cv] : c->vx[c->cv];
-            double* u = nup ? (comp ? nup->vy[nup->cv] : nup->vx[nup->cv]) : nullptr;
-            double* dn = ndn ? (comp ? ndn->vy[ndn->cv] : ndn->vx[ndn->cv]) : nullptr;
-            node_rows(me, u, dn, me, me + (size_t)c->P * (c->glo + c->nown) * prow);
-        }
-    }
-    auto elem_field = [&](double* me, double* u, double* dn, int nplanes, bool both) {
-        if (up) {
-            element_row_segs(c, nup, me, u, nplanes, top_row, 0, rank + 1, sends);
-            if (both) element_row_segs(c, nup, me, nullptr, nplanes, c->glo + c->nown, 0, rank + 1, recvs);
-        }
-        if (down) {
-            if (both) element_row_segs(c, ndn, me, dn, nplanes, bot_row, ndn ? ndn->glo + ndn->nown : 0, rank - 1, sends);
-            element_row_segs(c, ndn, me, nullptr, nplanes, 0, 0, rank - 1, recvs);
+    auto elem_field = [&](int f, int nplanes, bool both) {
+        for (int k = 0; k < nplanes; ++k) {
+            const int64_t pl = (int64_t)k * g.eplane;
+            if (up) {
+                seg(0, f, g.rank + 1, k, pl + top * g.epitch, g.nx);
+                if (both) seg(1, f, g.rank + 1, k, pl + ghost_hi * g.epitch, g.nx);
+            }
+            if (down) {
+                if (both) seg(0, f, g.rank - 1, k, pl + bot * g.epitch, g.nx);
+                seg(1, f, g.rank - 1, k, pl, g.nx);
+            }
         }
     };
-    if (what & HALO_S) elem_field(c->S[c->cs], nup ? nup->S[nup->cs] : nullptr, ndn ? ndn->S[ndn->cs] : nullptr, 3 * c->NS, false);
-    if (what & HALO_AH) {
-        elem_field(c->A, nup ? nup->A : nullptr, ndn ? ndn->A : nullptr, c->NA, true);
-        elem_field(c->H, nup ? nup->H : nullptr, ndn ? ndn->H : nullptr, c->NA, true);
-    }
-    if (what & (HALO_AH_SCR0 | HALO_AH_SCR1)) {
-        int b = (what & HALO_AH_SCR0) ? 0 : 1;
-        elem_field(c->Asc[b], nup ? nup->Asc[b] : nullptr, ndn ? ndn->Asc[b] : nullptr, c->NA, true);
-        elem_field(c->Hsc[b], nup ? nup->Hsc[b] : nullptr, ndn ? ndn->Hsc[b] : nullptr, c->NA, true);
-    }
-    // recv segments for the element "both" case were generated with src = my ghost rows; turn them into dsts
-    for (auto& r : recvs)
-        if (!r.dst) { r.dst = r.src; r.src = nullptr; }
+    if (what & NXSDG_HALO_V) { node_field(NXSDG_HF_VX); node_field(NXSDG_HF_VY); }
+    if (what & NXSDG_HALO_S) elem_field(NXSDG_HF_S, 3 * g.NS, false);
+    if (what & NXSDG_HALO_AH) { elem_field(NXSDG_HF_A, g.NA, true); elem_field(NXSDG_HF_H, g.NA, true); }
+    if (what & NXSDG_HALO_AH_SCR0) { elem_field(NXSDG_HF_A_SCR0, g.NA, true); elem_field(NXSDG_HF_H_SCR0, g.NA, true); }
+    if (what & NXSDG_HALO_AH_SCR1) { elem_field(NXSDG_HF_A_SCR1, g.NA, true); elem_field(NXSDG_HF_H_SCR1, g.NA, true); }
 }
 
-static nxsdg_status halo_nccl(nxsdg_ctx* c, int what) {
-    std::vector<Seg> sends, recvs;
-    halo_segments(c, what, sends, recvs);
+extern "C" nxsdg_status nxsdg_local_geometry(int32_t nx, int32_t ny, int32_t p, int32_t ns, int32_t na, int32_t nranks,
+                                             int32_t rank, int64_t* out8) {
+    if (!out8 || nx < 1 || nxsdg_partition(ny, p, nranks, rank, nullptr, nullptr, nullptr, nullptr)) return NXSDG_ERR_INVALID_ARG;
+    Geom g = make_geom(nx, ny, p, ns, na, nranks, rank);
+    const int64_t v[8] = {g.r0, g.nown, g.glo, g.erows_local, g.nrows_local, g.epitch, g.eplane, g.npitch};
+    memcpy(out8, v, sizeof v);
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_halo_plan(int32_t nx, int32_t ny, int32_t p, int32_t ns, int32_t na, int32_t nranks,
+                                        int32_t rank, uint32_t what, nxsdg_halo_seg* out, int32_t max, int32_t* n_out) {
+    if (!n_out || nx < 1 || nxsdg_partition(ny, p, nranks, rank, nullptr, nullptr, nullptr, nullptr)) return NXSDG_ERR_INVALID_ARG;
+    std::vector<nxsdg_halo_seg> v;
+    halo_plan(make_geom(nx, ny, p, ns, na, nranks, rank), what, v);
+    *n_out = (int32_t)v.size();
+    if (out) {
+        if ((int32_t)v.size() > max) return NXSDG_ERR_INVALID_ARG;
+        std::copy(v.begin(), v.end(), out);
+    }
+    return NXSDG_OK;
+}
+
+static double* halo_base(nxsdg_ctx* c, int field) {
+    switch (field) {
+        case NXSDG_HF_VX: return c->vx[c->cv];
+        case NXSDG_HF_VY: return c->vy[c->cv];
+        case NXSDG_HF_S: return c->S[c->cs];
+        case NXSDG_HF_A: return c->A;
+        case NXSDG_HF_H: return c->H;
+        case NXSDG_HF_A_SCR0: return c->Asc[0];
+        case NXSDG_HF_H_SCR0: return c->Hsc[0];
+        case NXSDG_HF_A_SCR1: return c->Asc[1];
+        default: return c->Hsc[1];
+    }
+}
+
+static nxsdg_status halo_nccl(nxsdg_ctx* c, uint32_t what) {
+    std::vector<nxsdg_halo_seg> plan;
+    halo_plan(c->geom, what, plan);
     NcclApi& api = nccl();
     if (api.GroupStart() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupStart");
-    for (auto& s : sends)
-        if (api.Send(s.src, s.n, kNcclFloat64, s.peer, c->comm, c->stream) != 0) { api.GroupEnd(); return fail(c, NXSDG_ERR_NCCL, "ncclSend"); }
-    for (auto& r : recvs)
-        if (api.Recv(r.dst, r.n, kNcclFloat64, r.peer, c->comm, c->stream) != 0) { api.GroupEnd(); return fail(c, NXSDG_ERR_NCCL, "ncclRecv"); }
+    for (const auto& sg : plan) {
+        double* ptr = halo_base(c, sg.field) + sg.offset;
+        const int r = sg.dir == 0 ? api.Send(ptr, (size_t)sg.count, kNcclFloat64, sg.peer, c->comm, c->stream)
+                                  : api.Recv(ptr, (size_t)sg.count, kNcclFloat64, sg.peer, c->comm, c->stream);
+        if (r != 0) { api.GroupEnd(); return fail(c, NXSDG_ERR_NCCL, "ncclSend/Recv: %d", r); }
+    }
     if (api.GroupEnd() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupEnd");
     return NXSDG_OK;
 }
 
-// Loopback: every context pushes its send segments straight into its neighbours'
-// ghost rows (all contexts share one stream, so ordering is the stream order).
-static nxsdg_status halo_loopback_all(std::vector<nxsdg_ctx*>& ctxs, int what) {
-    for (nxsdg_ctx* c : ctxs) {
-        std::vector<Seg> sends, recvs;
-        halo_segments(c, what, sends, recvs);
-        for (auto& s : sends)
-            CU(cudaMemcpyAsync(s.dst, s.src, s.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+// Loopback: pair rank r's k-th send to q with q's k-th recv from r and copy (all contexts
+// share one stream, so stream order is the exchange order).
+static nxsdg_status halo_loopback_all(std::vector<nxsdg_ctx*>& ctxs, uint32_t what) {
+    const int n = (int)ctxs.size();
+    std::vector<std::vector<nxsdg_halo_seg>> plans(n);
+    for (int r = 0; r < n; ++r) halo_plan(ctxs[r]->geom, what, plans[r]);
+    for (int r = 0; r < n; ++r) {
+        nxsdg_ctx* c = ctxs[r];
+        std::vector<int> kth(n, 0);
+        for (const auto& sg : plans[r]) {
+            if (sg.dir != 0) continue;
+            const int q = sg.peer;
+            int seen = -1;
+            const nxsdg_halo_seg* rv = nullptr;
+            for (const auto& t : plans[q])
+                if (t.dir == 1 && t.peer == r && ++seen == kth[q]) { rv = &t; break; }
+            ++kth[q];
+            if (!rv || rv->count != sg.count || rv->field != sg.field)
+                return fail(c, NXSDG_ERR_STATE, "halo plan mismatch between ranks %d and %d", r, q);
+            CU(cudaMemcpyAsync(halo_base(ctxs[q], rv->field) + rv->offset, halo_base(c, sg.field) + sg.offset,
+                               (size_t)sg.count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        }
     }
     return NXSDG_OK;
 }
 
-static nxsdg_status halo(nxsdg_ctx* c, int what) {
+static nxsdg_status halo(nxsdg_ctx* c, uint32_t what) {
     if (c->d.nranks == 1) return NXSDG_OK;
     if (c->d.transport == NXSDG_TRANSPORT_NCCL) return halo_nccl(c, what);
     return NXSDG_OK;   // loopback exchanges are driven by the group calls
@@ -772,7 +820,7 @@ static nxsdg_status launch_step(nxsdg_ctx* c, nxsdg_step st) {
 static nxsdg_status begin_step(nxsdg_ctx* c) {
     if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
     nxsdg_status s;
-    if ((s = halo(c, HALO_V | HALO_S | HALO_AH))) return s;
+    if ((s = halo(c, NXSDG_HALO_V | NXSDG_HALO_S | NXSDG_HALO_AH))) return s;
     if ((s = dispatch_prep(c))) return s;
     c->prepped = true;
     return NXSDG_OK;
@@ -790,15 +838,15 @@ static nxsdg_status one_subcycle(nxsdg_ctx* c, bool unfused) {
     nxsdg_status s;
     if (!unfused) {
         if ((s = launch_subcycle(c))) return s;
-        return halo(c, HALO_V | HALO_S);
+        return halo(c, NXSDG_HALO_V | NXSDG_HALO_S);
     }
     if ((s = ensure_debug_buffers(c))) return s;
     if ((s = launch_step(c, NXSDG_STEP_STRAIN))) return s;
     if ((s = launch_step(c, NXSDG_STEP_STRESS))) return s;
-    if ((s = halo(c, HALO_S))) return s;
+    if ((s = halo(c, NXSDG_HALO_S))) return s;
     if ((s = launch_step(c, NXSDG_STEP_DIVERGENCE))) return s;
     if ((s = launch_step(c, NXSDG_STEP_VELOCITY))) return s;
-    return halo(c, HALO_V);
+    return halo(c, NXSDG_HALO_V);
 }
 
 // Capture n fused subcycles into a CUDA graph (nranks == 1) and replay it.
@@ -934,10 +982,10 @@ extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
     if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_LOOPBACK)
         return fail(c, NXSDG_ERR_STATE, "loopback ranks advect through nxsdg_group_advect");
     nxsdg_status s;
-    if ((s = halo(c, HALO_V | HALO_AH))) return s;
+    if ((s = halo(c, NXSDG_HALO_V | NXSDG_HALO_AH))) return s;
     for (int st = 0; st < n_stages(c); ++st) {
         if ((s = advect_stage(c, dt, st))) return s;
-        if (st + 1 < n_stages(c) && (s = halo(c, stage_out_buf(c, st) == 0 ? HALO_AH_SCR0 : HALO_AH_SCR1))) return s;
+        if (st + 1 < n_stages(c) && (s = halo(c, stage_out_buf(c, st) == 0 ? NXSDG_HALO_AH_SCR0 : NXSDG_HALO_AH_SCR1))) return s;
     }
     return advect_finish(c);
 }
@@ -983,7 +1031,7 @@ extern "C" nxsdg_status nxsdg_group_mevp_substeps(nxsdg_ctx** ctxs, int32_t nr, 
     }
     const bool unfused = flags & NXSDG_UNFUSED;
     if (flags & NXSDG_BEGIN_STEP) {
-        if ((s = halo_loopback_all(v, HALO_V | HALO_S | HALO_AH))) return s;
+        if ((s = halo_loopback_all(v, NXSDG_HALO_V | NXSDG_HALO_S | NXSDG_HALO_AH))) return s;
         for (nxsdg_ctx* c : v) {
             cudaSetDevice(c->d.device);
             if ((s = dispatch_prep(c))) return s;
@@ -993,19 +1041,19 @@ extern "C" nxsdg_status nxsdg_group_mevp_substeps(nxsdg_ctx** ctxs, int32_t nr, 
     for (int i = 0; i < n; ++i) {
         if (!unfused) {
             for (nxsdg_ctx* c : v) if ((s = launch_subcycle(c))) return s;
-            if ((s = halo_loopback_all(v, HALO_V | HALO_S))) return s;
+            if ((s = halo_loopback_all(v, NXSDG_HALO_V | NXSDG_HALO_S))) return s;
         } else {
             for (nxsdg_ctx* c : v) {
                 if ((s = ensure_debug_buffers(c))) return s;
                 if ((s = launch_step(c, NXSDG_STEP_STRAIN))) return s;
                 if ((s = launch_step(c, NXSDG_STEP_STRESS))) return s;
             }
-            if ((s = halo_loopback_all(v, HALO_S))) return s;
+            if ((s = halo_loopback_all(v, NXSDG_HALO_S))) return s;
             for (nxsdg_ctx* c : v) {
                 if ((s = launch_step(c, NXSDG_STEP_DIVERGENCE))) return s;
                 if ((s = launch_step(c, NXSDG_STEP_VELOCITY))) return s;
             }
-            if ((s = halo_loopback_all(v, HALO_V))) return s;
+            if ((s = halo_loopback_all(v, NXSDG_HALO_V))) return s;
         }
     }
     return NXSDG_OK;
@@ -1016,11 +1064,11 @@ extern "C" nxsdg_status nxsdg_group_advect(nxsdg_ctx** ctxs, int32_t nr, double 
     std::vector<nxsdg_ctx*> v(ctxs, ctxs + nr);
     nxsdg_status s;
     for (nxsdg_ctx* c : v) GUARD(c);
-    if ((s = halo_loopback_all(v, HALO_V | HALO_AH))) return s;
+    if ((s = halo_loopback_all(v, NXSDG_HALO_V | NXSDG_HALO_AH))) return s;
     const int ns = n_stages(v[0]);
     for (int st = 0; st < ns; ++st) {
         for (nxsdg_ctx* c : v) if ((s = advect_stage(c, dt, st))) return s;
-        if (st + 1 < ns && (s = halo_loopback_all(v, stage_out_buf(v[0], st) == 0 ? HALO_AH_SCR0 : HALO_AH_SCR1))) return s;
+        if (st + 1 < ns && (s = halo_loopback_all(v, stage_out_buf(v[0], st) == 0 ? NXSDG_HALO_AH_SCR0 : NXSDG_HALO_AH_SCR1))) return s;
     }
     for (nxsdg_ctx* c : v) if ((s = advect_finish(c))) return s;
     return NXSDG_OK;

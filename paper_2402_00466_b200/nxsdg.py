@@ -82,6 +82,8 @@ def _load() -> C.CDLL:
         "nxsdg_bytes_per_element_subcycle": ([vp], dbl),
         "nxsdg_stream": ([vp], vp),
         "nxsdg_set_option": ([vp, i32, i64], i32),
+        "nxsdg_halo_plan": ([i32, i32, i32, i32, i32, i32, i32, u32, vp, i32, C.POINTER(i32)], i32),
+        "nxsdg_local_geometry": ([i32, i32, i32, i32, i32, i32, i32, C.POINTER(i64)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -96,8 +98,33 @@ EXPORTED = [
     "nxsdg_get_partition", "nxsdg_partition", "nxsdg_write_state", "nxsdg_read_state", "nxsdg_set_forcing",
     "nxsdg_mevp_substeps", "nxsdg_advect", "nxsdg_run_step", "nxsdg_synchronize", "nxsdg_nccl_unique_id",
     "nxsdg_loopback_connect", "nxsdg_group_mevp_substeps", "nxsdg_group_advect", "nxsdg_kernel_launches",
-    "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option",
+    "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option", "nxsdg_halo_plan",
+    "nxsdg_local_geometry",
 ]
+HALO_V, HALO_S, HALO_AH, HALO_AH_SCR0, HALO_AH_SCR1 = 1, 2, 4, 8, 16
+HF_VX, HF_VY, HF_S, HF_A, HF_H, HF_A_SCR0, HF_H_SCR0, HF_A_SCR1, HF_H_SCR1 = range(9)
+
+
+class HaloSeg(C.Structure):
+    _fields_ = [("dir", C.c_int32), ("field", C.c_int32), ("peer", C.c_int32), ("plane", C.c_int32),
+                ("offset", C.c_int64), ("count", C.c_int64)]
+
+
+def halo_plan(nx, ny, p, ns, na, nranks, rank, what):
+    """The ordered halo send/recv plan of one rank (pure host arithmetic, no GPU)."""
+    n = C.c_int32()
+    _chk(None, lib.nxsdg_halo_plan(nx, ny, p, ns, na, nranks, rank, what, None, 0, C.byref(n)), "halo_plan")
+    arr = (HaloSeg * max(1, n.value))()
+    _chk(None, lib.nxsdg_halo_plan(nx, ny, p, ns, na, nranks, rank, what, arr, n.value, C.byref(n)), "halo_plan")
+    return [dict(dir=s.dir, field=s.field, peer=s.peer, plane=s.plane, offset=s.offset, count=s.count)
+            for s in arr[:n.value]]
+
+
+def local_geometry(nx, ny, p, ns, na, nranks, rank) -> dict:
+    out = (C.c_int64 * 8)()
+    _chk(None, lib.nxsdg_local_geometry(nx, ny, p, ns, na, nranks, rank, out), "local_geometry")
+    keys = ("elem_row0", "elem_rows", "glo", "erows_local", "nrows_local", "epitch", "eplane", "npitch")
+    return dict(zip(keys, list(out)))
 
 
 def _chk(ctx, st: int, where: str):

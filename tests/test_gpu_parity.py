@@ -84,14 +84,15 @@ def test_full_subcycle_count(nx, ora, c, nsub):
     _check(got, ref, st, TOLN)
 
 
-@pytest.mark.parametrize("variant,ty,ctas", [(1, 32, 0), (0, 7, 0), (0, 64, 1), (0, 1, 2)])
-def test_fused_variants_and_tuning(nx, ora, variant, ty, ctas):
+@pytest.mark.parametrize("variant,ty,ctas,stages", [(1, 32, 0, 2), (0, 7, 0, 2), (0, 64, 1, 3), (0, 1, 2, 4),
+                                                    (0, 32, 3, 2), (0, 5, 1, 3)])
+def test_fused_variants_and_tuning(nx, ora, variant, ty, ctas, stages):
     """Both fused kernels (TMA-staged structured, table-driven) and several chunk heights /
     persistent grid sizes give the oracle's result (ragged 70x75 CG2 box, 5 subcycles)."""
     c = CASES[2]
     nxe, nye, p, ns, na, kind, lx, ly = c
     st = case(nxe, nye, p, ns, na, kind, lx, ly)
-    opts = {nx.OPT_FUSED_KERNEL: variant, nx.OPT_CHUNK_ROWS: ty, nx.OPT_CTAS_PER_SM: ctas}
+    opts = {nx.OPT_FUSED_KERNEL: variant, nx.OPT_CHUNK_ROWS: ty, nx.OPT_CTAS_PER_SM: ctas, nx.OPT_STAGES: stages}
     got = _gpu_run(nx, st, nxe, nye, p, ns, na, 5, lx, ly, options=opts)
     ref = ora.subcycles(ora_mesh(nxe, nye, p, ns, na, lx, ly), ora_params(nx.PhysParams()), 5, st)
     _check(got, ref, st, 1e-11)
