@@ -520,27 +520,30 @@ __device__ inline void edge_flux(int dir, const Cf<NA>& lo, const Cf<NA>& hi, co
         double vn = 0.0;
 #pragma unroll
         for (int j = 0; j <= P; ++j) vn = fma(T.L1[j][q], vn_nodes[j], vn);
-        double cA = 0.0, cH = 0.0;
-        if (vn > 0.0) {
+        // both traces, then a branch-free upwind select (lanes disagree on the flow direction)
+        double lA = 0.0, lH = 0.0, hA = 0.0, hH = 0.0;
 #pragma unroll
-            for (int k = 0; k < NA; ++k) { cA = fma(lo.A[k], T.psiedge[elo][k][q], cA); cH = fma(lo.H[k], T.psiedge[elo][k][q], cH); }
-        } else {
-#pragma unroll
-            for (int k = 0; k < NA; ++k) { cA = fma(hi.A[k], T.psiedge[ehi][k][q], cA); cH = fma(hi.H[k], T.psiedge[ehi][k][q], cH); }
+        for (int k = 0; k < NA; ++k) {
+            lA = fma(lo.A[k], T.psiedge[elo][k][q], lA); lH = fma(lo.H[k], T.psiedge[elo][k][q], lH);
+            hA = fma(hi.A[k], T.psiedge[ehi][k][q], hA); hH = fma(hi.H[k], T.psiedge[ehi][k][q], hH);
         }
-        FA[q] = open ? cA * vn : 0.0;
-        FH[q] = open ? cH * vn : 0.0;
+        const bool from_lo = vn > 0.0;
+        const double vo = open ? vn : 0.0;
+        FA[q] = (from_lo ? lA : hA) * vo;
+        FH[q] = (from_lo ? lH : hH) * vo;
     }
 }
 
+constexpr int ADV_ROWS = 4;   // block = 32 x ADV_ROWS elements
+
 template <int P, int NA>
-__global__ void __launch_bounds__(256) k_advect(AdvArgs a) {
+__global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect(AdvArgs a) {
     constexpr int NGP = P + 1, NG = NGP * NGP, NCG = (P + 1) * (P + 1);
     const RefTab& T = c_tab[P - 1];
-    __shared__ double sFA[8][32][NGP], sFH[8][32][NGP];
+    __shared__ double sFA[ADV_ROWS][32][NGP], sFH[ADV_ROWS][32][NGP];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int ix = blockIdx.x * 32 + tx;
-    const int lr = a.erow_begin + blockIdx.y * 8 + ty;
+    const int lr = a.erow_begin + blockIdx.y * ADV_ROWS + ty;
     const bool valid = ix < a.nx && lr < a.erow_end;
     const int ixc = valid ? ix : 0, lrc = valid ? lr : a.erow_begin;
     const int64_t e = (int64_t)lrc * a.epitch + ixc;

@@ -926,7 +926,7 @@ static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const d
     a.periodic = c->d.bc == NXSDG_BC_PERIODIC; a.erows_local = c->erows_local;
     a.ihx = 1.0 / (c->d.lx / c->d.nx); a.ihy = 1.0 / (c->d.ly / c->d.ny);
     a.dt = dt; a.a0 = a0; a.a1 = a1;
-    dim3 b(32, 8), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + 7) / 8));
+    dim3 b(32, ADV_ROWS), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + ADV_ROWS - 1) / ADV_ROWS));
     k_advect<P, NA><<<g, b, 0, c->stream>>>(a);
     LAUNCHED();
     return NXSDG_OK;
@@ -962,16 +962,11 @@ static nxsdg_status advect_stage(nxsdg_ctx* c, double dt, int stage) {
     return advect_t<2, 6>(c, dt, stage);
 }
 
-// copy the final stage buffer back into A, H (owned rows)
+// the final stage buffer becomes A, H (pointer swap; ghost rows are refreshed by the next exchange)
 static nxsdg_status advect_finish(nxsdg_ctx* c) {
     const int last = stage_out_buf(c, n_stages(c) - 1);
-    const size_t off = (size_t)c->glo * c->epitch, n = (size_t)c->nown * c->epitch;
-    for (int k = 0; k < c->NA; ++k) {
-        CU(cudaMemcpyAsync(c->A + k * c->eplane + off, c->Asc[last] + k * c->eplane + off, n * sizeof(double),
-                           cudaMemcpyDeviceToDevice, c->stream));
-        CU(cudaMemcpyAsync(c->H + k * c->eplane + off, c->Hsc[last] + k * c->eplane + off, n * sizeof(double),
-                           cudaMemcpyDeviceToDevice, c->stream));
-    }
+    std::swap(c->A, c->Asc[last]);
+    std::swap(c->H, c->Hsc[last]);
     c->prepped = false;
     return NXSDG_OK;
 }
