@@ -152,8 +152,10 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (default 32; one ring row each)
  *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy; default 2)
  *   NXSDG_OPT_STAGES        TMA pipeline depth per warp, 2..4 (default 2)
+ *   NXSDG_OPT_DYNAMIC       1 (default): warps claim work units from an atomic counter; 0: static round-robin
  * INVALID_ARG for an unknown option or value. */
-enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3 };
+enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
+       NXSDG_OPT_DYNAMIC = 4 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

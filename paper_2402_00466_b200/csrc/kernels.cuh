@@ -128,6 +128,8 @@ struct SubArgs {
     int top_boundary;               // node row P*erow_end is the global top row
     double ihx, ihy, fac, ainv, dmin2, beta, b1, kc;
     int repl;
+    int* work_counter;              // TMA kernel: dynamic unit counter (zeroed before the launch), or null
+    int chunk0, chunk_step, nsel;   // chunk selection: chunks chunk0 + i*chunk_step, i < nsel
 };
 
 template <int P>
@@ -137,9 +139,10 @@ __global__ void __launch_bounds__(128) k_subcycle(SubArgs a) {
     const RefTab& T = c_tab[P - 1];
     const int lane = threadIdx.x & 31;
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int strip = gwarp % a.nstrips, chunk = gwarp / a.nstrips;
-    const int lr0 = a.erow_begin + chunk * a.ty;
-    if (lr0 >= a.erow_end) return;               // whole warp exits together
+    const int strip = gwarp % a.nstrips, ci = gwarp / a.nstrips;
+    if (ci >= a.nsel) return;                    // whole warp exits together
+    const int lr0 = a.erow_begin + (a.chunk0 + ci * a.chunk_step) * a.ty;
+    if (lr0 >= a.erow_end) return;
     const int lr1 = min(lr0 + a.ty, a.erow_end);
     const int ix = strip * 31 - 1 + lane;
     const bool evalid = ix >= 0 && ix < a.nx;

@@ -106,6 +106,11 @@ struct nxsdg_ctx {
     int variant = 0;   // fused kernel: 0 = TMA-staged structured (p = 2), 1 = table-driven k_subcycle<P>
     int ctas_per_sm = 2;   // tuned on C4: 4 warps/SM beat the occupancy maximum
     int stages = 2;        // TMA pipeline depth 2..4
+    int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
+    int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
+    double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
+    cudaStream_t hstream = nullptr;                                 // halo stream (NCCL overlap)
+    cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
     K2Maps maps[2][2]; // [cv][cs]
     bool maps_ok = false;
     // transport
@@ -184,6 +189,12 @@ static void free_all(nxsdg_ctx* c) {
                        &c->ax, &c->ay, &c->nodec, &c->staging};
     for (auto b : bufs)
         if (*b) { cudaFree(*b); *b = nullptr; }
+    if (c->counters) { cudaFree(c->counters); c->counters = nullptr; c->ncounters = 0; }
+    if (c->hstage_send) { cudaFree(c->hstage_send); c->hstage_send = nullptr; }
+    if (c->hstage_recv) { cudaFree(c->hstage_recv); c->hstage_recv = nullptr; }
+    if (c->ev_bnd) { cudaEventDestroy(c->ev_bnd); c->ev_bnd = nullptr; }
+    if (c->ev_x) { cudaEventDestroy(c->ev_x); c->ev_x = nullptr; }
+    if (c->hstream) { cudaStreamDestroy(c->hstream); c->hstream = nullptr; }
     c->c1 = c->rx0 = c->ry0 = c->cafo = c->ox = c->oy = nullptr;
 }
 
@@ -321,6 +332,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_CTAS_PER_SM:
             if (value < 0 || value > 32) return fail(c, NXSDG_ERR_INVALID_ARG, "ctas per SM 0..32");
             c->ctas_per_sm = (int)value; break;
+        case NXSDG_OPT_DYNAMIC:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "dynamic 0|1");
+            c->dynamic = (int)value; break;
         case NXSDG_OPT_STAGES:
             if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
             c->stages = (int)value; break;
@@ -523,16 +537,17 @@ static void halo_plan(const Geom& g, uint32_t what, std::vector<nxsdg_halo_seg>&
         }
     };
     auto elem_field = [&](int f, int nplanes, bool both) {
-        for (int k = 0; k < nplanes; ++k) {
-            const int64_t pl = (int64_t)k * g.eplane;
-            if (up) {
-                seg(0, f, g.rank + 1, k, pl + top * g.epitch, g.nx);
-                if (both) seg(1, f, g.rank + 1, k, pl + ghost_hi * g.epitch, g.nx);
-            }
-            if (down) {
-                if (both) seg(0, f, g.rank - 1, k, pl + bot * g.epitch, g.nx);
-                seg(1, f, g.rank - 1, k, pl, g.nx);
-            }
+        // per kind [send up, recv up, send down, recv down], all planes: one packed message each
+        auto planes = [&](int dir, int peer, int64_t row) {
+            for (int k = 0; k < nplanes; ++k) seg(dir, f, peer, k, (int64_t)k * g.eplane + row * g.epitch, g.nx);
+        };
+        if (up) {
+            planes(0, g.rank + 1, top);
+            if (both) planes(1, g.rank + 1, ghost_hi);
+        }
+        if (down) {
+            if (both) planes(0, g.rank - 1, bot);
+            planes(1, g.rank - 1, 0);
         }
     };
     if (what & NXSDG_HALO_V) { node_field(NXSDG_HF_VX); node_field(NXSDG_HF_VY); }
@@ -578,50 +593,127 @@ static double* halo_base(nxsdg_ctx* c, int field) {
     }
 }
 
-static nxsdg_status halo_nccl(nxsdg_ctx* c, uint32_t what) {
+// Messages: consecutive plan segments with the same (dir, peer, field), equal counts and a
+// uniform stride (the planes of one element field) travel as one contiguous message, packed
+// into / unpacked from staging buffers with 2D copies.
+struct HaloMsg { int dir, peer, field; int64_t off0, count, stride, nseg, stage_off; };
+
+static void halo_messages(const Geom& g, uint32_t what, std::vector<HaloMsg>& out) {
     std::vector<nxsdg_halo_seg> plan;
-    halo_plan(c->geom, what, plan);
-    NcclApi& api = nccl();
-    if (api.GroupStart() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupStart");
+    halo_plan(g, what, plan);
     for (const auto& sg : plan) {
-        double* ptr = halo_base(c, sg.field) + sg.offset;
-        const int r = sg.dir == 0 ? api.Send(ptr, (size_t)sg.count, kNcclFloat64, sg.peer, c->comm, c->stream)
-                                  : api.Recv(ptr, (size_t)sg.count, kNcclFloat64, sg.peer, c->comm, c->stream);
-        if (r != 0) { api.GroupEnd(); return fail(c, NXSDG_ERR_NCCL, "ncclSend/Recv: %d", r); }
+        if (!out.empty()) {
+            HaloMsg& m = out.back();
+            if (m.dir == sg.dir && m.peer == sg.peer && m.field == sg.field && m.count == sg.count) {
+                const int64_t st = sg.offset - m.off0;
+                if (m.nseg == 1 && st > 0) { m.stride = st; ++m.nseg; continue; }
+                if (m.nseg > 1 && sg.offset == m.off0 + m.nseg * m.stride) { ++m.nseg; continue; }
+            }
+        }
+        out.push_back(HaloMsg{sg.dir, sg.peer, sg.field, sg.offset, sg.count, sg.count, 1, 0});
     }
-    if (api.GroupEnd() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupEnd");
+    int64_t so = 0, ro = 0;
+    for (auto& m : out) {
+        int64_t& o = m.dir == 0 ? so : ro;
+        m.stage_off = o;
+        o += round_up(m.count * m.nseg, 32);
+    }
+}
+
+static nxsdg_status ensure_halo_staging(nxsdg_ctx* c) {
+    if (c->hstage_send) return NXSDG_OK;
+    std::vector<HaloMsg> msgs;
+    halo_messages(c->geom, NXSDG_HALO_V | NXSDG_HALO_S | NXSDG_HALO_AH, msgs);
+    int64_t need = 64;
+    for (auto& m : msgs) need = std::max(need, m.stage_off + round_up(m.count * m.nseg, 32));
+    CU(cudaMalloc(&c->hstage_send, need * sizeof(double)));
+    CU(cudaMalloc(&c->hstage_recv, need * sizeof(double)));
     return NXSDG_OK;
 }
 
-// Loopback: pair rank r's k-th send to q with q's k-th recv from r and copy (all contexts
-// share one stream, so stream order is the exchange order).
+static nxsdg_status copy2d(nxsdg_ctx* c, double* dst, int64_t dpitch, const double* src, int64_t spitch,
+                           int64_t width, int64_t height, cudaStream_t st) {
+    CU(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, spitch * sizeof(double), width * sizeof(double), height,
+                         cudaMemcpyDeviceToDevice, st));
+    return NXSDG_OK;
+}
+
+static nxsdg_status pack_sends(nxsdg_ctx* c, const std::vector<HaloMsg>& msgs, cudaStream_t st) {
+    nxsdg_status s;
+    for (const auto& m : msgs)
+        if (m.dir == 0 && m.nseg > 1 &&
+            (s = copy2d(c, c->hstage_send + m.stage_off, m.count, halo_base(c, m.field) + m.off0, m.stride, m.count, m.nseg, st)))
+            return s;
+    return NXSDG_OK;
+}
+static nxsdg_status unpack_recvs(nxsdg_ctx* c, const std::vector<HaloMsg>& msgs, cudaStream_t st) {
+    nxsdg_status s;
+    for (const auto& m : msgs)
+        if (m.dir == 1 && m.nseg > 1 &&
+            (s = copy2d(c, halo_base(c, m.field) + m.off0, m.stride, c->hstage_recv + m.stage_off, m.count, m.count, m.nseg, st)))
+            return s;
+    return NXSDG_OK;
+}
+static double* msg_ptr(nxsdg_ctx* c, const HaloMsg& m) {
+    if (m.nseg == 1) return halo_base(c, m.field) + m.off0;
+    return (m.dir == 0 ? c->hstage_send : c->hstage_recv) + m.stage_off;
+}
+
+static nxsdg_status halo_nccl(nxsdg_ctx* c, uint32_t what, cudaStream_t st) {
+    nxsdg_status s = ensure_halo_staging(c);
+    if (s) return s;
+    std::vector<HaloMsg> msgs;
+    halo_messages(c->geom, what, msgs);
+    if ((s = pack_sends(c, msgs, st))) return s;
+    NcclApi& api = nccl();
+    if (api.GroupStart() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupStart");
+    for (const auto& m : msgs) {
+        const size_t n = (size_t)(m.count * m.nseg);
+        const int r = m.dir == 0 ? api.Send(msg_ptr(c, m), n, kNcclFloat64, m.peer, c->comm, st)
+                                 : api.Recv(msg_ptr(c, m), n, kNcclFloat64, m.peer, c->comm, st);
+        if (r != 0) { api.GroupEnd(); return fail(c, NXSDG_ERR_NCCL, "ncclSend/Recv: %d", r); }
+    }
+    if (api.GroupEnd() != 0) return fail(c, NXSDG_ERR_NCCL, "ncclGroupEnd");
+    return unpack_recvs(c, msgs, st);
+}
+
+// Loopback: the NCCL data flow with cudaMemcpyAsync in place of send/recv - pack on every
+// rank, copy rank r's k-th message to q into q's k-th receive from r, unpack on every rank
+// (all contexts share one stream, so stream order is the exchange order).
 static nxsdg_status halo_loopback_all(std::vector<nxsdg_ctx*>& ctxs, uint32_t what) {
     const int n = (int)ctxs.size();
-    std::vector<std::vector<nxsdg_halo_seg>> plans(n);
-    for (int r = 0; r < n; ++r) halo_plan(ctxs[r]->geom, what, plans[r]);
+    nxsdg_status s;
+    std::vector<std::vector<HaloMsg>> msgs(n);
+    for (int r = 0; r < n; ++r) {
+        if ((s = ensure_halo_staging(ctxs[r]))) return s;
+        halo_messages(ctxs[r]->geom, what, msgs[r]);
+        if ((s = pack_sends(ctxs[r], msgs[r], ctxs[r]->stream))) return s;
+    }
     for (int r = 0; r < n; ++r) {
         nxsdg_ctx* c = ctxs[r];
         std::vector<int> kth(n, 0);
-        for (const auto& sg : plans[r]) {
-            if (sg.dir != 0) continue;
-            const int q = sg.peer;
+        for (const auto& m : msgs[r]) {
+            if (m.dir != 0) continue;
+            const int q = m.peer;
             int seen = -1;
-            const nxsdg_halo_seg* rv = nullptr;
-            for (const auto& t : plans[q])
+            const HaloMsg* rv = nullptr;
+            for (const auto& t : msgs[q])
                 if (t.dir == 1 && t.peer == r && ++seen == kth[q]) { rv = &t; break; }
             ++kth[q];
-            if (!rv || rv->count != sg.count || rv->field != sg.field)
+            if (!rv || rv->count * rv->nseg != m.count * m.nseg || rv->field != m.field)
                 return fail(c, NXSDG_ERR_STATE, "halo plan mismatch between ranks %d and %d", r, q);
-            CU(cudaMemcpyAsync(halo_base(ctxs[q], rv->field) + rv->offset, halo_base(c, sg.field) + sg.offset,
-                               (size_t)sg.count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            CU(cudaMemcpyAsync(msg_ptr(ctxs[q], *rv), msg_ptr(c, m), (size_t)(m.count * m.nseg) * sizeof(double),
+                               cudaMemcpyDeviceToDevice, c->stream));
         }
     }
+    for (int r = 0; r < n; ++r)
+        if ((s = unpack_recvs(ctxs[r], msgs[r], ctxs[r]->stream))) return s;
     return NXSDG_OK;
 }
 
 static nxsdg_status halo(nxsdg_ctx* c, uint32_t what) {
     if (c->d.nranks == 1) return NXSDG_OK;
-    if (c->d.transport == NXSDG_TRANSPORT_NCCL) return halo_nccl(c, what);
+    if (c->d.transport == NXSDG_TRANSPORT_NCCL) return halo_nccl(c, what, c->stream);
     return NXSDG_OK;   // loopback exchanges are driven by the group calls
 }
 
@@ -676,7 +768,17 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     a.dmin2 = c->prm.DeltaMin * c->prm.DeltaMin;
     a.beta = c->prm.beta; a.b1 = 1.0 + c->prm.beta; a.kc = c->prm.dt * c->prm.f_c;
     a.repl = c->prm.replacement_pressure;
+    a.chunk0 = 0; a.chunk_step = 1; a.nsel = (c->nown + a.ty - 1) / a.ty;
     return a;
+}
+
+// chunk selections for the overlapped multi-rank subcycle
+enum { SEL_ALL = 0, SEL_BOUNDARY = 1, SEL_INTERIOR = 2 };
+static int n_chunks(const nxsdg_ctx* c) { return (c->nown + c->ty - 1) / c->ty; }
+static void select_chunks(const nxsdg_ctx* c, int sel, SubArgs& a) {
+    const int nc = n_chunks(c);
+    if (sel == SEL_BOUNDARY) { a.chunk0 = 0; a.chunk_step = nc > 1 ? nc - 1 : 1; a.nsel = nc > 1 ? 2 : 1; }
+    if (sel == SEL_INTERIOR) { a.chunk0 = 1; a.chunk_step = 1; a.nsel = nc - 2; }
 }
 
 // ---------------------------------------------------------------- TMA descriptors
@@ -725,7 +827,8 @@ static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0; }
 
 template <bool R, int ST>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
-    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage) + sizeof(uint64_t));
+    // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage) + sizeof(uint64_t) + sizeof(int4));
     static bool attr = false;
     if (!attr) {
         CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -735,18 +838,35 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST>, 32 * K2_WARPS, smem));
     if (c->ctas_per_sm > 0) occ = std::min(occ, c->ctas_per_sm);
-    const int nchunks = (c->nown + a.ty - 1) / a.ty;
-    const int64_t units = (int64_t)a.nstrips * nchunks;
+    const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     k_subcycle_tma<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->maps[cv][cs], a);
     return NXSDG_OK;
 }
 
-static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs) {
+static nxsdg_status ensure_counters(nxsdg_ctx* c, int n) {
+    if (c->ncounters >= n) return NXSDG_OK;
+    if (c->counters) cudaFree(c->counters);
+    c->counters = nullptr; c->ncounters = 0;
+    CU(cudaMalloc(&c->counters, sizeof(int) * (size_t)std::max(n, 128)));
+    c->ncounters = std::max(n, 128);
+    return NXSDG_OK;
+}
+
+// slot < 0: direct launch, zero slot 0 first; slot >= 0: inside a graph whose first node zeroes all slots
+static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int sel = SEL_ALL) {
     nxsdg_status st = build_maps(c);
     if (st) return st;
     SubArgs a = sub_args(c, cv, cs);
+    select_chunks(c, sel, a);
+    if (a.nsel <= 0) return NXSDG_OK;
+    if (slot < 0) {
+        if ((st = ensure_counters(c, 1))) return st;
+        CU(cudaMemsetAsync(c->counters, 0, sizeof(int), c->stream));
+        slot = 0;
+    }
+    a.work_counter = c->dynamic ? c->counters + slot : nullptr;
     switch (c->stages * 2 + (a.repl ? 1 : 0)) {
         case 4: return launch_tma_t<false, 2>(c, cv, cs, a);
         case 5: return launch_tma_t<true, 2>(c, cv, cs, a);
@@ -757,20 +877,55 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs) {
     }
 }
 
-static nxsdg_status launch_subcycle(nxsdg_ctx* c) {
+// One fused subcycle launch over the selected chunks (no ping-pong flip).
+static nxsdg_status launch_subcycle_sel(nxsdg_ctx* c, int sel) {
     if (use_tma(c)) {
-        nxsdg_status st = launch_tma(c, c->cv, c->cs);
+        nxsdg_status st = launch_tma(c, c->cv, c->cs, -1, sel);
         if (st) return st;
     } else {
         SubArgs a = sub_args(c, c->cv, c->cs);
-        const int nchunks = (c->nown + a.ty - 1) / a.ty;
-        const int64_t warps = (int64_t)a.nstrips * nchunks;
+        select_chunks(c, sel, a);
+        if (a.nsel <= 0) return NXSDG_OK;
+        const int64_t warps = (int64_t)a.nstrips * a.nsel;
         const unsigned blocks = (unsigned)((warps + 3) / 4);
         if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
         else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
     }
     LAUNCHED();
+    return NXSDG_OK;
+}
+
+static nxsdg_status launch_subcycle(nxsdg_ctx* c) {
+    nxsdg_status st = launch_subcycle_sel(c, SEL_ALL);
+    if (st) return st;
     c->cv ^= 1; c->cs ^= 1;
+    return NXSDG_OK;
+}
+
+// Multi-rank NCCL subcycle with overlap: boundary chunks (first and last
+// chunk rows, which produce every row a neighbour needs) -> event -> halo exchange on the
+// halo stream, concurrently the interior chunks on the main stream -> join.
+static nxsdg_status subcycle_overlapped(nxsdg_ctx* c) {
+    nxsdg_status st;
+    if (n_chunks(c) < 3) {
+        if ((st = launch_subcycle(c))) return st;
+        return halo(c, NXSDG_HALO_V | NXSDG_HALO_S);
+    }
+    if (!c->hstream) {
+        CU(cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
+    }
+    if ((st = launch_subcycle_sel(c, SEL_BOUNDARY))) return st;
+    c->cv ^= 1; c->cs ^= 1;                      // the exchange moves rows of the new state
+    CU(cudaEventRecord(c->ev_bnd, c->stream));
+    CU(cudaStreamWaitEvent(c->hstream, c->ev_bnd, 0));
+    if ((st = halo_nccl(c, NXSDG_HALO_V | NXSDG_HALO_S, c->hstream))) return st;
+    CU(cudaEventRecord(c->ev_x, c->hstream));
+    c->cv ^= 1; c->cs ^= 1;                      // interior reads the old state
+    if ((st = launch_subcycle_sel(c, SEL_INTERIOR))) return st;
+    c->cv ^= 1; c->cs ^= 1;
+    CU(cudaStreamWaitEvent(c->stream, c->ev_x, 0));
     return NXSDG_OK;
 }
 
@@ -837,6 +992,7 @@ static nxsdg_status check_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
 static nxsdg_status one_subcycle(nxsdg_ctx* c, bool unfused) {
     nxsdg_status s;
     if (!unfused) {
+        if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_NCCL) return subcycle_overlapped(c);
         if ((s = launch_subcycle(c))) return s;
         return halo(c, NXSDG_HALO_V | NXSDG_HALO_S);
     }
@@ -855,15 +1011,17 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
+        if (use_tma(c)) {   // descriptors and counters are created outside the capture
+            nxsdg_status st = build_maps(c);
+            if (!st) st = ensure_counters(c, n);
+            if (st) return st;
+        }
         CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         int cv = c->cv, cs = c->cs;
-        if (use_tma(c)) {
-            nxsdg_status st = build_maps(c);   // descriptors are encoded outside the capture
-            if (st) { cudaGraph_t junk; cudaStreamEndCapture(c->stream, &junk); if (junk) cudaGraphDestroy(junk); return st; }
-        }
+        if (use_tma(c)) CU(cudaMemsetAsync(c->counters, 0, sizeof(int) * (size_t)n, c->stream));
         for (int i = 0; i < n; ++i) {
             if (use_tma(c)) {
-                nxsdg_status st = launch_tma(c, cv, cs);
+                nxsdg_status st = launch_tma(c, cv, cs, i);
                 if (st) { cudaGraph_t junk; cudaStreamEndCapture(c->stream, &junk); if (junk) cudaGraphDestroy(junk); return st; }
             } else {
                 SubArgs a = sub_args(c, cv, cs);
@@ -1035,8 +1193,18 @@ extern "C" nxsdg_status nxsdg_group_mevp_substeps(nxsdg_ctx** ctxs, int32_t nr, 
     }
     for (int i = 0; i < n; ++i) {
         if (!unfused) {
-            for (nxsdg_ctx* c : v) if ((s = launch_subcycle(c))) return s;
+            // same split as the NCCL path: boundary chunks, exchange, interior chunks
+            for (nxsdg_ctx* c : v) {
+                if ((s = launch_subcycle_sel(c, n_chunks(c) < 3 ? SEL_ALL : SEL_BOUNDARY))) return s;
+                c->cv ^= 1; c->cs ^= 1;
+            }
             if ((s = halo_loopback_all(v, NXSDG_HALO_V | NXSDG_HALO_S))) return s;
+            for (nxsdg_ctx* c : v) {
+                if (n_chunks(c) < 3) continue;
+                c->cv ^= 1; c->cs ^= 1;
+                if ((s = launch_subcycle_sel(c, SEL_INTERIOR))) return s;
+                c->cv ^= 1; c->cs ^= 1;
+            }
         } else {
             for (nxsdg_ctx* c : v) {
                 if ((s = ensure_debug_buffers(c))) return s;

@@ -219,8 +219,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     }
     const int twarps = gridDim.x * K2_WARPS;
     const int gw = blockIdx.x * K2_WARPS + wib;
-    const int nchunks = (a.erow_end - a.erow_begin + a.ty - 1) / a.ty;
-    const int nunits = a.nstrips * nchunks;
+    const int nunits = a.nstrips * a.nsel;
     if (gw >= nunits) return;
     if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
@@ -228,18 +227,29 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     }
     __syncwarp();
 
+    // Work list: (strip, chunk) units.  A warp's first unit is gw; further units are claimed
+    // from a global counter (dynamic balancing; a.work_counter is zeroed before each launch),
+    // or round-robin (gw + k * twarps) when no counter is given.  Lane 0 runs the prefetch
+    // cursor and records each job in the stage's descriptor slot; all lanes read it back.
     struct Cur { int u, lr, lr1, ix0; bool ring, first, ok; };
     auto start_unit = [&](int u, Cur& c) {
         c.ok = u < nunits;
         if (!c.ok) return;
-        const int strip = u % a.nstrips, chunk = u / a.nstrips;
+        const int strip = u % a.nstrips, chunk = a.chunk0 + (u / a.nstrips) * a.chunk_step;
         const int lr0 = a.erow_begin + chunk * a.ty;
         c.u = u; c.lr1 = min(lr0 + a.ty, a.erow_end); c.ix0 = strip * 31;
         c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
     };
-    auto advance = [&](Cur& c) {
+    auto advance = [&](Cur& c) {          // lane 0 only
         ++c.lr; c.ring = false; c.first = false;
-        if (c.lr >= c.lr1) start_unit(c.u + twarps, c);
+        if (c.lr >= c.lr1) {
+            const int nu = a.work_counter ? twarps + atomicAdd(a.work_counter, 1) : c.u + twarps;
+            start_unit(nu, c);
+        }
+    };
+    int4* jobs = reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) + wib * STAGES;
+    auto record = [&](const Cur& c, int st) {   // lane 0
+        jobs[st] = make_int4(c.ok ? c.u : -1, c.lr, c.lr1, (c.ring ? 1 : 0) | (c.first ? 2 : 0));
     };
     auto issue = [&](const Cur& c, int s) {
         K2Stage* t = stg + s;
@@ -256,22 +266,37 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     const double ihx = a.ihx, ihy = a.ihy, fac = a.fac, hA = 0.5 * a.ainv;
     const int64_t npitch = a.npitch, eplane = a.eplane;
     // prologue: jobs 0 .. STAGES-2 in flight; job j lives in stage j % STAGES
-    Cur cur, pre;
-    start_unit(gw, cur);
-    pre = cur;
-    if (lane == 0) issue(pre, 0);
+    Cur pre;
+    if (lane == 0) {
+        start_unit(gw, pre);
+        record(pre, 0);
+        issue(pre, 0);
 #pragma unroll
-    for (int k = 1; k < STAGES - 1; ++k) {
-        advance(pre);
-        if (pre.ok && lane == 0) issue(pre, k);
+        for (int k = 1; k < STAGES - 1; ++k) {
+            advance(pre);
+            record(pre, k);
+            if (pre.ok) issue(pre, k);
+        }
     }
-    advance(pre);          // pre = job (current + STAGES - 1)
+    __syncwarp();
     uint32_t phase = 0;    // bit s = parity of stage s
     int s = 0;
     double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
-    while (cur.ok) {
+    for (;;) {
         const int sp = (s + STAGES - 1) % STAGES;
-        if (pre.ok && lane == 0) issue(pre, sp);
+        if (lane == 0) {
+            if (pre.ok) advance(pre);
+            record(pre, sp);
+            if (pre.ok) issue(pre, sp);
+        }
+        Cur cur;
+        {
+            const int4 jd = jobs[s];
+            cur.ok = jd.x >= 0;
+            if (!cur.ok) break;
+            cur.u = jd.x; cur.lr = jd.y; cur.lr1 = jd.z; cur.ring = jd.w & 1; cur.first = (jd.w & 2) != 0;
+            cur.ix0 = (cur.u % a.nstrips) * 31;
+        }
         mbar_wait(&bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
         const K2Stage& t = stg[s];
@@ -413,7 +438,6 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             }
         }
         __syncwarp();
-        advance(cur); advance(pre);
         s = (s + 1) % STAGES;
     }
 }

@@ -11,8 +11,9 @@ m.load(st)
 s = torch.cuda.ExternalStream(m.stream)
 n = 20
 res = []
-combos = [(0, ty, c, st) for st in (2, 3, 4) for c in (1, 2, 3) for ty in (32, 64)]
-for var, ty, c, stg in combos:
+combos = [(0, ty, c, st, dyn) for rep in range(2) for dyn in (0, 1) for st in (2, 3) for c in (2, 3) for ty in (32,)]
+for var, ty, c, stg, dyn in combos:
+    m.set_option(nxsdg.OPT_DYNAMIC, dyn)
     m.set_option(nxsdg.OPT_FUSED_KERNEL, var); m.set_option(nxsdg.OPT_CHUNK_ROWS, ty); m.set_option(nxsdg.OPT_CTAS_PER_SM, c)
     try:
         m.set_option(nxsdg.OPT_STAGES, stg)
@@ -28,4 +29,4 @@ for var, ty, c, stg in combos:
         t.append(e0.elapsed_time(e1) / n)
     ms = min(t)
     gbs = 680.0 * cfg.nx * cfg.ny / (ms * 1e-3) / 1e9
-    print(json.dumps({"variant": var, "ty": ty, "ctas": c, "stages": stg, "ms": ms, "alg_GBs": gbs, "frac": gbs / 6545.6}), flush=True)
+    print(json.dumps({"variant": var, "ty": ty, "ctas": c, "stages": stg, "dyn": dyn, "ms": ms, "alg_GBs": gbs, "frac": gbs / 6545.6}), flush=True)

@@ -206,13 +206,16 @@ def test_graph_replay_matches_eager_chunks(nx):
         np.testing.assert_array_equal(a[k], b[k])
 
 
-@pytest.mark.parametrize("nranks", [2, 3, 5])
-def test_loopback_strips_bitwise_equal_single(nx, nranks):
-    """Row strips with halo exchange give bitwise the single-GPU result (fused + advection)."""
+@pytest.mark.parametrize("nranks,ty,variant", [(2, 32, 0), (3, 32, 0), (5, 32, 0), (2, 4, 0), (3, 3, 0), (3, 4, 1)])
+def test_loopback_strips_bitwise_equal_single(nx, nranks, ty, variant):
+    """Row strips with halo exchange give bitwise the single-GPU result (fused + advection).
+    Small chunk heights (ty) give >= 3 chunks per rank, so the boundary/interior split with the
+    packed exchange in between (the NCCL overlap path's data flow) is exercised."""
     nxe, nye, lx, ly = 50, 47, 50e3, 47e3
     st = case(nxe, nye, 2, 6, 6, "random", lx, ly)
     prm = nx.PhysParams()
     with nx.Mesh(nxe, nye, lx, ly) as m:
+        m.set_option(nx.OPT_FUSED_KERNEL, variant)
         m.load(st)
         m.advect(prm.dt)
         m.mevp_substeps(6, begin_step=True)
@@ -221,6 +224,9 @@ def test_loopback_strips_bitwise_equal_single(nx, nranks):
     s = torch.cuda.Stream()
     ms = [nx.Mesh(nxe, nye, lx, ly, rank=r, nranks=nranks, transport=nx.TRANSPORT_LOOPBACK,
                   stream=s.cuda_stream) for r in range(nranks)]
+    for m in ms:
+        m.set_option(nx.OPT_CHUNK_ROWS, ty)
+        m.set_option(nx.OPT_FUSED_KERNEL, variant)
     nx.loopback_connect(ms)
     for m in ms:
         er0, ern = m.elem_row0, m.elem_rows
