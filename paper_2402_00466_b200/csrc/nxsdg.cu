@@ -22,6 +22,7 @@
 #include "../../include/nxsdg.h"
 #include "kernels.cuh"
 #include "subcycle_tma.cuh"
+#include "advect_q2.cuh"
 
 using namespace nxk;
 
@@ -1085,7 +1086,8 @@ static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const d
     a.ihx = 1.0 / (c->d.lx / c->d.nx); a.ihy = 1.0 / (c->d.ly / c->d.ny);
     a.dt = dt; a.a0 = a0; a.a1 = a1;
     dim3 b(32, ADV_ROWS), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + ADV_ROWS - 1) / ADV_ROWS));
-    k_advect<P, NA><<<g, b, 0, c->stream>>>(a);
+    if (P == 2 && NA == 6 && c->variant == 0) k_advect_q2<<<g, b, 0, c->stream>>>(a);   // structured
+    else k_advect<P, NA><<<g, b, 0, c->stream>>>(a);
     LAUNCHED();
     return NXSDG_OK;
 }

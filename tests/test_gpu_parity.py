@@ -139,6 +139,25 @@ def test_advection(nx, ora, na, bc):
         assert abs(got["A"][:, 0].sum() - st["A"][:, 0].sum()) < 1e-12 * abs(st["A"][:, 0]).sum()
 
 
+@pytest.mark.parametrize("bc", [0, 1])
+def test_advection_kernels_agree(nx, bc):
+    """Structured CG2/DG2 advection kernel vs the table-driven one (tables from K0)."""
+    nxe, nye, lx, ly = 70, 45, 70e3, 45e3
+    st = case(nxe, nye, 2, 6, 6, "random", lx, ly)
+    if bc == 1:
+        for k in ("vx", "vy"):
+            st[k][-1, :] = st[k][0, :]; st[k][:, -1] = st[k][:, 0]
+    out = []
+    for variant in (0, 1):
+        with nx.Mesh(nxe, nye, lx, ly, bc=bc) as m:
+            m.set_option(nx.OPT_FUSED_KERNEL, variant)
+            m.load(st)
+            m.advect(900.0)
+            out.append(m.state(("A", "H")))
+    e = parity(out[0], out[1], st, ("A", "H"))
+    assert max(e.values()) < 1e-12, e
+
+
 def test_outer_step_c3_shape(nx, ora):
     """Paper order: advect, then subcycles; 96x80 CG2/DG2 at C3 resolution (250 m)."""
     nxe, nye = 96, 80
