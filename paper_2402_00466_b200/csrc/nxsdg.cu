@@ -252,6 +252,7 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     {
         RefTab* dtab = nullptr;
         if (cudaMalloc(&dtab, sizeof(RefTab)) != cudaSuccess) return bail(NXSDG_ERR_OOM);
+        cudaMemsetAsync(dtab, 0, sizeof(RefTab), c->stream);   // struct padding is never written by K0
         for (int p = 1; p <= 2; ++p) {
             k_build_tables<<<1, 32, 0, c->stream>>>(dtab, p);
             ++c->launches;
