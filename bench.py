@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nsub", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--moving", action="store_true",
+                    help="NEXT-2: regenerate the moving-cyclone forcing on the GPU at every outer step (P:350 protocol)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-window", type=int, default=512, help="oracle window per --impl reference step")
     ap.add_argument("--cpu-window", type=int, default=640, help="oracle window of the cpu_baseline sample")
@@ -218,8 +220,13 @@ def main():
         if world > 1:
             dist.barrier()
 
+    tclock = [0.0]
+
     def step(ev=None):
         if ev: ev[0].record(stream)
+        if args.moving:
+            m.set_forcing_cyclone(tclock[0])
+            tclock[0] += prm.dt
         m.advect(prm.dt)
         if ev: ev[1].record(stream)
         m.mevp_substeps(0, begin_step=True)
@@ -305,6 +312,7 @@ def main():
                                    f"cyclone forcing; step = advect + prep + {cfg.nsub} fused mEVP subcycles",
                        "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el, "alpha": cfg.alpha, "beta": cfg.alpha,
                        "parallelism": f"row strips x{world}" if world > 1 else "1 GPU",
+                       "forcing": "moving cyclone regenerated on the GPU every step" if args.moving else "static (t = 0)",
                        "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},
             "breakdown_ms": {"advect": adv, "prep": prep, "subcycles": sub, "per_subcycle": kernel_ms},
             "roofline": {"bound": "hbm", "kernel": KERNEL, "achieved": achieved, "peak": peak, "unit": "GB/s",

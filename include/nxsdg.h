@@ -168,6 +168,11 @@ nxsdg_status nxsdg_read_state(nxsdg_ctx* ctx, nxsdg_field field, double* dst, in
 nxsdg_status nxsdg_set_forcing(nxsdg_ctx* ctx, const double* ox, const double* oy,
                                const double* ax, const double* ay, int64_t count, nxsdg_mem mem);
 
+/* Synthetic VP-benchmark forcing evaluated on the device at time t [s] (DESIGN.md §5 recipe:
+ * ocean gyre o, cyclone wind a moving at 51.2 km/day; global box coordinates), for multi-outer-step
+ * runs without host transfers.  Same effect as nxsdg_set_forcing with those fields. */
+nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* ctx, double t);
+
 /* ---- compute ----------------------------------------------------------------- */
 /* n_sub mEVP subcycles.  flags: NXSDG_BEGIN_STEP, NXSDG_UNFUSED.
  * STATE if forcing unset, or if no BEGIN_STEP happened since the last state write. */

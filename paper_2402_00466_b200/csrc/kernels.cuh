@@ -665,6 +665,36 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect(AdvArgs a) {
 }
 
 // --------------------------------------------------------------------------
+// Synthetic VP-benchmark forcing at time t (DESIGN.md §5 recipe; NEXT-2 moving cyclone), on the
+// owned node rows: o = 0.01 (2y/Ly - 1, 1 - 2x/Lx); a = -(W e / r0) exp(-r/r0) R_theta (x - c(t)),
+// c(t) = (Lx/2, Ly/2) + 51.2 km/day t (1, 1), W = 15 m/s, r0 = 100 km, theta = 72 deg.
+// --------------------------------------------------------------------------
+struct ForcingArgs {
+    double* ox; double* oy; double* ax; double* ay;
+    int64_t npitch;
+    int ncols, row_begin, row_end, global_row0;   // owned local node rows; global index of local row 0
+    double dxn, dyn, lx, ly, t;                    // node spacing hx/p, hy/p; global extents
+};
+
+__global__ void k_cyclone_forcing(ForcingArgs a) {
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jr = a.row_begin + blockIdx.y;
+    if (I >= a.ncols || jr >= a.row_end) return;
+    const double x = I * a.dxn, y = (a.global_row0 + jr) * a.dyn;
+    const int64_t n = (int64_t)jr * a.npitch + I;
+    a.ox[n] = 0.01 * (2.0 * y / a.ly - 1.0);
+    a.oy[n] = 0.01 * (1.0 - 2.0 * x / a.lx);
+    const double shift = 51.2 * (1000.0 / 86400.0) * a.t;
+    const double dx = x - (0.5 * a.lx + shift), dy = y - (0.5 * a.ly + shift);
+    const double r = sqrt(dx * dx + dy * dy);
+    const double W = 15.0, r0 = 100e3, th = 72.0 * 3.14159265358979323846 / 180.0;
+    const double sc = -(W * 2.71828182845904523536 / r0) * exp(-r / r0);
+    const double ct = cos(th), st = sin(th);
+    a.ax[n] = sc * (ct * dx + st * dy);
+    a.ay[n] = sc * (-st * dx + ct * dy);
+}
+
+// --------------------------------------------------------------------------
 // ABI layout conversion: AoS rows (n per element) <-> SoA planes.
 // --------------------------------------------------------------------------
 // compact ABI element e = row*nx + col  <->  device (row + row_off)*epitch + col

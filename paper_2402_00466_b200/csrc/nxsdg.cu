@@ -496,6 +496,24 @@ extern "C" nxsdg_status nxsdg_set_forcing(nxsdg_ctx* c, const double* ox, const 
     return NXSDG_OK;
 }
 
+extern "C" nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* c, double t) {
+    GUARD(c);
+    if (!(t == t)) return fail(c, NXSDG_ERR_INVALID_ARG, "t is NaN");
+    ForcingArgs a{};
+    a.ox = c->ox; a.oy = c->oy; a.ax = c->ax; a.ay = c->ay;
+    a.npitch = c->npitch; a.ncols = c->P * c->d.nx + 1;
+    a.row_begin = c->P * c->glo; a.row_end = (int)(c->P * c->glo + owned_node_rows(c));
+    a.global_row0 = (int)(c->P * (c->r0 - c->glo));
+    a.dxn = c->d.lx / c->d.nx / c->P; a.dyn = c->d.ly / c->d.ny / c->P;
+    a.lx = c->d.lx; a.ly = c->d.ly; a.t = t;
+    dim3 b(128), g((unsigned)((a.ncols + 127) / 128), (unsigned)(a.row_end - a.row_begin));
+    k_cyclone_forcing<<<g, b, 0, c->stream>>>(a);
+    LAUNCHED();
+    c->forcing_set = true;
+    c->prepped = false;
+    return NXSDG_OK;
+}
+
 // ---------------------------------------------------------------- halo exchange
 // Rows that cross a rank boundary:
 //   up   (r -> r+1): top owned element row of element fields; top P owned node rows of node fields

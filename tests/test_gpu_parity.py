@@ -169,6 +169,52 @@ def test_outer_step_c3_shape(nx, ora):
     _check(got, ref, st, TOLN, groups=("S", "v", "A", "H"))
 
 
+def test_multi_outer_step_moving_cyclone(nx, ora):
+    """NEXT-2: 4 outer steps (advect + 25 subcycles each) with the cyclone forcing regenerated on
+    the GPU at t_k = k dt, against the oracle fed the host recipe at the same times."""
+    nxe, nye = 64, 56
+    lx, ly = nxe * 2e3, nye * 2e3
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    prm = nx.PhysParams()
+    nsteps, nsub = 4, 25
+    X, Y = np.meshgrid(np.arange(2 * nxe + 1) * (lx / nxe / 2), np.arange(2 * nye + 1) * (ly / nye / 2))
+    ref = {k: v.copy() for k, v in st.items()}
+    om = ora_mesh(nxe, nye, 2, 6, 6, lx, ly)
+    with nx.Mesh(nxe, nye, lx, ly, params=prm) as m:
+        m.load(st)
+        for k in range(nsteps):
+            t = k * prm.dt
+            m.set_forcing_cyclone(t)
+            m.advect(prm.dt)
+            m.mevp_substeps(nsub, begin_step=True)
+            ref["ox"], ref["oy"], ref["ax"], ref["ay"] = (np.ascontiguousarray(a) for a in
+                                                          inputs.cyclone_forcing(X, Y, lx, ly, t))
+            ref = ora.outer_step(om, ora_params(prm), nsub, ref, do_advect=True)
+        got = m.state()
+    _check(got, ref, st, TOLN, groups=("S", "v", "A", "H"))
+
+
+def test_device_cyclone_forcing_equals_host_recipe(nx):
+    """nxsdg_set_forcing_cyclone(t) == nxsdg_set_forcing(inputs.cyclone_forcing(t)) (same subcycle result)."""
+    nxe, nye, lx, ly = 40, 30, 80e3, 60e3
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    X, Y = np.meshgrid(np.arange(2 * nxe + 1) * (lx / nxe / 2), np.arange(2 * nye + 1) * (ly / nye / 2))
+    t = 7 * 3600.0
+    host = [np.ascontiguousarray(a) for a in inputs.cyclone_forcing(X, Y, lx, ly, t)]
+    out = []
+    for dev in (True, False):
+        with nx.Mesh(nxe, nye, lx, ly) as m:
+            m.load({k: v for k, v in st.items() if k not in ("ox", "oy", "ax", "ay")})
+            if dev:
+                m.set_forcing_cyclone(t)
+            else:
+                m.set_forcing(*host)
+            m.mevp_substeps(3, begin_step=True)
+            out.append(m.state())
+    e = parity(out[0], out[1], st)
+    assert max(e.values()) < 1e-13, e
+
+
 def test_debug_steps_each_against_oracle(nx, ora):
     """Each Table 1 step alone (unfused kernels via nxsdg_run_step) against the oracle's step."""
     nxe, nye, p, ns, na = 33, 35, 2, 6, 6
