@@ -44,6 +44,7 @@ class OraMesh(C.Structure):
     _fields_ = [
         ("nx", C.c_int), ("ny", C.c_int), ("lx", C.c_double), ("ly", C.c_double),
         ("p", C.c_int), ("ns", C.c_int), ("na", C.c_int), ("bc", C.c_int),
+        ("verts", C.POINTER(C.c_double)),
     ]
 
 
@@ -86,9 +87,14 @@ class Mesh:
     ns: int = 6
     na: int = 6
     bc: int = 0
+    verts: np.ndarray | None = None   # (ny+1, nx+1, 2) vertex coordinates; None = box
 
     def c(self) -> OraMesh:
-        return OraMesh(self.nx, self.ny, self.lx, self.ly, self.p, self.ns, self.na, self.bc)
+        vp = None
+        if self.verts is not None:
+            self._vkeep = np.ascontiguousarray(self.verts, dtype=np.float64)
+            vp = self._vkeep.ctypes.data_as(_P)
+        return OraMesh(self.nx, self.ny, self.lx, self.ly, self.p, self.ns, self.na, self.bc, vp)
 
     @property
     def n_elem(self) -> int:

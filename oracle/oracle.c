@@ -123,17 +123,27 @@ void ora_cg_basis(int p, double s, double t, double* phi, double* dphids, double
         }
 }
 
-/* Bilinear (isoparametric Q1) element map from the four vertices
- * x_{a,b} = (a*hx, b*hy).  Returns |J|, fills J^{-1}
- * row-major ([ds/dx ds/dy; dt/dx dt/dy]). */
-double ora_element_jacobian(const ora_mesh* m, int ix, int iy, double s, double t, double Jinv[4]) {
+/* Bilinear (Q1) element map from the four vertices: the box x_{a,b} = (a*hx, b*hy), or the
+ * mesh's vertex array for general quads (R#23). */
+static void element_vertices(const ora_mesh* m, int ix, int iy, double X[4], double Y[4]) {
     double hx = m->lx / m->nx, hy = m->ly / m->ny;
-    double X[4], Y[4];
     for (int k = 0; k < 4; ++k) {
         int kx = k & 1, ky = k >> 1;
-        X[k] = (ix + kx) * hx;
-        Y[k] = (iy + ky) * hy;
+        if (m->verts) {
+            long v = (long)(iy + ky) * (m->nx + 1) + (ix + kx);
+            X[k] = m->verts[2 * v];
+            Y[k] = m->verts[2 * v + 1];
+        } else {
+            X[k] = (ix + kx) * hx;
+            Y[k] = (iy + ky) * hy;
+        }
     }
+}
+
+/* |J| of the bilinear map at (s,t); fills J^{-1} row-major ([ds/dx ds/dy; dt/dx dt/dy]). */
+double ora_element_jacobian(const ora_mesh* m, int ix, int iy, double s, double t, double Jinv[4]) {
+    double X[4], Y[4];
+    element_vertices(m, ix, iy, X, Y);
     double phi[4], ds[4], dt[4];
     ora_cg_basis(1, s, t, phi, ds, dt);
     double xs = 0, xt = 0, ys = 0, yt = 0;
@@ -151,15 +161,15 @@ double ora_element_jacobian(const ora_mesh* m, int ix, int iy, double s, double 
 
 /* Tangent vector of the element map along s (col 0) or t (col 1). */
 static void element_tangent(const ora_mesh* m, int ix, int iy, double s, double t, int col, double* T) {
-    double hx = m->lx / m->nx, hy = m->ly / m->ny;
+    double X[4], Y[4];
+    element_vertices(m, ix, iy, X, Y);
     double phi[4], ds[4], dt[4];
     ora_cg_basis(1, s, t, phi, ds, dt);
     double a = 0, b = 0;
     for (int k = 0; k < 4; ++k) {
-        int kx = k & 1, ky = k >> 1;
         double d = col == 0 ? ds[k] : dt[k];
-        a += d * (ix + kx) * hx;
-        b += d * (iy + ky) * hy;
+        a += d * X[k];
+        b += d * Y[k];
     }
     T[0] = a; T[1] = b;
 }

@@ -30,6 +30,9 @@ typedef struct {
     int ns;          /* DG stress dofs 3|6                          */
     int na;          /* DG advection dofs 1|3|6                     */
     int bc;          /* 0 closed (Dirichlet v=0), 1 periodic (advection only) */
+    const double* verts; /* NULL: axis-aligned box x_{a,b} = (a hx, b hy).  Else (ny+1) x (nx+1) x 2
+                            vertex coordinates, row-major: a general (distorted) quad mesh with the
+                            bilinear element map of its four vertices (R#23) */
 } ora_mesh;
 
 typedef struct {

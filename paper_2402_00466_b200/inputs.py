@@ -160,6 +160,20 @@ def make_case(nx, ny, p, ns, na, kind="warm", seed=SEED_BASE, lx=512e3, ly=512e3
                 ox=c(ox), oy=c(oy), ax=c(ax), ay=c(ay))
 
 
+def distorted_vertices(nx, ny, lx, ly, delta=0.25, seed=SEED_BASE + 7) -> np.ndarray:
+    """(ny+1, nx+1, 2) vertices of a box mesh whose interior vertices are moved by a seeded uniform
+    offset of up to delta * (hx, hy) / 2 per axis (distortion < 0.3 keeps every
+    quad convex, so all Jacobians stay positive).  Boundary vertices stay on the box."""
+    rng = np.random.default_rng(seed)
+    hx, hy = lx / nx, ly / ny
+    X, Y = np.meshgrid(np.arange(nx + 1) * hx, np.arange(ny + 1) * hy)
+    dx = rng.uniform(-0.5, 0.5, X.shape) * delta * hx
+    dy = rng.uniform(-0.5, 0.5, Y.shape) * delta * hy
+    dx[:, [0, -1]] = 0.0; dy[[0, -1], :] = 0.0
+    dx[[0, -1], :] = 0.0; dy[:, [0, -1]] = 0.0
+    return np.ascontiguousarray(np.stack([X + dx, Y + dy], axis=-1))
+
+
 def make_config_case(cfg: Config, window=None, t=0.0, seed=None) -> dict:
     idx = list(CONFIGS).index(cfg.name) if cfg.name in CONFIGS else 0
     return make_case(cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, kind=cfg.kind,

@@ -645,3 +645,80 @@ def test_oracle_threads_deterministic(ora):
         ora.L.ora_set_threads(n0)
     for k in a:
         np.testing.assert_array_equal(a[k], b[k])
+
+
+# ---------------------------------------------------------------- general (distorted) quads, R#23
+def _dmesh(nx=5, ny=4, lx=5e3, ly=4e3, delta=0.25, p=2, ns=6, na=6, seed=31):
+    V = inputs.distorted_vertices(nx, ny, lx, ly, delta, seed)
+    return Mesh(nx, ny, lx=lx, ly=ly, p=p, ns=ns, na=na, verts=V), V
+
+
+def test_distorted_element_area_is_shoelace(ora):
+    """The Gauss integral of |J| over a bilinear quad equals its polygon (shoelace) area; the
+    total equals the box area (boundary vertices fixed)."""
+    mesh, V = _dmesh()
+    x, w = ora.gauss(3)
+    tot = 0.0
+    for iy in range(mesh.ny):
+        for ix in range(mesh.nx):
+            area = sum(w[a] * w[b] * ora.jacobian(mesh, ix, iy, x[a], x[b])[0] for a in range(3) for b in range(3))
+            q = [V[iy, ix], V[iy, ix + 1], V[iy + 1, ix + 1], V[iy + 1, ix]]
+            shoe = 0.5 * sum(q[i][0] * q[(i + 1) % 4][1] - q[(i + 1) % 4][0] * q[i][1] for i in range(4))
+            assert abs(area - shoe) < 1e-9 * shoe and area > 0
+            tot += area
+    assert abs(tot - mesh.lx * mesh.ly) < 1e-9 * mesh.lx * mesh.ly
+
+
+def test_distorted_stress_rigid_constant(ora):
+    """SPEC S:318 on distorted elements: the projection of a constant is exact for any element
+    mass matrix, so E = 0, H = A = 1, alpha = 2 gives S11 = S11/2 + (-Pstar/4, 0, ...)."""
+    mesh, _ = _dmesh(p=1, ns=3, na=3)
+    N = mesh.n_elem
+    E = [np.zeros((N, 3))] * 3
+    H = np.tile([1.0, 0, 0], (N, 1)); A = H.copy()
+    S = [RNG.uniform(-1, 1, (N, 3)) for _ in range(3)]
+    o11, o12, o22 = ora.stress(mesh, Params(alpha=2.0), *E, H, A, *S)
+    add = np.array([-0.25 * 27500.0, 0, 0])
+    np.testing.assert_allclose(o11, 0.5 * S[0] + add, rtol=1e-13, atol=1e-9)
+    np.testing.assert_allclose(o12, 0.5 * S[1], rtol=1e-13, atol=1e-12)
+
+
+def _node_xy(mesh, V):
+    """Physical positions of the CG nodes: the bilinear map of their reference positions."""
+    p = mesh.p
+    X = np.zeros(mesh.node_shape); Y = np.zeros(mesh.node_shape)
+    for iy in range(mesh.ny):
+        for ix in range(mesh.nx):
+            q = V[iy:iy + 2, ix:ix + 2]
+            for jy in range(p + 1):
+                for jx in range(p + 1):
+                    s, t = jx / p, jy / p
+                    pt = (1 - s) * (1 - t) * q[0, 0] + s * (1 - t) * q[0, 1] + (1 - s) * t * q[1, 0] + s * t * q[1, 1]
+                    X[p * iy + jy, p * ix + jx], Y[p * iy + jy, p * ix + jx] = pt
+    return X, Y
+
+
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+def test_distorted_strain_linear_velocity(ora, p, ns):
+    """A physically linear velocity is reproduced by the (sub)parametric CG space on a bilinear
+    mesh, so E = sym(G) in the constant coefficient and 0 elsewhere."""
+    mesh, V = _dmesh(p=p, ns=ns, na=ns)
+    X, Y = _node_xy(mesh, V)
+    G = np.array([[3e-6, -7e-6], [5e-6, -2e-6]])
+    E11, E12, E22 = ora.strain(mesh, 0.1 + G[0, 0] * X + G[0, 1] * Y, -0.05 + G[1, 0] * X + G[1, 1] * Y)
+    tol = 1e-11 * 1e-5
+    for E, val in ((E11, G[0, 0]), (E22, G[1, 1]), (E12, 0.5 * (G[0, 1] + G[1, 0]))):
+        np.testing.assert_allclose(E[:, 0], val, atol=tol)
+        assert np.abs(E[:, 1:]).max() < tol
+
+
+def test_distorted_stress_scale_invariance(ora):
+    """iMJwPSI = M_K^{-1} [w |J| psi] is invariant under a uniform scaling of the element
+    (|J| cancels): scaling every vertex by 3 leaves the stress update unchanged."""
+    mesh, V = _dmesh()
+    E, H, A, S = _stress_inputs(mesh)
+    a = ora.stress(mesh, Params(), *E, H, A, *S)
+    big = Mesh(mesh.nx, mesh.ny, lx=3 * mesh.lx, ly=3 * mesh.ly, verts=3.0 * V)
+    b = ora.stress(big, Params(), *E, H, A, *S)
+    for x, y in zip(a, b):
+        np.testing.assert_allclose(x, y, rtol=1e-12, atol=1e-12 * np.abs(x).max())
