@@ -153,9 +153,11 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy; default 2)
  *   NXSDG_OPT_STAGES        TMA pipeline depth per warp, 2..4 (default 2)
  *   NXSDG_OPT_DYNAMIC       1 (default): warps claim work units from an atomic counter; 0: static round-robin
+ *   NXSDG_OPT_MAP_MODE      general quads (nxsdg_set_vertices): 0 = per-element iMJwPSI pre-assembled and
+ *                           stored, 1 (default) = recomputed on the fly from the 4 vertices
  * INVALID_ARG for an unknown option or value. */
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
-       NXSDG_OPT_DYNAMIC = 4 };
+       NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */
@@ -172,6 +174,13 @@ nxsdg_status nxsdg_set_forcing(nxsdg_ctx* ctx, const double* ox, const double* o
  * ocean gyre o, cyclone wind a moving at 51.2 km/day; global box coordinates), for multi-outer-step
  * runs without host transfers.  Same effect as nxsdg_set_forcing with those fields. */
 nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* ctx, double t);
+
+/* NEXT-1: switch the context to a general quadrilateral mesh with these vertices,
+ * (ny+1) x (nx+1) x 2 doubles row-major (count = 2 (nx+1)(ny+1)); elements map bilinearly from their
+ * four vertices.  In this mode only nxsdg_run_step(NXSDG_STEP_STRESS) is available
+ * (the paper's stress kernel, Listing 2, with the stored E, H, A, S and per-element inverse maps per
+ * NXSDG_OPT_MAP_MODE); mevp_substeps / advect / other steps return UNSUPPORTED.  Single rank only. */
+nxsdg_status nxsdg_set_vertices(nxsdg_ctx* ctx, const double* xy, int64_t count, nxsdg_mem mem);
 
 /* ---- compute ----------------------------------------------------------------- */
 /* n_sub mEVP subcycles.  flags: NXSDG_BEGIN_STEP, NXSDG_UNFUSED.

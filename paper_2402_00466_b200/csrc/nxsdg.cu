@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "subcycle_tma.cuh"
 #include "advect_q2.cuh"
+#include "general_quads.cuh"
 
 using namespace nxk;
 
@@ -110,6 +111,9 @@ struct nxsdg_ctx {
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
+    double* verts = nullptr; double* gmaps = nullptr;               // NEXT-1 general quads (stress step)
+    bool general = false, gmaps_ready = false;
+    int map_mode = 1;      // 0: iMJwPSI pre-assembled per element, 1: on the fly from the vertices
     cudaStream_t hstream = nullptr;                                 // halo stream (NCCL overlap)
     cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
     K2Maps maps[2][2]; // [cv][cs]
@@ -192,6 +196,8 @@ static void free_all(nxsdg_ctx* c) {
         if (*b) { cudaFree(*b); *b = nullptr; }
     if (c->counters) { cudaFree(c->counters); c->counters = nullptr; c->ncounters = 0; }
     if (c->hstage_send) { cudaFree(c->hstage_send); c->hstage_send = nullptr; }
+    if (c->verts) { cudaFree(c->verts); c->verts = nullptr; }
+    if (c->gmaps) { cudaFree(c->gmaps); c->gmaps = nullptr; }
     if (c->hstage_recv) { cudaFree(c->hstage_recv); c->hstage_recv = nullptr; }
     if (c->ev_bnd) { cudaEventDestroy(c->ev_bnd); c->ev_bnd = nullptr; }
     if (c->ev_x) { cudaEventDestroy(c->ev_x); c->ev_x = nullptr; }
@@ -337,6 +343,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_DYNAMIC:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "dynamic 0|1");
             c->dynamic = (int)value; break;
+        case NXSDG_OPT_MAP_MODE:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "map mode 0|1");
+            c->map_mode = (int)value; break;
         case NXSDG_OPT_STAGES:
             if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
             c->stages = (int)value; break;
@@ -512,6 +521,57 @@ extern "C" nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* c, double t) {
     c->forcing_set = true;
     c->prepped = false;
     return NXSDG_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-1: general quads (stress step)
+extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64_t count, nxsdg_mem mem) {
+    GUARD(c);
+    if (!xy || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE)) return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
+    if (c->d.nranks != 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads are single-rank");
+    const int64_t need = 2 * (int64_t)(c->d.nx + 1) * (c->d.ny + 1);
+    if (count != need) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)need);
+    if (!c->verts) CU(cudaMalloc(&c->verts, need * sizeof(double)));
+    CU(cudaMemcpyAsync(c->verts, xy, need * sizeof(double),
+                       mem == NXSDG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream));
+    if (mem == NXSDG_MEM_HOST) CU(cudaStreamSynchronize(c->stream));
+    c->general = true;
+    c->gmaps_ready = false;
+    return NXSDG_OK;
+}
+
+static GenArgs gen_args(nxsdg_ctx* c) {
+    GenArgs a{};
+    a.verts = c->verts; a.maps = c->gmaps; a.E = c->E; a.S = c->S[c->cs]; a.H = c->H; a.A = c->A;
+    a.eplane = c->eplane; a.epitch = c->epitch; a.nx = c->d.nx; a.ny = c->d.ny;
+    a.ainv = 1.0 / c->prm.alpha; a.fac = 1.0 - a.ainv; a.dmin2 = c->prm.DeltaMin * c->prm.DeltaMin;
+    a.Pstar = c->prm.Pstar; a.C_conc = c->prm.C_conc; a.repl = c->prm.replacement_pressure;
+    return a;
+}
+
+template <int P, int NA>
+static nxsdg_status general_stress_t(nxsdg_ctx* c) {
+    constexpr int NSG = Deg<P>::NS * Deg<P>::NG;
+    if (c->map_mode == 0 && !c->gmaps_ready) {
+        if (!c->gmaps) CU(cudaMalloc(&c->gmaps, (size_t)NSG * c->eplane * sizeof(double)));
+        GenArgs a = gen_args(c);
+        dim3 b(128), g((unsigned)((c->d.nx + 127) / 128), (unsigned)c->d.ny);
+        k_gen_maps<P><<<g, b, 0, c->stream>>>(a);
+        LAUNCHED();
+        c->gmaps_ready = true;
+    }
+    GenArgs a = gen_args(c);
+    dim3 b(128), g((unsigned)((c->d.nx + 127) / 128), (unsigned)c->d.ny);
+    if (c->map_mode == 0) k_stress_general<P, NA, false><<<g, b, 0, c->stream>>>(a);
+    else k_stress_general<P, NA, true><<<g, b, 0, c->stream>>>(a);
+    LAUNCHED();
+    return NXSDG_OK;
+}
+
+static nxsdg_status general_stress(nxsdg_ctx* c) {
+    if (c->P == 1) return c->NA == 1 ? general_stress_t<1, 1>(c) : general_stress_t<1, 3>(c);
+    if (c->NA == 1) return general_stress_t<2, 1>(c);
+    if (c->NA == 3) return general_stress_t<2, 3>(c);
+    return general_stress_t<2, 6>(c);
 }
 
 // ---------------------------------------------------------------- halo exchange
@@ -1004,6 +1064,7 @@ static nxsdg_status begin_step(nxsdg_ctx* c) {
 static nxsdg_status check_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
     if (n < 0 || (flags & ~(uint32_t)(NXSDG_BEGIN_STEP | NXSDG_UNFUSED))) return fail(c, NXSDG_ERR_INVALID_ARG, "bad n/flags");
     if (c->d.bc != NXSDG_BC_CLOSED) return fail(c, NXSDG_ERR_UNSUPPORTED, "mEVP substeps need the closed box");
+    if (c->general) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: only the stress step (NEXT-1)");
     if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
     if (!(flags & NXSDG_BEGIN_STEP) && !c->prepped) return fail(c, NXSDG_ERR_STATE, "first call of an outer step needs NXSDG_BEGIN_STEP");
     return NXSDG_OK;
@@ -1083,11 +1144,15 @@ extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t fl
 extern "C" nxsdg_status nxsdg_run_step(nxsdg_ctx* c, nxsdg_step st) {
     GUARD(c);
     if (st < NXSDG_STEP_STRAIN || st > NXSDG_STEP_VELOCITY) return fail(c, NXSDG_ERR_INVALID_ARG, "bad step");
-    if ((st == NXSDG_STEP_STRESS || st == NXSDG_STEP_VELOCITY) && !c->prepped)
+    if (st == NXSDG_STEP_VELOCITY && !c->prepped)
         return fail(c, NXSDG_ERR_STATE, "needs a BEGIN_STEP (nxsdg_mevp_substeps(ctx, 0, NXSDG_BEGIN_STEP))");
     if (c->d.nranks > 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "debug steps are single-rank");
     nxsdg_status s = ensure_debug_buffers(c);
     if (s) return s;
+    if (c->general) {
+        if (st != NXSDG_STEP_STRESS) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: only the stress step");
+        return general_stress(c);
+    }
     return launch_step(c, st);
 }
 
@@ -1153,6 +1218,7 @@ static nxsdg_status advect_finish(nxsdg_ctx* c) {
 extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
     GUARD(c);
     if (!(dt >= 0.0)) return fail(c, NXSDG_ERR_INVALID_ARG, "dt < 0");
+    if (c->general) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: only the stress step (NEXT-1)");
     if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_LOOPBACK)
         return fail(c, NXSDG_ERR_STATE, "loopback ranks advect through nxsdg_group_advect");
     nxsdg_status s;

@@ -29,7 +29,7 @@ CG_FIELDS = {"vx", "vy", "Fx", "Fy"}
 BEGIN_STEP, UNFUSED = 1, 2
 STEPS = {"strain": 0, "stress": 1, "divergence": 2, "velocity": 3}
 TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1, 2
-OPT_FUSED_KERNEL, OPT_CHUNK_ROWS, OPT_CTAS_PER_SM, OPT_STAGES, OPT_DYNAMIC = 0, 1, 2, 3, 4
+OPT_FUSED_KERNEL, OPT_CHUNK_ROWS, OPT_CTAS_PER_SM, OPT_STAGES, OPT_DYNAMIC, OPT_MAP_MODE = 0, 1, 2, 3, 4, 5
 
 
 class NxsdgError(RuntimeError):
@@ -83,6 +83,7 @@ def _load() -> C.CDLL:
         "nxsdg_stream": ([vp], vp),
         "nxsdg_set_option": ([vp, i32, i64], i32),
         "nxsdg_set_forcing_cyclone": ([vp, dbl], i32),
+        "nxsdg_set_vertices": ([vp, vp, i64, i32], i32),
         "nxsdg_halo_plan": ([i32, i32, i32, i32, i32, i32, i32, u32, vp, i32, C.POINTER(i32)], i32),
         "nxsdg_local_geometry": ([i32, i32, i32, i32, i32, i32, i32, C.POINTER(i64)], i32),
     }
@@ -100,7 +101,7 @@ EXPORTED = [
     "nxsdg_mevp_substeps", "nxsdg_advect", "nxsdg_run_step", "nxsdg_synchronize", "nxsdg_nccl_unique_id",
     "nxsdg_loopback_connect", "nxsdg_group_mevp_substeps", "nxsdg_group_advect", "nxsdg_kernel_launches",
     "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option", "nxsdg_halo_plan",
-    "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone",
+    "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone", "nxsdg_set_vertices",
 ]
 HALO_V, HALO_S, HALO_AH, HALO_AH_SCR0, HALO_AH_SCR1 = 1, 2, 4, 8, 16
 HF_VX, HF_VY, HF_S, HF_A, HF_H, HF_A_SCR0, HF_H_SCR0, HF_A_SCR1, HF_H_SCR1 = range(9)
@@ -262,6 +263,10 @@ class Mesh:
         if len({(n, m) for _, n, m in ps}) != 1:
             raise ValueError("forcing arrays must match in size and memory kind")
         _chk(self.h, lib.nxsdg_set_forcing(self.h, *[p for p, _, _ in ps], ps[0][1], ps[0][2]), "set_forcing")
+
+    def set_vertices(self, xy):
+        p, n, mem = _ptr_mem(xy)
+        _chk(self.h, lib.nxsdg_set_vertices(self.h, p, n, mem), "set_vertices")
 
     def set_forcing_cyclone(self, t: float):
         _chk(self.h, lib.nxsdg_set_forcing_cyclone(self.h, float(t)), "set_forcing_cyclone")

@@ -215,6 +215,40 @@ def test_device_cyclone_forcing_equals_host_recipe(nx):
     assert max(e.values()) < 1e-13, e
 
 
+@pytest.mark.parametrize("p,ns,na", [(2, 6, 6), (1, 3, 3), (2, 6, 1)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_general_quads_stress(nx, ora, p, ns, na, mode):
+    """NEXT-1: Listing 2 on a distorted quad mesh with per-element inverse maps pre-assembled
+    (mode 0) or recomputed on the fly from the vertices (mode 1), two updates."""
+    nxe, nye, lx, ly = 45, 38, 45e3, 38e3
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.28)
+    r = np.random.default_rng(17)
+    N = nxe * nye
+    E = [r.normal(0, 1e-6, (N, ns)) for _ in range(3)]
+    H = r.uniform(-0.1, 0.1, (N, na)); H[:, 0] = r.uniform(0.2, 2.0, N)
+    A = r.uniform(-0.1, 0.1, (N, na)); A[:, 0] = r.uniform(0.7, 1.05, N)
+    S = [r.uniform(-1e4, 1e4, (N, ns)) for _ in range(3)]
+    prm = nx.PhysParams(alpha=40.0)
+    with nx.Mesh(nxe, nye, lx, ly, p, ns, na, params=prm) as m:
+        m.set_vertices(V)
+        m.set_option(nx.OPT_MAP_MODE, mode)
+        for k, v in zip(("E11", "E12", "E22", "H", "A", "S11", "S12", "S22"), (*E, H, A, *S)):
+            m.write_state(k, np.ascontiguousarray(v))
+        m.run_step("stress"); m.run_step("stress")
+        got = dict(zip(("S11", "S12", "S22"), (m.read_state(k) for k in ("S11", "S12", "S22"))))
+        with pytest.raises(nx.NxsdgError) as ex:
+            m.mevp_substeps(1)
+        assert ex.value.status in (nx.ERR_UNSUPPORTED, nx.ERR_STATE)
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=p, ns=ns, na=na, verts=V)
+    ref = ora.stress(om, ora_params(prm), *E, H, A, *S)
+    ref = ora.stress(om, ora_params(prm), *E, H, A, *ref)
+    from tests.parity import group_err
+    e = group_err(got, dict(zip(("S11", "S12", "S22"), ref)), ("S11", "S12", "S22"))
+    de = group_err({k: got[k] - s0 for k, s0 in zip(("S11", "S12", "S22"), S)},
+                   {k: r_ - s0 for k, r_, s0 in zip(("S11", "S12", "S22"), ref, S)}, ("S11", "S12", "S22"))
+    assert e < 1e-12 and de < 1e-12, (e, de)
+
+
 def test_debug_steps_each_against_oracle(nx, ora):
     """Each Table 1 step alone (unfused kernels via nxsdg_run_step) against the oracle's step."""
     nxe, nye, p, ns, na = 33, 35, 2, 6, 6
