@@ -266,11 +266,15 @@ def main():
     peak, peak_src = measured_peak_hbm()
     traffic = ncu_traffic_per_launch()
 
-    # e2e: the same metric through the C ABI with pinned HOST buffers, copies inside the timed region
+    # e2e: the same metric through the C ABI with pinned HOST buffers, copies inside the timed region.
+    # The model state (v, S, A, H) lives on the device across outer steps; each outer step's external
+    # input is the forcing F (ocean current o, wind a), uploaded with nxsdg_set_forcing from
+    # pinned host memory, and its result is read back (v, nxsdg_read_state) - DESIGN.md §6.
     e2e = None
     if args.e2e_steps > 0:
-        pinned = {k: torch.from_numpy(v).pin_memory() for k, v in st.items()}
-        outv = {k: torch.empty(pinned[k].shape, dtype=torch.float64).pin_memory() for k in ("vx", "vy")}
+        fkeys = ("ox", "oy", "ax", "ay")
+        pinned = {k: torch.from_numpy(st[k]).pin_memory() for k in fkeys}
+        outv = {k: torch.empty(st[k].shape, dtype=torch.float64).pin_memory() for k in ("vx", "vy")}
         h2d = sum(v.numel() * 8 for v in pinned.values())
         d2h = sum(v.numel() * 8 for v in outv.values())
         barrier()
@@ -278,7 +282,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            m.load(pinned)
+            m.set_forcing(*(pinned[k] for k in fkeys))
             step()
             for k in ("vx", "vy"):
                 m.read_state(k, outv[k])
@@ -291,6 +295,7 @@ def main():
             ems = t.item()
         e2e = {"value": n_el * cfg.nsub * args.e2e_steps / (ems * 1e-3), "unit": "element-updates/s",
                "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
+               "h2d": "forcing o, a (pinned host -> nxsdg_set_forcing)", "d2h": "velocity v (nxsdg_read_state)",
                "steps": args.e2e_steps, "wall_s": time.perf_counter() - te}
 
     cpu = None

@@ -177,9 +177,10 @@ nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* ctx, double t);
 
 /* NEXT-1: switch the context to a general quadrilateral mesh with these vertices,
  * (ny+1) x (nx+1) x 2 doubles row-major (count = 2 (nx+1)(ny+1)); elements map bilinearly from their
- * four vertices.  In this mode only nxsdg_run_step(NXSDG_STEP_STRESS) is available
- * (the paper's stress kernel, Listing 2, with the stored E, H, A, S and per-element inverse maps per
- * NXSDG_OPT_MAP_MODE); mevp_substeps / advect / other steps return UNSUPPORTED.  Single rank only. */
+ * four vertices.  In this mode the stress step (Listing 2) uses per-element inverse
+ * maps per NXSDG_OPT_MAP_MODE, every nxsdg_run_step step and nxsdg_advect (closed box) run the
+ * general-geometry kernels, and nxsdg_mevp_substeps requires NXSDG_UNFUSED (the fused kernels are
+ * box-specialised: UNSUPPORTED otherwise).  Single rank only. */
 nxsdg_status nxsdg_set_vertices(nxsdg_ctx* ctx, const double* xy, int64_t count, nxsdg_mem mem);
 
 /* ---- compute ----------------------------------------------------------------- */

@@ -50,9 +50,8 @@ __device__ __forceinline__ void gen_wdet(double c0, double d1, double d2, double
 // M = c0 D + d1 M_S + d2 M_T, D = diag(1, 1/12, 1/12, 1/180, 1/180, 1/144), M_S couples
 // (0,1) 1/12, (1,3) 1/180, (2,5) 1/144 and M_T (0,2) 1/12, (2,4) 1/180, (1,5) 1/144 (exact
 // moments of the centred Legendre family; the Gauss rule integrates them exactly).
-template <int P>
-__device__ __forceinline__ void gen_mass_chol(double c0, double d1, double d2, double (&L)[Deg<P>::NS * (Deg<P>::NS + 1) / 2]) {
-    constexpr int NS = Deg<P>::NS;
+template <int NS>
+__device__ __forceinline__ void gen_mass_chol_n(double c0, double d1, double d2, double (&L)[NS * (NS + 1) / 2]) {
     const double D[6] = {1.0, 1.0 / 12.0, 1.0 / 12.0, 1.0 / 180.0, 1.0 / 180.0, 1.0 / 144.0};
     auto Mij = [&](int i, int j) -> double {   // lower triangle, indices are compile-time after unrolling
         if (i == j) return c0 * D[i];
@@ -84,6 +83,11 @@ __device__ __forceinline__ void gen_mass_chol(double c0, double d1, double d2, d
         }
     }
 }
+template <int P>
+__device__ __forceinline__ void gen_mass_chol(double c0, double d1, double d2, double (&L)[Deg<P>::NS * (Deg<P>::NS + 1) / 2]) {
+    gen_mass_chol_n<Deg<P>::NS>(c0, d1, d2, L);
+}
+
 template <int NS>
 __device__ __forceinline__ void chol_solve(const double (&L)[NS * (NS + 1) / 2], double (&b)[NS]) {
 #pragma unroll

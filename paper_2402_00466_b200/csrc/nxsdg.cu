@@ -24,6 +24,7 @@
 #include "subcycle_tma.cuh"
 #include "advect_q2.cuh"
 #include "general_quads.cuh"
+#include "general_steps.cuh"
 
 using namespace nxk;
 
@@ -113,6 +114,7 @@ struct nxsdg_ctx {
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
     double* verts = nullptr; double* gmaps = nullptr;               // NEXT-1 general quads (stress step)
     bool general = false, gmaps_ready = false;
+    double* mlump = nullptr; double* gcontrib = nullptr;           // general quads: lumped masses, div scratch
     int map_mode = 1;      // 0: iMJwPSI pre-assembled per element, 1: on the fly from the vertices
     cudaStream_t hstream = nullptr;                                 // halo stream (NCCL overlap)
     cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
@@ -198,6 +200,8 @@ static void free_all(nxsdg_ctx* c) {
     if (c->hstage_send) { cudaFree(c->hstage_send); c->hstage_send = nullptr; }
     if (c->verts) { cudaFree(c->verts); c->verts = nullptr; }
     if (c->gmaps) { cudaFree(c->gmaps); c->gmaps = nullptr; }
+    if (c->mlump) { cudaFree(c->mlump); c->mlump = nullptr; }
+    if (c->gcontrib) { cudaFree(c->gcontrib); c->gcontrib = nullptr; }
     if (c->hstage_recv) { cudaFree(c->hstage_recv); c->hstage_recv = nullptr; }
     if (c->ev_bnd) { cudaEventDestroy(c->ev_bnd); c->ev_bnd = nullptr; }
     if (c->ev_x) { cudaEventDestroy(c->ev_x); c->ev_x = nullptr; }
@@ -524,6 +528,45 @@ extern "C" nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* c, double t) {
 }
 
 // ---------------------------------------------------------------- NEXT-1: general quads (stress step)
+static nxsdg_status ensure_debug_buffers(nxsdg_ctx* c);
+
+static GenStepArgs gen_step_args(nxsdg_ctx* c) {
+    GenStepArgs a{};
+    a.verts = c->verts;
+    a.vx_in = c->vx[c->cv]; a.vy_in = c->vy[c->cv]; a.vx_out = c->vx[c->cv ^ 1]; a.vy_out = c->vy[c->cv ^ 1];
+    a.S = c->S[c->cs]; a.E = c->E; a.Fx = c->Fx; a.Fy = c->Fy; a.contrib = c->gcontrib; a.mlump = c->mlump;
+    a.H = c->H; a.A = c->A;
+    a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.ox = c->ox; a.oy = c->oy;
+    a.eplane = c->eplane; a.epitch = c->epitch; a.npitch = c->npitch; a.nx = c->d.nx; a.ny = c->d.ny;
+    a.beta = c->prm.beta; a.b1 = 1.0 + c->prm.beta; a.kc = c->prm.dt * c->prm.f_c;
+    return a;
+}
+
+// one unfused step on the general mesh (strain / divergence / velocity; stress is general_stress)
+static nxsdg_status general_step(nxsdg_ctx* c, nxsdg_step st) {
+    GenStepArgs a = gen_step_args(c);
+    dim3 be(128), ge((unsigned)((c->d.nx + 127) / 128), (unsigned)c->d.ny);
+    dim3 bn(128), gn((unsigned)((c->P * c->d.nx + 1 + 127) / 128), (unsigned)(c->P * c->d.ny + 1));
+    const bool p1 = c->P == 1;
+    switch (st) {
+        case NXSDG_STEP_STRAIN:
+            if (p1) k_strain_gen<1><<<ge, be, 0, c->stream>>>(a); else k_strain_gen<2><<<ge, be, 0, c->stream>>>(a);
+            break;
+        case NXSDG_STEP_DIVERGENCE:
+            if (p1) k_div_contrib_gen<1><<<ge, be, 0, c->stream>>>(a); else k_div_contrib_gen<2><<<ge, be, 0, c->stream>>>(a);
+            LAUNCHED();
+            if (p1) k_div_gather_gen<1><<<gn, bn, 0, c->stream>>>(a); else k_div_gather_gen<2><<<gn, bn, 0, c->stream>>>(a);
+            break;
+        case NXSDG_STEP_VELOCITY:
+            if (p1) k_velocity_gen<1><<<gn, bn, 0, c->stream>>>(a); else k_velocity_gen<2><<<gn, bn, 0, c->stream>>>(a);
+            break;
+        default: return fail(c, NXSDG_ERR_INVALID_ARG, "bad step");
+    }
+    LAUNCHED();
+    if (st == NXSDG_STEP_VELOCITY) c->cv ^= 1;
+    return NXSDG_OK;
+}
+
 extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64_t count, nxsdg_mem mem) {
     GUARD(c);
     if (!xy || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE)) return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
@@ -536,6 +579,16 @@ extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64
     if (mem == NXSDG_MEM_HOST) CU(cudaStreamSynchronize(c->stream));
     c->general = true;
     c->gmaps_ready = false;
+    nxsdg_status st = ensure_debug_buffers(c);
+    if (st) return st;
+    const size_t nn = (size_t)c->npitch * c->nrows_local;
+    if (!c->mlump) CU(cudaMalloc(&c->mlump, nn * sizeof(double)));
+    if (!c->gcontrib) CU(cudaMalloc(&c->gcontrib, (size_t)2 * (c->P + 1) * (c->P + 1) * c->eplane * sizeof(double)));
+    GenStepArgs a = gen_step_args(c);
+    dim3 b(128), g((unsigned)((c->P * c->d.nx + 1 + 127) / 128), (unsigned)(c->P * c->d.ny + 1));
+    if (c->P == 1) k_gen_lumped<1><<<g, b, 0, c->stream>>>(a);
+    else k_gen_lumped<2><<<g, b, 0, c->stream>>>(a);
+    LAUNCHED();
     return NXSDG_OK;
 }
 
@@ -1064,7 +1117,8 @@ static nxsdg_status begin_step(nxsdg_ctx* c) {
 static nxsdg_status check_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
     if (n < 0 || (flags & ~(uint32_t)(NXSDG_BEGIN_STEP | NXSDG_UNFUSED))) return fail(c, NXSDG_ERR_INVALID_ARG, "bad n/flags");
     if (c->d.bc != NXSDG_BC_CLOSED) return fail(c, NXSDG_ERR_UNSUPPORTED, "mEVP substeps need the closed box");
-    if (c->general) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: only the stress step (NEXT-1)");
+    if (c->general && !(flags & NXSDG_UNFUSED) && n > 0)
+        return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: the subcycle runs unfused (NXSDG_UNFUSED)");
     if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
     if (!(flags & NXSDG_BEGIN_STEP) && !c->prepped) return fail(c, NXSDG_ERR_STATE, "first call of an outer step needs NXSDG_BEGIN_STEP");
     return NXSDG_OK;
@@ -1078,6 +1132,12 @@ static nxsdg_status one_subcycle(nxsdg_ctx* c, bool unfused) {
         return halo(c, NXSDG_HALO_V | NXSDG_HALO_S);
     }
     if ((s = ensure_debug_buffers(c))) return s;
+    if (c->general) {
+        if ((s = general_step(c, NXSDG_STEP_STRAIN))) return s;
+        if ((s = general_stress(c))) return s;
+        if ((s = general_step(c, NXSDG_STEP_DIVERGENCE))) return s;
+        return general_step(c, NXSDG_STEP_VELOCITY);
+    }
     if ((s = launch_step(c, NXSDG_STEP_STRAIN))) return s;
     if ((s = launch_step(c, NXSDG_STEP_STRESS))) return s;
     if ((s = halo(c, NXSDG_HALO_S))) return s;
@@ -1149,10 +1209,7 @@ extern "C" nxsdg_status nxsdg_run_step(nxsdg_ctx* c, nxsdg_step st) {
     if (c->d.nranks > 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "debug steps are single-rank");
     nxsdg_status s = ensure_debug_buffers(c);
     if (s) return s;
-    if (c->general) {
-        if (st != NXSDG_STEP_STRESS) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: only the stress step");
-        return general_stress(c);
-    }
+    if (c->general) return st == NXSDG_STEP_STRESS ? general_stress(c) : general_step(c, st);
     return launch_step(c, st);
 }
 
@@ -1170,7 +1227,10 @@ static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const d
     a.ihx = 1.0 / (c->d.lx / c->d.nx); a.ihy = 1.0 / (c->d.ly / c->d.ny);
     a.dt = dt; a.a0 = a0; a.a1 = a1;
     dim3 b(32, ADV_ROWS), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + ADV_ROWS - 1) / ADV_ROWS));
-    if (P == 2 && NA == 6 && c->variant == 0) k_advect_q2<<<g, b, 0, c->stream>>>(a);   // structured
+    if (c->general) {
+        GenAdvArgs ga{a, c->verts, c->d.ny};
+        k_advect_gen<P, NA><<<g, b, 0, c->stream>>>(ga);
+    } else if (P == 2 && NA == 6 && c->variant == 0) k_advect_q2<<<g, b, 0, c->stream>>>(a);   // structured
     else k_advect<P, NA><<<g, b, 0, c->stream>>>(a);
     LAUNCHED();
     return NXSDG_OK;
@@ -1218,7 +1278,7 @@ static nxsdg_status advect_finish(nxsdg_ctx* c) {
 extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
     GUARD(c);
     if (!(dt >= 0.0)) return fail(c, NXSDG_ERR_INVALID_ARG, "dt < 0");
-    if (c->general) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: only the stress step (NEXT-1)");
+    if (c->general && c->d.bc != NXSDG_BC_CLOSED) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: closed box only");
     if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_LOOPBACK)
         return fail(c, NXSDG_ERR_STATE, "loopback ranks advect through nxsdg_group_advect");
     nxsdg_status s;

@@ -237,7 +237,7 @@ def test_general_quads_stress(nx, ora, p, ns, na, mode):
         m.run_step("stress"); m.run_step("stress")
         got = dict(zip(("S11", "S12", "S22"), (m.read_state(k) for k in ("S11", "S12", "S22"))))
         with pytest.raises(nx.NxsdgError) as ex:
-            m.mevp_substeps(1)
+            m.mevp_substeps(1)     # fused subcycle on a general mesh
         assert ex.value.status in (nx.ERR_UNSUPPORTED, nx.ERR_STATE)
     om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=p, ns=ns, na=na, verts=V)
     ref = ora.stress(om, ora_params(prm), *E, H, A, *S)
@@ -247,6 +247,55 @@ def test_general_quads_stress(nx, ora, p, ns, na, mode):
     de = group_err({k: got[k] - s0 for k, s0 in zip(("S11", "S12", "S22"), S)},
                    {k: r_ - s0 for k, r_, s0 in zip(("S11", "S12", "S22"), ref, S)}, ("S11", "S12", "S22"))
     assert e < 1e-12 and de < 1e-12, (e, de)
+
+
+@pytest.mark.parametrize("p,ns,na,nsub", [(2, 6, 6, 1), (2, 6, 6, 12), (1, 3, 3, 1), (1, 3, 3, 10), (2, 6, 3, 5)])
+def test_general_quads_outer_step(nx, ora, p, ns, na, nsub):
+    """NEXT-1: advection + prep + unfused mEVP subcycles on a distorted mesh vs the oracle with the
+    same vertices (1 subcycle: 1e-12; several: 1e-10)."""
+    nxe, nye, lx, ly = 37, 33, 37e3, 33e3
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.28)
+    st = case(nxe, nye, p, ns, na, "random", lx, ly)
+    prm = nx.PhysParams(alpha=300.0, beta=300.0)
+    with nx.Mesh(nxe, nye, lx, ly, p, ns, na, params=prm) as m:
+        m.set_vertices(V)
+        m.load(st)
+        m.advect(prm.dt)
+        m.mevp_substeps(nsub, begin_step=True, unfused=True)
+        got = m.state()
+        with pytest.raises(nx.NxsdgError):
+            m.mevp_substeps(1, begin_step=False, unfused=False)   # the fused kernels are box-only
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=p, ns=ns, na=na, verts=V)
+    ref = ora.outer_step(om, ora_params(prm), nsub, st, do_advect=True)
+    _check(got, ref, st, TOL1 if nsub == 1 else TOLN, groups=("S", "v", "A", "H"))
+
+
+def test_general_quads_steps_each(nx, ora):
+    """NEXT-1: strain, divergence and velocity alone on a distorted mesh vs the oracle."""
+    nxe, nye, lx, ly = 29, 31, 29e3, 31e3
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.28)
+    st = case(nxe, nye, 2, 6, 6, "random", lx, ly)
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, verts=V)
+    prm = nx.PhysParams()
+    from tests.parity import group_err
+    with nx.Mesh(nxe, nye, lx, ly) as m:
+        m.set_vertices(V)
+        m.load(st)
+        m.mevp_substeps(0, begin_step=True)
+        m.run_step("strain")
+        E = {k: m.read_state(k) for k in ("E11", "E12", "E22")}
+        rE = dict(zip(("E11", "E12", "E22"), ora.strain(om, st["vx"], st["vy"])))
+        assert group_err(E, rE, ("E11", "E12", "E22")) < 1e-12
+        m.run_step("divergence")
+        F = {"Fx": m.read_state("Fx"), "Fy": m.read_state("Fy")}
+        rF = dict(zip(("Fx", "Fy"), ora.divergence(om, st["S11"], st["S12"], st["S22"])))
+        assert group_err(F, rF, ("Fx", "Fy")) < 1e-12
+        m.run_step("velocity")
+        v = m.state(("vx", "vy"))
+        Hn, An = ora.prep(om, st["H"], st["A"])
+        rv = ora.velocity(om, ora_params(prm), rF["Fx"], rF["Fy"], ora.lumped_mass(om), Hn, An, st["vx"], st["vy"],
+                          st["ox"], st["oy"], st["ax"], st["ay"], st["vx"], st["vy"])
+        assert group_err(v, {"vx": rv[0], "vy": rv[1]}, ("vx", "vy")) < 1e-12
 
 
 def test_debug_steps_each_against_oracle(nx, ora):
