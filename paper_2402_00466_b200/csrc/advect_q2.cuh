@@ -86,6 +86,12 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_q2(AdvArgs a) {
     const int ixc = valid ? ix : 0, lrc = valid ? lr : a.erow_begin;
     const int64_t e = (int64_t)lrc * a.epitch + ixc;
     Cf<6> me; load_coef<2, 6>(a, e, me);
+    // RK combine input c0 (stages 2, 3): loaded up front so its latency overlaps the compute
+    double c0A[6], c0H[6];
+    if (a.a0 != 0.0) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) { c0A[k] = a.A0[k * a.eplane + e]; c0H[k] = a.H0[k * a.eplane + e]; }
+    }
     double ux[3][3], uy[3][3];
 #pragma unroll
     for (int jy = 0; jy < 3; ++jy)
@@ -188,11 +194,11 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_q2(AdvArgs a) {
         L[0] += a.ihy * m0; L[1] += a.ihy * m1; L[2] -= a.ihy * 0.5 * m0; L[3] += a.ihy * m2;
         L[4] += a.ihy * m0 * (1.0 / 6.0); L[5] -= a.ihy * 0.5 * m1;
         double* out = tr == 0 ? a.Aout : a.Hout;
-        const double* c0 = tr == 0 ? a.A0 : a.H0;
+        const double* c0 = tr == 0 ? c0A : c0H;
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
             const double v = a.a1 * fma(a.dt, L[k] * mr[k], c[k]);
-            out[k * a.eplane + eo] = (a.a0 != 0.0) ? fma(a.a0, c0[k * a.eplane + eo], v) : v;
+            out[k * a.eplane + eo] = (a.a0 != 0.0) ? fma(a.a0, c0[k], v) : v;
         }
     }
 }
