@@ -193,11 +193,15 @@ def main():
     if args.impl == "reference":
         return run_reference(args, cfg)
 
+    rank, local = _env_int("RANK", 0), _env_int("LOCAL_RANK", 0)
+    if os.environ.get("NXSDG_NCCL_HOSTID_PER_RANK"):
+        # test knob: several ranks on one GPU look like separate hosts to NCCL (socket transport)
+        os.environ["NCCL_HOSTID"] = f"nxsdg-rank{rank}"
     import torch
     import torch.distributed as dist
     from paper_2402_00466_b200 import nxsdg
 
-    rank, local = _env_int("RANK", 0), _env_int("LOCAL_RANK", 0)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
