@@ -63,7 +63,12 @@ typedef enum {
     NXSDG_ERR_OOM = 6          /* device allocation failed                           */
 } nxsdg_status;
 
-typedef enum { NXSDG_MEM_HOST = 0, NXSDG_MEM_DEVICE = 1 } nxsdg_mem;
+/* HOST_ASYNC: pinned host memory, copied on the context's copy stream; the call returns at once and
+ * the caller keeps the buffer unchanged until nxsdg_synchronize.  Accepted by nxsdg_set_forcing (the
+ * forcing is staged and takes effect at the next BEGIN_STEP, so the upload of step k+1's forcing
+ * overlaps step k) and by nxsdg_read_state for NXSDG_VX / NXSDG_VY (a snapshot of v at that point in
+ * the stream, read back while later work runs). */
+typedef enum { NXSDG_MEM_HOST = 0, NXSDG_MEM_DEVICE = 1, NXSDG_MEM_HOST_ASYNC = 2 } nxsdg_mem;
 
 typedef enum {
     NXSDG_BC_CLOSED = 0,   /* v = 0 on the box boundary, zero advective boundary flux (R#16)   */
@@ -195,7 +200,9 @@ nxsdg_status nxsdg_advect(nxsdg_ctx* ctx, double dt);
 /* Debug: one unfused step on the current state (needs BEGIN_STEP for STRESS/VELOCITY). */
 nxsdg_status nxsdg_run_step(nxsdg_ctx* ctx, nxsdg_step step);
 
-nxsdg_status nxsdg_synchronize(nxsdg_ctx* ctx);
+nxsdg_status nxsdg_synchronize(nxsdg_ctx* ctx);   /* waits for the context stream and the copy stream */
+/* Make the context stream wait for every HOST_ASYNC copy issued so far (stream-ordered join). */
+nxsdg_status nxsdg_stream_join(nxsdg_ctx* ctx);
 
 /* ---- multi-rank plumbing ------------------------------------------------------- */
 /* Fill 128 bytes with a fresh ncclUniqueId (rank 0; broadcast it to the others). */

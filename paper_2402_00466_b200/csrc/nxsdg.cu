@@ -113,6 +113,13 @@ struct nxsdg_ctx {
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
     double* verts = nullptr; double* gmaps = nullptr;               // NEXT-1 general quads (stress step)
+    // NXSDG_MEM_HOST_ASYNC: copies on a copy stream, forcing staged until the next BEGIN_STEP
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_fup = nullptr, ev_fcons = nullptr, ev_vsnap[2] = {nullptr, nullptr}, ev_vdone[2] = {nullptr, nullptr};
+    cudaEvent_t ev_cjoin = nullptr;
+    double* fstage[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* vsnap[2] = {nullptr, nullptr};
+    bool fpending = false;
     bool general = false, gmaps_ready = false;
     double* mlump = nullptr; double* gcontrib = nullptr;           // general quads: lumped masses, div scratch
     int map_mode = 1;      // 0: iMJwPSI pre-assembled per element, 1: on the fly from the vertices
@@ -199,6 +206,16 @@ static void free_all(nxsdg_ctx* c) {
     if (c->counters) { cudaFree(c->counters); c->counters = nullptr; c->ncounters = 0; }
     if (c->hstage_send) { cudaFree(c->hstage_send); c->hstage_send = nullptr; }
     if (c->verts) { cudaFree(c->verts); c->verts = nullptr; }
+    for (int k = 0; k < 4; ++k) if (c->fstage[k]) { cudaFree(c->fstage[k]); c->fstage[k] = nullptr; }
+    for (int k = 0; k < 2; ++k) {
+        if (c->vsnap[k]) { cudaFree(c->vsnap[k]); c->vsnap[k] = nullptr; }
+        if (c->ev_vsnap[k]) { cudaEventDestroy(c->ev_vsnap[k]); c->ev_vsnap[k] = nullptr; }
+        if (c->ev_vdone[k]) { cudaEventDestroy(c->ev_vdone[k]); c->ev_vdone[k] = nullptr; }
+    }
+    if (c->ev_fup) { cudaEventDestroy(c->ev_fup); c->ev_fup = nullptr; }
+    if (c->ev_fcons) { cudaEventDestroy(c->ev_fcons); c->ev_fcons = nullptr; }
+    if (c->ev_cjoin) { cudaEventDestroy(c->ev_cjoin); c->ev_cjoin = nullptr; }
+    if (c->cstream) { cudaStreamDestroy(c->cstream); c->cstream = nullptr; }
     if (c->gmaps) { cudaFree(c->gmaps); c->gmaps = nullptr; }
     if (c->mlump) { cudaFree(c->mlump); c->mlump = nullptr; }
     if (c->gcontrib) { cudaFree(c->gcontrib); c->gcontrib = nullptr; }
@@ -455,8 +472,29 @@ extern "C" nxsdg_status nxsdg_write_state(nxsdg_ctx* c, nxsdg_field f, const dou
     return NXSDG_OK;
 }
 
+static nxsdg_status ensure_async(nxsdg_ctx* c);
+
 extern "C" nxsdg_status nxsdg_read_state(nxsdg_ctx* c, nxsdg_field f, double* dst, int64_t count, nxsdg_mem mem) {
     GUARD(c);
+    if (mem == NXSDG_MEM_HOST_ASYNC) {
+        if (!dst || (f != NXSDG_VX && f != NXSDG_VY)) return fail(c, NXSDG_ERR_INVALID_ARG, "HOST_ASYNC reads: vx, vy");
+        const int64_t rows = owned_node_rows(c), cols = (int64_t)c->P * c->d.nx + 1;
+        if (count != rows * cols) return fail(c, NXSDG_ERR_INVALID_ARG, "count mismatch");
+        nxsdg_status s = ensure_async(c);
+        if (s) return s;
+        const int k = f == NXSDG_VX ? 0 : 1;
+        const size_t nn = (size_t)c->npitch * c->nrows_local;
+        if (!c->vsnap[k] && (s = alloc(c, &c->vsnap[k], nn))) return s;
+        // snapshot on the context stream (after the work issued so far), D2H on the copy stream
+        CU(cudaStreamWaitEvent(c->stream, c->ev_vdone[k], 0));
+        CU(cudaMemcpyAsync(c->vsnap[k], cg_base(c, f), nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        CU(cudaEventRecord(c->ev_vsnap[k], c->stream));
+        CU(cudaStreamWaitEvent(c->cstream, c->ev_vsnap[k], 0));
+        CU(cudaMemcpy2DAsync(dst, cols * sizeof(double), c->vsnap[k] + (size_t)c->P * c->glo * c->npitch,
+                             c->npitch * sizeof(double), cols * sizeof(double), rows, cudaMemcpyDeviceToHost, c->cstream));
+        CU(cudaEventRecord(c->ev_vdone[k], c->cstream));
+        return NXSDG_OK;
+    }
     if (!dst || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE) || f < 0 || f >= NXSDG_NFIELDS)
         return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
     if (is_dg(f)) {
@@ -492,14 +530,64 @@ extern "C" nxsdg_status nxsdg_read_state(nxsdg_ctx* c, nxsdg_field f, double* ds
     return NXSDG_OK;
 }
 
+static nxsdg_status ensure_async(nxsdg_ctx* c) {
+    if (c->cstream) return NXSDG_OK;
+    CU(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    cudaEvent_t* evs[] = {&c->ev_fup, &c->ev_fcons, &c->ev_vsnap[0], &c->ev_vsnap[1], &c->ev_vdone[0], &c->ev_vdone[1], &c->ev_cjoin};
+    for (auto e : evs) CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return NXSDG_OK;
+}
+
+// BEGIN_STEP: bring a staged (HOST_ASYNC) forcing into place on the context stream
+static nxsdg_status consume_forcing(nxsdg_ctx* c) {
+    if (!c->fpending) return NXSDG_OK;
+    CU(cudaStreamWaitEvent(c->stream, c->ev_fup, 0));
+    const size_t bytes = (size_t)c->npitch * c->nrows_local * sizeof(double);
+    CU(cudaMemcpyAsync(c->ox, c->fstage[0], bytes, cudaMemcpyDeviceToDevice, c->stream));   // o lives in the
+    CU(cudaMemcpyAsync(c->oy, c->fstage[1], bytes, cudaMemcpyDeviceToDevice, c->stream));   // node-constant tensor
+    std::swap(c->ax, c->fstage[2]);
+    std::swap(c->ay, c->fstage[3]);
+    CU(cudaEventRecord(c->ev_fcons, c->stream));
+    c->fpending = false;
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_stream_join(nxsdg_ctx* c) {
+    GUARD(c);
+    if (!c->cstream) return NXSDG_OK;
+    CU(cudaEventRecord(c->ev_cjoin, c->cstream));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_cjoin, 0));
+    return NXSDG_OK;
+}
+
 extern "C" nxsdg_status nxsdg_set_forcing(nxsdg_ctx* c, const double* ox, const double* oy, const double* ax,
                                           const double* ay, int64_t count, nxsdg_mem mem) {
     GUARD(c);
-    if (!ox || !oy || !ax || !ay || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE))
+    if (!ox || !oy || !ax || !ay || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE && mem != NXSDG_MEM_HOST_ASYNC))
         return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
     const int64_t need = owned_node_rows(c) * ((int64_t)c->P * c->d.nx + 1);
     if (count != need) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)need);
     nxsdg_status s;
+    if (mem == NXSDG_MEM_HOST_ASYNC) {
+        if ((s = ensure_async(c))) return s;
+        const size_t nn = (size_t)c->npitch * c->nrows_local;
+        for (int k = 0; k < 4; ++k)
+            if (!c->fstage[k]) {
+                if ((s = alloc(c, &c->fstage[k], nn))) return s;
+            }
+        CU(cudaStreamWaitEvent(c->cstream, c->ev_fcons, 0));   // the previous staging has been consumed
+        const double* src[4] = {ox, oy, ax, ay};
+        const int64_t rows = owned_node_rows(c), cols = (int64_t)c->P * c->d.nx + 1;
+        for (int k = 0; k < 4; ++k)
+            CU(cudaMemcpy2DAsync(c->fstage[k] + (size_t)c->P * c->glo * c->npitch, c->npitch * sizeof(double), src[k],
+                                 cols * sizeof(double), cols * sizeof(double), rows, cudaMemcpyHostToDevice, c->cstream));
+        CU(cudaEventRecord(c->ev_fup, c->cstream));
+        c->fpending = true;
+        c->forcing_set = true;
+        c->prepped = false;
+        return NXSDG_OK;
+    }
+    c->fpending = false;
     if ((s = copy_in_nodes(c, c->ox, ox, count, mem))) return s;
     if ((s = copy_in_nodes(c, c->oy, oy, count, mem))) return s;
     if ((s = copy_in_nodes(c, c->ax, ax, count, mem))) return s;
@@ -1108,6 +1196,7 @@ static nxsdg_status launch_step(nxsdg_ctx* c, nxsdg_step st) {
 static nxsdg_status begin_step(nxsdg_ctx* c) {
     if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
     nxsdg_status s;
+    if ((s = consume_forcing(c))) return s;
     if ((s = halo(c, NXSDG_HALO_V | NXSDG_HALO_S | NXSDG_HALO_AH))) return s;
     if ((s = dispatch_prep(c))) return s;
     c->prepped = true;
@@ -1292,6 +1381,7 @@ extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
 
 extern "C" nxsdg_status nxsdg_synchronize(nxsdg_ctx* c) {
     GUARD(c);
+    if (c->cstream) CU(cudaStreamSynchronize(c->cstream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaGetLastError());
     return NXSDG_OK;
@@ -1331,6 +1421,7 @@ extern "C" nxsdg_status nxsdg_group_mevp_substeps(nxsdg_ctx** ctxs, int32_t nr, 
     }
     const bool unfused = flags & NXSDG_UNFUSED;
     if (flags & NXSDG_BEGIN_STEP) {
+        for (nxsdg_ctx* c : v) if ((s = consume_forcing(c))) return s;
         if ((s = halo_loopback_all(v, NXSDG_HALO_V | NXSDG_HALO_S | NXSDG_HALO_AH))) return s;
         for (nxsdg_ctx* c : v) {
             cudaSetDevice(c->d.device);

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libnxsdg.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_STATE, ERR_CUDA, ERR_NCCL, ERR_OOM = range(7)
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "STATE", 4: "CUDA", 5: "NCCL", 6: "OOM"}
-MEM_HOST, MEM_DEVICE = 0, 1
+MEM_HOST, MEM_DEVICE, MEM_HOST_ASYNC = 0, 1, 2
 BC_CLOSED, BC_PERIODIC = 0, 1
 FIELDS = {"vx": 0, "vy": 1, "S11": 2, "S12": 3, "S22": 4, "A": 5, "H": 6, "E11": 7, "E12": 8, "E22": 9,
           "Fx": 10, "Fy": 11}
@@ -84,6 +84,7 @@ def _load() -> C.CDLL:
         "nxsdg_set_option": ([vp, i32, i64], i32),
         "nxsdg_set_forcing_cyclone": ([vp, dbl], i32),
         "nxsdg_set_vertices": ([vp, vp, i64, i32], i32),
+        "nxsdg_stream_join": ([vp], i32),
         "nxsdg_halo_plan": ([i32, i32, i32, i32, i32, i32, i32, u32, vp, i32, C.POINTER(i32)], i32),
         "nxsdg_local_geometry": ([i32, i32, i32, i32, i32, i32, i32, C.POINTER(i64)], i32),
     }
@@ -101,7 +102,7 @@ EXPORTED = [
     "nxsdg_mevp_substeps", "nxsdg_advect", "nxsdg_run_step", "nxsdg_synchronize", "nxsdg_nccl_unique_id",
     "nxsdg_loopback_connect", "nxsdg_group_mevp_substeps", "nxsdg_group_advect", "nxsdg_kernel_launches",
     "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option", "nxsdg_halo_plan",
-    "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone", "nxsdg_set_vertices",
+    "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone", "nxsdg_set_vertices", "nxsdg_stream_join",
 ]
 HALO_V, HALO_S, HALO_AH, HALO_AH_SCR0, HALO_AH_SCR1 = 1, 2, 4, 8, 16
 HF_VX, HF_VY, HF_S, HF_A, HF_H, HF_A_SCR0, HF_H_SCR0, HF_A_SCR1, HF_H_SCR1 = range(9)
@@ -251,18 +252,30 @@ class Mesh:
         p, n, mem = _ptr_mem(arr)
         _chk(self.h, lib.nxsdg_write_state(self.h, FIELDS[field], p, n, mem), f"write_state({field})")
 
-    def read_state(self, field: str, out=None):
+    def read_state(self, field: str, out=None, asynchronous: bool = False):
         if out is None:
             out = np.empty(self.shape(field), dtype=np.float64)
         p, n, mem = _ptr_mem(out)
+        if asynchronous:
+            if mem != MEM_HOST:
+                raise ValueError("asynchronous reads go to pinned host memory")
+            mem = MEM_HOST_ASYNC
         _chk(self.h, lib.nxsdg_read_state(self.h, FIELDS[field], p, n, mem), f"read_state({field})")
         return out
 
-    def set_forcing(self, ox, oy, ax, ay):
+    def set_forcing(self, ox, oy, ax, ay, asynchronous: bool = False):
         ps = [_ptr_mem(a) for a in (ox, oy, ax, ay)]
         if len({(n, m) for _, n, m in ps}) != 1:
             raise ValueError("forcing arrays must match in size and memory kind")
-        _chk(self.h, lib.nxsdg_set_forcing(self.h, *[p for p, _, _ in ps], ps[0][1], ps[0][2]), "set_forcing")
+        mem = ps[0][2]
+        if asynchronous:
+            if mem != MEM_HOST:
+                raise ValueError("asynchronous forcing comes from pinned host memory")
+            mem = MEM_HOST_ASYNC
+        _chk(self.h, lib.nxsdg_set_forcing(self.h, *[p for p, _, _ in ps], ps[0][1], mem), "set_forcing")
+
+    def stream_join(self):
+        _chk(self.h, lib.nxsdg_stream_join(self.h), "stream_join")
 
     def set_vertices(self, xy):
         p, n, mem = _ptr_mem(xy)

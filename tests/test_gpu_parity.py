@@ -194,6 +194,48 @@ def test_multi_outer_step_moving_cyclone(nx, ora):
     _check(got, ref, st, TOLN, groups=("S", "v", "A", "H"))
 
 
+def test_async_forcing_and_readback_pipeline(nx):
+    """NXSDG_MEM_HOST_ASYNC: step k+1's forcing uploaded while step k runs and v read back while
+    the next step runs give bitwise the synchronous results (per-step readbacks and final state)."""
+    import torch
+    nxe, nye = 48, 40
+    lx, ly = nxe * 2e3, nye * 2e3
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    prm = nx.PhysParams()
+    X, Y = np.meshgrid(np.arange(2 * nxe + 1) * (lx / nxe / 2), np.arange(2 * nye + 1) * (ly / nye / 2))
+    forc = [[np.ascontiguousarray(a) for a in inputs.cyclone_forcing(X, Y, lx, ly, k * 3600.0)] for k in range(4)]
+    sync_v, final = [], {}
+    with nx.Mesh(nxe, nye, lx, ly, params=prm) as m:
+        m.load(st)
+        for k in range(4):
+            m.set_forcing(*forc[k])
+            m.advect(prm.dt)
+            m.mevp_substeps(15, begin_step=True)
+            sync_v.append((m.read_state("vx"), m.read_state("vy")))
+        final = m.state()
+    pin = [[torch.from_numpy(a).pin_memory() for a in f] for f in forc]
+    outs = [(torch.empty(X.shape, dtype=torch.float64).pin_memory(),
+             torch.empty(X.shape, dtype=torch.float64).pin_memory()) for _ in range(4)]
+    with nx.Mesh(nxe, nye, lx, ly, params=prm) as m:
+        m.load({k: v for k, v in st.items() if k not in ("ox", "oy", "ax", "ay")})
+        m.set_forcing(*pin[0], asynchronous=True)
+        for k in range(4):
+            m.advect(prm.dt)
+            m.mevp_substeps(15, begin_step=True)
+            if k + 1 < 4:
+                m.set_forcing(*pin[k + 1], asynchronous=True)
+            m.read_state("vx", outs[k][0], asynchronous=True)
+            m.read_state("vy", outs[k][1], asynchronous=True)
+        m.stream_join()
+        m.synchronize()
+        got = m.state()
+    for k in range(4):
+        np.testing.assert_array_equal(outs[k][0].numpy(), sync_v[k][0])
+        np.testing.assert_array_equal(outs[k][1].numpy(), sync_v[k][1])
+    for key in final:
+        np.testing.assert_array_equal(got[key], final[key])
+
+
 def test_device_cyclone_forcing_equals_host_recipe(nx):
     """nxsdg_set_forcing_cyclone(t) == nxsdg_set_forcing(inputs.cyclone_forcing(t)) (same subcycle result)."""
     nxe, nye, lx, ly = 40, 30, 80e3, 60e3
