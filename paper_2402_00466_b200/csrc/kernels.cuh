@@ -697,6 +697,16 @@ __global__ void k_cyclone_forcing(ForcingArgs a) {
 // --------------------------------------------------------------------------
 // ABI layout conversion: AoS rows (n per element) <-> SoA planes.
 // --------------------------------------------------------------------------
+// NEXT-3 mixed precision: FP64 <-> FP32 copies of the stress / P_g planes at call boundaries
+__global__ void k_cvt_d2f(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (float)src[i];
+}
+__global__ void k_cvt_f2d(const float* __restrict__ src, double* __restrict__ dst, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (double)src[i];
+}
+
 // compact ABI element e = row*nx + col  <->  device (row + row_off)*epitch + col
 __global__ void k_aos_to_soa(const double* src, double* dst, int64_t nelem, int n, int64_t eplane, int64_t row_off,
                              int nx, int64_t epitch) {

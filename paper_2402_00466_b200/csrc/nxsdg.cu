@@ -127,6 +127,10 @@ struct nxsdg_ctx {
     cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
     K2Maps maps[2][2]; // [cv][cs]
     bool maps_ok = false;
+    int precision = 0; // 0: FP64 storage; 1 (NEXT-3): S and P_g stored in FP32, arithmetic FP64
+    float* S32[2] = {nullptr, nullptr}; float* Pg32 = nullptr;
+    K2Maps maps32[2][2];
+    bool maps32_ok = false, pg32_ok = false;
     // transport
     ncclComm_t comm = nullptr;
     std::vector<nxsdg_ctx*> peers;   // loopback: all ranks' contexts
@@ -204,6 +208,8 @@ static void free_all(nxsdg_ctx* c) {
     for (auto b : bufs)
         if (*b) { cudaFree(*b); *b = nullptr; }
     if (c->counters) { cudaFree(c->counters); c->counters = nullptr; c->ncounters = 0; }
+    for (int k = 0; k < 2; ++k) if (c->S32[k]) { cudaFree(c->S32[k]); c->S32[k] = nullptr; }
+    if (c->Pg32) { cudaFree(c->Pg32); c->Pg32 = nullptr; }
     if (c->hstage_send) { cudaFree(c->hstage_send); c->hstage_send = nullptr; }
     if (c->verts) { cudaFree(c->verts); c->verts = nullptr; }
     for (int k = 0; k < 4; ++k) if (c->fstage[k]) { cudaFree(c->fstage[k]); c->fstage[k] = nullptr; }
@@ -322,6 +328,7 @@ extern "C" double nxsdg_bytes_per_element_subcycle(const nxsdg_ctx* c) {
     // one fused pass: v gather P^2*2, S read+write 2*3NS, P_g NG,
     // per node (P^2 per element): 6 constants + v write 2
     const double p2 = (double)c->P * c->P;
+    if (c->precision == 1) return 8.0 * (2 * p2 + 8.0 * p2) + 4.0 * (6.0 * c->NS + c->NG);   // S, P_g in FP32
     return 8.0 * (2 * p2 + 6.0 * c->NS + c->NG + 8.0 * p2);
 }
 
@@ -364,6 +371,12 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_DYNAMIC:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "dynamic 0|1");
             c->dynamic = (int)value; break;
+        case NXSDG_OPT_PRECISION:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "precision 0|1");
+            if (value == 1 && (c->P != 2 || c->d.nranks != 1))
+                return fail(c, NXSDG_ERR_UNSUPPORTED, "FP32 storage: CG2/DG2, single rank");
+            if (value == 1 && c->stages > 3) c->stages = 3;
+            c->precision = (int)value; c->pg32_ok = false; break;
         case NXSDG_OPT_MAP_MODE:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "map mode 0|1");
             c->map_mode = (int)value; break;
@@ -1031,7 +1044,8 @@ static nxsdg_status build_maps(nxsdg_ctx* c) {
     const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 8, (cuuint64_t)c->eplane * 8};
     const cuuint64_t ns[2] = {(cuuint64_t)c->npitch * 8, (cuuint64_t)c->nn * 8};
     const cuuint64_t dS[3] = {nx, er, 18}, dP[3] = {nx, er, 9}, dV[2] = {ncols, nr}, dC[3] = {ncols, nr, 6};
-    const cuuint32_t bS[3] = {K2_ECOLS, 1, 18}, bP[3] = {K2_ECOLS, 1, 9}, bV[2] = {K2_VCOLS, 3}, bC[3] = {K2_CCOLS, 2, 6};
+    const cuuint32_t bS[3] = {K2Cols<double>::E, 1, 18}, bP[3] = {K2Cols<double>::E, 1, 9}, bV[2] = {K2_VCOLS, 3},
+                     bC[3] = {K2_CCOLS, 2, 6};
     for (int v = 0; v < 2; ++v)
         for (int s = 0; s < 2; ++s) {
             K2Maps& M = c->maps[v][s];
@@ -1044,25 +1058,70 @@ static nxsdg_status build_maps(nxsdg_ctx* c) {
     return NXSDG_OK;
 }
 
+static bool encode_f32(CUtensorMap* m, const void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                       const cuuint32_t* box) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// NEXT-3: FP32 stress / P_g buffers and their tensor maps (v and node-constant maps as in FP64)
+static nxsdg_status build_maps32(nxsdg_ctx* c) {
+    nxsdg_status st = build_maps(c);
+    if (st || c->maps32_ok) return st;
+    const size_t ne = (size_t)c->eplane;
+    for (int k = 0; k < 2; ++k)
+        if (!c->S32[k]) CU(cudaMalloc(&c->S32[k], 3 * (size_t)c->NS * ne * sizeof(float)));
+    if (!c->Pg32) CU(cudaMalloc(&c->Pg32, (size_t)c->NG * ne * sizeof(float)));
+    const cuuint64_t nx = c->d.nx, er = c->erows_local;
+    const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 4, (cuuint64_t)c->eplane * 4};
+    const cuuint64_t dS[3] = {nx, er, 18}, dP[3] = {nx, er, 9};
+    const cuuint32_t bS[3] = {K2Cols<float>::E, 1, 18}, bP[3] = {K2Cols<float>::E, 1, 9};
+    for (int v = 0; v < 2; ++v)
+        for (int s = 0; s < 2; ++s) {
+            K2Maps& M = c->maps32[v][s];
+            M = c->maps[v][s];
+            if (!encode_f32(&M.S, c->S32[s], dS, es, bS) || !encode_f32(&M.Pg, c->Pg32, dP, es, bP))
+                return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled (fp32) failed");
+        }
+    c->maps32_ok = true;
+    return NXSDG_OK;
+}
+
+static nxsdg_status cvt(nxsdg_ctx* c, const double* src, float* dst, int64_t n) {
+    k_cvt_d2f<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(src, dst, n);
+    LAUNCHED();
+    return NXSDG_OK;
+}
+static nxsdg_status cvt(nxsdg_ctx* c, const float* src, double* dst, int64_t n) {
+    k_cvt_f2d<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(src, dst, n);
+    LAUNCHED();
+    return NXSDG_OK;
+}
+
 static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0; }
 
-template <bool R, int ST>
+template <bool R, int ST, typename SF>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
-    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage) + sizeof(uint64_t) + sizeof(int4));
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage<SF>) + sizeof(uint64_t) + sizeof(int4));
     static bool attr = false;
     if (!attr) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST>, 32 * K2_WARPS, smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF>, 32 * K2_WARPS, smem));
     if (c->ctas_per_sm > 0) occ = std::min(occ, c->ctas_per_sm);
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
-    k_subcycle_tma<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->maps[cv][cs], a);
+    const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
+    k_subcycle_tma<R, ST, SF><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
     return NXSDG_OK;
 }
 
@@ -1088,13 +1147,23 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int 
         slot = 0;
     }
     a.work_counter = c->dynamic ? c->counters + slot : nullptr;
+    if (c->precision == 1) {
+        if ((st = build_maps32(c))) return st;
+        a.S_out = reinterpret_cast<double*>(c->S32[cs ^ 1]);   // the kernel stores FP32
+        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
+            case 4: return launch_tma_t<false, 2, float>(c, cv, cs, a);
+            case 5: return launch_tma_t<true, 2, float>(c, cv, cs, a);
+            case 6: return launch_tma_t<false, 3, float>(c, cv, cs, a);
+            default: return launch_tma_t<true, 3, float>(c, cv, cs, a);
+        }
+    }
     switch (c->stages * 2 + (a.repl ? 1 : 0)) {
-        case 4: return launch_tma_t<false, 2>(c, cv, cs, a);
-        case 5: return launch_tma_t<true, 2>(c, cv, cs, a);
-        case 6: return launch_tma_t<false, 3>(c, cv, cs, a);
-        case 7: return launch_tma_t<true, 3>(c, cv, cs, a);
-        case 8: return launch_tma_t<false, 4>(c, cv, cs, a);
-        default: return launch_tma_t<true, 4>(c, cv, cs, a);
+        case 4: return launch_tma_t<false, 2, double>(c, cv, cs, a);
+        case 5: return launch_tma_t<true, 2, double>(c, cv, cs, a);
+        case 6: return launch_tma_t<false, 3, double>(c, cv, cs, a);
+        case 7: return launch_tma_t<true, 3, double>(c, cv, cs, a);
+        case 8: return launch_tma_t<false, 4, double>(c, cv, cs, a);
+        default: return launch_tma_t<true, 4, double>(c, cv, cs, a);
     }
 }
 
@@ -1237,7 +1306,7 @@ static nxsdg_status one_subcycle(nxsdg_ctx* c, bool unfused) {
 
 // Capture n fused subcycles into a CUDA graph (nranks == 1) and replay it.
 static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
-    auto key = std::make_tuple(n, c->cv, c->cs);
+    auto key = std::make_tuple(n, c->cv, c->cs + 2 * c->precision);
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
@@ -1284,6 +1353,18 @@ extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t fl
         return fail(c, NXSDG_ERR_STATE, "loopback ranks step through nxsdg_group_mevp_substeps");
     if ((flags & NXSDG_BEGIN_STEP) && (s = begin_step(c))) return s;
     const bool unfused = flags & NXSDG_UNFUSED;
+    if (!unfused && c->d.nranks == 1 && n > 0 && c->precision == 1 && use_tma(c)) {
+        // NEXT-3: the FP64 state is the ABI-visible copy; the subcycles run on FP32 S / P_g
+        if ((s = build_maps32(c))) return s;
+        const int64_t nS = 3 * (int64_t)c->NS * c->eplane;
+        if ((flags & NXSDG_BEGIN_STEP) || !c->pg32_ok) {
+            if ((s = cvt(c, c->Pg, c->Pg32, (int64_t)c->NG * c->eplane))) return s;
+            c->pg32_ok = true;
+        }
+        if ((s = cvt(c, c->S[c->cs], c->S32[c->cs], nS))) return s;
+        if ((s = run_graph(c, n))) return s;
+        return cvt(c, c->S32[c->cs], c->S[c->cs], nS);
+    }
     if (!unfused && c->d.nranks == 1 && n > 0) return run_graph(c, n);
     for (int i = 0; i < n; ++i)
         if ((s = one_subcycle(c, unfused))) return s;

@@ -34,14 +34,20 @@ constexpr int K2_WARPS = 2;          // warps per CTA (independent work lists)
 constexpr int K2_MAX_STAGES = 4;     // pipeline depth is a template parameter (2..4)
 constexpr int K2_VCOLS = 66;         // node columns per v box: 2*32 + 2
 constexpr int K2_CCOLS = 62;         // owned node columns per const box: 2*31
-constexpr int K2_ECOLS = 34;         // element columns per S / P_g box: the TMA start column must be even
-                                     // (16-B aligned for FP64), so the box starts at (ix0-1) & ~1
+// Element columns per S / P_g box.  The TMA start column must be 16-B aligned: for FP64 storage
+// the box starts at (ix0-1) & ~1 and is 34 wide, for FP32 storage (NEXT-3 mixed precision) at
+// (ix0-1) & ~3 and 36 wide; lanes read at the offset (ix0-1) - start.
+template <typename SF> struct K2Cols { static constexpr int E = sizeof(SF) == 8 ? 34 : 36, ALIGN = 16 / sizeof(SF); };
+__host__ __device__ constexpr int round128(int b) { return (b + 127) / 128 * 128; }
 
+template <typename SF>
 struct __align__(128) K2Stage {
-    double S[18][K2_ECOLS];          // 4896 B   planes S11[0..6), S12[0..6), S22[0..6)
-    double pads[12];                 //   96 B  -> 4992
-    double Pg[9][K2_ECOLS];          // 2448 B
-    double padp[14];                 //  112 B  -> 2560
+    static constexpr int EC = K2Cols<SF>::E;
+    static constexpr int SB = round128(18 * EC * (int)sizeof(SF)), PB = round128(9 * EC * (int)sizeof(SF));
+    SF S[18][EC];                    // planes S11[0..6), S12[0..6), S22[0..6)
+    unsigned char pads[SB - 18 * EC * (int)sizeof(SF)];
+    SF Pg[9][EC];
+    unsigned char padp[PB - 9 * EC * (int)sizeof(SF)];
     double vx[3][K2_VCOLS];          // 1584 B
     double padx[10];                 //   80 B  -> 1664
     double vy[3][K2_VCOLS];
@@ -49,10 +55,13 @@ struct __align__(128) K2Stage {
     double C[6][2][K2_CCOLS];        // 5952 B  c1, rx0, ry0, cafo, ox, oy
     double padc[8];                  //   64 B  -> 6016
 };
-static_assert(sizeof(K2Stage) == 16896, "stage layout");
-static_assert(offsetof(K2Stage, Pg) % 128 == 0 && offsetof(K2Stage, vx) % 128 == 0 &&
-              offsetof(K2Stage, vy) % 128 == 0 && offsetof(K2Stage, C) % 128 == 0, "TMA dst alignment");
-constexpr uint32_t K2_TX_BYTES = 27 * K2_ECOLS * 8 + 2 * 3 * K2_VCOLS * 8 + 6 * 2 * K2_CCOLS * 8;
+static_assert(sizeof(K2Stage<double>) == 16896, "stage layout");
+static_assert(offsetof(K2Stage<double>, Pg) % 128 == 0 && offsetof(K2Stage<double>, vx) % 128 == 0 &&
+              offsetof(K2Stage<double>, vy) % 128 == 0 && offsetof(K2Stage<double>, C) % 128 == 0, "TMA dst alignment");
+static_assert(offsetof(K2Stage<float>, Pg) % 128 == 0 && offsetof(K2Stage<float>, vx) % 128 == 0 &&
+              offsetof(K2Stage<float>, C) % 128 == 0, "TMA dst alignment (fp32)");
+template <typename SF>
+__host__ __device__ constexpr uint32_t k2_tx_bytes() { return 27 * K2Cols<SF>::E * sizeof(SF) + 2 * 3 * K2_VCOLS * 8 + 6 * 2 * K2_CCOLS * 8; }
 
 struct K2Maps {
     CUtensorMap S, Pg, vx, vy, C;    // 5 x 128 B, 64-B aligned
@@ -207,12 +216,15 @@ __device__ __forceinline__ void div_t(const double S[6], double h, double r[3][3
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool REPL, int STAGES>
+template <bool REPL, int STAGES, typename SF>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
+    using Stage = K2Stage<SF>;
+    constexpr int AL = K2Cols<SF>::ALIGN;
+    SF* const S_out = reinterpret_cast<SF*>(a.S_out);   // FP32 buffers in mixed-precision mode
     extern __shared__ __align__(1024) unsigned char k2_smem[];   // no static smem: base stays 1024-B aligned
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    K2Stage* stg = reinterpret_cast<K2Stage*>(k2_smem) + wib * STAGES;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * STAGES * sizeof(K2Stage)) + wib * STAGES;
+    Stage* stg = reinterpret_cast<Stage*>(k2_smem) + wib * STAGES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * STAGES * sizeof(Stage)) + wib * STAGES;
     if ((su32(k2_smem) & 127u) != 0u) {                          // TMA destinations need 128-B alignment
         printf("nxsdg: dynamic smem misaligned %u\n", su32(k2_smem));
         __trap();
@@ -252,10 +264,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         jobs[st] = make_int4(c.ok ? c.u : -1, c.lr, c.lr1, (c.ring ? 1 : 0) | (c.first ? 2 : 0));
     };
     auto issue = [&](const Cur& c, int s) {
-        K2Stage* t = stg + s;
+        Stage* t = stg + s;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], K2_TX_BYTES);
-        const int xs = (c.ix0 - 1) & ~1;   // even start column (arithmetic: -1 -> -2)
+        mbar_expect_tx(&bar[s], k2_tx_bytes<SF>());
+        const int xs = (c.ix0 - 1) & ~(AL - 1);   // 16-B aligned start column (arithmetic: -1 -> -2 / -4)
         tma3(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0);
         tma3(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0);
         tma2(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
@@ -299,9 +311,9 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         }
         mbar_wait(&bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
-        const K2Stage& t = stg[s];
+        const Stage& t = stg[s];
         const int ix = cur.ix0 - 1 + lane, lr = cur.lr;
-        const int eo = (cur.ix0 - 1) - ((cur.ix0 - 1) & ~1);   // 0 or 1: lane offset inside the S / P_g box
+        const int eo = (cur.ix0 - 1) - ((cur.ix0 - 1) & ~(AL - 1));   // lane offset inside the S / P_g box
         if (cur.first) { carx[0] = carx[1] = cary[0] = cary[1] = 0.0; }
 
         // ---- node values of this element (local box columns 2*lane .. 2*lane+2)
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             const double x = e11[g], y = e22[g], z = e12[g];
             const double draw2 = fma(z, z, fma(1.5 * x, y, 1.25 * fma(x, x, y * y)));
             const double rD = rsqrt_nr(draw2 + a.dmin2);
-            const double ph = t.Pg[g][eo + lane] * hA;
+            const double ph = (double)t.Pg[g][eo + lane] * hA;
             const double pr = ph * rD;
             // replacement pressure (R#4): P_r/2 = (P/2) Draw/Delta, Draw = draw2 * rsqrt(draw2)
             const double sub = REPL ? pr * (draw2 > 0.0 ? draw2 * rsqrt_nr(draw2) : 0.0) : ph;
@@ -351,7 +363,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         double S11[6], S12[6], S22[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-            S11[k] = t.S[k][eo + lane]; S12[k] = t.S[6 + k][eo + lane]; S22[k] = t.S[12 + k][eo + lane];
+            S11[k] = (double)t.S[k][eo + lane]; S12[k] = (double)t.S[6 + k][eo + lane];
+            S22[k] = (double)t.S[12 + k][eo + lane];
         }
         project(e11, 1.0, fac, S11);
         project(e12, 0.5, fac, S12);
@@ -361,9 +374,9 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             const int64_t e = (int64_t)lr * a.epitch + ix;
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
-                a.S_out[k * eplane + e] = S11[k];
-                a.S_out[(6 + k) * eplane + e] = S12[k];
-                a.S_out[(12 + k) * eplane + e] = S22[k];
+                S_out[k * eplane + e] = (SF)S11[k];
+                S_out[(6 + k) * eplane + e] = (SF)S12[k];
+                S_out[(12 + k) * eplane + e] = (SF)S22[k];
             }
         }
         // ---- divergence contributions: rX = D_s S11 / hx + D_t S12 / hy, rY likewise

@@ -109,6 +109,20 @@ def test_fused_variants_agree(nx):
     assert max(e.values()) < 1e-12, e
 
 
+@pytest.mark.parametrize("nsub,tol_s,tol_v", [(1, 1e-6, 1e-8), (20, 1e-5, 1e-6)])
+def test_fp32_storage_variant(nx, ora, nsub, tol_s, tol_v):
+    """NEXT-3: S and P_g stored in FP32 (arithmetic and v in FP64).  Tolerance from FP32
+    rounding (unit roundoff 6e-8 per store, amplified over the subcycles): S <= 1e-6 after one
+    subcycle / 1e-5 after 20; v increments <= 1e-8 / 1e-6."""
+    nxe, nye, lx, ly = 64, 56, 128e3, 112e3
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    got = _gpu_run(nx, st, nxe, nye, 2, 6, 6, nsub, lx, ly, options={nx.OPT_PRECISION: 1})
+    ref = ora.subcycles(ora_mesh(nxe, nye, 2, 6, 6, lx, ly), ora_params(nx.PhysParams()), nsub, st)
+    e = parity(got, ref, st)
+    assert e["S"] <= tol_s and e["dS"] <= tol_s and e["dv"] <= tol_v, e
+    assert e["S"] > 1e-11     # really ran in reduced storage precision
+
+
 def test_c2_full_config(nx, ora):
     """C2: 256x256 CG2/DG2 warm box + cyclone, 100 subcycles (oracle ~1 min on 8 cores)."""
     cfg = inputs.CONFIGS["C2"]
