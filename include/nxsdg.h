@@ -238,6 +238,12 @@ nxsdg_status nxsdg_local_geometry(int32_t nx, int32_t ny, int32_t cg_degree, int
                                   int32_t nranks, int32_t rank, int64_t* out8);
 
 /* ---- introspection ------------------------------------------------------------- */
+/* The K0 reference-element tables of degree p (1|2) as built on the device (row a0), flattened:
+ * gx[ngp], gw[ngp] (Gauss rule on [0,1]), psi[6][ng] (DG basis at the Gauss points), phi, dphi/ds,
+ * dphi/dt [ncg][ng] (CG basis), mref[6] (reference DG mass), R[6][ng] (iMJwPSI of the reference
+ * element), Ds, Dt [ncg][6] (divergence composites); ngp = p+1, ng = ncg = ngp^2.  With out == NULL
+ * only *needed is set. */
+nxsdg_status nxsdg_debug_reference_tables(nxsdg_ctx* ctx, int32_t p, double* out, int64_t count, int64_t* needed);
 /* Number of kernels this context has launched (for the bench's gpu_launches claim). */
 int64_t nxsdg_kernel_launches(const nxsdg_ctx* ctx);
 /* Algorithmic HBM bytes per element-subcycle of the fused kernel. */

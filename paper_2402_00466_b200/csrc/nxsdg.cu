@@ -45,6 +45,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -62,6 +63,7 @@ NcclApi& nccl() {
     api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
     api.loaded = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
                  api.GroupStart && api.GroupEnd;
     return api;
@@ -1462,6 +1464,11 @@ extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
 
 extern "C" nxsdg_status nxsdg_synchronize(nxsdg_ctx* c) {
     GUARD(c);
+    if (c->comm && nccl().CommGetAsyncError) {   // failure detection: a broken peer surfaces here
+        ncclResult_t ar = 0;
+        if (nccl().CommGetAsyncError(c->comm, &ar) != 0 || ar != 0)
+            return fail(c, NXSDG_ERR_NCCL, "NCCL async error %d", (int)ar);
+    }
     if (c->cstream) CU(cudaStreamSynchronize(c->cstream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaGetLastError());
@@ -1469,6 +1476,32 @@ extern "C" nxsdg_status nxsdg_synchronize(nxsdg_ctx* c) {
 }
 
 // ---------------------------------------------------------------- multi-rank plumbing
+// K0 tables for tests (a0): {gx[ngp], gw[ngp], psi[6][ng], phi[ncg][ng], dphis[ncg][ng], dphit[ncg][ng],
+// mref[6], R[6][ng], Ds[ncg][6], Dt[ncg][6]} of degree p, flattened in this order.
+extern "C" nxsdg_status nxsdg_debug_reference_tables(nxsdg_ctx* c, int32_t p, double* out, int64_t count, int64_t* needed) {
+    GUARD(c);
+    if (p != 1 && p != 2) return fail(c, NXSDG_ERR_INVALID_ARG, "p 1|2");
+    const int ngp = p + 1, ng = ngp * ngp, ncg = ng;
+    const int64_t n = 2 * ngp + 6 * ng + 3 * ncg * ng + 6 + 6 * ng + 2 * ncg * 6;
+    if (needed) *needed = n;
+    if (!out) return NXSDG_OK;
+    if (count < n) return fail(c, NXSDG_ERR_INVALID_ARG, "count < %lld", (long long)n);
+    RefTab T;
+    CU(cudaMemcpyFromSymbol(&T, c_tab, sizeof(RefTab), (p - 1) * sizeof(RefTab), cudaMemcpyDeviceToHost));
+    int64_t o = 0;
+    for (int i = 0; i < ngp; ++i) out[o++] = T.gx[i];
+    for (int i = 0; i < ngp; ++i) out[o++] = T.gw[i];
+    for (int k = 0; k < 6; ++k) for (int g = 0; g < ng; ++g) out[o++] = T.psi[k][g];
+    for (int j = 0; j < ncg; ++j) for (int g = 0; g < ng; ++g) out[o++] = T.phi[j][g];
+    for (int j = 0; j < ncg; ++j) for (int g = 0; g < ng; ++g) out[o++] = T.dphis[j][g];
+    for (int j = 0; j < ncg; ++j) for (int g = 0; g < ng; ++g) out[o++] = T.dphit[j][g];
+    for (int k = 0; k < 6; ++k) out[o++] = T.mref[k];
+    for (int k = 0; k < 6; ++k) for (int g = 0; g < ng; ++g) out[o++] = T.R[k][g];
+    for (int j = 0; j < ncg; ++j) for (int k = 0; k < 6; ++k) out[o++] = T.Ds[j][k];
+    for (int j = 0; j < ncg; ++j) for (int k = 0; k < 6; ++k) out[o++] = T.Dt[j][k];
+    return NXSDG_OK;
+}
+
 extern "C" nxsdg_status nxsdg_nccl_unique_id(void* out128) {
     if (!out128) return NXSDG_ERR_INVALID_ARG;
     NcclApi& api = nccl();

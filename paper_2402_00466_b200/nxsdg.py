@@ -85,6 +85,7 @@ def _load() -> C.CDLL:
         "nxsdg_set_forcing_cyclone": ([vp, dbl], i32),
         "nxsdg_set_vertices": ([vp, vp, i64, i32], i32),
         "nxsdg_stream_join": ([vp], i32),
+        "nxsdg_debug_reference_tables": ([vp, i32, vp, i64, C.POINTER(i64)], i32),
         "nxsdg_halo_plan": ([i32, i32, i32, i32, i32, i32, i32, u32, vp, i32, C.POINTER(i32)], i32),
         "nxsdg_local_geometry": ([i32, i32, i32, i32, i32, i32, i32, C.POINTER(i64)], i32),
     }
@@ -103,6 +104,7 @@ EXPORTED = [
     "nxsdg_loopback_connect", "nxsdg_group_mevp_substeps", "nxsdg_group_advect", "nxsdg_kernel_launches",
     "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option", "nxsdg_halo_plan",
     "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone", "nxsdg_set_vertices", "nxsdg_stream_join",
+    "nxsdg_debug_reference_tables",
 ]
 HALO_V, HALO_S, HALO_AH, HALO_AH_SCR0, HALO_AH_SCR1 = 1, 2, 4, 8, 16
 HF_VX, HF_VY, HF_S, HF_A, HF_H, HF_A_SCR0, HF_H_SCR0, HF_A_SCR1, HF_H_SCR1 = range(9)
@@ -273,6 +275,20 @@ class Mesh:
                 raise ValueError("asynchronous forcing comes from pinned host memory")
             mem = MEM_HOST_ASYNC
         _chk(self.h, lib.nxsdg_set_forcing(self.h, *[p for p, _, _ in ps], ps[0][1], mem), "set_forcing")
+
+    def reference_tables(self, p: int) -> dict:
+        """K0 device tables of degree p (see include/nxsdg.h), split into named arrays."""
+        need = C.c_int64()
+        _chk(self.h, lib.nxsdg_debug_reference_tables(self.h, p, None, 0, C.byref(need)), "tables")
+        buf = np.empty(need.value)
+        _chk(self.h, lib.nxsdg_debug_reference_tables(self.h, p, buf.ctypes.data, need.value, C.byref(need)), "tables")
+        ngp = p + 1; ng = ngp * ngp
+        shapes = [("gx", (ngp,)), ("gw", (ngp,)), ("psi", (6, ng)), ("phi", (ng, ng)), ("dphis", (ng, ng)),
+                  ("dphit", (ng, ng)), ("mref", (6,)), ("R", (6, ng)), ("Ds", (ng, 6)), ("Dt", (ng, 6))]
+        out, o = {}, 0
+        for name, shp in shapes:
+            n = int(np.prod(shp)); out[name] = buf[o:o + n].reshape(shp); o += n
+        return out
 
     def stream_join(self):
         _chk(self.h, lib.nxsdg_stream_join(self.h), "stream_join")

@@ -386,6 +386,53 @@ def test_debug_steps_each_against_oracle(nx, ora):
         assert group_err(v, {"vx": rv[0], "vy": rv[1]}, ("vx", "vy")) < 1e-12
 
 
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+def test_k0_tables_match_oracle_bases(nx, ora, p, ns):
+    """Row a0: the device-built reference tables equal the oracle's Gauss rule, DG/CG bases and
+    reference mass (<= 1e-15), and R = M_ref^{-1} psi w equals the oracle's element map on a unit box."""
+    with nx.Mesh(4, 4, 4.0, 4.0, p, ns, ns) as m:
+        T = m.reference_tables(p)
+    ngp = p + 1
+    x, w = ora.gauss(ngp)
+    np.testing.assert_allclose(T["gx"], x, atol=1e-15); np.testing.assert_allclose(T["gw"], w, atol=1e-15)
+    G = [(x[gx], x[gy]) for gy in range(ngp) for gx in range(ngp)]
+    for g, (s_, t_) in enumerate(G):
+        np.testing.assert_allclose(T["psi"][:, g], ora.dg_basis(6, s_, t_) if ngp == 3 else
+                                   np.r_[ora.dg_basis(6, s_, t_)], atol=1e-15)
+        phi, ds, dt = ora.cg_basis(p, s_, t_)
+        np.testing.assert_allclose(T["phi"][:, g], phi, atol=1e-14)
+        np.testing.assert_allclose(T["dphis"][:, g], ds, atol=1e-13)
+        np.testing.assert_allclose(T["dphit"][:, g], dt, atol=1e-13)
+    M = ora.element_mass(oracle.Mesh(1, 1, lx=1.0, ly=1.0, p=p, ns=ns, na=ns), 0, 0, ns, ngp)
+    np.testing.assert_allclose(T["mref"][:ns], np.diag(M), atol=1e-15)
+    colsol = np.linalg.solve(M, np.array([w[gx] * w[gy] * ora.dg_basis(ns, x[gx], x[gy])
+                                          for gy in range(ngp) for gx in range(ngp)]).T)
+    np.testing.assert_allclose(T["R"][:ns], colsol, atol=1e-13)
+
+
+def test_checkpoint_resume_bitwise(nx):
+    """State = (v, S, A, H) + forcing: reading it at an outer-step boundary and writing it into a
+    fresh context resumes bitwise (SURVEY §5 checkpoint/resume)."""
+    nxe, nye, lx, ly = 45, 41, 90e3, 82e3
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    prm = nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly, params=prm) as m:
+        m.load(st)
+        for _ in range(2):
+            m.advect(prm.dt); m.mevp_substeps(9, begin_step=True)
+        ref = m.state()
+    with nx.Mesh(nxe, nye, lx, ly, params=prm) as m:
+        m.load(st)
+        m.advect(prm.dt); m.mevp_substeps(9, begin_step=True)
+        ckpt = m.state()
+    with nx.Mesh(nxe, nye, lx, ly, params=prm) as m:
+        m.load({**ckpt, **{k: st[k] for k in ("ox", "oy", "ax", "ay")}})
+        m.advect(prm.dt); m.mevp_substeps(9, begin_step=True)
+        got = m.state()
+    for k in ref:
+        np.testing.assert_array_equal(got[k], ref[k])
+
+
 def test_bitwise_run_to_run(nx):
     nxe, nye = 70, 75
     st = case(nxe, nye, 2, 6, 6, "warm", 140e3, 150e3)
