@@ -177,6 +177,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--fp32-storage", action="store_true",
                     help="NEXT-3: S and P_g stored in FP32 inside the fused subcycles (arithmetic FP64)")
+    ap.add_argument("--fp32-stress", action="store_true",
+                    help="NEXT-3: as --fp32-storage plus the stress update (strain, Listing 2, projection) in FP32")
     ap.add_argument("--moving", action="store_true",
                     help="NEXT-2: regenerate the moving-cyclone forcing on the GPU at every outer step (P:350 protocol)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -216,8 +218,8 @@ def main():
     st = gen_rank_state(cfg, rank, world)
     kw = dict(rank=rank, nranks=world, transport=nxsdg.TRANSPORT_NCCL, nccl_id=nid) if world > 1 else {}
     m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, device=local, **kw)
-    if args.fp32_storage:
-        m.set_option(nxsdg.OPT_PRECISION, 1)
+    if args.fp32_storage or args.fp32_stress:
+        m.set_option(nxsdg.OPT_PRECISION, 2 if args.fp32_stress else 1)
     m.load(st)
     stream = torch.cuda.ExternalStream(m.stream)
     n_el = cfg.nx * cfg.ny   # whole job
@@ -326,7 +328,8 @@ def main():
             "metric": "FP64 mEVP element-updates/s", "value": value, "unit": "element-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak" if cname == "C5" else "strong", "vs_baseline": None,
-            "dtype": "f64" if not args.fp32_storage else "f64 arithmetic, f32 S/P_g storage", "data": "synthetic",
+            "dtype": ("f32 stress arithmetic + S/P_g storage, f64 divergence/velocity" if args.fp32_stress else
+                      "f64 arithmetic, f32 S/P_g storage" if args.fp32_storage else "f64"), "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} CG{cfg.p}/DG{cfg.p} (n_S={cfg.ns}, n_A={cfg.na}) warm box + "
                                    f"cyclone forcing; step = advect + prep + {cfg.nsub} fused mEVP subcycles",
                        "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el, "alpha": cfg.alpha, "beta": cfg.alpha,

@@ -155,12 +155,14 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_FUSED_KERNEL  0 (default): TMA-staged structured kernel for p = 2 (table-driven for p = 1);
  *                           1: table-driven register kernel k_subcycle<p> (reference-table variant)
  *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (default 32; one ring row each)
- *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy; default 2)
+ *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy;
+ *                           -1 (default) = tuned: 2 with FP64 S/P_g storage, 4 with FP32 storage)
  *   NXSDG_OPT_STAGES        TMA pipeline depth per warp, 2..4 (default 2)
  *   NXSDG_OPT_DYNAMIC       1 (default): warps claim work units from an atomic counter; 0: static round-robin
  *   NXSDG_OPT_PRECISION     0 (default): FP64 everywhere; 1 (NEXT-3): the fused CG2/DG2 subcycles keep
  *                           S and P_g in FP32 storage (arithmetic and the v state stay FP64); the FP64 S
- *                           seen through the ABI is converted at each nxsdg_mevp_substeps call (single rank)
+ *                           seen through the ABI is converted at each nxsdg_mevp_substeps call (single rank);
+ *                           2: as 1 and the stress update (strain, Listing 2, projection) in FP32 arithmetic
  *   NXSDG_OPT_MAP_MODE      general quads (nxsdg_set_vertices): 0 = per-element iMJwPSI pre-assembled and
  *                           stored, 1 (default) = recomputed on the fly from the 4 vertices
  * INVALID_ARG for an unknown option or value. */

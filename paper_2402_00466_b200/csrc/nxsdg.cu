@@ -109,7 +109,7 @@ struct nxsdg_ctx {
     int64_t launches = 0;
     int ty = 32;       // fused kernel chunk rows
     int variant = 0;   // fused kernel: 0 = TMA-staged structured (p = 2), 1 = table-driven k_subcycle<P>
-    int ctas_per_sm = 2;   // tuned on C4: 4 warps/SM beat the occupancy maximum
+    int ctas_per_sm = -1;  // -1 = tuned default on C4: 2 (FP64 S, P_g), 4 (FP32 storage)
     int stages = 2;        // TMA pipeline depth 2..4
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
@@ -330,7 +330,7 @@ extern "C" double nxsdg_bytes_per_element_subcycle(const nxsdg_ctx* c) {
     // one fused pass: v gather P^2*2, S read+write 2*3NS, P_g NG,
     // per node (P^2 per element): 6 constants + v write 2
     const double p2 = (double)c->P * c->P;
-    if (c->precision == 1) return 8.0 * (2 * p2 + 8.0 * p2) + 4.0 * (6.0 * c->NS + c->NG);   // S, P_g in FP32
+    if (c->precision >= 1) return 8.0 * (2 * p2 + 8.0 * p2) + 4.0 * (6.0 * c->NS + c->NG);   // S, P_g in FP32
     return 8.0 * (2 * p2 + 6.0 * c->NS + c->NG + 8.0 * p2);
 }
 
@@ -368,16 +368,16 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value < 1 || value > (1 << 20)) return fail(c, NXSDG_ERR_INVALID_ARG, "chunk rows >= 1");
             c->ty = (int)value; break;
         case NXSDG_OPT_CTAS_PER_SM:
-            if (value < 0 || value > 32) return fail(c, NXSDG_ERR_INVALID_ARG, "ctas per SM 0..32");
+            if (value < -1 || value > 32) return fail(c, NXSDG_ERR_INVALID_ARG, "ctas per SM -1..32");
             c->ctas_per_sm = (int)value; break;
         case NXSDG_OPT_DYNAMIC:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "dynamic 0|1");
             c->dynamic = (int)value; break;
         case NXSDG_OPT_PRECISION:
-            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "precision 0|1");
-            if (value == 1 && (c->P != 2 || c->d.nranks != 1))
+            if (value < 0 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "precision 0|1|2");
+            if (value >= 1 && (c->P != 2 || c->d.nranks != 1))
                 return fail(c, NXSDG_ERR_UNSUPPORTED, "FP32 storage: CG2/DG2, single rank");
-            if (value == 1 && c->stages > 3) c->stages = 3;
+            if (value >= 1 && c->stages > 3) c->stages = 3;
             c->precision = (int)value; c->pg32_ok = false; break;
         case NXSDG_OPT_MAP_MODE:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "map mode 0|1");
@@ -1106,24 +1106,25 @@ static nxsdg_status cvt(nxsdg_ctx* c, const float* src, double* dst, int64_t n) 
 
 static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0; }
 
-template <bool R, int ST, typename SF>
+template <bool R, int ST, typename SF, typename CT = double>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
     const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage<SF>) + sizeof(uint64_t) + sizeof(int4));
     static bool attr = false;
     if (!attr) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF>, 32 * K2_WARPS, smem));
-    if (c->ctas_per_sm > 0) occ = std::min(occ, c->ctas_per_sm);
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT>, 32 * K2_WARPS, smem));
+    const int cap = c->ctas_per_sm < 0 ? (sizeof(SF) == 8 ? 2 : 4) : c->ctas_per_sm;
+    if (cap > 0) occ = std::min(occ, cap);
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
+    k_subcycle_tma<R, ST, SF, CT><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
     return NXSDG_OK;
 }
 
@@ -1149,6 +1150,16 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int 
         slot = 0;
     }
     a.work_counter = c->dynamic ? c->counters + slot : nullptr;
+    if (c->precision == 2) {
+        if ((st = build_maps32(c))) return st;
+        a.S_out = reinterpret_cast<double*>(c->S32[cs ^ 1]);   // FP32 storage, FP32 stress arithmetic
+        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
+            case 4: return launch_tma_t<false, 2, float, float>(c, cv, cs, a);
+            case 5: return launch_tma_t<true, 2, float, float>(c, cv, cs, a);
+            case 6: return launch_tma_t<false, 3, float, float>(c, cv, cs, a);
+            default: return launch_tma_t<true, 3, float, float>(c, cv, cs, a);
+        }
+    }
     if (c->precision == 1) {
         if ((st = build_maps32(c))) return st;
         a.S_out = reinterpret_cast<double*>(c->S32[cs ^ 1]);   // the kernel stores FP32
@@ -1355,7 +1366,7 @@ extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t fl
         return fail(c, NXSDG_ERR_STATE, "loopback ranks step through nxsdg_group_mevp_substeps");
     if ((flags & NXSDG_BEGIN_STEP) && (s = begin_step(c))) return s;
     const bool unfused = flags & NXSDG_UNFUSED;
-    if (!unfused && c->d.nranks == 1 && n > 0 && c->precision == 1 && use_tma(c)) {
+    if (!unfused && c->d.nranks == 1 && n > 0 && c->precision >= 1 && use_tma(c)) {
         // NEXT-3: the FP64 state is the ABI-visible copy; the subcycles run on FP32 S / P_g
         if ((s = build_maps32(c))) return s;
         const int64_t nS = 3 * (int64_t)c->NS * c->eplane;

@@ -121,68 +121,77 @@ constexpr double kQ = 1.0 / 15.0;                // S^2 - 1/12 at S = +-kA
 constexpr double kQ0 = -1.0 / 12.0;              // ... at S = 0
 constexpr double kC = 10.0 * kA / 3.0;           // 12 * (5/18) * kA: first-moment scale
 
+// The stress part is templated on the arithmetic type T (double; float for NEXT-3's F32 stress
+// update).  Node differences are formed in FP64 and then converted.
+__device__ __forceinline__ float rsqrt_t(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double rsqrt_t(double x) { return rsqrt_nr(x); }
+
 // strain coefficients of d/ds v (k = 0..5, k = 3 identically zero)
-__device__ __forceinline__ void strain_s(const double V[3][3], double E[6]) {
-    double s0[3], s1[3];
+template <typename T>
+__device__ __forceinline__ void strain_s(const double V[3][3], T E[6]) {
+    T s0[3], s1[3];
 #pragma unroll
     for (int jy = 0; jy < 3; ++jy) {
-        const double d01 = V[jy][1] - V[jy][0], d12 = V[jy][2] - V[jy][1];
+        const T d01 = (T)(V[jy][1] - V[jy][0]), d12 = (T)(V[jy][2] - V[jy][1]);
         s0[jy] = d01 + d12; s1[jy] = d12 - d01;
     }
-    E[0] = (s0[0] + s0[2] + 4.0 * s0[1]) * (1.0 / 6.0);
-    E[1] = (s1[0] + s1[2] + 4.0 * s1[1]) * (2.0 / 3.0);
+    E[0] = (s0[0] + s0[2] + T(4) * s0[1]) * T(1.0 / 6.0);
+    E[1] = (s1[0] + s1[2] + T(4) * s1[1]) * T(2.0 / 3.0);
     E[2] = s0[2] - s0[0];
-    E[3] = 0.0;
-    E[4] = 2.0 * (s0[0] + s0[2]) - 4.0 * s0[1];
-    E[5] = 4.0 * (s1[2] - s1[0]);
+    E[3] = T(0);
+    E[4] = T(2) * (s0[0] + s0[2]) - T(4) * s0[1];
+    E[5] = T(4) * (s1[2] - s1[0]);
 }
 // strain coefficients of d/dt v (k = 4 identically zero)
-__device__ __forceinline__ void strain_t(const double V[3][3], double E[6]) {
-    double t0[3], t1[3];
+template <typename T>
+__device__ __forceinline__ void strain_t(const double V[3][3], T E[6]) {
+    T t0[3], t1[3];
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx) {
-        const double d01 = V[1][jx] - V[0][jx], d12 = V[2][jx] - V[1][jx];
+        const T d01 = (T)(V[1][jx] - V[0][jx]), d12 = (T)(V[2][jx] - V[1][jx]);
         t0[jx] = d01 + d12; t1[jx] = d12 - d01;
     }
-    E[0] = (t0[0] + t0[2] + 4.0 * t0[1]) * (1.0 / 6.0);
+    E[0] = (t0[0] + t0[2] + T(4) * t0[1]) * T(1.0 / 6.0);
     E[1] = t0[2] - t0[0];
-    E[2] = (t1[0] + t1[2] + 4.0 * t1[1]) * (2.0 / 3.0);
-    E[3] = 2.0 * (t0[0] + t0[2]) - 4.0 * t0[1];
-    E[4] = 0.0;
-    E[5] = 4.0 * (t1[2] - t1[0]);
+    E[2] = (t1[0] + t1[2] + T(4) * t1[1]) * T(2.0 / 3.0);
+    E[3] = T(2) * (t0[0] + t0[2]) - T(4) * t0[1];
+    E[4] = T(0);
+    E[5] = T(4) * (t1[2] - t1[0]);
 }
 // values at the 9 Gauss points (g = gy*3 + gx) of sum_k E_k psi_k; HAS3/HAS4 drop known zeros
-template <bool HAS3, bool HAS4>
-__device__ __forceinline__ void eval_gp(const double E[6], double e[9]) {
-    const double c0 = HAS4 ? fma(E[4], kQ, E[0]) : E[0];
-    const double c1 = HAS4 ? fma(E[4], kQ0, E[0]) : E[0];
-    const double t2 = kA * E[2], t5 = kA * E[5];
-    const double Av[3] = {c0 - t2, c1, c0 + t2};
-    const double Bv[3] = {E[1] - t5, E[1], E[1] + t5};
+template <bool HAS3, bool HAS4, typename T>
+__device__ __forceinline__ void eval_gp(const T E[6], T e[9]) {
+    const T a = T(kA), q = T(kQ), q0 = T(kQ0);
+    const T c0 = HAS4 ? fma(E[4], q, E[0]) : E[0];
+    const T c1 = HAS4 ? fma(E[4], q0, E[0]) : E[0];
+    const T t2 = a * E[2], t5 = a * E[5];
+    const T Av[3] = {c0 - t2, c1, c0 + t2};
+    const T Bv[3] = {E[1] - t5, E[1], E[1] + t5};
 #pragma unroll
     for (int gy = 0; gy < 3; ++gy) {
-        const double Pq = HAS3 ? fma(E[3], kQ, Av[gy]) : Av[gy];
-        e[gy * 3 + 0] = fma(-kA, Bv[gy], Pq);
-        e[gy * 3 + 2] = fma(kA, Bv[gy], Pq);
-        e[gy * 3 + 1] = HAS3 ? fma(E[3], kQ0, Av[gy]) : Av[gy];
+        const T Pq = HAS3 ? fma(E[3], q, Av[gy]) : Av[gy];
+        e[gy * 3 + 0] = fma(-a, Bv[gy], Pq);
+        e[gy * 3 + 2] = fma(a, Bv[gy], Pq);
+        e[gy * 3 + 1] = HAS3 ? fma(E[3], q0, Av[gy]) : Av[gy];
     }
 }
 // S_k <- fac S_k + sc * (R G)_k  (R = M_ref^{-1} psi_k(g) w_g) by 1D moments
-__device__ __forceinline__ void project(const double G[9], double sc, double fac, double S[6]) {
-    double X0[3], X1[3], X2[3];
+template <typename T>
+__device__ __forceinline__ void project(const T G[9], double sc, T fac, T S[6]) {
+    T X0[3], X1[3], X2[3];
 #pragma unroll
     for (int gy = 0; gy < 3; ++gy) {
-        const double s = G[gy * 3] + G[gy * 3 + 2], d = G[gy * 3 + 2] - G[gy * 3], m = G[gy * 3 + 1];
-        X0[gy] = fma(5.0, s, 8.0 * m);
+        const T s = G[gy * 3] + G[gy * 3 + 2], d = G[gy * 3 + 2] - G[gy * 3], m = G[gy * 3 + 1];
+        X0[gy] = fma(T(5), s, T(8) * m);
         X1[gy] = d;
-        X2[gy] = fma(-2.0, m, s);
+        X2[gy] = fma(T(-2), m, s);
     }
-    const double p0 = fma(5.0, X0[0] + X0[2], 8.0 * X0[1]) * (sc / 324.0);
-    const double p1 = fma(5.0, X1[0] + X1[2], 8.0 * X1[1]) * (sc * kC / 18.0);
-    const double p2 = (X0[2] - X0[0]) * (sc * kC / 18.0);
-    const double p3 = fma(5.0, X2[0] + X2[2], 8.0 * X2[1]) * (sc * 10.0 / 54.0);
-    const double p4 = fma(-2.0, X0[1], X0[0] + X0[2]) * (sc * 10.0 / 54.0);
-    const double p5 = (X1[2] - X1[0]) * (sc * kC * kC);
+    const T p0 = fma(T(5), X0[0] + X0[2], T(8) * X0[1]) * T(sc / 324.0);
+    const T p1 = fma(T(5), X1[0] + X1[2], T(8) * X1[1]) * T(sc * kC / 18.0);
+    const T p2 = (X0[2] - X0[0]) * T(sc * kC / 18.0);
+    const T p3 = fma(T(5), X2[0] + X2[2], T(8) * X2[1]) * T(sc * 10.0 / 54.0);
+    const T p4 = fma(T(-2), X0[1], X0[0] + X0[2]) * T(sc * 10.0 / 54.0);
+    const T p5 = (X1[2] - X1[0]) * T(sc * kC * kC);
     S[0] = fma(fac, S[0], p0); S[1] = fma(fac, S[1], p1); S[2] = fma(fac, S[2], p2);
     S[3] = fma(fac, S[3], p3); S[4] = fma(fac, S[4], p4); S[5] = fma(fac, S[5], p5);
 }
@@ -216,7 +225,7 @@ __device__ __forceinline__ void div_t(const double S[6], double h, double r[3][3
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool REPL, int STAGES, typename SF>
+template <bool REPL, int STAGES, typename SF, typename CT>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
     using Stage = K2Stage<SF>;
     constexpr int AL = K2Cols<SF>::ALIGN;
@@ -326,20 +335,21 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             Vy[jy][0] = b2.x; Vy[jy][1] = b2.y; Vy[jy][2] = t.vy[jy][2 * lane + 2];
         }
         // ---- strain (Table 1 "strain"): DG coefficients, then Gauss-point values
-        double e11[9], e12[9], e22[9];
+        CT e11[9], e12[9], e22[9];
         {
-            double Es[6], Et[6], E[6];
-            strain_s(Vx, Es);
+            CT Es[6], Et[6], E[6];
+            const CT cihx = (CT)ihx, cihy = (CT)ihy;
+            strain_s<CT>(Vx, Es);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) E[k] = ihx * Es[k];
+            for (int k = 0; k < 6; ++k) E[k] = cihx * Es[k];
             eval_gp<false, true>(E, e11);
-            strain_t(Vy, Et);
+            strain_t<CT>(Vy, Et);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) E[k] = ihy * Et[k];
+            for (int k = 0; k < 6; ++k) E[k] = cihy * Et[k];
             eval_gp<true, false>(E, e22);
-            strain_t(Vx, Et);
-            strain_s(Vy, Es);
-            const double hx2 = 0.5 * ihx, hy2 = 0.5 * ihy;
+            strain_t<CT>(Vx, Et);
+            strain_s<CT>(Vy, Es);
+            const CT hx2 = CT(0.5) * cihx, hy2 = CT(0.5) * cihy;
 #pragma unroll
             for (int k = 0; k < 6; ++k) E[k] = fma(hy2, Et[k], hx2 * Es[k]);
             eval_gp<true, true>(E, e12);
@@ -347,28 +357,33 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in:
         //      g11 = alpha^{-1} (P/Delta (5/8 e11 + 3/8 e22) - P/2) = ph (rD (1.25 e11 + 0.75 e22) - 1)
         //      g12 = alpha^{-1} P/Delta e12/4 = (ph rD e12) / 2 (the 1/2 goes into the projection)
+        const CT cdmin2 = (CT)a.dmin2, chA = (CT)hA;
 #pragma unroll
         for (int g = 0; g < 9; ++g) {
-            const double x = e11[g], y = e22[g], z = e12[g];
-            const double draw2 = fma(z, z, fma(1.5 * x, y, 1.25 * fma(x, x, y * y)));
-            const double rD = rsqrt_nr(draw2 + a.dmin2);
-            const double ph = (double)t.Pg[g][eo + lane] * hA;
-            const double pr = ph * rD;
+            const CT x = e11[g], y = e22[g], z = e12[g];
+            const CT draw2 = fma(z, z, fma(CT(1.5) * x, y, CT(1.25) * fma(x, x, y * y)));
+            const CT rD = rsqrt_t(draw2 + cdmin2);
+            const CT ph = (CT)t.Pg[g][eo + lane] * chA;
+            const CT pr = ph * rD;
             // replacement pressure (R#4): P_r/2 = (P/2) Draw/Delta, Draw = draw2 * rsqrt(draw2)
-            const double sub = REPL ? pr * (draw2 > 0.0 ? draw2 * rsqrt_nr(draw2) : 0.0) : ph;
-            e11[g] = fma(pr, fma(1.25, x, 0.75 * y), -sub);
-            e22[g] = fma(pr, fma(1.25, y, 0.75 * x), -sub);
+            const CT sub = REPL ? pr * (draw2 > CT(0) ? draw2 * rsqrt_t(draw2) : CT(0)) : ph;
+            e11[g] = fma(pr, fma(CT(1.25), x, CT(0.75) * y), -sub);
+            e22[g] = fma(pr, fma(CT(1.25), y, CT(0.75) * x), -sub);
             e12[g] = pr * z;
         }
-        double S11[6], S12[6], S22[6];
+        CT C11[6], C12[6], C22[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-            S11[k] = (double)t.S[k][eo + lane]; S12[k] = (double)t.S[6 + k][eo + lane];
-            S22[k] = (double)t.S[12 + k][eo + lane];
+            C11[k] = (CT)t.S[k][eo + lane]; C12[k] = (CT)t.S[6 + k][eo + lane];
+            C22[k] = (CT)t.S[12 + k][eo + lane];
         }
-        project(e11, 1.0, fac, S11);
-        project(e12, 0.5, fac, S12);
-        project(e22, 1.0, fac, S22);
+        const CT cfac = (CT)fac;
+        project(e11, 1.0, cfac, C11);
+        project(e12, 0.5, cfac, C12);
+        project(e22, 1.0, cfac, C22);
+        double S11[6], S12[6], S22[6];   // the divergence and velocity stay FP64
+#pragma unroll
+        for (int k = 0; k < 6; ++k) { S11[k] = (double)C11[k]; S12[k] = (double)C12[k]; S22[k] = (double)C22[k]; }
         const bool evalid = ix >= 0 && ix < a.nx;
         if (!cur.ring && evalid && lane >= 1) {
             const int64_t e = (int64_t)lr * a.epitch + ix;

@@ -109,14 +109,19 @@ def test_fused_variants_agree(nx):
     assert max(e.values()) < 1e-12, e
 
 
-@pytest.mark.parametrize("nsub,tol_s,tol_v", [(1, 1e-6, 1e-8), (20, 1e-5, 1e-6)])
-def test_fp32_storage_variant(nx, ora, nsub, tol_s, tol_v):
-    """NEXT-3: S and P_g stored in FP32 (arithmetic and v in FP64).  Tolerance from FP32
-    rounding (unit roundoff 6e-8 per store, amplified over the subcycles): S <= 1e-6 after one
-    subcycle / 1e-5 after 20; v increments <= 1e-8 / 1e-6."""
+@pytest.mark.parametrize("prec,nsub,tol_s,tol_v", [(1, 1, 1e-6, 1e-8), (1, 20, 1e-5, 1e-6),
+                                                   (2, 1, 4e-4, 4e-4), (2, 20, 4e-4, 4e-4)])
+def test_fp32_variant(nx, ora, prec, nsub, tol_s, tol_v):
+    """NEXT-3.  prec 1: S and P_g stored in FP32 (arithmetic and v in FP64); tolerance
+    from FP32 rounding (unit roundoff 6e-8 per store, amplified over the subcycles): S <= 1e-6
+    after one subcycle / 1e-5 after 20; v increments <= 1e-8 / 1e-6.  prec 2: additionally the
+    stress update (strain, Listing 2, projection) in FP32 arithmetic: the strain's rounding is
+    amplified by the VP law's P/Delta.  DESIGN.md §4 measures that amplification in FP64 (the
+    oracle's plain/FMA floor 7.5e-13 = kappa u64 with kappa ~ 6.8e3 on this case), so the bound is
+    kappa u32 = 6.8e3 * 6e-8 = 4e-4 (measured 1.4e-5 after 1 subcycle, 1.5e-6 after 20)."""
     nxe, nye, lx, ly = 64, 56, 128e3, 112e3
     st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
-    got = _gpu_run(nx, st, nxe, nye, 2, 6, 6, nsub, lx, ly, options={nx.OPT_PRECISION: 1})
+    got = _gpu_run(nx, st, nxe, nye, 2, 6, 6, nsub, lx, ly, options={nx.OPT_PRECISION: prec})
     ref = ora.subcycles(ora_mesh(nxe, nye, 2, 6, 6, lx, ly), ora_params(nx.PhysParams()), nsub, st)
     e = parity(got, ref, st)
     assert e["S"] <= tol_s and e["dS"] <= tol_s and e["dv"] <= tol_v, e
