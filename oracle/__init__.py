@@ -154,7 +154,7 @@ class Oracle:
         return x[:ngp].copy(), w[:ngp].copy()
 
     def dg_basis(self, n: int, s: float, t: float) -> np.ndarray:
-        out = np.zeros(6)
+        out = np.zeros(8)
         self.L.ora_dg_basis(n, C.c_double(s), C.c_double(t), _ptr(out))
         return out[:n].copy()
 

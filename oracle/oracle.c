@@ -29,7 +29,7 @@
 #include <omp.h>
 #endif
 
-#define MAXN 6      /* max DG dofs      */
+#define MAXN 8      /* max DG dofs      */
 #define MAXCG 9     /* max CG dofs      */
 #define MAXG 9      /* max Gauss points */
 
@@ -76,24 +76,27 @@ int ora_gauss(int ngp, double* x, double* w) {
 }
 
 /* DG basis, R#5: centred Legendre on the reference square, S = s-1/2, T = t-1/2:
- * {1, S, T, S^2-1/12, T^2-1/12, S*T}, first n of them.  PSI_1_1 = {1.0}. */
+ * {1, S, T, S^2-1/12, T^2-1/12, S*T}, first n of them.  PSI_1_1 = {1.0}.
+ * n = 8 (R#24): + (S^2-1/12) T, S (T^2-1/12) -- the full gradient space of Q2. */
 void ora_dg_basis(int n, double s, double t, double* psi) {
     double S = s - 0.5, T = t - 0.5;
-    double all[6];
+    double all[8];
     all[0] = 1.0;
     all[1] = S;
     all[2] = T;
     all[3] = S * S - 1.0 / 12.0;
     all[4] = T * T - 1.0 / 12.0;
     all[5] = S * T;
+    all[6] = (S * S - 1.0 / 12.0) * T;
+    all[7] = S * (T * T - 1.0 / 12.0);
     for (int k = 0; k < n; ++k) psi[k] = all[k];
 }
 
 /* Reference-coordinate gradient of the DG basis above. */
 static void ora_dg_basis_grad(int n, double s, double t, double* dpsids, double* dpsidt) {
     double S = s - 0.5, T = t - 0.5;
-    double ds[6] = {0.0, 1.0, 0.0, 2.0 * S, 0.0, T};
-    double dt[6] = {0.0, 0.0, 1.0, 0.0, 2.0 * T, S};
+    double ds[8] = {0.0, 1.0, 0.0, 2.0 * S, 0.0, T, 2.0 * S * T, T * T - 1.0 / 12.0};
+    double dt[8] = {0.0, 0.0, 1.0, 0.0, 2.0 * T, S, S * S - 1.0 / 12.0, 2.0 * S * T};
     for (int k = 0; k < n; ++k) { dpsids[k] = ds[k]; dpsidt[k] = dt[k]; }
 }
 
@@ -234,7 +237,7 @@ static int solve_mass(int n, const double* M, double* b) {
 static int check_mesh(const ora_mesh* m) {
     if (!m || m->nx < 1 || m->ny < 1 || !(m->lx > 0) || !(m->ly > 0)) return -1;
     if (m->p == 1 && m->ns != 3) return -2;
-    if (m->p == 2 && m->ns != 6) return -2;
+    if (m->p == 2 && m->ns != 6 && m->ns != 8) return -2;
     if (m->p != 1 && m->p != 2) return -2;
     if (m->na != 1 && m->na != 3 && m->na != 6) return -2;
     if (m->p == 1 && m->na == 6) return -2;

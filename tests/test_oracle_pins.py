@@ -49,14 +49,23 @@ def test_dg_mass_closed_form(ora):
     s, t = sp.symbols("s t")
     S, T = s - sp.Rational(1, 2), t - sp.Rational(1, 2)
     # exact norms of the orthogonal family (closed form)
-    exact = [1, sp.Rational(1, 12), sp.Rational(1, 12), sp.Rational(1, 180), sp.Rational(1, 180), sp.Rational(1, 144)]
-    fam = [sp.Integer(1), S, T, S**2 - sp.Rational(1, 12), T**2 - sp.Rational(1, 12), S * T]
+    exact = [1, sp.Rational(1, 12), sp.Rational(1, 12), sp.Rational(1, 180), sp.Rational(1, 180), sp.Rational(1, 144),
+             sp.Rational(1, 2160), sp.Rational(1, 2160)]
+    fam = [sp.Integer(1), S, T, S**2 - sp.Rational(1, 12), T**2 - sp.Rational(1, 12), S * T,
+           (S**2 - sp.Rational(1, 12)) * T, S * (T**2 - sp.Rational(1, 12))]
     for k, f in enumerate(fam):
         assert sp.integrate(sp.integrate(f * f, (s, 0, 1)), (t, 0, 1)) == exact[k]
+        for l in range(k):   # orthogonal family (R#5, R#24)
+            assert sp.integrate(sp.integrate(f * fam[l], (s, 0, 1)), (t, 0, 1)) == 0
+    for k, f in enumerate(fam):   # the oracle's basis is this family, in this order
+        for (sv, tv) in [(0.1, 0.7), (0.9, 0.35)]:
+            assert abs(ora.dg_basis(8, sv, tv)[k] - float(f.subs({s: sv, t: tv}))) < 1e-15
     for (hx, hy) in [(1.0, 1.0), (2.0, 3.0)]:
         mesh = Mesh(4, 3, lx=4 * hx, ly=3 * hy)
         M = ora.element_mass(mesh, 2, 1, 6, 3)
-        np.testing.assert_allclose(M, np.diag([float(e) for e in exact]) * hx * hy, rtol=1e-14, atol=1e-15)
+        np.testing.assert_allclose(M, np.diag([float(e) for e in exact[:6]]) * hx * hy, rtol=1e-14, atol=1e-15)
+        M8 = ora.element_mass(mesh, 1, 2, 8, 3)
+        np.testing.assert_allclose(M8, np.diag([float(e) for e in exact]) * hx * hy, rtol=1e-14, atol=1e-15)
         M3 = ora.element_mass(mesh, 0, 0, 3, 2)
         np.testing.assert_allclose(M3, np.diag([1, 1 / 12, 1 / 12]) * hx * hy, rtol=1e-14, atol=1e-15)
 
@@ -96,7 +105,7 @@ def test_lumped_mass_closed_form(ora, p, ns):
     """O7: int phi_j = |K| x {1/4} (Q1) or {1/36, 1/9, 4/9} (Q2 corner/edge/centre);
     assembled masses follow by adjacency; sum = Lx Ly."""
     nx, ny, lx, ly = 4, 3, 8.0, 9.0
-    mesh = Mesh(nx, ny, lx=lx, ly=ly, p=p, ns=ns, na=ns)
+    mesh = Mesh(nx, ny, lx=lx, ly=ly, p=p, ns=ns, na=min(ns, 6))
     m = ora.lumped_mass(mesh)
     K = (lx / nx) * (ly / ny)
     w1 = {1: [0.5, 0.5], 2: [1 / 6, 2 / 3, 1 / 6]}[p]  # 1D integrals of the Lagrange basis
@@ -122,20 +131,20 @@ def _nodal(mesh, f):
     return f(X, Y)
 
 
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_strain_constant_velocity_is_zero(ora, p, ns):
     """north_star pin: zero strain rate for constant velocity."""
-    mesh = Mesh(5, 4, lx=50e3, ly=40e3, p=p, ns=ns, na=ns)
+    mesh = Mesh(5, 4, lx=50e3, ly=40e3, p=p, ns=ns, na=min(ns, 6))
     vx = np.full(mesh.node_shape, 0.37); vy = np.full(mesh.node_shape, -0.21)
     for E in ora.strain(mesh, vx, vy):
         assert np.abs(E).max() < 1e-13 * 0.37 / 1e4
 
 
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_strain_linear_velocity_exact(ora, p, ns):
     """north_star pin: v = v0 + G x gives E11 = G11, E22 = G22, E12 = (G12 + G21)/2 in the
     constant coefficient and 0 elsewhere (G12 != G21 catches a transposed gradient)."""
-    mesh = Mesh(6, 5, lx=60e3, ly=50e3, p=p, ns=ns, na=ns)
+    mesh = Mesh(6, 5, lx=60e3, ly=50e3, p=p, ns=ns, na=min(ns, 6))
     G = np.array([[3e-6, -7e-6], [5e-6, -2e-6]])
     vx = _nodal(mesh, lambda X, Y: 0.1 + G[0, 0] * X + G[0, 1] * Y)
     vy = _nodal(mesh, lambda X, Y: -0.05 + G[1, 0] * X + G[1, 1] * Y)
@@ -166,8 +175,9 @@ def _brute_strain(mesh, vx, vy):
     q, w = 0.5 * (xi + 1), 0.5 * wi
     L, dL = _lagrange_1d(p)
     fam = [lambda S, T: 1 + 0 * S, lambda S, T: S, lambda S, T: T, lambda S, T: S * S - 1 / 12,
-           lambda S, T: T * T - 1 / 12, lambda S, T: S * T][:ns]
-    norm = np.array([1, 1 / 12, 1 / 12, 1 / 180, 1 / 180, 1 / 144])[:ns]
+           lambda S, T: T * T - 1 / 12, lambda S, T: S * T, lambda S, T: (S * S - 1 / 12) * T,
+           lambda S, T: S * (T * T - 1 / 12)][:ns]
+    norm = np.array([1, 1 / 12, 1 / 12, 1 / 180, 1 / 180, 1 / 144, 1 / 2160, 1 / 2160])[:ns]
     out = [np.zeros((mesh.n_elem, ns)) for _ in range(3)]
     for iy in range(mesh.ny):
         for ix in range(mesh.nx):
@@ -190,10 +200,10 @@ def _brute_strain(mesh, vx, vy):
     return out  # order E11, E12, E22
 
 
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_strain_brute_force(ora, p, ns):
     """north_star pin (brute force on tiny meshes): random nodal v on a 3x2 mesh."""
-    mesh = Mesh(3, 2, lx=3e3, ly=2.5e3, p=p, ns=ns, na=ns)
+    mesh = Mesh(3, 2, lx=3e3, ly=2.5e3, p=p, ns=ns, na=min(ns, 6))
     vx = RNG.uniform(-0.2, 0.2, mesh.node_shape); vy = RNG.uniform(-0.2, 0.2, mesh.node_shape)
     got = ora.strain(mesh, vx, vy)
     ref = _brute_strain(mesh, vx, vy)
@@ -218,6 +228,40 @@ def test_strain_quadratic_cg2_exact(ora):
             np.testing.assert_allclose(E12[e], [0.5 * xc, 0.5, 0, 0, 0, 0], atol=1e-12)
 
 
+@pytest.mark.parametrize("ns,exact", [(8, True), (6, False)])
+def test_strain_ns8_is_the_gradient_space_of_q2(ora, ns, exact):
+    """R#24 (stress "in the gradient of the velocity space"): with n_S = 8 the DG strain of
+    ANY CG2 velocity equals its symmetric gradient pointwise (the L2 projection onto a space that
+    contains it); with n_S = 6 it does not (the S T^2, S^2 T parts are lost).  The pointwise
+    gradient comes from independent Vandermonde Lagrange bases, the DG evaluation from sympy's
+    family in R#24's order."""
+    mesh = Mesh(3, 2, lx=3e3, ly=2.5e3, p=2, ns=ns, na=6)
+    r = np.random.default_rng(11)
+    vx = r.uniform(-0.2, 0.2, mesh.node_shape); vy = r.uniform(-0.2, 0.2, mesh.node_shape)
+    E11, E12, E22 = ora.strain(mesh, vx, vy)
+    hx, hy = mesh.lx / mesh.nx, mesh.ly / mesh.ny
+    L, dL = _lagrange_1d(2)
+    fam = [lambda S, T: 1 + 0 * S, lambda S, T: S, lambda S, T: T, lambda S, T: S * S - 1 / 12,
+           lambda S, T: T * T - 1 / 12, lambda S, T: S * T, lambda S, T: (S * S - 1 / 12) * T,
+           lambda S, T: S * (T * T - 1 / 12)][:ns]
+    worst = 0.0
+    scale = 0.2 / min(hx, hy)
+    for iy in range(mesh.ny):
+        for ix in range(mesh.nx):
+            e = iy * mesh.nx + ix
+            ux = vx[2 * iy:2 * iy + 3, 2 * ix:2 * ix + 3]; uy = vy[2 * iy:2 * iy + 3, 2 * ix:2 * ix + 3]
+            for (sv, tv) in r.uniform(0, 1, (5, 2)):
+                Ls, Lt, dLs, dLt = L(sv), L(tv), dL(sv), dL(tv)
+                g = ((Lt @ ux @ dLs) / hx, 0.5 * ((dLt @ ux @ Ls) / hy + (Lt @ uy @ dLs) / hx), (dLt @ uy @ Ls) / hy)
+                psi = np.array([f(sv - 0.5, tv - 0.5) for f in fam])
+                for Ec, gc in zip((E11, E12, E22), g):
+                    worst = max(worst, abs(Ec[e] @ psi - gc) / scale)
+    if exact:
+        assert worst < 1e-13, worst
+    else:
+        assert worst > 1e-3, worst
+
+
 # ---------------------------------------------------------------- stress
 def _stress_inputs(mesh, seed=3):
     r = np.random.default_rng(seed)
@@ -229,7 +273,7 @@ def _stress_inputs(mesh, seed=3):
     return E, H, A, S
 
 
-@pytest.mark.parametrize("p,ns,na", [(1, 3, 3), (2, 6, 6), (2, 6, 1)])
+@pytest.mark.parametrize("p,ns,na", [(1, 3, 3), (2, 6, 6), (2, 6, 1), (2, 8, 6)])
 def test_stress_zero_thickness_decays_exactly(ora, p, ns, na):
     """SPEC S:317 / Listing 1: H = 0 -> P = 0 -> S <- (1 - 1/alpha) S exactly."""
     mesh = Mesh(3, 3, lx=3e3, ly=3e3, p=p, ns=ns, na=na)
@@ -350,10 +394,10 @@ def test_stress_clamps(ora):
 
 
 # ---------------------------------------------------------------- divergence
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_divergence_constant_stress_interior_zero(ora, p, ns):
     """north_star pin: zero divergence of a constant interior stress."""
-    mesh = Mesh(5, 4, lx=5e3, ly=4e3, p=p, ns=ns, na=ns)
+    mesh = Mesh(5, 4, lx=5e3, ly=4e3, p=p, ns=ns, na=min(ns, 6))
     N = mesh.n_elem
     S = [np.zeros((N, ns)) for _ in range(3)]
     S[0][:, 0], S[1][:, 0], S[2][:, 0] = 1200.0, -300.0, 700.0
@@ -362,12 +406,12 @@ def test_divergence_constant_stress_interior_zero(ora, p, ns):
     assert np.abs(Fx[:, 0]).max() > 1.0  # boundary traction is not zero
 
 
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_divergence_linear_stress(ora, p, ns):
     """Linear sigma: F_j / m_j = div sigma exactly at interior nodes (lumped mass, exact quadrature).
     sigma11 = a x, sigma12 = b y, sigma22 = d y  ->  div sigma = (a + b, d)."""
     nx, ny, lx, ly = 5, 4, 5e3, 4e3
-    mesh = Mesh(nx, ny, lx=lx, ly=ly, p=p, ns=ns, na=ns)
+    mesh = Mesh(nx, ny, lx=lx, ly=ly, p=p, ns=ns, na=min(ns, 6))
     hx, hy = lx / nx, ly / ny
     a, b, d = 3.0, -2.0, 5.0
     S = [np.zeros((mesh.n_elem, ns)) for _ in range(3)]
@@ -384,18 +428,18 @@ def test_divergence_linear_stress(ora, p, ns):
     np.testing.assert_allclose((Fy / m)[1:-1, 1:-1], d, rtol=1e-10)
 
 
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_divergence_strain_adjointness(ora, p, ns):
     """Identity of the weak forms: sum_j v_j . F_j = -sum_K int sigma : eps(v) = -sum_K |K| sum_k
     ||psi_k||^2 (S11 E11 + 2 S12 E12 + S22 E22)_k (sigma in the DG space, exact quadrature).
     A sign or transposition error in either the strain or the divergence breaks it."""
-    mesh = Mesh(4, 3, lx=4e3, ly=3e3, p=p, ns=ns, na=ns)
+    mesh = Mesh(4, 3, lx=4e3, ly=3e3, p=p, ns=ns, na=min(ns, 6))
     vx = RNG.uniform(-1, 1, mesh.node_shape); vy = RNG.uniform(-1, 1, mesh.node_shape)
     S = [RNG.uniform(-1, 1, (mesh.n_elem, ns)) for _ in range(3)]
     E11, E12, E22 = ora.strain(mesh, vx, vy)
     Fx, Fy = ora.divergence(mesh, *S)
     lhs = (vx * Fx + vy * Fy).sum()
-    norm = np.array([1, 1 / 12, 1 / 12, 1 / 180, 1 / 180, 1 / 144])[:ns]
+    norm = np.array([1, 1 / 12, 1 / 12, 1 / 180, 1 / 180, 1 / 144, 1 / 2160, 1 / 2160])[:ns]
     K = 1e6
     rhs = -K * ((S[0] * E11 + 2 * S[1] * E12 + S[2] * E22) * norm).sum()
     assert abs(lhs - rhs) < 1e-12 * max(abs(lhs), 1.0) * 10
@@ -405,7 +449,7 @@ def test_divergence_brute_force(ora):
     """Brute force (tiny mesh): F = -int sigma . grad phi with an 8-point numpy rule and
     Vandermonde Lagrange bases, assembled by scatter over elements."""
     p, ns = 2, 6
-    mesh = Mesh(3, 2, lx=3e3, ly=2.5e3, p=p, ns=ns, na=ns)
+    mesh = Mesh(3, 2, lx=3e3, ly=2.5e3, p=p, ns=ns, na=min(ns, 6))
     hx, hy = 1e3, 1.25e3
     S = [RNG.uniform(-1, 1, (mesh.n_elem, ns)) for _ in range(3)]
     xi, wi = np.polynomial.legendre.leggauss(8)
@@ -698,11 +742,11 @@ def _node_xy(mesh, V):
     return X, Y
 
 
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_distorted_strain_linear_velocity(ora, p, ns):
     """A physically linear velocity is reproduced by the (sub)parametric CG space on a bilinear
     mesh, so E = sym(G) in the constant coefficient and 0 elsewhere."""
-    mesh, V = _dmesh(p=p, ns=ns, na=ns)
+    mesh, V = _dmesh(p=p, ns=ns, na=min(ns, 6))
     X, Y = _node_xy(mesh, V)
     G = np.array([[3e-6, -7e-6], [5e-6, -2e-6]])
     E11, E12, E22 = ora.strain(mesh, 0.1 + G[0, 0] * X + G[0, 1] * Y, -0.05 + G[1, 0] * X + G[1, 1] * Y)
