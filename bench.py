@@ -183,6 +183,8 @@ def main():
                     help="NEXT-3: as --fp32-storage plus the stress update (strain, Listing 2, projection) in FP32")
     ap.add_argument("--moving", action="store_true",
                     help="NEXT-2: regenerate the moving-cyclone forcing on the GPU at every outer step (P:350 protocol)")
+    ap.add_argument("--ns", type=int, default=None, choices=[6, 8],
+                    help="NEXT-4: n_S = 8 stress space (full gradient space of Q2, table-driven fused kernel)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-window", type=int, default=512, help="oracle window per --impl reference step")
     ap.add_argument("--cpu-window", type=int, default=640, help="oracle window of the cpu_baseline sample")
@@ -195,6 +197,9 @@ def main():
                             cfg.kind, cfg.advect, cfg.alpha)
     if args.nsub:
         cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, args.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect,
+                            cfg.alpha)
+    if args.ns and args.ns != cfg.ns:
+        cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, args.ns, cfg.na, cfg.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect,
                             cfg.alpha)
     if args.impl == "reference":
         return run_reference(args, cfg)
@@ -276,7 +281,8 @@ def main():
     kernel_ms = sub / cfg.nsub
     achieved = bpe * n_el_rank / (kernel_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak_hbm()
-    traffic = ncu_traffic_per_launch()
+    traffic = ncu_traffic_per_launch() if cfg.ns == 6 and not (args.fp32_storage or args.fp32_stress) else None
+    kernel = KERNEL if cfg.ns == 6 else "k_subcycle<2,8> (table-driven fused strain+stress+divergence+velocity, n_S = 8)"
 
     # e2e: the same metric through the C ABI with pinned HOST buffers, copies inside the timed region.
     # The model state (v, S, A, H) lives on the device across outer steps; each outer step's external
@@ -341,7 +347,7 @@ def main():
                        "forcing": "moving cyclone regenerated on the GPU every step" if args.moving else "static (t = 0)",
                        "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},
             "breakdown_ms": {"advect": adv, "prep": prep, "subcycles": sub, "per_subcycle": kernel_ms},
-            "roofline": {"bound": "hbm", "kernel": KERNEL, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bpe * n_el_rank, "bytes_per_element_subcycle": bpe},
             "clocks": clk.summary(),

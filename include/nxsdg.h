@@ -108,7 +108,7 @@ typedef struct {
     int32_t nx, ny;       /* global elements per direction, >= 1                                  */
     double lx, ly;        /* box extents [m], > 0; hx = lx/nx, hy = ly/ny                         */
     int32_t cg_degree;    /* p: 1 | 2                                                             */
-    int32_t n_stress;     /* n_S: 3 with p = 1, 6 with p = 2 (R#6)                                */
+    int32_t n_stress;     /* n_S: 3 with p = 1; 6 (R#6) or 8 (full gradient space of Q2, R#24) with p = 2 */
     int32_t n_adv;        /* n_A: 1 | 3 (p = 1), 1 | 3 | 6 (p = 2) (R#7)                          */
     int32_t bc;           /* nxsdg_bc                                                             */
     int32_t rank, nranks; /* row-strip partition, 1 <= nranks <= ny                               */
@@ -241,10 +241,10 @@ nxsdg_status nxsdg_local_geometry(int32_t nx, int32_t ny, int32_t cg_degree, int
 
 /* ---- introspection ------------------------------------------------------------- */
 /* The K0 reference-element tables of degree p (1|2) as built on the device (row a0), flattened:
- * gx[ngp], gw[ngp] (Gauss rule on [0,1]), psi[6][ng] (DG basis at the Gauss points), phi, dphi/ds,
- * dphi/dt [ncg][ng] (CG basis), mref[6] (reference DG mass), R[6][ng] (iMJwPSI of the reference
- * element), Ds, Dt [ncg][6] (divergence composites); ngp = p+1, ng = ncg = ngp^2.  With out == NULL
- * only *needed is set. */
+ * gx[ngp], gw[ngp] (Gauss rule on [0,1]), psi[nd][ng] (DG basis at the Gauss points), phi, dphi/ds,
+ * dphi/dt [ncg][ng] (CG basis), mref[nd] (reference DG mass), R[nd][ng] (iMJwPSI of the reference
+ * element), Ds, Dt [ncg][nd] (divergence composites); ngp = p+1, ng = ncg = ngp^2, nd = 8 when p = 2
+ * and the context has n_S = 8 (R#24), else 6.  With out == NULL only *needed is set. */
 nxsdg_status nxsdg_debug_reference_tables(nxsdg_ctx* ctx, int32_t p, double* out, int64_t count, int64_t* needed);
 /* Number of kernels this context has launched (for the bench's gpu_launches claim). */
 int64_t nxsdg_kernel_launches(const nxsdg_ctx* ctx);

@@ -268,6 +268,13 @@ int ora_strain(const ora_mesh* m, const double* vx, const double* vy,
         double M[MAXN * MAXN];
         ora_element_mass(m, ix, iy, ns, ngp, M);
         double b11[MAXN] = {0}, b12[MAXN] = {0}, b22[MAXN] = {0};
+        /* grad v_h = sum_j (v_j - c) grad phi_j for any constant c, because the CG basis is a
+         * partition of unity (sum_j grad phi_j = 0).  With c = the element's mean nodal velocity the
+         * sum no longer cancels large equal parts: on smooth fields the plain sum loses ~|v|/|dv| ulps,
+         * which the VP law then amplifies by P/Delta past the parity bar (R#20). */
+        double cx = 0.0, cy = 0.0;
+        for (int j = 0; j < ncg; ++j) { long n = elem_node(m, ix, iy, j); cx += vx[n]; cy += vy[n]; }
+        cx /= ncg; cy /= ncg;
         for (int gy = 0; gy < ngp; ++gy)
             for (int gx = 0; gx < ngp; ++gx) {
                 double s = xg[gx], t = xg[gy], w = wg[gx] * wg[gy];
@@ -280,8 +287,9 @@ int ora_strain(const ora_mesh* m, const double* vx, const double* vy,
                     double gxj, gyj;
                     phys_grad(Jinv, dps[j], dpt[j], &gxj, &gyj);
                     long n = elem_node(m, ix, iy, j);
-                    dvxdx += vx[n] * gxj; dvxdy += vx[n] * gyj;
-                    dvydx += vy[n] * gxj; dvydy += vy[n] * gyj;
+                    double ux = vx[n] - cx, uy = vy[n] - cy;
+                    dvxdx += ux * gxj; dvxdy += ux * gyj;
+                    dvydx += uy * gxj; dvydy += uy * gyj;
                 }
                 double eps11 = dvxdx, eps22 = dvydy, eps12 = 0.5 * (dvxdy + dvydx);
                 double psi[MAXN];

@@ -14,8 +14,9 @@
 
 namespace nxk {
 
-template <int P> struct Deg {
-    static constexpr int NS = (P == 1) ? 3 : 6;   // DG stress dofs (R#6)
+template <int P, int NS_ = (P == 1) ? 3 : 6> struct Deg {
+    static constexpr int NS = NS_;                // DG stress dofs (R#6; 8 = R#24)
+    static constexpr int TAB = tab_index(P, NS_);  // c_tab slot
     static constexpr int NGP = P + 1;             // Listing 2
     static constexpr int NG = NGP * NGP;
     static constexpr int NCG = (P + 1) * (P + 1);
@@ -132,11 +133,11 @@ struct SubArgs {
     int chunk0, chunk_step, nsel;   // chunk selection: chunks chunk0 + i*chunk_step, i < nsel
 };
 
-template <int P>
+template <int P, int NS_ = Deg<P>::NS>
 __global__ void __launch_bounds__(128) k_subcycle(SubArgs a) {
-    using D = Deg<P>;
+    using D = Deg<P, NS_>;
     constexpr int NS = D::NS, NG = D::NG, NCG = D::NCG;
-    const RefTab& T = c_tab[P - 1];
+    const RefTab& T = c_tab[D::TAB];
     const int lane = threadIdx.x & 31;
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int strip = gwarp % a.nstrips, ci = gwarp / a.nstrips;
@@ -349,11 +350,11 @@ struct StepArgs {
 };
 
 // Table 1 "strain": E_c = R . eps_c(g), eps from the CG gradient at the Gauss points.
-template <int P>
+template <int P, int NS_ = Deg<P>::NS>
 __global__ void k_strain(StepArgs a) {
-    using D = Deg<P>;
+    using D = Deg<P, NS_>;
     constexpr int NS = D::NS, NG = D::NG;
-    const RefTab& T = c_tab[P - 1];
+    const RefTab& T = c_tab[D::TAB];
     int ix = blockIdx.x * blockDim.x + threadIdx.x;
     int lr = a.erow_begin + blockIdx.y;
     if (ix >= a.nx || lr >= a.erow_end) return;
@@ -388,11 +389,11 @@ __global__ void k_strain(StepArgs a) {
 }
 
 // Listing 2 literally, with the stored E and P from H, A.
-template <int P, int NA>
+template <int P, int NA, int NS_ = Deg<P>::NS>
 __global__ void k_stress(StepArgs a) {
-    using D = Deg<P>;
+    using D = Deg<P, NS_>;
     constexpr int NS = D::NS, NG = D::NG;
-    const RefTab& T = c_tab[P - 1];
+    const RefTab& T = c_tab[D::TAB];
     int ix = blockIdx.x * blockDim.x + threadIdx.x;
     int lr = a.erow_begin + blockIdx.y;
     if (ix >= a.nx || lr >= a.erow_end) return;
@@ -427,10 +428,10 @@ __global__ void k_stress(StepArgs a) {
 }
 
 // Table 1 "divergence": F_j = -|K| sum_{K ∋ j} (ihx Ds[j].S11 + ihy Dt[j].S12, ...), per-node gather.
-template <int P>
+template <int P, int NS_ = Deg<P>::NS>
 __global__ void k_divergence(StepArgs a) {
-    constexpr int NS = Deg<P>::NS;
-    const RefTab& T = c_tab[P - 1];
+    constexpr int NS = NS_;
+    const RefTab& T = c_tab[Deg<P, NS_>::TAB];
     int I = blockIdx.x * blockDim.x + threadIdx.x;
     int jr = a.node_row_begin + blockIdx.y;
     if (I > P * a.nx || jr >= a.node_row_end) return;

@@ -241,7 +241,8 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     if (d->nranks < 1 || d->nranks > d->ny || d->rank < 0 || d->rank >= d->nranks) return NXSDG_ERR_INVALID_ARG;
     if (d->bc != NXSDG_BC_CLOSED && d->bc != NXSDG_BC_PERIODIC) return NXSDG_ERR_INVALID_ARG;
     bool ok_deg = (d->cg_degree == 1 && d->n_stress == 3 && (d->n_adv == 1 || d->n_adv == 3)) ||
-                  (d->cg_degree == 2 && d->n_stress == 6 && (d->n_adv == 1 || d->n_adv == 3 || d->n_adv == 6));
+                  (d->cg_degree == 2 && (d->n_stress == 6 || d->n_stress == 8) &&
+                   (d->n_adv == 1 || d->n_adv == 3 || d->n_adv == 6));
     if (!ok_deg) return NXSDG_ERR_UNSUPPORTED;
     if (d->bc == NXSDG_BC_PERIODIC && d->nranks > 1) return NXSDG_ERR_UNSUPPORTED;
     if (d->nranks > 1 && d->transport != NXSDG_TRANSPORT_NCCL && d->transport != NXSDG_TRANSPORT_LOOPBACK)
@@ -283,15 +284,16 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     c->c1 = c->nodec; c->rx0 = c->nodec + nn; c->ry0 = c->nodec + 2 * nn; c->cafo = c->nodec + 3 * nn;
     c->ox = c->nodec + 4 * nn; c->oy = c->nodec + 5 * nn;
 #undef AL
-    // K0: reference-element tables into __constant__ (both degrees; tiny)
+    // K0: reference-element tables into __constant__ (all three spaces; tiny)
     {
         RefTab* dtab = nullptr;
         if (cudaMalloc(&dtab, sizeof(RefTab)) != cudaSuccess) return bail(NXSDG_ERR_OOM);
         cudaMemsetAsync(dtab, 0, sizeof(RefTab), c->stream);   // struct padding is never written by K0
-        for (int p = 1; p <= 2; ++p) {
-            k_build_tables<<<1, 32, 0, c->stream>>>(dtab, p);
+        const int spaces[3][2] = {{1, 3}, {2, 6}, {2, 8}};
+        for (const auto& sp : spaces) {
+            k_build_tables<<<1, 32, 0, c->stream>>>(dtab, sp[0], sp[1]);
             ++c->launches;
-            if (cudaMemcpyToSymbolAsync(c_tab, dtab, sizeof(RefTab), (p - 1) * sizeof(RefTab),
+            if (cudaMemcpyToSymbolAsync(c_tab, dtab, sizeof(RefTab), tab_index(sp[0], sp[1]) * sizeof(RefTab),
                                         cudaMemcpyDeviceToDevice, c->stream) != cudaSuccess) {
                 cudaFree(dtab); return bail(NXSDG_ERR_CUDA);
             }
@@ -375,8 +377,8 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             c->dynamic = (int)value; break;
         case NXSDG_OPT_PRECISION:
             if (value < 0 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "precision 0|1|2");
-            if (value >= 1 && (c->P != 2 || c->d.nranks != 1))
-                return fail(c, NXSDG_ERR_UNSUPPORTED, "FP32 storage: CG2/DG2, single rank");
+            if (value >= 1 && (c->P != 2 || c->NS != 6 || c->d.nranks != 1))
+                return fail(c, NXSDG_ERR_UNSUPPORTED, "FP32 storage: CG2/DG2 (n_S = 6), single rank");
             if (value >= 1 && c->stages > 3) c->stages = 3;
             c->precision = (int)value; c->pg32_ok = false; break;
         case NXSDG_OPT_MAP_MODE:
@@ -674,6 +676,7 @@ extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64
     GUARD(c);
     if (!xy || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE)) return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
     if (c->d.nranks != 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads are single-rank");
+    if (c->NS == 8) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: n_S = 3 | 6");
     const int64_t need = 2 * (int64_t)(c->d.nx + 1) * (c->d.ny + 1);
     if (count != need) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)need);
     if (!c->verts) CU(cudaMalloc(&c->verts, need * sizeof(double)));
@@ -1045,8 +1048,9 @@ static nxsdg_status build_maps(nxsdg_ctx* c) {
     const cuuint64_t nx = c->d.nx, er = c->erows_local, ncols = 2 * (cuuint64_t)c->d.nx + 1, nr = c->nrows_local;
     const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 8, (cuuint64_t)c->eplane * 8};
     const cuuint64_t ns[2] = {(cuuint64_t)c->npitch * 8, (cuuint64_t)c->nn * 8};
-    const cuuint64_t dS[3] = {nx, er, 18}, dP[3] = {nx, er, 9}, dV[2] = {ncols, nr}, dC[3] = {ncols, nr, 6};
-    const cuuint32_t bS[3] = {K2Cols<double>::E, 1, 18}, bP[3] = {K2Cols<double>::E, 1, 9}, bV[2] = {K2_VCOLS, 3},
+    const cuuint64_t nS = 3 * (cuuint64_t)c->NS;
+    const cuuint64_t dS[3] = {nx, er, nS}, dP[3] = {nx, er, 9}, dV[2] = {ncols, nr}, dC[3] = {ncols, nr, 6};
+    const cuuint32_t bS[3] = {K2Cols<double>::E, 1, (cuuint32_t)nS}, bP[3] = {K2Cols<double>::E, 1, 9}, bV[2] = {K2_VCOLS, 3},
                      bC[3] = {K2_CCOLS, 2, 6};
     for (int v = 0; v < 2; ++v)
         for (int s = 0; s < 2; ++s) {
@@ -1080,8 +1084,9 @@ static nxsdg_status build_maps32(nxsdg_ctx* c) {
     if (!c->Pg32) CU(cudaMalloc(&c->Pg32, (size_t)c->NG * ne * sizeof(float)));
     const cuuint64_t nx = c->d.nx, er = c->erows_local;
     const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 4, (cuuint64_t)c->eplane * 4};
-    const cuuint64_t dS[3] = {nx, er, 18}, dP[3] = {nx, er, 9};
-    const cuuint32_t bS[3] = {K2Cols<float>::E, 1, 18}, bP[3] = {K2Cols<float>::E, 1, 9};
+    const cuuint64_t nS = 3 * (cuuint64_t)c->NS;
+    const cuuint64_t dS[3] = {nx, er, nS}, dP[3] = {nx, er, 9};
+    const cuuint32_t bS[3] = {K2Cols<float>::E, 1, (cuuint32_t)nS}, bP[3] = {K2Cols<float>::E, 1, 9};
     for (int v = 0; v < 2; ++v)
         for (int s = 0; s < 2; ++s) {
             K2Maps& M = c->maps32[v][s];
@@ -1106,25 +1111,25 @@ static nxsdg_status cvt(nxsdg_ctx* c, const float* src, double* dst, int64_t n) 
 
 static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0; }
 
-template <bool R, int ST, typename SF, typename CT = double>
+template <bool R, int ST, typename SF, typename CT = double, int NS = 6>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
-    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage<SF>) + sizeof(uint64_t) + sizeof(int4));
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage<SF, NS>) + sizeof(uint64_t) + sizeof(int4));
     static bool attr = false;
     if (!attr) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT>, 32 * K2_WARPS, smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS>, 32 * K2_WARPS, smem));
     const int cap = c->ctas_per_sm < 0 ? (sizeof(SF) == 8 ? 2 : 4) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF, CT><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
+    k_subcycle_tma<R, ST, SF, CT, NS><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
     return NXSDG_OK;
 }
 
@@ -1170,6 +1175,16 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int 
             default: return launch_tma_t<true, 3, float>(c, cv, cs, a);
         }
     }
+    if (c->NS == 8) {
+        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
+            case 4: return launch_tma_t<false, 2, double, double, 8>(c, cv, cs, a);
+            case 5: return launch_tma_t<true, 2, double, double, 8>(c, cv, cs, a);
+            case 6: return launch_tma_t<false, 3, double, double, 8>(c, cv, cs, a);
+            case 7: return launch_tma_t<true, 3, double, double, 8>(c, cv, cs, a);
+            case 8: return launch_tma_t<false, 4, double, double, 8>(c, cv, cs, a);
+            default: return launch_tma_t<true, 4, double, double, 8>(c, cv, cs, a);
+        }
+    }
     switch (c->stages * 2 + (a.repl ? 1 : 0)) {
         case 4: return launch_tma_t<false, 2, double>(c, cv, cs, a);
         case 5: return launch_tma_t<true, 2, double>(c, cv, cs, a);
@@ -1192,6 +1207,7 @@ static nxsdg_status launch_subcycle_sel(nxsdg_ctx* c, int sel) {
         const int64_t warps = (int64_t)a.nstrips * a.nsel;
         const unsigned blocks = (unsigned)((warps + 3) / 4);
         if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
+        else if (c->NS == 8) k_subcycle<2, 8><<<blocks, 128, 0, c->stream>>>(a);
         else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
     }
     LAUNCHED();
@@ -1251,15 +1267,15 @@ static StepArgs step_args(nxsdg_ctx* c) {
     return a;
 }
 
-template <int P, int NA>
+template <int P, int NA, int NS = Deg<P>::NS>
 static nxsdg_status launch_step_t(nxsdg_ctx* c, nxsdg_step st) {
     StepArgs a = step_args(c);
     dim3 be(128), ge((unsigned)((c->d.nx + 127) / 128), (unsigned)c->nown);
     dim3 bn(128), gn((unsigned)((P * c->d.nx + 1 + 127) / 128), (unsigned)(a.node_row_end - a.node_row_begin));
     switch (st) {
-        case NXSDG_STEP_STRAIN: k_strain<P><<<ge, be, 0, c->stream>>>(a); break;
-        case NXSDG_STEP_STRESS: k_stress<P, NA><<<ge, be, 0, c->stream>>>(a); break;
-        case NXSDG_STEP_DIVERGENCE: k_divergence<P><<<gn, bn, 0, c->stream>>>(a); break;
+        case NXSDG_STEP_STRAIN: k_strain<P, NS><<<ge, be, 0, c->stream>>>(a); break;
+        case NXSDG_STEP_STRESS: k_stress<P, NA, NS><<<ge, be, 0, c->stream>>>(a); break;
+        case NXSDG_STEP_DIVERGENCE: k_divergence<P, NS><<<gn, bn, 0, c->stream>>>(a); break;
         case NXSDG_STEP_VELOCITY: k_velocity<P><<<gn, bn, 0, c->stream>>>(a); break;
     }
     LAUNCHED();
@@ -1269,6 +1285,11 @@ static nxsdg_status launch_step_t(nxsdg_ctx* c, nxsdg_step st) {
 
 static nxsdg_status launch_step(nxsdg_ctx* c, nxsdg_step st) {
     if (c->P == 1) return c->NA == 1 ? launch_step_t<1, 1>(c, st) : launch_step_t<1, 3>(c, st);
+    if (c->NS == 8) {
+        if (c->NA == 1) return launch_step_t<2, 1, 8>(c, st);
+        if (c->NA == 3) return launch_step_t<2, 3, 8>(c, st);
+        return launch_step_t<2, 6, 8>(c, st);
+    }
     if (c->NA == 1) return launch_step_t<2, 1>(c, st);
     if (c->NA == 3) return launch_step_t<2, 3>(c, st);
     return launch_step_t<2, 6>(c, st);
@@ -1340,6 +1361,7 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
                 const int nchunks = (c->nown + a.ty - 1) / a.ty;
                 const unsigned blocks = (unsigned)(((int64_t)a.nstrips * nchunks + 3) / 4);
                 if (c->P == 1) k_subcycle<1><<<blocks, 128, 0, c->stream>>>(a);
+                else if (c->NS == 8) k_subcycle<2, 8><<<blocks, 128, 0, c->stream>>>(a);
                 else k_subcycle<2><<<blocks, 128, 0, c->stream>>>(a);
             }
             cv ^= 1; cs ^= 1;
@@ -1487,29 +1509,32 @@ extern "C" nxsdg_status nxsdg_synchronize(nxsdg_ctx* c) {
 }
 
 // ---------------------------------------------------------------- multi-rank plumbing
-// K0 tables for tests (a0): {gx[ngp], gw[ngp], psi[6][ng], phi[ncg][ng], dphis[ncg][ng], dphit[ncg][ng],
-// mref[6], R[6][ng], Ds[ncg][6], Dt[ncg][6]} of degree p, flattened in this order.
+// K0 tables for tests (a0): {gx[ngp], gw[ngp], psi[nd][ng], phi[ncg][ng], dphis[ncg][ng], dphit[ncg][ng],
+// mref[nd], R[nd][ng], Ds[ncg][nd], Dt[ncg][nd]} of degree p, flattened in this order; nd = 8 for the
+// (2, 8) space of a context with n_S = 8 and p = 2, else 6.
 extern "C" nxsdg_status nxsdg_debug_reference_tables(nxsdg_ctx* c, int32_t p, double* out, int64_t count, int64_t* needed) {
     GUARD(c);
     if (p != 1 && p != 2) return fail(c, NXSDG_ERR_INVALID_ARG, "p 1|2");
     const int ngp = p + 1, ng = ngp * ngp, ncg = ng;
-    const int64_t n = 2 * ngp + 6 * ng + 3 * ncg * ng + 6 + 6 * ng + 2 * ncg * 6;
+    const int nd = (p == 2 && c->NS == 8) ? 8 : 6;
+    const int64_t n = 2 * ngp + nd * ng + 3 * ncg * ng + nd + nd * ng + 2 * ncg * nd;
     if (needed) *needed = n;
     if (!out) return NXSDG_OK;
     if (count < n) return fail(c, NXSDG_ERR_INVALID_ARG, "count < %lld", (long long)n);
     RefTab T;
-    CU(cudaMemcpyFromSymbol(&T, c_tab, sizeof(RefTab), (p - 1) * sizeof(RefTab), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyFromSymbol(&T, c_tab, sizeof(RefTab), tab_index(p, p == 2 ? c->NS : 3) * sizeof(RefTab),
+                            cudaMemcpyDeviceToHost));
     int64_t o = 0;
     for (int i = 0; i < ngp; ++i) out[o++] = T.gx[i];
     for (int i = 0; i < ngp; ++i) out[o++] = T.gw[i];
-    for (int k = 0; k < 6; ++k) for (int g = 0; g < ng; ++g) out[o++] = T.psi[k][g];
+    for (int k = 0; k < nd; ++k) for (int g = 0; g < ng; ++g) out[o++] = T.psi[k][g];
     for (int j = 0; j < ncg; ++j) for (int g = 0; g < ng; ++g) out[o++] = T.phi[j][g];
     for (int j = 0; j < ncg; ++j) for (int g = 0; g < ng; ++g) out[o++] = T.dphis[j][g];
     for (int j = 0; j < ncg; ++j) for (int g = 0; g < ng; ++g) out[o++] = T.dphit[j][g];
-    for (int k = 0; k < 6; ++k) out[o++] = T.mref[k];
-    for (int k = 0; k < 6; ++k) for (int g = 0; g < ng; ++g) out[o++] = T.R[k][g];
-    for (int j = 0; j < ncg; ++j) for (int k = 0; k < 6; ++k) out[o++] = T.Ds[j][k];
-    for (int j = 0; j < ncg; ++j) for (int k = 0; k < 6; ++k) out[o++] = T.Dt[j][k];
+    for (int k = 0; k < nd; ++k) out[o++] = T.mref[k];
+    for (int k = 0; k < nd; ++k) for (int g = 0; g < ng; ++g) out[o++] = T.R[k][g];
+    for (int j = 0; j < ncg; ++j) for (int k = 0; k < nd; ++k) out[o++] = T.Ds[j][k];
+    for (int j = 0; j < ncg; ++j) for (int k = 0; k < nd; ++k) out[o++] = T.Dt[j][k];
     return NXSDG_OK;
 }
 

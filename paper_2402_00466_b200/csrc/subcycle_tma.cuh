@@ -6,7 +6,7 @@
 // (+ one ring row below).  Differences:
 //  * data staging: for every element row ("job") lane 0 issues five TMA loads
 //    (cp.async.bulk.tensor) into a per-warp shared-memory stage, double-buffered and
-//    tracked by an mbarrier: S (18 planes x 32 elements), P_g (9 x 32), vx / vy (3 node
+//    tracked by an mbarrier: S (3 n_S planes x 34 elements), P_g (9 x 34), vx / vy (3 node
 //    rows x 66 columns) and the six node constants (2 rows x 62 columns).  The next job's
 //    loads are in flight while the current one computes; OOB boxes are zero-filled, which
 //    also covers the ragged right edge and the ring at ix0-1 = -1.  Warps are persistent and
@@ -40,28 +40,22 @@ constexpr int K2_CCOLS = 62;         // owned node columns per const box: 2*31
 template <typename SF> struct K2Cols { static constexpr int E = sizeof(SF) == 8 ? 34 : 36, ALIGN = 16 / sizeof(SF); };
 __host__ __device__ constexpr int round128(int b) { return (b + 127) / 128 * 128; }
 
-template <typename SF>
+// One job's shared-memory stage; every TMA destination starts on a 128-B boundary.
+template <typename SF, int NS = 6>
 struct __align__(128) K2Stage {
     static constexpr int EC = K2Cols<SF>::E;
-    static constexpr int SB = round128(18 * EC * (int)sizeof(SF)), PB = round128(9 * EC * (int)sizeof(SF));
-    SF S[18][EC];                    // planes S11[0..6), S12[0..6), S22[0..6)
-    unsigned char pads[SB - 18 * EC * (int)sizeof(SF)];
-    SF Pg[9][EC];
-    unsigned char padp[PB - 9 * EC * (int)sizeof(SF)];
-    double vx[3][K2_VCOLS];          // 1584 B
-    double padx[10];                 //   80 B  -> 1664
-    double vy[3][K2_VCOLS];
-    double pady[10];
-    double C[6][2][K2_CCOLS];        // 5952 B  c1, rx0, ry0, cafo, ox, oy
-    double padc[8];                  //   64 B  -> 6016
+    alignas(128) SF S[3 * NS][EC];             // planes S11[0..NS), S12[0..NS), S22[0..NS)
+    alignas(128) SF Pg[9][EC];
+    alignas(128) double vx[3][K2_VCOLS];       // 1584 B
+    alignas(128) double vy[3][K2_VCOLS];
+    alignas(128) double C[6][2][K2_CCOLS];     // 5952 B  c1, rx0, ry0, cafo, ox, oy
 };
 static_assert(sizeof(K2Stage<double>) == 16896, "stage layout");
-static_assert(offsetof(K2Stage<double>, Pg) % 128 == 0 && offsetof(K2Stage<double>, vx) % 128 == 0 &&
-              offsetof(K2Stage<double>, vy) % 128 == 0 && offsetof(K2Stage<double>, C) % 128 == 0, "TMA dst alignment");
-static_assert(offsetof(K2Stage<float>, Pg) % 128 == 0 && offsetof(K2Stage<float>, vx) % 128 == 0 &&
-              offsetof(K2Stage<float>, C) % 128 == 0, "TMA dst alignment (fp32)");
-template <typename SF>
-__host__ __device__ constexpr uint32_t k2_tx_bytes() { return 27 * K2Cols<SF>::E * sizeof(SF) + 2 * 3 * K2_VCOLS * 8 + 6 * 2 * K2_CCOLS * 8; }
+static_assert(sizeof(K2Stage<double, 8>) == 18432, "stage layout (n_S = 8)");
+template <typename SF, int NS = 6>
+__host__ __device__ constexpr uint32_t k2_tx_bytes() {
+    return (3 * NS + 9) * K2Cols<SF>::E * sizeof(SF) + 2 * 3 * K2_VCOLS * 8 + 6 * 2 * K2_CCOLS * 8;
+}
 
 struct K2Maps {
     CUtensorMap S, Pg, vx, vy, C;    // 5 x 128 B, 64-B aligned
@@ -126,9 +120,10 @@ constexpr double kC = 10.0 * kA / 3.0;           // 12 * (5/18) * kA: first-mome
 __device__ __forceinline__ float rsqrt_t(float x) { return rsqrtf(x); }
 __device__ __forceinline__ double rsqrt_t(double x) { return rsqrt_nr(x); }
 
-// strain coefficients of d/ds v (k = 0..5, k = 3 identically zero)
-template <typename T>
-__device__ __forceinline__ void strain_s(const double V[3][3], T E[6]) {
+// strain coefficients of d/ds v (k = 0..NS-1; k = 3 and 6 identically zero: no l2(S) part).
+// The n_S = 8 space (R#24) adds E_7 = <d/ds v, l1(S) l2(T)> / (1/2160) = 8 (second difference of s1).
+template <typename T, int NS>
+__device__ __forceinline__ void strain_s(const double V[3][3], T (&E)[NS]) {
     T s0[3], s1[3];
 #pragma unroll
     for (int jy = 0; jy < 3; ++jy) {
@@ -141,10 +136,14 @@ __device__ __forceinline__ void strain_s(const double V[3][3], T E[6]) {
     E[3] = T(0);
     E[4] = T(2) * (s0[0] + s0[2]) - T(4) * s0[1];
     E[5] = T(4) * (s1[2] - s1[0]);
+    if constexpr (NS == 8) {
+        E[6] = T(0);
+        E[7] = T(8) * (s1[0] + s1[2] - T(2) * s1[1]);
+    }
 }
-// strain coefficients of d/dt v (k = 4 identically zero)
-template <typename T>
-__device__ __forceinline__ void strain_t(const double V[3][3], T E[6]) {
+// strain coefficients of d/dt v (k = 4 and 7 identically zero; n_S = 8 adds E_6)
+template <typename T, int NS>
+__device__ __forceinline__ void strain_t(const double V[3][3], T (&E)[NS]) {
     T t0[3], t1[3];
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx) {
@@ -157,27 +156,42 @@ __device__ __forceinline__ void strain_t(const double V[3][3], T E[6]) {
     E[3] = T(2) * (t0[0] + t0[2]) - T(4) * t0[1];
     E[4] = T(0);
     E[5] = T(4) * (t1[2] - t1[0]);
+    if constexpr (NS == 8) {
+        E[6] = T(8) * (t1[0] + t1[2] - T(2) * t1[1]);
+        E[7] = T(0);
+    }
 }
-// values at the 9 Gauss points (g = gy*3 + gx) of sum_k E_k psi_k; HAS3/HAS4 drop known zeros
-template <bool HAS3, bool HAS4, typename T>
-__device__ __forceinline__ void eval_gp(const T E[6], T e[9]) {
+// values at the 9 Gauss points (g = gy*3 + gx) of sum_k E_k psi_k; HAS3/HAS4 drop known zeros.
+// e(S, T) = A(T) + S B(T) + q(S) Q(T): A = E0 + E2 T + E4 q(T), B = E1 + E5 T (+ E7 q(T)),
+// Q = E3 (+ E6 T) -- the bracketed terms are the n_S = 8 functions (R#24).
+template <bool HAS3, bool HAS4, typename T, int NS>
+__device__ __forceinline__ void eval_gp(const T (&E)[NS], T e[9]) {
     const T a = T(kA), q = T(kQ), q0 = T(kQ0);
     const T c0 = HAS4 ? fma(E[4], q, E[0]) : E[0];
     const T c1 = HAS4 ? fma(E[4], q0, E[0]) : E[0];
     const T t2 = a * E[2], t5 = a * E[5];
     const T Av[3] = {c0 - t2, c1, c0 + t2};
-    const T Bv[3] = {E[1] - t5, E[1], E[1] + t5};
+    T Bv[3] = {E[1] - t5, E[1], E[1] + t5};
+    T Qv[3] = {E[3], E[3], E[3]};
+    if constexpr (NS == 8) {
+        const T b7 = fma(E[7], q, E[1]);                    // E1 + E7 q(T) at T = +-a
+        Bv[0] = b7 - t5; Bv[1] = fma(E[7], q0, E[1]); Bv[2] = b7 + t5;
+        const T t6 = a * E[6];
+        Qv[0] = E[3] - t6; Qv[2] = E[3] + t6;
+    }
+    constexpr bool HASQ = HAS3 || NS == 8;
 #pragma unroll
     for (int gy = 0; gy < 3; ++gy) {
-        const T Pq = HAS3 ? fma(E[3], q, Av[gy]) : Av[gy];
+        const T Pq = HASQ ? fma(Qv[gy], q, Av[gy]) : Av[gy];
         e[gy * 3 + 0] = fma(-a, Bv[gy], Pq);
         e[gy * 3 + 2] = fma(a, Bv[gy], Pq);
-        e[gy * 3 + 1] = HAS3 ? fma(E[3], q0, Av[gy]) : Av[gy];
+        e[gy * 3 + 1] = HASQ ? fma(Qv[gy], q0, Av[gy]) : Av[gy];
     }
 }
-// S_k <- fac S_k + sc * (R G)_k  (R = M_ref^{-1} psi_k(g) w_g) by 1D moments
-template <typename T>
-__device__ __forceinline__ void project(const T G[9], double sc, T fac, T S[6]) {
+// S_k <- fac S_k + sc * (R G)_k  (R = M_ref^{-1} psi_k(g) w_g) by 1D moments;
+// n_S = 8: p6 = 2160 sum w q(S) T G, p7 = 2160 sum w S q(T) G, both (100 a / 9) x second moments
+template <typename T, int NS>
+__device__ __forceinline__ void project(const T G[9], double sc, T fac, T (&S)[NS]) {
     T X0[3], X1[3], X2[3];
 #pragma unroll
     for (int gy = 0; gy < 3; ++gy) {
@@ -194,13 +208,21 @@ __device__ __forceinline__ void project(const T G[9], double sc, T fac, T S[6]) 
     const T p5 = (X1[2] - X1[0]) * T(sc * kC * kC);
     S[0] = fma(fac, S[0], p0); S[1] = fma(fac, S[1], p1); S[2] = fma(fac, S[2], p2);
     S[3] = fma(fac, S[3], p3); S[4] = fma(fac, S[4], p4); S[5] = fma(fac, S[5], p5);
+    if constexpr (NS == 8) {
+        const T p6 = (X2[2] - X2[0]) * T(sc * 100.0 * kA / 9.0);
+        const T p7 = fma(T(-2), X1[1], X1[0] + X1[2]) * T(sc * 100.0 * kA / 9.0);
+        S[6] = fma(fac, S[6], p6); S[7] = fma(fac, S[7], p7);
+    }
 }
-// r[jx][jy] += sum_k Ds[j][k] S_k * h  (d/ds part, uses k = 0,1,2,4,5)
-__device__ __forceinline__ void div_s(const double S[6], double h, double r[3][3]) {
+// r[jx][jy] += sum_k Ds[j][k] S_k * h  (d/ds part, uses k = 0,1,2,4,5 and 7)
+template <int NS>
+__device__ __forceinline__ void div_s(const double (&S)[NS], double h, double r[3][3]) {
     const double u = fma(S[4], h * (1.0 / 90.0), S[0] * (h / 6.0)), v = S[2] * (h / 12.0);
     const double Z0[3] = {u - v, fma(S[0], h * (2.0 / 3.0), -S[4] * (h / 45.0)), u + v};
-    const double p = S[1] * (h / 6.0), w = S[5] * (h / 12.0);
-    const double Z1[3] = {p - w, S[1] * (h * 2.0 / 3.0), p + w};
+    double p = S[1] * (h / 6.0), m = S[1] * (h * 2.0 / 3.0);
+    if constexpr (NS == 8) { p = fma(S[7], h * (1.0 / 90.0), p); m = fma(S[7], -h * (1.0 / 45.0), m); }
+    const double w = S[5] * (h / 12.0);
+    const double Z1[3] = {p - w, m, p + w};
 #pragma unroll
     for (int jy = 0; jy < 3; ++jy) {
         const double t = Z1[jy] * (1.0 / 3.0);
@@ -209,12 +231,15 @@ __device__ __forceinline__ void div_s(const double S[6], double h, double r[3][3
         r[2][jy] += t + Z0[jy];
     }
 }
-// r[jx][jy] += sum_k Dt[j][k] S_k * h  (d/dt part, uses k = 0,1,2,3,5)
-__device__ __forceinline__ void div_t(const double S[6], double h, double r[3][3]) {
+// r[jx][jy] += sum_k Dt[j][k] S_k * h  (d/dt part, uses k = 0,1,2,3,5 and 6)
+template <int NS>
+__device__ __forceinline__ void div_t(const double (&S)[NS], double h, double r[3][3]) {
     const double u = fma(S[3], h * (1.0 / 90.0), S[0] * (h / 6.0)), v = S[1] * (h / 12.0);
     const double W0[3] = {u - v, fma(S[0], h * (2.0 / 3.0), -S[3] * (h / 45.0)), u + v};
-    const double p = S[2] * (h / 6.0), w = S[5] * (h / 12.0);
-    const double W1[3] = {p - w, S[2] * (h * 2.0 / 3.0), p + w};
+    double p = S[2] * (h / 6.0), m = S[2] * (h * 2.0 / 3.0);
+    if constexpr (NS == 8) { p = fma(S[6], h * (1.0 / 90.0), p); m = fma(S[6], -h * (1.0 / 45.0), m); }
+    const double w = S[5] * (h / 12.0);
+    const double W1[3] = {p - w, m, p + w};
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx) {
         const double t = W1[jx] * (1.0 / 3.0);
@@ -225,9 +250,9 @@ __device__ __forceinline__ void div_t(const double S[6], double h, double r[3][3
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool REPL, int STAGES, typename SF, typename CT>
+template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
-    using Stage = K2Stage<SF>;
+    using Stage = K2Stage<SF, NS>;
     constexpr int AL = K2Cols<SF>::ALIGN;
     SF* const S_out = reinterpret_cast<SF*>(a.S_out);   // FP32 buffers in mixed-precision mode
     extern __shared__ __align__(1024) unsigned char k2_smem[];   // no static smem: base stays 1024-B aligned
@@ -275,7 +300,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     auto issue = [&](const Cur& c, int s) {
         Stage* t = stg + s;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], k2_tx_bytes<SF>());
+        mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS>());
         const int xs = (c.ix0 - 1) & ~(AL - 1);   // 16-B aligned start column (arithmetic: -1 -> -2 / -4)
         tma3(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0);
         tma3(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0);
@@ -337,21 +362,21 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         // ---- strain (Table 1 "strain"): DG coefficients, then Gauss-point values
         CT e11[9], e12[9], e22[9];
         {
-            CT Es[6], Et[6], E[6];
+            CT Es[NS], Et[NS], E[NS];
             const CT cihx = (CT)ihx, cihy = (CT)ihy;
-            strain_s<CT>(Vx, Es);
+            strain_s(Vx, Es);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) E[k] = cihx * Es[k];
+            for (int k = 0; k < NS; ++k) E[k] = cihx * Es[k];
             eval_gp<false, true>(E, e11);
-            strain_t<CT>(Vy, Et);
+            strain_t(Vy, Et);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) E[k] = cihy * Et[k];
+            for (int k = 0; k < NS; ++k) E[k] = cihy * Et[k];
             eval_gp<true, false>(E, e22);
-            strain_t<CT>(Vx, Et);
-            strain_s<CT>(Vy, Es);
+            strain_t(Vx, Et);
+            strain_s(Vy, Es);
             const CT hx2 = CT(0.5) * cihx, hy2 = CT(0.5) * cihy;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) E[k] = fma(hy2, Et[k], hx2 * Es[k]);
+            for (int k = 0; k < NS; ++k) E[k] = fma(hy2, Et[k], hx2 * Es[k]);
             eval_gp<true, true>(E, e12);
         }
         // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in:
@@ -371,27 +396,27 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             e22[g] = fma(pr, fma(CT(1.25), y, CT(0.75) * x), -sub);
             e12[g] = pr * z;
         }
-        CT C11[6], C12[6], C22[6];
+        CT C11[NS], C12[NS], C22[NS];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            C11[k] = (CT)t.S[k][eo + lane]; C12[k] = (CT)t.S[6 + k][eo + lane];
-            C22[k] = (CT)t.S[12 + k][eo + lane];
+        for (int k = 0; k < NS; ++k) {
+            C11[k] = (CT)t.S[k][eo + lane]; C12[k] = (CT)t.S[NS + k][eo + lane];
+            C22[k] = (CT)t.S[2 * NS + k][eo + lane];
         }
         const CT cfac = (CT)fac;
         project(e11, 1.0, cfac, C11);
         project(e12, 0.5, cfac, C12);
         project(e22, 1.0, cfac, C22);
-        double S11[6], S12[6], S22[6];   // the divergence and velocity stay FP64
+        double S11[NS], S12[NS], S22[NS];   // the divergence and velocity stay FP64
 #pragma unroll
-        for (int k = 0; k < 6; ++k) { S11[k] = (double)C11[k]; S12[k] = (double)C12[k]; S22[k] = (double)C22[k]; }
+        for (int k = 0; k < NS; ++k) { S11[k] = (double)C11[k]; S12[k] = (double)C12[k]; S22[k] = (double)C22[k]; }
         const bool evalid = ix >= 0 && ix < a.nx;
         if (!cur.ring && evalid && lane >= 1) {
             const int64_t e = (int64_t)lr * a.epitch + ix;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) {
+            for (int k = 0; k < NS; ++k) {
                 S_out[k * eplane + e] = (SF)S11[k];
-                S_out[(6 + k) * eplane + e] = (SF)S12[k];
-                S_out[(12 + k) * eplane + e] = (SF)S22[k];
+                S_out[(NS + k) * eplane + e] = (SF)S12[k];
+                S_out[(2 * NS + k) * eplane + e] = (SF)S22[k];
             }
         }
         // ---- divergence contributions: rX = D_s S11 / hx + D_t S12 / hy, rY likewise

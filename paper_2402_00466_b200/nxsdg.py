@@ -283,8 +283,9 @@ class Mesh:
         buf = np.empty(need.value)
         _chk(self.h, lib.nxsdg_debug_reference_tables(self.h, p, buf.ctypes.data, need.value, C.byref(need)), "tables")
         ngp = p + 1; ng = ngp * ngp
-        shapes = [("gx", (ngp,)), ("gw", (ngp,)), ("psi", (6, ng)), ("phi", (ng, ng)), ("dphis", (ng, ng)),
-                  ("dphit", (ng, ng)), ("mref", (6,)), ("R", (6, ng)), ("Ds", (ng, 6)), ("Dt", (ng, 6))]
+        nd = 8 if (p == 2 and self.ns == 8) else 6
+        shapes = [("gx", (ngp,)), ("gw", (ngp,)), ("psi", (nd, ng)), ("phi", (ng, ng)), ("dphis", (ng, ng)),
+                  ("dphit", (ng, ng)), ("mref", (nd,)), ("R", (nd, ng)), ("Ds", (ng, nd)), ("Dt", (ng, nd))]
         out, o = {}, 0
         for name, shp in shapes:
             n = int(np.prod(shp)); out[name] = buf[o:o + n].reshape(shp); o += n

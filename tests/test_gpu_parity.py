@@ -359,9 +359,10 @@ def test_general_quads_steps_each(nx, ora):
         assert group_err(v, {"vx": rv[0], "vy": rv[1]}, ("vx", "vy")) < 1e-12
 
 
-def test_debug_steps_each_against_oracle(nx, ora):
+@pytest.mark.parametrize("ns", [6, 8])
+def test_debug_steps_each_against_oracle(nx, ora, ns):
     """Each Table 1 step alone (unfused kernels via nxsdg_run_step) against the oracle's step."""
-    nxe, nye, p, ns, na = 33, 35, 2, 6, 6
+    nxe, nye, p, na = 33, 35, 2, 6
     lx, ly = 33e3, 35e3
     st = case(nxe, nye, p, ns, na, "random", lx, ly)
     om = ora_mesh(nxe, nye, p, ns, na, lx, ly)
@@ -391,28 +392,124 @@ def test_debug_steps_each_against_oracle(nx, ora):
         assert group_err(v, {"vx": rv[0], "vy": rv[1]}, ("vx", "vy")) < 1e-12
 
 
-@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6)])
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
 def test_k0_tables_match_oracle_bases(nx, ora, p, ns):
     """Row a0: the device-built reference tables equal the oracle's Gauss rule, DG/CG bases and
     reference mass (<= 1e-15), and R = M_ref^{-1} psi w equals the oracle's element map on a unit box."""
-    with nx.Mesh(4, 4, 4.0, 4.0, p, ns, ns) as m:
+    with nx.Mesh(4, 4, 4.0, 4.0, p, ns, min(ns, 6)) as m:
         T = m.reference_tables(p)
+    nd = 8 if ns == 8 else 6
     ngp = p + 1
     x, w = ora.gauss(ngp)
     np.testing.assert_allclose(T["gx"], x, atol=1e-15); np.testing.assert_allclose(T["gw"], w, atol=1e-15)
     G = [(x[gx], x[gy]) for gy in range(ngp) for gx in range(ngp)]
     for g, (s_, t_) in enumerate(G):
-        np.testing.assert_allclose(T["psi"][:, g], ora.dg_basis(6, s_, t_) if ngp == 3 else
-                                   np.r_[ora.dg_basis(6, s_, t_)], atol=1e-15)
+        np.testing.assert_allclose(T["psi"][:, g], ora.dg_basis(nd, s_, t_), atol=1e-15)
         phi, ds, dt = ora.cg_basis(p, s_, t_)
         np.testing.assert_allclose(T["phi"][:, g], phi, atol=1e-14)
         np.testing.assert_allclose(T["dphis"][:, g], ds, atol=1e-13)
         np.testing.assert_allclose(T["dphit"][:, g], dt, atol=1e-13)
-    M = ora.element_mass(oracle.Mesh(1, 1, lx=1.0, ly=1.0, p=p, ns=ns, na=ns), 0, 0, ns, ngp)
+    M = ora.element_mass(oracle.Mesh(1, 1, lx=1.0, ly=1.0, p=p, ns=ns, na=min(ns, 6)), 0, 0, ns, ngp)
     np.testing.assert_allclose(T["mref"][:ns], np.diag(M), atol=1e-15)
     colsol = np.linalg.solve(M, np.array([w[gx] * w[gy] * ora.dg_basis(ns, x[gx], x[gy])
                                           for gy in range(ngp) for gx in range(ngp)]).T)
     np.testing.assert_allclose(T["R"][:ns], colsol, atol=1e-13)
+
+
+# ---------------------------------------------------------------- NEXT-4: n_S = 8 (R#24)
+NS8_CASES = [
+    (37, 29, 2, 8, 6, "warm", 512e3, 512e3),
+    (70, 75, 2, 8, 6, "warm", 140e3, 150e3),       # 3 strips x 3 chunks, ragged
+    (45, 40, 2, 8, 3, "random", 45e3, 40e3),
+    (1, 5, 2, 8, 6, "random", 1e3, 5e3),
+    (6, 1, 2, 8, 1, "random", 6e3, 1e3),
+]
+
+
+@pytest.mark.parametrize("mode", ["tma", "table", "unfused"])
+@pytest.mark.parametrize("c", NS8_CASES, ids=[f"{c[0]}x{c[1]}na{c[4]}{c[5]}" for c in NS8_CASES])
+def test_ns8_one_subcycle(nx, ora, c, mode):
+    """NEXT-4: the full gradient space of Q2 as stress space; the TMA-staged
+    structured kernel k_subcycle_tma<..., 8>, the table-driven k_subcycle<2, 8> and the unfused
+    steps, one subcycle, north_star bar."""
+    nxe, nye, p, ns, na, kind, lx, ly = c
+    st = case(nxe, nye, p, ns, na, kind, lx, ly)
+    got = _gpu_run(nx, st, nxe, nye, p, ns, na, 1, lx, ly, unfused=mode == "unfused",
+                   options={nx.OPT_FUSED_KERNEL: 1} if mode == "table" else None)
+    ref = ora.subcycles(ora_mesh(nxe, nye, p, ns, na, lx, ly), ora_params(nx.PhysParams()), 1, st)
+    _check(got, ref, st, TOL1)
+
+
+@pytest.mark.parametrize("c,nsub", [(NS8_CASES[0], 100), (NS8_CASES[1], 30)], ids=["37x29x100", "70x75x30"])
+def test_ns8_full_count(nx, ora, c, nsub):
+    nxe, nye, p, ns, na, kind, lx, ly = c
+    st = case(nxe, nye, p, ns, na, kind, lx, ly)
+    got = _gpu_run(nx, st, nxe, nye, p, ns, na, nsub, lx, ly)
+    ref = ora.subcycles(ora_mesh(nxe, nye, p, ns, na, lx, ly), ora_params(nx.PhysParams()), nsub, st)
+    _check(got, ref, st, TOLN)
+
+
+def test_ns8_kernels_agree(nx):
+    """TMA structured vs table-driven n_S = 8 kernels: same result to rounding after 3 subcycles."""
+    nxe, nye, lx, ly = 64, 40, 64e3, 40e3
+    st = case(nxe, nye, 2, 8, 6, "random", lx, ly)
+    a = _gpu_run(nx, st, nxe, nye, 2, 8, 6, 3, lx, ly, options={nx.OPT_FUSED_KERNEL: 0})
+    b = _gpu_run(nx, st, nxe, nye, 2, 8, 6, 3, lx, ly, options={nx.OPT_FUSED_KERNEL: 1})
+    e = parity(a, b, st)
+    assert max(e.values()) < 1e-12, e
+
+
+def test_ns8_outer_step(nx, ora):
+    """Advection + BEGIN_STEP + 20 subcycles with n_S = 8 (A, H advected in DG2, n_A = 6)."""
+    nxe, nye, lx, ly = 64, 50, 128e3, 100e3
+    st = case(nxe, nye, 2, 8, 6, "warm", lx, ly)
+    prm = nx.PhysParams()
+    got = _gpu_run(nx, st, nxe, nye, 2, 8, 6, 20, lx, ly, advect_dt=prm.dt)
+    ref = ora.outer_step(ora_mesh(nxe, nye, 2, 8, 6, lx, ly), ora_params(prm), 20, st)
+    _check(got, ref, st, TOLN, groups=("S", "v", "A", "H"))
+
+
+def test_ns8_loopback_strips_bitwise(nx):
+    """n_S = 8 row strips (3 ranks, loopback transport; S halo has 24 planes) equal one GPU bitwise."""
+    nxe, nye, lx, ly = 40, 37, 40e3, 37e3
+    st = case(nxe, nye, 2, 8, 6, "random", lx, ly)
+    prm = nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly, 2, 8, 6) as m:
+        m.load(st)
+        m.advect(prm.dt)
+        m.mevp_substeps(5, begin_step=True)
+        ref = m.state()
+    import torch
+    s = torch.cuda.Stream()
+    ms = [nx.Mesh(nxe, nye, lx, ly, 2, 8, 6, rank=r, nranks=3, transport=nx.TRANSPORT_LOOPBACK,
+                  stream=s.cuda_stream) for r in range(3)]
+    for m in ms:
+        m.set_option(nx.OPT_CHUNK_ROWS, 4)
+    nx.loopback_connect(ms)
+    for m in ms:
+        er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
+        loc = {k: st[k][nr0:nr0 + nrn].copy() for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
+        for k in ("S11", "S12", "S22", "A", "H"):
+            loc[k] = st[k][er0 * nxe:(er0 + ern) * nxe].copy()
+        m.load(loc)
+    nx.group_advect(ms, prm.dt)
+    nx.group_mevp_substeps(ms, 5, begin_step=True)
+    got = {k: np.concatenate([m.read_state(k) for m in ms]) for k in ref}
+    for m in ms:
+        m.destroy()
+    for k in ref:
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+
+
+def test_ns8_unsupported_combinations(nx):
+    """FP32 storage and general quads are n_S = 6 features: UNSUPPORTED, not a silent fallback."""
+    with nx.Mesh(8, 8, 8e3, 8e3, 2, 8, 6) as m:
+        with pytest.raises(nx.NxsdgError) as e:
+            m.set_option(nx.OPT_PRECISION, 1)
+        assert e.value.status == nx.ERR_UNSUPPORTED
+        with pytest.raises(nx.NxsdgError) as e:
+            m.set_vertices(np.zeros((9, 9, 2)))
+        assert e.value.status == nx.ERR_UNSUPPORTED
 
 
 def test_checkpoint_resume_bitwise(nx):
