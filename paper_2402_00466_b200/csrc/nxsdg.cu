@@ -201,9 +201,17 @@ static nxsdg_status alloc(nxsdg_ctx* c, double** p, size_t n) {
     return NXSDG_OK;
 }
 
-static void free_all(nxsdg_ctx* c) {
+// Destroy the cached subcycle graphs (their captured launch arguments went stale); a replay may
+// still be in flight on the stream, so wait for it first.
+static void drop_graphs(nxsdg_ctx* c) {
+    if (c->graphs.empty()) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
+}
+
+static void free_all(nxsdg_ctx* c) {
+    drop_graphs(c);
     double** bufs[] = {&c->S[0], &c->S[1], &c->Pg, &c->A, &c->H, &c->Asc[0], &c->Asc[1], &c->Hsc[0], &c->Hsc[1],
                        &c->E, &c->Fx, &c->Fy, &c->vx[0], &c->vx[1], &c->vy[0], &c->vy[1],
                        &c->ax, &c->ay, &c->nodec, &c->staging};
@@ -355,8 +363,7 @@ extern "C" nxsdg_status nxsdg_set_params(nxsdg_ctx* c, const nxsdg_params* p) {
     if (s) return s;
     c->prm = *p;
     c->prepped = false;
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);   // captured launch arguments are stale
-    c->graphs.clear();
+    drop_graphs(c);   // captured launch arguments are stale
     return NXSDG_OK;
 }
 
@@ -389,8 +396,7 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             c->stages = (int)value; break;
         default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
     }
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
-    c->graphs.clear();
+    drop_graphs(c);
     return NXSDG_OK;
 }
 
