@@ -185,6 +185,9 @@ def main():
                     help="NEXT-2: regenerate the moving-cyclone forcing on the GPU at every outer step (P:350 protocol)")
     ap.add_argument("--ns", type=int, default=None, choices=[6, 8],
                     help="NEXT-4: n_S = 8 stress space (full gradient space of Q2, table-driven fused kernel)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 halo transport: p2p = copy-engine stores into the neighbours' buffers over peer "
+                         "memory with a device-side flag handshake (CUDA IPC); nccl = ncclSend/ncclRecv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-window", type=int, default=512, help="oracle window per --impl reference step")
     ap.add_argument("--cpu-window", type=int, default=640, help="oracle window of the cpu_baseline sample")
@@ -214,17 +217,22 @@ def main():
 
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    kw = {}
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(nxsdg.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nid = bytes(idt.cpu().numpy().tobytes())
+        if args.transport == "nccl":
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(nxsdg.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            kw = dict(rank=rank, nranks=world, transport=nxsdg.TRANSPORT_NCCL, nccl_id=bytes(idt.cpu().numpy().tobytes()))
+        else:
+            kw = dict(rank=rank, nranks=world, transport=nxsdg.TRANSPORT_P2P)
     prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
     st = gen_rank_state(cfg, rank, world)
-    kw = dict(rank=rank, nranks=world, transport=nxsdg.TRANSPORT_NCCL, nccl_id=nid) if world > 1 else {}
     m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, device=local, **kw)
+    if world > 1 and args.transport == "p2p":
+        nxsdg.p2p_connect_group(m, rank, world, dist.all_gather_object)
     if args.fp32_storage or args.fp32_stress:
         m.set_option(nxsdg.OPT_PRECISION, 2 if args.fp32_stress else 1)
     m.load(st)
@@ -343,7 +351,7 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} CG{cfg.p}/DG{cfg.p} (n_S={cfg.ns}, n_A={cfg.na}) warm box + "
                                    f"cyclone forcing; step = advect + prep + {cfg.nsub} fused mEVP subcycles",
                        "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el, "alpha": cfg.alpha, "beta": cfg.alpha,
-                       "parallelism": f"row strips x{world}" if world > 1 else "1 GPU",
+                       "parallelism": f"row strips x{world} ({args.transport} halo)" if world > 1 else "1 GPU",
                        "forcing": "moving cyclone regenerated on the GPU every step" if args.moving else "static (t = 0)",
                        "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},
             "breakdown_ms": {"advect": adv, "prep": prep, "subcycles": sub, "per_subcycle": kernel_ms},
@@ -356,6 +364,8 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        barrier()      # P2P: no rank unmaps / frees while a neighbour could still touch its buffers
     m.destroy()
     if world > 1:
         dist.destroy_process_group()

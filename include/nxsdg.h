@@ -101,7 +101,10 @@ typedef enum {
 typedef enum {
     NXSDG_TRANSPORT_NONE = 0,     /* nranks == 1                                                  */
     NXSDG_TRANSPORT_NCCL = 1,     /* one process per GPU, ncclSend/ncclRecv halo rows              */
-    NXSDG_TRANSPORT_LOOPBACK = 2  /* all ranks' contexts in one process (tests), cudaMemcpyAsync  */
+    NXSDG_TRANSPORT_LOOPBACK = 2, /* all ranks' contexts in one process (tests), cudaMemcpyAsync  */
+    NXSDG_TRANSPORT_P2P = 3       /* halo rows copied straight into the neighbours' buffers over
+                                     peer memory (NVLink / NVSwitch), device-side flag handshake;
+                                     no NCCL (nxsdg_p2p_export / nxsdg_p2p_connect)                */
 } nxsdg_transport;
 
 typedef struct {
@@ -212,6 +215,23 @@ nxsdg_status nxsdg_stream_join(nxsdg_ctx* ctx);
 /* ---- multi-rank plumbing ------------------------------------------------------- */
 /* Fill 128 bytes with a fresh ncclUniqueId (rank 0; broadcast it to the others). */
 nxsdg_status nxsdg_nccl_unique_id(void* out128);
+/* P2P transport (SURVEY §8(e) "device-initiated peer stores").  Each halo exchange
+ * copies the halo plan's send rows with the copy engine directly into the receive rows of the
+ * neighbour's buffers (one 2D copy per message, no staging, no NCCL), then writes the exchange
+ * number into the neighbour's flag word (cuStreamWriteValue32, fenced) and makes the context
+ * stream wait on the device until both neighbours have written it into ours
+ * (cuStreamWaitValue32 >=).  The host never blocks.
+ * nxsdg_p2p_export: an opaque blob (*needed bytes; blob == NULL: size only) with CUDA IPC handles
+ *   of this rank's exchanged buffers and flag pair; give it to ranks r-1 and r+1 (e.g. with
+ *   torch.distributed all_gather_object).  STATE unless the context uses NXSDG_TRANSPORT_P2P.
+ * nxsdg_p2p_connect: map the neighbours' blobs (NULL where no neighbour exists); INVALID_ARG for a
+ *   blob of another mesh / rank, UNSUPPORTED without peer access between the devices, CUDA when
+ *   cudaIpcOpenMemHandle fails.  Every rank must connect before its first halo exchange (STATE).
+ * nxsdg_p2p_connect_local: the same for all ranks' contexts living in this process (tests; each
+ *   context on its own stream - ranks then run concurrently and synchronise on the device). */
+nxsdg_status nxsdg_p2p_export(nxsdg_ctx* ctx, void* blob, int64_t cap, int64_t* needed);
+nxsdg_status nxsdg_p2p_connect(nxsdg_ctx* ctx, const void* lower_blob, const void* upper_blob);
+nxsdg_status nxsdg_p2p_connect_local(nxsdg_ctx** ctxs, int32_t n);
 /* Link the contexts of a loopback partition (ctxs[r] has rank r), all in this process,
  * all on one device and one stream.  INVALID_ARG otherwise. */
 nxsdg_status nxsdg_loopback_connect(nxsdg_ctx** ctxs, int32_t n);

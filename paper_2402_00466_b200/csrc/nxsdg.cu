@@ -80,6 +80,8 @@ struct Geom {
 };
 static Geom make_geom(int nx, int ny, int p, int ns, int na, int nranks, int rank);
 
+constexpr int kP2PBufs = 12;   // vx0 vx1 vy0 vy1 S0 S1 A H Asc0 Asc1 Hsc0 Hsc1
+
 struct nxsdg_ctx {
     nxsdg_mesh_desc d{};
     nxsdg_params prm{};
@@ -136,6 +138,14 @@ struct nxsdg_ctx {
     // transport
     ncclComm_t comm = nullptr;
     std::vector<nxsdg_ctx*> peers;   // loopback: all ranks' contexts
+    // P2P transport: the exchanged allocations in a fixed order (advection swaps A/H with its
+    // scratch buffers, identically on every rank, so a field's current allocation has the same
+    // index on both sides), this rank's two flag words and the neighbours' mapped buffers
+    double* orig[kP2PBufs] = {};
+    uint32_t* flags = nullptr;       // [0] written by the lower neighbour, [1] by the upper one
+    struct Peer { bool on = false, ipc = false; double* buf[kP2PBufs] = {}; uint32_t* flags = nullptr; Geom g{}; } peer[2];
+    uint32_t p2p_seq = 0;
+    bool p2p_ok = false;
     // graphs: key = (n_sub, cv, cs)
     std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
 };
@@ -212,6 +222,14 @@ static void drop_graphs(nxsdg_ctx* c) {
 
 static void free_all(nxsdg_ctx* c) {
     drop_graphs(c);
+    for (auto& pr : c->peer) {
+        if (pr.ipc) {
+            for (double* b : pr.buf) if (b) cudaIpcCloseMemHandle(b);
+            if (pr.flags) cudaIpcCloseMemHandle(pr.flags);
+        }
+        pr = nxsdg_ctx::Peer{};
+    }
+    if (c->flags) { cudaFree(c->flags); c->flags = nullptr; }
     double** bufs[] = {&c->S[0], &c->S[1], &c->Pg, &c->A, &c->H, &c->Asc[0], &c->Asc[1], &c->Hsc[0], &c->Hsc[1],
                        &c->E, &c->Fx, &c->Fy, &c->vx[0], &c->vx[1], &c->vy[0], &c->vy[1],
                        &c->ax, &c->ay, &c->nodec, &c->staging};
@@ -253,7 +271,8 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
                    (d->n_adv == 1 || d->n_adv == 3 || d->n_adv == 6));
     if (!ok_deg) return NXSDG_ERR_UNSUPPORTED;
     if (d->bc == NXSDG_BC_PERIODIC && d->nranks > 1) return NXSDG_ERR_UNSUPPORTED;
-    if (d->nranks > 1 && d->transport != NXSDG_TRANSPORT_NCCL && d->transport != NXSDG_TRANSPORT_LOOPBACK)
+    if (d->nranks > 1 && d->transport != NXSDG_TRANSPORT_NCCL && d->transport != NXSDG_TRANSPORT_LOOPBACK &&
+        d->transport != NXSDG_TRANSPORT_P2P)
         return NXSDG_ERR_INVALID_ARG;
     if (d->transport == NXSDG_TRANSPORT_NCCL && d->nranks > 1 && !d->nccl_id) return NXSDG_ERR_INVALID_ARG;
     if (!(prm->alpha > 1.0) || !(prm->beta > 0.0) || !(prm->dt > 0.0) || !(prm->rho_ice > 0.0) ||
@@ -291,6 +310,15 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     c->nn = (int64_t)nn;
     c->c1 = c->nodec; c->rx0 = c->nodec + nn; c->ry0 = c->nodec + 2 * nn; c->cafo = c->nodec + 3 * nn;
     c->ox = c->nodec + 4 * nn; c->oy = c->nodec + 5 * nn;
+    {
+        double* const o[kP2PBufs] = {c->vx[0], c->vx[1], c->vy[0], c->vy[1], c->S[0], c->S[1],
+                                     c->A, c->H, c->Asc[0], c->Asc[1], c->Hsc[0], c->Hsc[1]};
+        std::copy(o, o + kP2PBufs, c->orig);
+    }
+    if (d->nranks > 1 && d->transport == NXSDG_TRANSPORT_P2P) {
+        if (cudaMalloc(&c->flags, 2 * sizeof(uint32_t)) != cudaSuccess) return bail(NXSDG_ERR_OOM);
+        if (cudaMemset(c->flags, 0, 2 * sizeof(uint32_t)) != cudaSuccess) return bail(NXSDG_ERR_CUDA);
+    }
 #undef AL
     // K0: reference-element tables into __constant__ (all three spaces; tiny)
     {
@@ -956,10 +984,187 @@ static nxsdg_status halo_loopback_all(std::vector<nxsdg_ctx*>& ctxs, uint32_t wh
     return NXSDG_OK;
 }
 
+// ---- P2P transport (NXSDG_TRANSPORT_P2P): no NCCL, no staging.  Every send segment of the halo
+// plan is copied by the copy engine straight from this rank's buffer into the matching receive
+// rows of the neighbour's buffer (peer memory over NVLink / NVSwitch: a CUDA IPC mapping across
+// processes, a plain device pointer inside one process), then this rank bumps its word in each
+// neighbour's flag pair (cuStreamWriteValue32, fenced) and its stream waits, on the device, until
+// both neighbours have bumped its own pair to the same exchange number (cuStreamWaitValue32 GEQ).
+// Every rank issues the same sequence of halo calls, so exchange numbers match.  Race freedom:
+// an exchange writes only ghost rows of the buffer the preceding kernel produced, which no kernel
+// of the receiver reads before the receiver's own wait for this exchange; and the sender can only
+// reach its next exchange after waiting for the receiver's signal of this one, which the receiver
+// issues after the kernels that read the previous contents of those ghost rows.
+typedef CUresult (*PFN_sv32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps { PFN_sv32 write = nullptr, wait = nullptr; };
+static MemOps& memops() {
+    static MemOps m;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr; cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) m.write = (PFN_sv32)p;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) m.wait = (PFN_sv32)p;
+    }
+    return m;
+}
+
+static int p2p_index(const nxsdg_ctx* c, const double* b) {
+    for (int i = 0; i < kP2PBufs; ++i) if (c->orig[i] == b) return i;
+    return -1;
+}
+
+static nxsdg_status halo_p2p(nxsdg_ctx* c, uint32_t what, cudaStream_t st) {
+    if (!c->p2p_ok) return fail(c, NXSDG_ERR_STATE, "P2P transport not connected (nxsdg_p2p_connect)");
+    MemOps& mo = memops();
+    if (!mo.write || !mo.wait) return fail(c, NXSDG_ERR_UNSUPPORTED, "stream memory operations unavailable");
+    std::vector<HaloMsg> mine, theirs[2];
+    halo_messages(c->geom, what, mine);
+    for (int sd = 0; sd < 2; ++sd) if (c->peer[sd].on) halo_messages(c->peer[sd].g, what, theirs[sd]);
+    int kth[2] = {0, 0};
+    for (const auto& m : mine) {
+        if (m.dir != 0) continue;
+        const int sd = m.peer < c->d.rank ? 0 : 1;
+        const nxsdg_ctx::Peer& pr = c->peer[sd];
+        if (!pr.on) return fail(c, NXSDG_ERR_STATE, "P2P neighbour %d not connected", m.peer);
+        const HaloMsg* rv = nullptr;
+        int seen = -1;
+        for (const auto& t : theirs[sd])
+            if (t.dir == 1 && t.peer == c->d.rank && ++seen == kth[sd]) { rv = &t; break; }
+        ++kth[sd];
+        double* base = halo_base(c, m.field);
+        const int bi = p2p_index(c, base);
+        if (!rv || bi < 0 || rv->count != m.count || rv->nseg != m.nseg)
+            return fail(c, NXSDG_ERR_STATE, "P2P halo plan mismatch with rank %d", m.peer);
+        nxsdg_status s = copy2d(c, pr.buf[bi] + rv->off0, rv->stride, base + m.off0, m.stride, m.count, m.nseg, st);
+        if (s) return s;
+    }
+    const uint32_t seq = ++c->p2p_seq;
+    for (int sd = 0; sd < 2; ++sd)   // I am my lower neighbour's upper one (word 1) and vice versa
+        if (c->peer[sd].on && mo.write((CUstream)st, (CUdeviceptr)(c->peer[sd].flags + (sd == 0 ? 1 : 0)), seq, 0) != CUDA_SUCCESS)
+            return fail(c, NXSDG_ERR_CUDA, "cuStreamWriteValue32 failed");
+    for (int sd = 0; sd < 2; ++sd)
+        if (c->peer[sd].on && mo.wait((CUstream)st, (CUdeviceptr)(c->flags + sd), seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return fail(c, NXSDG_ERR_CUDA, "cuStreamWaitValue32 failed");
+    return NXSDG_OK;
+}
+
+static nxsdg_status halo_on(nxsdg_ctx* c, uint32_t what, cudaStream_t st) {
+    if (c->d.transport == NXSDG_TRANSPORT_NCCL) return halo_nccl(c, what, st);
+    return halo_p2p(c, what, st);
+}
+
 static nxsdg_status halo(nxsdg_ctx* c, uint32_t what) {
     if (c->d.nranks == 1) return NXSDG_OK;
-    if (c->d.transport == NXSDG_TRANSPORT_NCCL) return halo_nccl(c, what, c->stream);
+    if (c->d.transport == NXSDG_TRANSPORT_NCCL || c->d.transport == NXSDG_TRANSPORT_P2P) return halo_on(c, what, c->stream);
     return NXSDG_OK;   // loopback exchanges are driven by the group calls
+}
+
+struct P2PBlob {
+    uint32_t magic, version;
+    int32_t rank, nranks, nx, ny, P, NS, NA, device;
+    cudaIpcMemHandle_t h[kP2PBufs + 1];   // buffers, then the flag pair
+};
+constexpr uint32_t kP2PMagic = 0x4e585032u;   // "NXP2"
+
+extern "C" nxsdg_status nxsdg_p2p_export(nxsdg_ctx* c, void* blob, int64_t cap, int64_t* needed) {
+    GUARD(c);
+    if (needed) *needed = (int64_t)sizeof(P2PBlob);
+    if (c->d.transport != NXSDG_TRANSPORT_P2P || c->d.nranks < 2) return fail(c, NXSDG_ERR_STATE, "not a P2P rank");
+    if (!blob) return NXSDG_OK;
+    if (cap < (int64_t)sizeof(P2PBlob)) return fail(c, NXSDG_ERR_INVALID_ARG, "cap < %zu", sizeof(P2PBlob));
+    P2PBlob b{};
+    b.magic = kP2PMagic; b.version = 1;
+    b.rank = c->d.rank; b.nranks = c->d.nranks; b.nx = c->d.nx; b.ny = c->d.ny;
+    b.P = c->P; b.NS = c->NS; b.NA = c->NA; b.device = c->d.device;
+    cudaSetDevice(c->d.device);
+    for (int i = 0; i < kP2PBufs; ++i) CU(cudaIpcGetMemHandle(&b.h[i], c->orig[i]));
+    CU(cudaIpcGetMemHandle(&b.h[kP2PBufs], c->flags));
+    memcpy(blob, &b, sizeof b);
+    return NXSDG_OK;
+}
+
+static bool p2p_blob_ok(const nxsdg_ctx* c, const P2PBlob& b, int rank) {
+    return b.magic == kP2PMagic && b.version == 1 && b.rank == rank && b.nranks == c->d.nranks && b.nx == c->d.nx &&
+           b.ny == c->d.ny && b.P == c->P && b.NS == c->NS && b.NA == c->NA;
+}
+
+static void p2p_finish_connect(nxsdg_ctx* c) {
+    bool ok = true;
+    if (c->d.rank > 0 && !c->peer[0].on) ok = false;
+    if (c->d.rank + 1 < c->d.nranks && !c->peer[1].on) ok = false;
+    for (int sd = 0; sd < 2; ++sd)
+        if (c->peer[sd].on)
+            c->peer[sd].g = make_geom(c->d.nx, c->d.ny, c->P, c->NS, c->NA, c->d.nranks, c->d.rank + (sd == 0 ? -1 : 1));
+    c->p2p_ok = ok;
+}
+
+extern "C" nxsdg_status nxsdg_p2p_connect(nxsdg_ctx* c, const void* lower, const void* upper) {
+    GUARD(c);
+    if (c->d.transport != NXSDG_TRANSPORT_P2P || c->d.nranks < 2) return fail(c, NXSDG_ERR_STATE, "not a P2P rank");
+    if (c->p2p_ok) return fail(c, NXSDG_ERR_STATE, "already connected");
+    const void* blobs[2] = {lower, upper};
+    const int want[2] = {c->d.rank > 0, c->d.rank + 1 < c->d.nranks};
+    cudaSetDevice(c->d.device);
+    for (int sd = 0; sd < 2; ++sd) {
+        if (!want[sd]) continue;
+        if (!blobs[sd]) return fail(c, NXSDG_ERR_INVALID_ARG, "missing %s neighbour blob", sd ? "upper" : "lower");
+        P2PBlob b;
+        memcpy(&b, blobs[sd], sizeof b);
+        if (!p2p_blob_ok(c, b, c->d.rank + (sd == 0 ? -1 : 1)))
+            return fail(c, NXSDG_ERR_INVALID_ARG, "%s neighbour blob does not match this mesh", sd ? "upper" : "lower");
+        if (b.device != c->d.device) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, c->d.device, b.device);
+            if (!can) return fail(c, NXSDG_ERR_UNSUPPORTED, "no peer access from device %d to %d", c->d.device, b.device);
+        }
+        nxsdg_ctx::Peer& pr = c->peer[sd];
+        pr.ipc = true;
+        for (int i = 0; i <= kP2PBufs; ++i) {
+            void* ptr = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.h[i], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(c, NXSDG_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+            }
+            if (i < kP2PBufs) pr.buf[i] = (double*)ptr; else pr.flags = (uint32_t*)ptr;
+        }
+        pr.on = true;
+    }
+    p2p_finish_connect(c);
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_p2p_connect_local(nxsdg_ctx** ctxs, int32_t n) {
+    if (!ctxs || n < 2) return NXSDG_ERR_INVALID_ARG;
+    for (int i = 0; i < n; ++i)
+        if (!ctxs[i] || ctxs[i]->d.rank != i || ctxs[i]->d.nranks != n || ctxs[i]->d.transport != NXSDG_TRANSPORT_P2P ||
+            ctxs[i]->p2p_ok)
+            return NXSDG_ERR_INVALID_ARG;
+    for (int i = 0; i < n; ++i) {
+        nxsdg_ctx* c = ctxs[i];
+        for (int sd = 0; sd < 2; ++sd) {
+            const int q = i + (sd == 0 ? -1 : 1);
+            if (q < 0 || q >= n) continue;
+            if (ctxs[q]->d.device != c->d.device) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, c->d.device, ctxs[q]->d.device);
+                if (!can) return fail(c, NXSDG_ERR_UNSUPPORTED, "no peer access between devices");
+                cudaSetDevice(c->d.device);
+                cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[q]->d.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(c, NXSDG_ERR_CUDA, "peer access");
+                cudaGetLastError();
+            }
+            nxsdg_ctx::Peer& pr = c->peer[sd];
+            std::copy(ctxs[q]->orig, ctxs[q]->orig + kP2PBufs, pr.buf);
+            pr.flags = ctxs[q]->flags;
+            pr.ipc = false; pr.on = true;
+        }
+        p2p_finish_connect(c);
+    }
+    return NXSDG_OK;
 }
 
 // ---------------------------------------------------------------- launches
@@ -1245,7 +1450,7 @@ static nxsdg_status subcycle_overlapped(nxsdg_ctx* c) {
     c->cv ^= 1; c->cs ^= 1;                      // the exchange moves rows of the new state
     CU(cudaEventRecord(c->ev_bnd, c->stream));
     CU(cudaStreamWaitEvent(c->hstream, c->ev_bnd, 0));
-    if ((st = halo_nccl(c, NXSDG_HALO_V | NXSDG_HALO_S, c->hstream))) return st;
+    if ((st = halo_on(c, NXSDG_HALO_V | NXSDG_HALO_S, c->hstream))) return st;
     CU(cudaEventRecord(c->ev_x, c->hstream));
     c->cv ^= 1; c->cs ^= 1;                      // interior reads the old state
     if ((st = launch_subcycle_sel(c, SEL_INTERIOR))) return st;
@@ -1325,7 +1530,7 @@ static nxsdg_status check_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
 static nxsdg_status one_subcycle(nxsdg_ctx* c, bool unfused) {
     nxsdg_status s;
     if (!unfused) {
-        if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_NCCL) return subcycle_overlapped(c);
+        if (c->d.nranks > 1 && c->d.transport != NXSDG_TRANSPORT_LOOPBACK) return subcycle_overlapped(c);
         if ((s = launch_subcycle(c))) return s;
         return halo(c, NXSDG_HALO_V | NXSDG_HALO_S);
     }

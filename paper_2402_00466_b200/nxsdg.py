@@ -28,7 +28,7 @@ FIELDS = {"vx": 0, "vy": 1, "S11": 2, "S12": 3, "S22": 4, "A": 5, "H": 6, "E11":
 CG_FIELDS = {"vx", "vy", "Fx", "Fy"}
 BEGIN_STEP, UNFUSED = 1, 2
 STEPS = {"strain": 0, "stress": 1, "divergence": 2, "velocity": 3}
-TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1, 2
+TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_P2P = 0, 1, 2, 3
 OPT_FUSED_KERNEL, OPT_CHUNK_ROWS, OPT_CTAS_PER_SM, OPT_STAGES, OPT_DYNAMIC, OPT_MAP_MODE, OPT_PRECISION = 0, 1, 2, 3, 4, 5, 6
 
 
@@ -88,6 +88,9 @@ def _load() -> C.CDLL:
         "nxsdg_debug_reference_tables": ([vp, i32, vp, i64, C.POINTER(i64)], i32),
         "nxsdg_halo_plan": ([i32, i32, i32, i32, i32, i32, i32, u32, vp, i32, C.POINTER(i32)], i32),
         "nxsdg_local_geometry": ([i32, i32, i32, i32, i32, i32, i32, C.POINTER(i64)], i32),
+        "nxsdg_p2p_export": ([vp, vp, i64, C.POINTER(i64)], i32),
+        "nxsdg_p2p_connect": ([vp, vp, vp], i32),
+        "nxsdg_p2p_connect_local": ([C.POINTER(vp), i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -104,7 +107,7 @@ EXPORTED = [
     "nxsdg_loopback_connect", "nxsdg_group_mevp_substeps", "nxsdg_group_advect", "nxsdg_kernel_launches",
     "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option", "nxsdg_halo_plan",
     "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone", "nxsdg_set_vertices", "nxsdg_stream_join",
-    "nxsdg_debug_reference_tables",
+    "nxsdg_debug_reference_tables", "nxsdg_p2p_export", "nxsdg_p2p_connect", "nxsdg_p2p_connect_local",
 ]
 HALO_V, HALO_S, HALO_AH, HALO_AH_SCR0, HALO_AH_SCR1 = 1, 2, 4, 8, 16
 HF_VX, HF_VY, HF_S, HF_A, HF_H, HF_A_SCR0, HF_H_SCR0, HF_A_SCR1, HF_H_SCR1 = range(9)
@@ -291,6 +294,19 @@ class Mesh:
             n = int(np.prod(shp)); out[name] = buf[o:o + n].reshape(shp); o += n
         return out
 
+    def p2p_export(self) -> bytes:
+        """Opaque blob with CUDA IPC handles of this rank's exchanged buffers (P2P transport)."""
+        need = C.c_int64()
+        _chk(self.h, lib.nxsdg_p2p_export(self.h, None, 0, C.byref(need)), "p2p_export")
+        buf = (C.c_char * need.value)()
+        _chk(self.h, lib.nxsdg_p2p_export(self.h, buf, need.value, C.byref(need)), "p2p_export")
+        return bytes(buf)
+
+    def p2p_connect(self, lower: bytes | None, upper: bytes | None):
+        lo = C.create_string_buffer(lower, len(lower)) if lower else None
+        hi = C.create_string_buffer(upper, len(upper)) if upper else None
+        _chk(self.h, lib.nxsdg_p2p_connect(self.h, lo, hi), "p2p_connect")
+
     def stream_join(self):
         _chk(self.h, lib.nxsdg_stream_join(self.h), "stream_join")
 
@@ -329,6 +345,17 @@ class Mesh:
 def _handles(meshes):
     arr = (C.c_void_p * len(meshes))(*[m.h for m in meshes])
     return arr
+
+
+def p2p_connect_local(meshes):
+    _chk(None, lib.nxsdg_p2p_connect_local(_handles(meshes), len(meshes)), "p2p_connect_local")
+
+
+def p2p_connect_group(mesh, rank: int, world: int, all_gather_object):
+    """Exchange P2P blobs with torch.distributed-style all_gather_object and connect this rank."""
+    blobs = [None] * world
+    all_gather_object(blobs, mesh.p2p_export())
+    mesh.p2p_connect(blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank + 1 < world else None)
 
 
 def loopback_connect(meshes):

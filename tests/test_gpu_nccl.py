@@ -38,9 +38,20 @@ def test_nccl_strips_bitwise_equal_single(n, ty):
     assert d["bitwise_equal"], d
 
 
-def test_bench_torchrun_two_ranks():
+@pytest.mark.parametrize("n,ty,ns", [(2, 4, 6), (3, 4, 6), (2, 32, 8)])
+def test_p2p_ipc_strips_bitwise_equal_single(n, ty, ns):
+    """P2P transport across processes (CUDA IPC mappings exchanged through torch.distributed)."""
+    r = _torchrun(n, ["scripts/p2p_two_rank.py"], {"TY": str(ty), "NS": str(ns)})
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-3000:]
+    d = json.loads(lines[-1])
+    assert d["bitwise_equal"], d
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_bench_torchrun_two_ranks(transport):
     r = _torchrun(2, ["bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "C2",
-                      "--e2e-steps", "1"])
+                      "--e2e-steps", "1", "--transport", transport])
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and len(lines) == 1, r.stdout[-2000:] + r.stderr[-3000:]
     d = json.loads(lines[0])

@@ -641,6 +641,58 @@ def test_loopback_strips_bitwise_equal_single(nx, nranks, ty, variant):
         np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
 
 
+@pytest.mark.parametrize("nranks,ty,ns", [(2, 4, 6), (3, 4, 6), (2, 32, 6), (3, 5, 8)])
+def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns):
+    """P2P transport inside one process: every rank on its OWN stream, so the ranks run
+    concurrently and the only ordering between them is the device-side flag handshake; halo rows
+    are copied straight into the neighbours' buffers.  Advection, fused subcycles (boundary /
+    interior overlap with ty = 4) and unfused subcycles: bitwise equal to one context."""
+    nxe, nye, lx, ly = 50, 47, 50e3, 47e3
+    st = case(nxe, nye, 2, ns, 6, "random", lx, ly)
+    prm = nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly, 2, ns, 6) as m:
+        m.load(st)
+        m.advect(prm.dt)
+        m.mevp_substeps(6, begin_step=True)
+        m.mevp_substeps(2, begin_step=False, unfused=True)
+        ref = m.state()
+    ms = [nx.Mesh(nxe, nye, lx, ly, 2, ns, 6, rank=r, nranks=nranks, transport=nx.TRANSPORT_P2P) for r in range(nranks)]
+    assert len({m.stream for m in ms}) == nranks
+    nx.p2p_connect_local(ms)
+    for m in ms:
+        m.set_option(nx.OPT_CHUNK_ROWS, ty)
+        er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
+        loc = {k: st[k][nr0:nr0 + nrn].copy() for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
+        for k in ("S11", "S12", "S22", "A", "H"):
+            loc[k] = st[k][er0 * nxe:(er0 + ern) * nxe].copy()
+        m.load(loc)
+    for m in ms:
+        m.advect(prm.dt)
+    for m in ms:
+        m.mevp_substeps(6, begin_step=True)
+    for m in ms:
+        m.mevp_substeps(2, begin_step=False, unfused=True)
+    for m in ms:
+        m.synchronize()
+    got = {k: np.concatenate([m.read_state(k) for m in ms]) for k in ref}
+    for m in ms:
+        m.destroy()
+    for k in ref:
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+
+
+def test_p2p_unconnected_is_state_error(nx):
+    ms = [nx.Mesh(20, 20, 20e3, 20e3, rank=r, nranks=2, transport=nx.TRANSPORT_P2P) for r in range(2)]
+    st = case(20, 20, 2, 6, 6, "random", 20e3, 20e3)
+    with pytest.raises(nx.NxsdgError) as e:
+        ms[0].advect(120.0)
+    assert e.value.status == nx.ERR_STATE
+    with pytest.raises(nx.NxsdgError):
+        ms[0].p2p_connect(ms[0].p2p_export(), None)   # rank 0 has no lower neighbour; wrong rank blob
+    for m in ms:
+        m.destroy()
+
+
 def test_state_roundtrip_and_errors(nx):
     with nx.Mesh(9, 7, 9e3, 7e3) as m:
         st = case(9, 7, 2, 6, 6, "random", 9e3, 7e3)
