@@ -159,7 +159,8 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *                           1: table-driven register kernel k_subcycle<p> (reference-table variant)
  *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (default 32; one ring row each)
  *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy;
- *                           -1 (default) = tuned: 2 with FP64 S/P_g storage, 4 with FP32 storage)
+ *                           -1 (default) = tuned: 2 with FP64 S/P_g storage, 4 with FP32 storage,
+ *                           3 for the fused general-quad kernel)
  *   NXSDG_OPT_STAGES        TMA pipeline depth per warp, 2..4 (default 2)
  *   NXSDG_OPT_DYNAMIC       1 (default): warps claim work units from an atomic counter; 0: static round-robin
  *   NXSDG_OPT_PRECISION     0 (default): FP64 everywhere; 1 (NEXT-3): the fused CG2/DG2 subcycles keep

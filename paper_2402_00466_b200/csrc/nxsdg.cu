@@ -22,6 +22,7 @@
 #include "../../include/nxsdg.h"
 #include "kernels.cuh"
 #include "subcycle_tma.cuh"
+#include "subcycle_gen.cuh"
 #include "advect_q2.cuh"
 #include "general_quads.cuh"
 #include "general_steps.cuh"
@@ -131,6 +132,8 @@ struct nxsdg_ctx {
     cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
     K2Maps maps[2][2]; // [cv][cs]
     bool maps_ok = false;
+    K2GenMaps gen_maps[2][2];   // NEXT-1 fused general-quad subcycle: + vertices, lumped masses
+    bool gen_maps_ok = false;
     int precision = 0; // 0: FP64 storage; 1 (NEXT-3): S and P_g stored in FP32, arithmetic FP64
     float* S32[2] = {nullptr, nullptr}; float* Pg32 = nullptr;
     K2Maps maps32[2][2];
@@ -368,6 +371,7 @@ extern "C" double nxsdg_bytes_per_element_subcycle(const nxsdg_ctx* c) {
     // one fused pass: v gather P^2*2, S read+write 2*3NS, P_g NG,
     // per node (P^2 per element): 6 constants + v write 2
     const double p2 = (double)c->P * c->P;
+    if (c->general) return 8.0 * (2 * p2 + 6.0 * c->NS + c->NG + 8.0 * p2) + 8.0 * (2.0 + p2);   // + vertex, lumped masses
     if (c->precision >= 1) return 8.0 * (2 * p2 + 8.0 * p2) + 4.0 * (6.0 * c->NS + c->NG);   // S, P_g in FP32
     return 8.0 * (2 * p2 + 6.0 * c->NS + c->NG + 8.0 * p2);
 }
@@ -412,7 +416,7 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             c->dynamic = (int)value; break;
         case NXSDG_OPT_PRECISION:
             if (value < 0 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "precision 0|1|2");
-            if (value >= 1 && (c->P != 2 || c->NS != 6 || c->d.nranks != 1))
+            if (value >= 1 && (c->P != 2 || c->NS != 6 || c->d.nranks != 1 || c->general))
                 return fail(c, NXSDG_ERR_UNSUPPORTED, "FP32 storage: CG2/DG2 (n_S = 6), single rank");
             if (value >= 1 && c->stages > 3) c->stages = 3;
             c->precision = (int)value; c->pg32_ok = false; break;
@@ -711,6 +715,7 @@ extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64
     if (!xy || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE)) return fail(c, NXSDG_ERR_INVALID_ARG, "bad argument");
     if (c->d.nranks != 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads are single-rank");
     if (c->NS == 8) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: n_S = 3 | 6");
+    if (c->precision != 0) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: FP64 storage only");
     const int64_t need = 2 * (int64_t)(c->d.nx + 1) * (c->d.ny + 1);
     if (count != need) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)need);
     if (!c->verts) CU(cudaMalloc(&c->verts, need * sizeof(double)));
@@ -719,6 +724,8 @@ extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64
     if (mem == NXSDG_MEM_HOST) CU(cudaStreamSynchronize(c->stream));
     c->general = true;
     c->gmaps_ready = false;
+    c->gen_maps_ok = false;
+    drop_graphs(c);
     nxsdg_status st = ensure_debug_buffers(c);
     if (st) return st;
     const size_t nn = (size_t)c->npitch * c->nrows_local;
@@ -1320,7 +1327,49 @@ static nxsdg_status cvt(nxsdg_ctx* c, const float* src, double* dst, int64_t n) 
     return NXSDG_OK;
 }
 
-static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0; }
+static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0 && (!c->general || c->NS == 6); }
+
+// NEXT-1: the fused general-quad subcycle stages the vertex rows and the lumped node masses too
+static nxsdg_status build_gen_maps(nxsdg_ctx* c) {
+    nxsdg_status st = build_maps(c);
+    if (st || c->gen_maps_ok) return st;
+    const cuuint64_t dX[2] = {2 * (cuuint64_t)(c->d.nx + 1), (cuuint64_t)(c->d.ny + 1)};
+    const cuuint64_t sX[1] = {2 * (cuuint64_t)(c->d.nx + 1) * 8};
+    const cuuint32_t bX[2] = {K2_VCOLS, 2};
+    const cuuint64_t dM[2] = {2 * (cuuint64_t)c->d.nx + 1, (cuuint64_t)c->nrows_local};
+    const cuuint64_t sM[1] = {(cuuint64_t)c->npitch * 8};
+    const cuuint32_t bM[2] = {K2_CCOLS, 2};
+    for (int v = 0; v < 2; ++v)
+        for (int s2 = 0; s2 < 2; ++s2) {
+            K2GenMaps& G = c->gen_maps[v][s2];
+            const K2Maps& B = c->maps[v][s2];
+            G.S = B.S; G.Pg = B.Pg; G.vx = B.vx; G.vy = B.vy; G.C = B.C;
+            if (!encode(&G.X, c->verts, 2, dX, sX, bX) || !encode(&G.M, c->mlump, 2, dM, sM, bM))
+                return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled (general) failed");
+        }
+    c->gen_maps_ok = true;
+    return NXSDG_OK;
+}
+
+template <bool R, int ST>
+static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2GenStage) + sizeof(uint64_t) + sizeof(int4));
+    static bool attr = false;
+    if (!attr) {
+        CU(cudaFuncSetAttribute(k_subcycle_gen<R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    int nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_gen<R, ST>, 32 * K2_WARPS, smem));
+    const int cap = c->ctas_per_sm < 0 ? 3 : c->ctas_per_sm;   // tuned on C4 (profiles/tune_gen_r01.log)
+    if (cap > 0) occ = std::min(occ, cap);
+    const int64_t units = (int64_t)a.nstrips * a.nsel;
+    const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
+    k_subcycle_gen<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->gen_maps[cv][cs], a);
+    return NXSDG_OK;
+}
 
 template <bool R, int ST, typename SF, typename CT = double, int NS = 6>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
@@ -1366,6 +1415,15 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int 
         slot = 0;
     }
     a.work_counter = c->dynamic ? c->counters + slot : nullptr;
+    if (c->general) {
+        if ((st = build_gen_maps(c))) return st;
+        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
+            case 4: return launch_gen_t<false, 2>(c, cv, cs, a);
+            case 5: return launch_gen_t<true, 2>(c, cv, cs, a);
+            case 6: return launch_gen_t<false, 3>(c, cv, cs, a);
+            default: return launch_gen_t<true, 3>(c, cv, cs, a);
+        }
+    }
     if (c->precision == 2) {
         if ((st = build_maps32(c))) return st;
         a.S_out = reinterpret_cast<double*>(c->S32[cs ^ 1]);   // FP32 storage, FP32 stress arithmetic
@@ -1520,8 +1578,9 @@ static nxsdg_status begin_step(nxsdg_ctx* c) {
 static nxsdg_status check_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
     if (n < 0 || (flags & ~(uint32_t)(NXSDG_BEGIN_STEP | NXSDG_UNFUSED))) return fail(c, NXSDG_ERR_INVALID_ARG, "bad n/flags");
     if (c->d.bc != NXSDG_BC_CLOSED) return fail(c, NXSDG_ERR_UNSUPPORTED, "mEVP substeps need the closed box");
-    if (c->general && !(flags & NXSDG_UNFUSED) && n > 0)
-        return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: the subcycle runs unfused (NXSDG_UNFUSED)");
+    if (c->general && !(flags & NXSDG_UNFUSED) && n > 0 && !use_tma(c))
+        return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: the fused subcycle needs CG2/DG2 and the TMA kernel; "
+                                              "use NXSDG_UNFUSED");
     if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
     if (!(flags & NXSDG_BEGIN_STEP) && !c->prepped) return fail(c, NXSDG_ERR_STATE, "first call of an outer step needs NXSDG_BEGIN_STEP");
     return NXSDG_OK;

@@ -1,0 +1,354 @@
+// NEXT-1 fused: the whole mEVP subcycle (strain -> Listing 2 -> divergence gather -> velocity) on a
+// GENERAL quad mesh (bilinear map of each element's four vertices, DESIGN R#23) in one pass, with
+// the geometry recomputed on the fly from the vertices - nothing per element is stored.
+//
+// Same warp mapping, TMA job pipeline and node gather as k_subcycle_tma (CG2/DG2, n_S = 6); each job
+// additionally stages the element row's two vertex rows and the two owned rows of lumped node masses.
+// Per element:
+//   geometry   a = X10-X00, b = X01-X00, c = X11-X01-X10+X00:  J(s,t) = [a + c t | b + c s],
+//              |J| = c0 + d1 S + d2 T (centred, exactly linear), M_K = c0 D + d1 M_S + d2 M_T
+//              (closed form, Cholesky with reciprocal diagonal: general_quads.cuh)
+//   strain     the reference derivatives d/ds v, d/dt v at the Gauss points are exact in the n_S = 8
+//              space (R#24), so their coefficients come from the same node differences as the box
+//              kernel; w |J| eps = w adj(J)^T grad_ref v; E_c = M_K^{-1} sum_g w psi (|J| eps_c)(g)
+//   stress     Listing 2 at the Gauss points with P_g from the outer-step prep; then
+//              S <- (1 - 1/alpha) S + M_K^{-1} sum_g w |J_g| psi r(g)
+//   divergence r_j = sum_g w sigma(g) . adj(J_g)^T grad_ref phi_j(g), evaluated separably with the
+//              1D Lagrange values / derivatives at the Gauss abscissae; F / m with the lumped mass
+#pragma once
+#include "subcycle_tma.cuh"
+#include "general_quads.cuh"
+
+namespace nxk {
+
+struct K2GenMaps {
+    CUtensorMap S, Pg, vx, vy, C, X, M;    // box-kernel maps + vertices + lumped masses
+};
+
+struct __align__(128) K2GenStage {
+    K2Stage<double, 6> b;
+    alignas(128) double X[2][K2_VCOLS];    // vertex rows lr, lr+1: 33 vertices x (x, y)
+    alignas(128) double M[2][K2_CCOLS];    // lumped masses of node rows 2 lr, 2 lr + 1 (owned columns)
+};
+__host__ __device__ constexpr uint32_t k2g_tx_bytes() {
+    return k2_tx_bytes<double, 6>() + 2 * K2_VCOLS * 8 + 2 * K2_CCOLS * 8;
+}
+
+// q-th 1D Lagrange value / derivative of node j at the Gauss abscissa S_q in {-a, 0, a}:
+//   L0 = 2S^2 - S, L1 = 1 - 4S^2, L2 = 2S^2 + S;  L0' = 4S - 1, L1' = -8S, L2' = 4S + 1  (2a^2 = 0.3)
+__device__ __forceinline__ double lag_v(int j, int q) {
+    const double s = (q - 1) * kA;
+    return j == 0 ? fma(2.0 * s, s, -s) : (j == 1 ? fma(-4.0 * s, s, 1.0) : fma(2.0 * s, s, s));
+}
+__device__ __forceinline__ double lag_d(int j, int q) {
+    const double s = (q - 1) * kA;
+    return j == 0 ? fma(4.0, s, -1.0) : (j == 1 ? -8.0 * s : fma(4.0, s, 1.0));
+}
+
+// b = M_ref (R G) scaled back to plain moments sum_g w psi_k G_g (project() divides by M_ref)
+__device__ __forceinline__ void moments(const double G[9], double sc, double (&b)[6]) {
+    const double mref[6] = {1.0, 1.0 / 12.0, 1.0 / 12.0, 1.0 / 180.0, 1.0 / 180.0, 1.0 / 144.0};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b[k] = 0.0;
+    project(G, sc, 0.0, b);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b[k] *= mref[k];
+}
+
+template <bool REPL, int STAGES>
+__global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_constant__ K2GenMaps maps, SubArgs a) {
+    using Stage = K2GenStage;
+    extern __shared__ __align__(1024) unsigned char k2_smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    Stage* stg = reinterpret_cast<Stage*>(k2_smem) + wib * STAGES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * STAGES * sizeof(Stage)) + wib * STAGES;
+    const int twarps = gridDim.x * K2_WARPS;
+    const int gw = blockIdx.x * K2_WARPS + wib;
+    const int nunits = a.nstrips * a.nsel;
+    if (gw >= nunits) return;
+    if (lane == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    struct Cur { int u, lr, lr1, ix0; bool ring, first, ok; };
+    auto start_unit = [&](int u, Cur& c) {
+        c.ok = u < nunits;
+        if (!c.ok) return;
+        const int strip = u % a.nstrips, chunk = a.chunk0 + (u / a.nstrips) * a.chunk_step;
+        const int lr0 = a.erow_begin + chunk * a.ty;
+        c.u = u; c.lr1 = min(lr0 + a.ty, a.erow_end); c.ix0 = strip * 31;
+        c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
+    };
+    auto advance = [&](Cur& c) {
+        ++c.lr; c.ring = false; c.first = false;
+        if (c.lr >= c.lr1) {
+            const int nu = a.work_counter ? twarps + atomicAdd(a.work_counter, 1) : c.u + twarps;
+            start_unit(nu, c);
+        }
+    };
+    int4* jobs = reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) + wib * STAGES;
+    auto record = [&](const Cur& c, int st) {
+        jobs[st] = make_int4(c.ok ? c.u : -1, c.lr, c.lr1, (c.ring ? 1 : 0) | (c.first ? 2 : 0));
+    };
+    auto issue = [&](const Cur& c, int s) {
+        Stage* t = stg + s;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], k2g_tx_bytes());
+        const int xs = (c.ix0 - 1) & ~1;
+        tma3(&t->b.S[0][0], &maps.S, &bar[s], xs, c.lr, 0);
+        tma3(&t->b.Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0);
+        tma2(&t->b.vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
+        tma2(&t->b.vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
+        tma3(&t->b.C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0);
+        tma2(&t->X[0][0], &maps.X, &bar[s], 2 * (c.ix0 - 1), c.lr);
+        tma2(&t->M[0][0], &maps.M, &bar[s], 2 * c.ix0, 2 * c.lr);
+    };
+
+    const double fac = a.fac, hA = 0.5 * a.ainv;
+    const int64_t npitch = a.npitch, eplane = a.eplane;
+    Cur pre;
+    if (lane == 0) {
+        start_unit(gw, pre);
+        record(pre, 0);
+        issue(pre, 0);
+#pragma unroll
+        for (int k = 1; k < STAGES - 1; ++k) {
+            advance(pre);
+            record(pre, k);
+            if (pre.ok) issue(pre, k);
+        }
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    int s = 0;
+    double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
+    for (;;) {
+        const int sp = (s + STAGES - 1) % STAGES;
+        if (lane == 0) {
+            if (pre.ok) advance(pre);
+            record(pre, sp);
+            if (pre.ok) issue(pre, sp);
+        }
+        Cur cur;
+        {
+            const int4 jd = jobs[s];
+            cur.ok = jd.x >= 0;
+            if (!cur.ok) break;
+            cur.u = jd.x; cur.lr = jd.y; cur.lr1 = jd.z; cur.ring = jd.w & 1; cur.first = (jd.w & 2) != 0;
+            cur.ix0 = (cur.u % a.nstrips) * 31;
+        }
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+        const Stage& t = stg[s];
+        const int ix = cur.ix0 - 1 + lane, lr = cur.lr;
+        const int eo = (cur.ix0 - 1) - ((cur.ix0 - 1) & ~1);
+        const bool evalid = ix >= 0 && ix < a.nx;
+        if (cur.first) { carx[0] = carx[1] = cary[0] = cary[1] = 0.0; }
+
+        // ---- geometry of this element (zero-filled boxes outside the mesh: use a unit square there)
+        double ax_, ay_, bx_, by_, cx_, cy_;
+        {
+            const double x00 = t.X[0][2 * lane], y00 = t.X[0][2 * lane + 1];
+            const double x10 = t.X[0][2 * lane + 2], y10 = t.X[0][2 * lane + 3];
+            const double x01 = t.X[1][2 * lane], y01 = t.X[1][2 * lane + 1];
+            const double x11 = t.X[1][2 * lane + 2], y11 = t.X[1][2 * lane + 3];
+            ax_ = x10 - x00; ay_ = y10 - y00; bx_ = x01 - x00; by_ = y01 - y00;
+            cx_ = (x11 - x01) - ax_; cy_ = (y11 - y01) - ay_;
+            if (!evalid) { ax_ = 1.0; ay_ = 0.0; bx_ = 0.0; by_ = 1.0; cx_ = 0.0; cy_ = 0.0; }
+        }
+        const double d0 = ax_ * by_ - bx_ * ay_, d1 = ax_ * cy_ - cx_ * ay_, d2 = cx_ * by_ - bx_ * cy_;
+        const double c0 = d0 + 0.5 * (d1 + d2);
+        double L[21];
+        gen_mass_chol_n<6>(c0, d1, d2, L);
+        // J columns at the Gauss point (gx, gy): x_s = ax + cx t, x_t = bx + cx s, y_s = ay + cy t, y_t = by + cy s
+        auto jac = [&](int gx, int gy, double& xs, double& xt, double& ys, double& yt) {
+            const double sg = 0.5 + (gx - 1) * kA, tg = 0.5 + (gy - 1) * kA;
+            xs = fma(cx_, tg, ax_); xt = fma(cx_, sg, bx_); ys = fma(cy_, tg, ay_); yt = fma(cy_, sg, by_);
+        };
+
+        // ---- node values (local box columns 2*lane .. 2*lane+2)
+        double Vx[3][3], Vy[3][3];
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+            const double2 a2 = *reinterpret_cast<const double2*>(&t.b.vx[jy][2 * lane]);
+            const double2 b2 = *reinterpret_cast<const double2*>(&t.b.vy[jy][2 * lane]);
+            Vx[jy][0] = a2.x; Vx[jy][1] = a2.y; Vx[jy][2] = t.b.vx[jy][2 * lane + 2];
+            Vy[jy][0] = b2.x; Vy[jy][1] = b2.y; Vy[jy][2] = t.b.vy[jy][2 * lane + 2];
+        }
+        // ---- strain: pointwise reference derivatives at the Gauss points, w |J| eps, projection
+        double e11[9], e12[9], e22[9];
+        {
+            double Dsx[9], Dtx[9], Dsy[9], Dty[9];
+            {
+                double E8[8];
+                strain_s(Vx, E8); eval_gp<false, true>(E8, Dsx);
+                strain_t(Vx, E8); eval_gp<true, false>(E8, Dtx);
+                strain_s(Vy, E8); eval_gp<false, true>(E8, Dsy);
+                strain_t(Vy, E8); eval_gp<true, false>(E8, Dty);
+            }
+#pragma unroll
+            for (int gy = 0; gy < 3; ++gy)
+#pragma unroll
+                for (int gx = 0; gx < 3; ++gx) {
+                    const int g = gy * 3 + gx;
+                    double xs, xt, ys, yt;
+                    jac(gx, gy, xs, xt, ys, yt);
+                    e11[g] = fma(yt, Dsx[g], -ys * Dtx[g]);                                   // |J| d vx / dx
+                    e22[g] = fma(xs, Dty[g], -xt * Dsy[g]);                                   // |J| d vy / dy
+                    e12[g] = 0.5 * (fma(xs, Dtx[g], -xt * Dsx[g]) + fma(yt, Dsy[g], -ys * Dty[g]));
+                }
+            double E11[6], E12[6], E22[6];
+            moments(e11, 1.0, E11); moments(e12, 1.0, E12); moments(e22, 1.0, E22);
+            chol_solve<6>(L, E11); chol_solve<6>(L, E12); chol_solve<6>(L, E22);
+            eval_gp<true, true>(E11, e11); eval_gp<true, true>(E12, e12); eval_gp<true, true>(E22, e22);
+        }
+        // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in as in the box kernel
+#pragma unroll
+        for (int g = 0; g < 9; ++g) {
+            const double x = e11[g], y = e22[g], z = e12[g];
+            const double draw2 = fma(z, z, fma(1.5 * x, y, 1.25 * fma(x, x, y * y)));
+            const double rD = rsqrt_nr(draw2 + a.dmin2);
+            const double ph = t.b.Pg[g][eo + lane] * hA;
+            const double pr = ph * rD;
+            const double sub = REPL ? pr * (draw2 > 0.0 ? draw2 * rsqrt_nr(draw2) : 0.0) : ph;
+            const double jd = fma(d1, (g % 3 - 1) * kA, fma(d2, (g / 3 - 1) * kA, c0));   // |J_g|
+            e11[g] = jd * fma(pr, fma(1.25, x, 0.75 * y), -sub);
+            e22[g] = jd * fma(pr, fma(1.25, y, 0.75 * x), -sub);
+            e12[g] = jd * (pr * z);
+        }
+        double S11[6], S12[6], S22[6];
+        moments(e11, 1.0, S11); moments(e12, 0.5, S12); moments(e22, 1.0, S22);
+        chol_solve<6>(L, S11); chol_solve<6>(L, S12); chol_solve<6>(L, S22);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            S11[k] = fma(fac, t.b.S[k][eo + lane], S11[k]);
+            S12[k] = fma(fac, t.b.S[6 + k][eo + lane], S12[k]);
+            S22[k] = fma(fac, t.b.S[12 + k][eo + lane], S22[k]);
+        }
+        if (!cur.ring && evalid && lane >= 1) {
+            const int64_t e = (int64_t)lr * a.epitch + ix;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                a.S_out[k * eplane + e] = S11[k];
+                a.S_out[(6 + k) * eplane + e] = S12[k];
+                a.S_out[(12 + k) * eplane + e] = S22[k];
+            }
+        }
+        // ---- divergence: r_j = sum_g w sigma . adj(J)^T grad_ref phi_j, separable in (gx, gy)
+        double rX[3][3], rY[3][3];
+        {
+            double s11[9], s12[9], s22[9];
+            eval_gp<true, true>(S11, s11); eval_gp<true, true>(S12, s12); eval_gp<true, true>(S22, s22);
+            double AX[9], BX[9], AY[9], BY[9];
+            const double w1[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+#pragma unroll
+            for (int gy = 0; gy < 3; ++gy)
+#pragma unroll
+                for (int gx = 0; gx < 3; ++gx) {
+                    const int g = gy * 3 + gx;
+                    double xs, xt, ys, yt;
+                    jac(gx, gy, xs, xt, ys, yt);
+                    const double w = w1[gx] * w1[gy];
+                    AX[g] = w * fma(s11[g], yt, -s12[g] * xt);     // coefficient of d phi / ds
+                    BX[g] = w * fma(s12[g], xs, -s11[g] * ys);     // coefficient of d phi / dt
+                    AY[g] = w * fma(s12[g], yt, -s22[g] * xt);
+                    BY[g] = w * fma(s22[g], xs, -s12[g] * ys);
+                }
+#pragma unroll
+            for (int jx = 0; jx < 3; ++jx) {
+                double uAX[3], uBX[3], uAY[3], uBY[3];   // per gy: sum over gx
+#pragma unroll
+                for (int gy = 0; gy < 3; ++gy) {
+                    double pax = 0.0, pbx = 0.0, pay = 0.0, pby = 0.0;
+#pragma unroll
+                    for (int gx = 0; gx < 3; ++gx) {
+                        const double dl = lag_d(jx, gx), lv = lag_v(jx, gx);
+                        pax = fma(AX[gy * 3 + gx], dl, pax); pbx = fma(BX[gy * 3 + gx], lv, pbx);
+                        pay = fma(AY[gy * 3 + gx], dl, pay); pby = fma(BY[gy * 3 + gx], lv, pby);
+                    }
+                    uAX[gy] = pax; uBX[gy] = pbx; uAY[gy] = pay; uBY[gy] = pby;
+                }
+#pragma unroll
+                for (int jy = 0; jy < 3; ++jy) {
+                    double sx = 0.0, sy = 0.0;
+#pragma unroll
+                    for (int gy = 0; gy < 3; ++gy) {
+                        const double lv = lag_v(jy, gy), dl = lag_d(jy, gy);
+                        sx = fma(uAX[gy], lv, fma(uBX[gy], dl, sx));
+                        sy = fma(uAY[gy], lv, fma(uBY[gy], dl, sy));
+                    }
+                    rX[jx][jy] = evalid ? sx : 0.0;
+                    rY[jx][jy] = evalid ? sy : 0.0;
+                }
+            }
+        }
+        // ---- per-node gather (row below, W, E) + velocity update with the lumped mass (R#11)
+        const bool nvalid = lane >= 1 && ix >= 0 && ix <= a.nx && !cur.ring;
+        double sumx[2][2], sumy[2][2];
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+            const double wx = __shfl_up_sync(0xffffffffu, rX[2][jy], 1);
+            const double wy = __shfl_up_sync(0xffffffffu, rY[2][jy], 1);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                double sx = rX[q][jy], sy = rY[q][jy];
+                if (q == 0) { sx = wx + sx; sy = wy + sy; }
+                if (jy == 2) { carx[q] = sx; cary[q] = sy; continue; }
+                if (jy == 0) { sx = carx[q] + sx; sy = cary[q] + sy; }
+                sumx[jy][q] = sx; sumy[jy][q] = sy;
+            }
+        }
+        if (nvalid) {
+            const bool brow0 = lr == a.erow_begin && a.bottom_boundary;
+#pragma unroll
+            for (int jy = 0; jy < 2; ++jy) {
+                double nvx[2], nvy[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int I = 2 * ix + q;
+                    const int cc = 2 * lane - 2 + q;
+                    const double mass = t.M[jy][cc];
+                    const double im = mass > 0.0 ? -rcp_nr(mass) : 0.0;       // F = -r / m
+                    const double fx = sumx[jy][q] * im, fy = sumy[jy][q] * im;
+                    const double vxo = Vx[jy][q], vyo = Vy[jy][q];
+                    const double c1 = t.b.C[0][jy][cc], r0x = t.b.C[1][jy][cc], r0y = t.b.C[2][jy][cc];
+                    const double cf = t.b.C[3][jy][cc], oxv = t.b.C[4][jy][cc], oyv = t.b.C[5][jy][cc];
+                    const double dx = oxv - vxo, dy = oyv - vyo;
+                    const double w2 = fma(dx, dx, dy * dy);
+                    const double w = w2 > 0.0 ? w2 * rsqrt_nr(w2) : 0.0;
+                    const double cw = cf * w;
+                    const double rden = rcp_nr(fma(c1, a.b1, cw));
+                    const double cb = c1 * a.beta, ck = c1 * a.kc;
+                    const double ux = (fma(cb, vxo, r0x) + fma(cw, oxv, fma(ck, vyo, fx))) * rden;
+                    const double uy = (fma(cb, vyo, r0y) + fma(cw, oyv, fma(-ck, vxo, fy))) * rden;
+                    const bool bnd = (I == 0) || (I == 2 * a.nx) || (jy == 0 && brow0);
+                    nvx[q] = bnd ? 0.0 : ux;
+                    nvy[q] = bnd ? 0.0 : uy;
+                }
+                const int64_t n = (int64_t)(2 * lr + jy) * npitch + 2 * ix;
+                if (ix < a.nx) {
+                    *reinterpret_cast<double2*>(a.vx_out + n) = make_double2(nvx[0], nvx[1]);
+                    *reinterpret_cast<double2*>(a.vy_out + n) = make_double2(nvy[0], nvy[1]);
+                } else {
+                    a.vx_out[n] = 0.0;
+                    a.vy_out[n] = 0.0;
+                }
+            }
+        }
+        if (a.top_boundary && lr == a.erow_end - 1 && nvalid) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int I = 2 * ix + q;
+                if (I > 2 * a.nx) continue;
+                a.vx_out[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+                a.vy_out[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+            }
+        }
+        __syncwarp();
+        s = (s + 1) % STAGES;
+    }
+}
+
+}  // namespace nxk

@@ -368,11 +368,55 @@ def test_general_quads_outer_step(nx, ora, p, ns, na, nsub):
         m.advect(prm.dt)
         m.mevp_substeps(nsub, begin_step=True, unfused=True)
         got = m.state()
-        with pytest.raises(nx.NxsdgError):
-            m.mevp_substeps(1, begin_step=False, unfused=False)   # the fused kernels are box-only
+        if p == 1:
+            with pytest.raises(nx.NxsdgError):
+                m.mevp_substeps(1, begin_step=False, unfused=False)   # fused general quads: CG2/DG2 only
     om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=p, ns=ns, na=na, verts=V)
     ref = ora.outer_step(om, ora_params(prm), nsub, st, do_advect=True)
     _check(got, ref, st, TOL1 if nsub == 1 else TOLN, groups=("S", "v", "A", "H"))
+
+
+@pytest.mark.parametrize("shape,nsub,delta,kind", [((37, 33), 1, 0.28, "random"), ((37, 33), 12, 0.28, "random"),
+                                                  ((70, 75), 1, 0.25, "warm"), ((70, 75), 30, 0.25, "warm"),
+                                                  ((1, 5), 1, 0.2, "random"), ((6, 1), 1, 0.2, "random")])
+def test_general_quads_fused_subcycles(nx, ora, shape, nsub, delta, kind):
+    """NEXT-1 fused: k_subcycle_gen (strain + stress + divergence + velocity in one TMA-staged pass,
+    geometry on the fly from the vertices) after advection + prep, vs the oracle with the same
+    vertices; ragged shapes span several warp strips / chunks (1 subcycle: 1e-12; more: 1e-10)."""
+    nxe, nye = shape
+    lx, ly = nxe * 2e3, nye * 2e3
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, delta)
+    st = case(nxe, nye, 2, 6, 6, kind, lx, ly)
+    prm = nx.PhysParams(alpha=300.0, beta=300.0) if kind == "random" else nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly, 2, 6, 6, params=prm) as m:
+        m.set_vertices(V)
+        m.load(st)
+        m.advect(prm.dt)
+        m.mevp_substeps(nsub, begin_step=True)
+        got = m.state()
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=2, ns=6, na=6, verts=V)
+    ref = ora.outer_step(om, ora_params(prm), nsub, st, do_advect=True)
+    _check(got, ref, st, TOL1 if nsub == 1 else TOLN, groups=("S", "v"))
+    # A, H: fields only - on the warm box one advection step changes them by ~1e-4 relative, so
+    # their increments are ill-conditioned (as in tests/test_gpu_full_size.py)
+    e = parity(got, ref, st, ("A", "H"))
+    assert e["A"] <= 1e-12 and e["H"] <= 1e-12, e
+
+
+def test_general_quads_fused_equals_box_on_a_box(nx):
+    """A 'general' mesh whose vertices form the axis-aligned box runs k_subcycle_gen; it must agree
+    with the box kernel to rounding (the geometry collapses to hx, hy)."""
+    nxe, nye, lx, ly = 64, 40, 128e3, 80e3
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.0)
+    a = _gpu_run(nx, st, nxe, nye, 2, 6, 6, 5, lx, ly)
+    with nx.Mesh(nxe, nye, lx, ly, 2, 6, 6) as m:
+        m.set_vertices(V)
+        m.load(st)
+        m.mevp_substeps(5, begin_step=True)
+        b = m.state()
+    e = parity(a, b, st)
+    assert max(e.values()) < 1e-12, e
 
 
 def test_general_quads_steps_each(nx, ora):
