@@ -169,9 +169,12 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *                           2: as 1 and the stress update (strain, Listing 2, projection) in FP32 arithmetic
  *   NXSDG_OPT_MAP_MODE      general quads (nxsdg_set_vertices): 0 = per-element iMJwPSI pre-assembled and
  *                           stored, 1 (default) = recomputed on the fly from the 4 vertices
+ *   NXSDG_OPT_P2P_FUSED_STORES  P2P transport with the TMA kernel: 1 (default) = the fused subcycle kernel stores
+ *                           the halo rows (v node rows, S element row) straight into the neighbours' buffers as
+ *                           it computes them, the exchange is the flag handshake alone; 0 = copy-engine copies
  * INVALID_ARG for an unknown option or value. */
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
-       NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6 };
+       NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

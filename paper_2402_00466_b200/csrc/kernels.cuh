@@ -131,6 +131,14 @@ struct SubArgs {
     int repl;
     int* work_counter;              // TMA kernel: dynamic unit counter (zeroed before the launch), or null
     int chunk0, chunk_step, nsel;   // chunk selection: chunks chunk0 + i*chunk_step, i < nsel
+    // P2P transport, fused peer stores (TMA kernel): the rows a neighbour needs are stored straight
+    // into its buffers (peer memory) as they are computed; null pointers = off
+    double* peer_vx_up; double* peer_vy_up; double* peer_S_up;   // upper neighbour's new-state buffers
+    double* peer_vx_dn; double* peer_vy_dn;                      // lower neighbour's
+    int up_node_row0;               // local node rows >= this go up (to the neighbour's rows 0 ..)
+    int up_elem_row;                // local element row whose S goes up (to the neighbour's row 0)
+    int dn_node_row, dn_dst_row;    // local node row that goes down, and its row at the neighbour
+    int64_t peer_up_eplane;         // the upper neighbour's element plane stride
 };
 
 template <int P, int NS_ = Deg<P>::NS>

@@ -149,6 +149,7 @@ struct nxsdg_ctx {
     struct Peer { bool on = false, ipc = false; double* buf[kP2PBufs] = {}; uint32_t* flags = nullptr; Geom g{}; } peer[2];
     uint32_t p2p_seq = 0;
     bool p2p_ok = false;
+    int p2p_fused = 1;               // NXSDG_OPT_P2P_FUSED_STORES
     // graphs: key = (n_sub, cv, cs)
     std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
 };
@@ -423,6 +424,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_MAP_MODE:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "map mode 0|1");
             c->map_mode = (int)value; break;
+        case NXSDG_OPT_P2P_FUSED_STORES:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "p2p fused stores 0|1");
+            c->p2p_fused = (int)value; break;
         case NXSDG_OPT_STAGES:
             if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
             c->stages = (int)value; break;
@@ -1208,6 +1212,13 @@ static nxsdg_status dispatch_prep(nxsdg_ctx* c) {
     return launch_prep<2, 6>(c);
 }
 
+static bool use_tma(const nxsdg_ctx* c);
+// P2P + the TMA box kernel in FP64: the subcycle's halo rows travel as peer stores from the kernel
+static bool p2p_fused_stores(const nxsdg_ctx* c) {
+    return c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_P2P && c->p2p_ok && c->p2p_fused && use_tma(c) &&
+           !c->general && c->precision == 0;
+}
+
 static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     SubArgs a{};
     a.S_in = c->S[cs]; a.S_out = c->S[cs ^ 1]; a.Pg = c->Pg;
@@ -1226,6 +1237,20 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     a.beta = c->prm.beta; a.b1 = 1.0 + c->prm.beta; a.kc = c->prm.dt * c->prm.f_c;
     a.repl = c->prm.replacement_pressure;
     a.chunk0 = 0; a.chunk_step = 1; a.nsel = (c->nown + a.ty - 1) / a.ty;
+    if (p2p_fused_stores(c)) {   // the new state goes to v[cv ^ 1], S[cs ^ 1] on every rank
+        const int iv = p2p_index(c, c->vx[cv ^ 1]), iw = p2p_index(c, c->vy[cv ^ 1]), is = p2p_index(c, c->S[cs ^ 1]);
+        if (c->peer[1].on) {
+            a.peer_vx_up = c->peer[1].buf[iv]; a.peer_vy_up = c->peer[1].buf[iw]; a.peer_S_up = c->peer[1].buf[is];
+            a.up_node_row0 = c->P * (c->glo + c->nown - 1);
+            a.up_elem_row = c->glo + c->nown - 1;
+            a.peer_up_eplane = c->peer[1].g.eplane;
+        }
+        if (c->peer[0].on) {
+            a.peer_vx_dn = c->peer[0].buf[iv]; a.peer_vy_dn = c->peer[0].buf[iw];
+            a.dn_node_row = c->P * c->glo;
+            a.dn_dst_row = c->P * (c->peer[0].g.glo + c->peer[0].g.nown);
+        }
+    }
     return a;
 }
 
@@ -1497,7 +1522,7 @@ static nxsdg_status subcycle_overlapped(nxsdg_ctx* c) {
     nxsdg_status st;
     if (n_chunks(c) < 3) {
         if ((st = launch_subcycle(c))) return st;
-        return halo(c, NXSDG_HALO_V | NXSDG_HALO_S);
+        return halo(c, p2p_fused_stores(c) ? 0u : (uint32_t)(NXSDG_HALO_V | NXSDG_HALO_S));
     }
     if (!c->hstream) {
         CU(cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking));
@@ -1508,7 +1533,7 @@ static nxsdg_status subcycle_overlapped(nxsdg_ctx* c) {
     c->cv ^= 1; c->cs ^= 1;                      // the exchange moves rows of the new state
     CU(cudaEventRecord(c->ev_bnd, c->stream));
     CU(cudaStreamWaitEvent(c->hstream, c->ev_bnd, 0));
-    if ((st = halo_on(c, NXSDG_HALO_V | NXSDG_HALO_S, c->hstream))) return st;
+    if ((st = halo_on(c, p2p_fused_stores(c) ? 0u : (uint32_t)(NXSDG_HALO_V | NXSDG_HALO_S), c->hstream))) return st;
     CU(cudaEventRecord(c->ev_x, c->hstream));
     c->cv ^= 1; c->cs ^= 1;                      // interior reads the old state
     if ((st = launch_subcycle_sel(c, SEL_INTERIOR))) return st;

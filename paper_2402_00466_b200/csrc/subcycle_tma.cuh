@@ -418,6 +418,15 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                 S_out[(NS + k) * eplane + e] = (SF)S12[k];
                 S_out[(2 * NS + k) * eplane + e] = (SF)S22[k];
             }
+            if (a.peer_S_up != nullptr && lr == a.up_elem_row) {   // P2P: the neighbour's ghost element row 0
+                const int64_t pe = a.peer_up_eplane;
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    a.peer_S_up[k * pe + ix] = S11[k];
+                    a.peer_S_up[(NS + k) * pe + ix] = S12[k];
+                    a.peer_S_up[(2 * NS + k) * pe + ix] = S22[k];
+                }
+            }
         }
         // ---- divergence contributions: rX = D_s S11 / hx + D_t S12 / hy, rY likewise
         double rX[3][3], rY[3][3];
@@ -470,13 +479,31 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                     nvx[q] = bnd ? 0.0 : ux;
                     nvy[q] = bnd ? 0.0 : uy;
                 }
-                const int64_t n = (int64_t)(2 * lr + jy) * npitch + 2 * ix;
+                const int jr = 2 * lr + jy;
+                const int64_t n = (int64_t)jr * npitch + 2 * ix;
                 if (ix < a.nx) {
                     *reinterpret_cast<double2*>(a.vx_out + n) = make_double2(nvx[0], nvx[1]);
                     *reinterpret_cast<double2*>(a.vy_out + n) = make_double2(nvy[0], nvy[1]);
                 } else {                                  // ix == nx: only the boundary column 2 nx
                     a.vx_out[n] = 0.0;
                     a.vy_out[n] = 0.0;
+                }
+                // P2P fused peer stores: the same values into the neighbours' ghost node rows (a strip
+                // of one element row sends its bottom node row both ways)
+#pragma unroll
+                for (int d = 0; d < 2; ++d) {
+                    double* pvx = d == 0 ? a.peer_vx_up : a.peer_vx_dn;
+                    double* pvy = d == 0 ? a.peer_vy_up : a.peer_vy_dn;
+                    const bool hit = pvx != nullptr && (d == 0 ? jr >= a.up_node_row0 : jr == a.dn_node_row);
+                    if (!hit) continue;
+                    const int64_t pn = (int64_t)(d == 0 ? jr - a.up_node_row0 : a.dn_dst_row) * npitch + 2 * ix;
+                    if (ix < a.nx) {
+                        *reinterpret_cast<double2*>(pvx + pn) = make_double2(nvx[0], nvx[1]);
+                        *reinterpret_cast<double2*>(pvy + pn) = make_double2(nvy[0], nvy[1]);
+                    } else {
+                        pvx[pn] = 0.0;
+                        pvy[pn] = 0.0;
+                    }
                 }
             }
         }

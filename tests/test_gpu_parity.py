@@ -685,12 +685,15 @@ def test_loopback_strips_bitwise_equal_single(nx, nranks, ty, variant):
         np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
 
 
-@pytest.mark.parametrize("nranks,ty,ns", [(2, 4, 6), (3, 4, 6), (2, 32, 6), (3, 5, 8)])
-def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns):
+@pytest.mark.parametrize("nranks,ty,ns,fused", [(2, 4, 6, 1), (3, 4, 6, 1), (2, 32, 6, 1), (3, 5, 8, 1),
+                                                (3, 4, 6, 0), (2, 32, 8, 0), (47, 1, 6, 1), (47, 1, 6, 0)])
+def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns, fused):
     """P2P transport inside one process: every rank on its OWN stream, so the ranks run
     concurrently and the only ordering between them is the device-side flag handshake; halo rows
     are copied straight into the neighbours' buffers.  Advection, fused subcycles (boundary /
-    interior overlap with ty = 4) and unfused subcycles: bitwise equal to one context."""
+    interior overlap with ty = 4) and unfused subcycles: bitwise equal to one context.  fused = 1:
+    the fused kernel stores the halo rows into the neighbours' buffers itself (the exchange is the
+    flag handshake alone); 0: copy-engine copies.  47 ranks: one element row per strip."""
     nxe, nye, lx, ly = 50, 47, 50e3, 47e3
     st = case(nxe, nye, 2, ns, 6, "random", lx, ly)
     prm = nx.PhysParams()
@@ -705,6 +708,7 @@ def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns):
     nx.p2p_connect_local(ms)
     for m in ms:
         m.set_option(nx.OPT_CHUNK_ROWS, ty)
+        m.set_option(nx.OPT_P2P_FUSED_STORES, fused)
         er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
         loc = {k: st[k][nr0:nr0 + nrn].copy() for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
         for k in ("S11", "S12", "S22", "A", "H"):
