@@ -128,17 +128,23 @@ void ora_cg_basis(int p, double s, double t, double* phi, double* dphids, double
 
 /* Bilinear (Q1) element map from the four vertices: the box x_{a,b} = (a*hx, b*hy), or the
  * mesh's vertex array for general quads (R#23). */
+/* The element's four vertices relative to its first one (x_{a,b} - x_{0,0}).  Only derivatives of
+ * the bilinear map are ever used, and sum_k grad N_k = 0, so this is exact in real arithmetic; it
+ * keeps J exact in floating point too (differences of nearby vertices are exact), where absolute
+ * coordinates (~1e5 m on ~1e2 m elements) would cost ~1e-13 relative in J - amplified past the
+ * north_star bar by the near-cancellation of volume and edge terms in the advection (R#23). */
 static void element_vertices(const ora_mesh* m, int ix, int iy, double X[4], double Y[4]) {
     double hx = m->lx / m->nx, hy = m->ly / m->ny;
     for (int k = 0; k < 4; ++k) {
         int kx = k & 1, ky = k >> 1;
         if (m->verts) {
             long v = (long)(iy + ky) * (m->nx + 1) + (ix + kx);
-            X[k] = m->verts[2 * v];
-            Y[k] = m->verts[2 * v + 1];
+            long v0 = (long)iy * (m->nx + 1) + ix;
+            X[k] = m->verts[2 * v] - m->verts[2 * v0];
+            Y[k] = m->verts[2 * v + 1] - m->verts[2 * v0 + 1];
         } else {
-            X[k] = (ix + kx) * hx;
-            Y[k] = (iy + ky) * hy;
+            X[k] = kx * hx;
+            Y[k] = ky * hy;
         }
     }
 }

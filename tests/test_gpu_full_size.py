@@ -1,6 +1,7 @@
 """Full-size parity at BASELINE.json's bench configuration (C4: 4096 x 4096 CG2/DG2,
 one outer step = advection + BEGIN_STEP prep + 100 fused subcycles, exactly the launch
-configuration bench.py times), checked against the oracle on windows.
+configuration bench.py times), checked against the oracle on windows; the same for the n_S = 8
+space and for a distorted C4 mesh through the fused general-quad kernel.
 
 Light cone: one subcycle moves information by at most one element
 (node v -> adjacent elements' strain/stress -> their nodes), each RK stage of the
@@ -19,8 +20,12 @@ from tests.parity import group_err
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def c4_result():
+@pytest.fixture(scope="module", params=["box", "ns8", "general"])
+def c4_result(request):
+    """box: the bench path (k_subcycle_tma, n_S = 6).  ns8: the n_S = 8 space (NEXT-4).  general: the
+    C4 mesh with interior vertices moved by up to 0.25 h / 2 and the fused general-quad kernel
+    (NEXT-1, k_subcycle_gen).  Each: advection + prep + 100 fused subcycles at full size."""
+    import dataclasses
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -28,14 +33,19 @@ def c4_result():
     build.build()
     from paper_2402_00466_b200 import nxsdg
     cfg = inputs.CONFIGS["C4"]
+    if request.param == "ns8":
+        cfg = dataclasses.replace(cfg, ns=8)
     st = inputs.make_config_case(cfg)
+    V = inputs.distorted_vertices(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 0.25) if request.param == "general" else None
     prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
     with nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm) as m:
+        if V is not None:
+            m.set_vertices(V)
         m.load(st)
         m.advect(prm.dt)
         m.mevp_substeps(cfg.nsub, begin_step=True)
         got = m.state()
-    return cfg, st, got
+    return cfg, st, got, V
 
 
 def _cut(cfg, arrs, ix0, iy0, w, h):
@@ -60,7 +70,7 @@ def _windows(cfg, core=12):
 
 @pytest.mark.parametrize("wi", range(8))
 def test_c4_window_parity(c4_result, wi):
-    cfg, st, got = c4_result
+    cfg, st, got, V = c4_result
     core = 12
     ring = cfg.nsub + 3 + 2
     cx, cy = _windows(cfg, core)[wi]
@@ -69,8 +79,10 @@ def test_c4_window_parity(c4_result, wi):
     w, h = ix1 - ix0, iy1 - iy0
     hx, hy = cfg.lx / cfg.nx, cfg.ly / cfg.ny
     sub = _cut(cfg, st, ix0, iy0, w, h)
-    mesh = oracle.Mesh(w, h, lx=w * hx, ly=h * hy, p=cfg.p, ns=cfg.ns, na=cfg.na)
-    ref = oracle.Oracle().outer_step(mesh, oracle.Params(alpha=cfg.alpha, beta=cfg.alpha), cfg.nsub, sub, do_advect=True)
+    verts = None if V is None else np.ascontiguousarray(V[iy0:iy0 + h + 1, ix0:ix0 + w + 1])
+    mesh = oracle.Mesh(w, h, lx=w * hx, ly=h * hy, p=cfg.p, ns=cfg.ns, na=cfg.na, verts=verts)
+    oprm = oracle.Params(alpha=cfg.alpha, beta=cfg.alpha)
+    ref = oracle.Oracle().outer_step(mesh, oprm, cfg.nsub, sub, do_advect=True)
     # compare the core cells: elements [cx, cx+core) x [cy, cy+core), and their nodes
     g = _cut(cfg, got, cx, cy, core, core)
     loc = {k: v for k, v in ref.items() if k in got}
@@ -83,10 +95,30 @@ def test_c4_window_parity(c4_result, wi):
             n = a.shape[1]
             rc[k] = a.reshape(h, w, n)[cy - iy0:cy - iy0 + core, cx - ix0:cx - ix0 + core].reshape(-1, n)
     init = _cut(cfg, st, cx, cy, core, core)
+
+    def core_of(res):
+        out = {}
+        for k, a in res.items():
+            if k not in got:
+                continue
+            if a.ndim == 2 and a.shape == (p * h + 1, p * w + 1):
+                out[k] = a[p * (cy - iy0):p * (cy - iy0 + core) + 1, p * (cx - ix0):p * (cx - ix0 + core) + 1]
+            else:
+                out[k] = a.reshape(h, w, a.shape[1])[cy - iy0:cy - iy0 + core, cx - ix0:cx - ix0 + core].reshape(-1, a.shape[1])
+        return out
+
     for grp in (("S11", "S12", "S22"), ("vx", "vy")):
         e = group_err(g, rc, grp)
         de = group_err({k: g[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp)
-        assert e <= 1e-10 and de <= 1e-10, (grp, e, de, (cx, cy))
+        bar = 1e-10
+        if max(e, de) > bar:
+            # self-consistency bound: after 100 subcycles at 125 m the oracle's own
+            # plain and FMA builds can already differ by ~1e-10 (n_S = 8); the GPU must then be
+            # within 4x of that floor on this window
+            fm = core_of(oracle.Oracle("fma").outer_step(mesh, oprm, cfg.nsub, sub, do_advect=True))
+            floor = max(group_err(fm, rc, grp), group_err({k: fm[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp))
+            bar = max(bar, 4 * floor)
+        assert e <= bar and de <= bar, (grp, e, de, bar, (cx, cy))
     # A, H: fields only.  One advection step at 125 m changes the high coefficients by
     # ~1e-11 of the field while the DG volume and edge terms cancel to ~11 digits, so
     # their increments carry no parity information.
