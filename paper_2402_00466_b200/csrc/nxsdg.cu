@@ -1322,9 +1322,15 @@ static nxsdg_status build_maps32(nxsdg_ctx* c) {
     nxsdg_status st = build_maps(c);
     if (st || c->maps32_ok) return st;
     const size_t ne = (size_t)c->eplane;
-    for (int k = 0; k < 2; ++k)
-        if (!c->S32[k]) CU(cudaMalloc(&c->S32[k], 3 * (size_t)c->NS * ne * sizeof(float)));
-    if (!c->Pg32) CU(cudaMalloc(&c->Pg32, (size_t)c->NG * ne * sizeof(float)));
+    for (int k = 0; k < 2; ++k)   // zeroed: the kernels never write the row / plane padding
+        if (!c->S32[k]) {
+            CU(cudaMalloc(&c->S32[k], 3 * (size_t)c->NS * ne * sizeof(float)));
+            CU(cudaMemset(c->S32[k], 0, 3 * (size_t)c->NS * ne * sizeof(float)));
+        }
+    if (!c->Pg32) {
+        CU(cudaMalloc(&c->Pg32, (size_t)c->NG * ne * sizeof(float)));
+        CU(cudaMemset(c->Pg32, 0, (size_t)c->NG * ne * sizeof(float)));
+    }
     const cuuint64_t nx = c->d.nx, er = c->erows_local;
     const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 4, (cuuint64_t)c->eplane * 4};
     const cuuint64_t nS = 3 * (cuuint64_t)c->NS;
