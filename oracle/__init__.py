@@ -246,6 +246,19 @@ class Oracle:
                "advect")
         return A, H
 
+    def limit(self, mesh: Mesh, c, lo: float, hi: float = float("inf")):
+        c = _f(c).copy()
+        m = mesh.c()
+        _check(self.L.ora_limit(C.byref(m), C.c_double(lo), C.c_double(hi), _ptr(c)), "limit")
+        return c
+
+    def advect_limited(self, mesh: Mesh, dt: float, vx, vy, A, H, limiter: int = 1):
+        A = _f(A).copy(); H = _f(H).copy()
+        m = mesh.c()
+        _check(self.L.ora_advect_limited(C.byref(m), C.c_double(dt), _ptr(_f(vx)), _ptr(_f(vy)), _ptr(A), _ptr(H),
+                                         int(limiter)), "advect_limited")
+        return A, H
+
     def outer_step(self, mesh: Mesh, prm: Params, nsub: int, st: dict, do_advect: bool = True) -> dict:
         out = {k: _f(v).copy() for k, v in st.items()}
         m, pr = mesh.c(), prm.c()

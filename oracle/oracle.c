@@ -691,7 +691,11 @@ int ora_advect_rhs(const ora_mesh* m, const double* vx, const double* vy,
 
 /* Explicit RK of the advection ("higher order explicit Runge-Kutta"; R#18):
  * na=1 forward Euler, na=3 SSP-RK2 (Heun), na=6 SSP-RK3 (Shu-Osher). */
-static int advect_one(const ora_mesh* m, double dt, const double* vx, const double* vy, double* c) {
+int ora_limit(const ora_mesh* m, double lo, double hi, double* c);
+
+/* SSP-RK stages; with limiter != 0 the bound-preserving limiter (R#25) acts on every stage value. */
+static int advect_one(const ora_mesh* m, double dt, const double* vx, const double* vy, double* c,
+                      int limiter, double lo, double hi) {
     long n = (long)m->nx * m->ny * m->na;
     double* c0 = (double*)malloc(sizeof(double) * n);
     double* c1 = (double*)malloc(sizeof(double) * n);
@@ -701,17 +705,21 @@ static int advect_one(const ora_mesh* m, double dt, const double* vx, const doub
     memcpy(c0, c, sizeof(double) * n);
     if ((rc = ora_advect_rhs(m, vx, vy, c0, L))) goto done;
     for (long i = 0; i < n; ++i) c1[i] = c0[i] + dt * L[i];
+    if (limiter) ora_limit(m, lo, hi, c1);
     if (m->na == 1) {
         memcpy(c, c1, sizeof(double) * n);
     } else if (m->na == 3) {
         if ((rc = ora_advect_rhs(m, vx, vy, c1, L))) goto done;
         for (long i = 0; i < n; ++i) c[i] = 0.5 * c0[i] + 0.5 * (c1[i] + dt * L[i]);
+        if (limiter) ora_limit(m, lo, hi, c);
     } else {
         if ((rc = ora_advect_rhs(m, vx, vy, c1, L))) goto done;
         double* c2 = c; /* reuse output as stage 2 */
         for (long i = 0; i < n; ++i) c2[i] = 0.75 * c0[i] + 0.25 * (c1[i] + dt * L[i]);
+        if (limiter) ora_limit(m, lo, hi, c2);
         if ((rc = ora_advect_rhs(m, vx, vy, c2, L))) goto done;
         for (long i = 0; i < n; ++i) c[i] = (1.0 / 3.0) * c0[i] + (2.0 / 3.0) * (c2[i] + dt * L[i]);
+        if (limiter) ora_limit(m, lo, hi, c);
     }
 done:
     free(c0); free(c1); free(L);
@@ -721,8 +729,69 @@ done:
 int ora_advect(const ora_mesh* m, double dt, const double* vx, const double* vy,
                double* A, double* H) {
     int rc = check_mesh(m); if (rc) return rc;
-    if ((rc = advect_one(m, dt, vx, vy, A))) return rc;
-    return advect_one(m, dt, vx, vy, H);
+    if ((rc = advect_one(m, dt, vx, vy, A, 0, 0.0, 0.0))) return rc;
+    return advect_one(m, dt, vx, vy, H, 0, 0.0, 0.0);
+}
+
+/* NEXT-4 (R#25): bound-preserving scaling limiter of Zhang & Shu (maximum-principle-satisfying DG),
+ * per element: with the physical mean cbar = int c |J| / int |J| (Gauss rule of the advection) and
+ * the extremes cmin, cmax of c over the points where the scheme evaluates it - the ngp x ngp volume
+ * Gauss points and the ngp Gauss points of each of the 4 edges -
+ *   theta = min(1, (cbar - lo) / (cbar - cmin) if cmin < lo, (hi - cbar) / (cmax - cbar) if cmax > hi),
+ * clamped to [0, 1], and c <- cbar + theta (c - cbar): the mean (mass) is kept, the values at the
+ * check points land in [lo, hi] (hi = +inf for no upper bound). */
+int ora_limit(const ora_mesh* m, double lo, double hi, double* c) {
+    int rc = check_mesh(m); if (rc) return rc;
+    int na = m->na, ngp = ora_ngp(m->ns), ng = ngp * ngp;
+    if (na == 1) return 0;                       /* DG0: c is its own mean */
+    double xg[3], wg[3];
+    ora_gauss(ngp, xg, wg);
+    long N = (long)m->nx * m->ny;
+#pragma omp parallel for schedule(static)
+    for (long e = 0; e < N; ++e) {
+        int ix = (int)(e % m->nx), iy = (int)(e / m->nx);
+        double* ce = c + e * na;
+        double psi[MAXN], mass = 0.0, integ = 0.0;
+        double cmin = INFINITY, cmax = -INFINITY;
+        for (int gy = 0; gy < ngp; ++gy)
+            for (int gx = 0; gx < ngp; ++gx) {
+                double s = xg[gx], t = xg[gy], w = wg[gx] * wg[gy];
+                double detJ = ora_element_jacobian(m, ix, iy, s, t, NULL);
+                ora_dg_basis(na, s, t, psi);
+                double v = 0.0;
+                for (int k = 0; k < na; ++k) v += ce[k] * psi[k];
+                integ += w * detJ * v;
+                mass += w * detJ;
+                cmin = fmin(cmin, v); cmax = fmax(cmax, v);
+            }
+        for (int edge = 0; edge < 4; ++edge)
+            for (int q = 0; q < ngp; ++q) {
+                double s = edge == 0 ? 1.0 : (edge == 1 ? 0.0 : xg[q]);
+                double t = edge == 2 ? 1.0 : (edge == 3 ? 0.0 : xg[q]);
+                ora_dg_basis(na, s, t, psi);
+                double v = 0.0;
+                for (int k = 0; k < na; ++k) v += ce[k] * psi[k];
+                cmin = fmin(cmin, v); cmax = fmax(cmax, v);
+            }
+        double cbar = integ / mass, theta = 1.0;
+        if (cmin < lo) theta = fmin(theta, (cbar - lo) / (cbar - cmin));
+        if (cmax > hi) theta = fmin(theta, (hi - cbar) / (cmax - cbar));
+        theta = fmax(0.0, fmin(1.0, theta));
+        if (theta < 1.0) {
+            /* c <- cbar + theta (c - cbar): psi_0 = 1, so the constant goes into coefficient 0 */
+            for (int k = 0; k < na; ++k) ce[k] *= theta;
+            ce[0] += (1.0 - theta) * cbar;
+        }
+    }
+    (void)ng;
+    return 0;
+}
+
+int ora_advect_limited(const ora_mesh* m, double dt, const double* vx, const double* vy,
+                       double* A, double* H, int limiter) {
+    int rc = check_mesh(m); if (rc) return rc;
+    if ((rc = advect_one(m, dt, vx, vy, A, limiter, 0.0, 1.0))) return rc;       /* A in [0, 1] */
+    return advect_one(m, dt, vx, vy, H, limiter, 0.0, INFINITY);                  /* H >= 0      */
 }
 
 /* One outer step in paper order (R#15): advect A, H with the current v,

@@ -77,6 +77,11 @@ int ora_advect_rhs(const ora_mesh* m, const double* vx, const double* vy,
                    const double* c, double* rhs);
 int ora_advect(const ora_mesh* m, double dt, const double* vx, const double* vy,
                double* A, double* H);
+/* NEXT-4 (R#25): Zhang-Shu bound-preserving scaling limiter (keeps the |J|-weighted element mean)
+ * and advection with it applied after every SSP-RK stage (A in [0,1], H >= 0). */
+int ora_limit(const ora_mesh* m, double lo, double hi, double* c);
+int ora_advect_limited(const ora_mesh* m, double dt, const double* vx, const double* vy,
+                       double* A, double* H, int limiter);
 int ora_outer_step(const ora_mesh* m, const ora_params* prm, int nsub, int do_advect,
                    const double* ox, const double* oy, const double* ax, const double* ay,
                    double* vx, double* vy, double* S11, double* S12, double* S22,

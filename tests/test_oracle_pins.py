@@ -766,3 +766,112 @@ def test_distorted_stress_scale_invariance(ora):
     b = ora.stress(big, Params(), *E, H, A, *S)
     for x, y in zip(a, b):
         np.testing.assert_allclose(x, y, rtol=1e-12, atol=1e-12 * np.abs(x).max())
+
+
+# ---------------------------------------------------------------- NEXT-4: bound-preserving limiter (R#25)
+_FAM6 = [lambda S, T: 1 + 0 * S, lambda S, T: S, lambda S, T: T, lambda S, T: S * S - 1 / 12,
+         lambda S, T: T * T - 1 / 12, lambda S, T: S * T]
+
+
+def _check_points(ngp=3):
+    x, _ = np.polynomial.legendre.leggauss(ngp)
+    q = 0.5 * (x + 1)
+    pts = [(a, b) for b in q for a in q]
+    pts += [(1.0, b) for b in q] + [(0.0, b) for b in q] + [(a, 1.0) for a in q] + [(a, 0.0) for a in q]
+    return pts
+
+
+def _eval6(c, s, t):
+    return sum(c[k] * f(s - 0.5, t - 0.5) for k, f in enumerate(_FAM6))
+
+
+def _phys_mean(c, X, Y):
+    """|J|-weighted mean of the DG2 polynomial over a bilinear element (independent 6-point rule)."""
+    xi, wi = np.polynomial.legendre.leggauss(6)
+    q, w = 0.5 * (xi + 1), 0.5 * wi
+    num = den = 0.0
+    for a in range(6):
+        for b in range(6):
+            s, t = q[a], q[b]
+            xs = (X[1] - X[0]) * (1 - t) + (X[3] - X[2]) * t; xt = (X[2] - X[0]) * (1 - s) + (X[3] - X[1]) * s
+            ys = (Y[1] - Y[0]) * (1 - t) + (Y[3] - Y[2]) * t; yt = (Y[2] - Y[0]) * (1 - s) + (Y[3] - Y[1]) * s
+            dj = xs * yt - xt * ys
+            num += w[a] * w[b] * dj * _eval6(c, s, t); den += w[a] * w[b] * dj
+    return num / den
+
+
+def test_limiter_closed_form(ora):
+    """R#25, Zhang-Shu: c = 0.9 + 0.4 S on a box element peaks at the east edge (S = 1/2) at 1.1, so
+    theta = (1 - 0.9) / (1.1 - 0.9) = 1/2 and the slope halves; the mean stays; no upper bound -> unchanged."""
+    mesh = Mesh(1, 1, lx=1.0, ly=1.0, p=2, ns=6, na=6)
+    c = np.array([[0.9, 0.4, 0.0, 0.0, 0.0, 0.0]])
+    np.testing.assert_allclose(ora.limit(mesh, c, 0.0, 1.0), [[0.9, 0.2, 0, 0, 0, 0]], atol=1e-15)
+    np.testing.assert_array_equal(ora.limit(mesh, c, 0.0), c)
+    # mean below the lower bound cannot be fixed: theta = 0 leaves the mean alone
+    c2 = np.array([[-0.1, 0.3, 0.1, 0.0, 0.02, 0.0]])
+    np.testing.assert_allclose(ora.limit(mesh, c2, 0.0, 1.0), [[-0.1, 0, 0, 0, 0, 0]], atol=1e-15)
+
+
+@pytest.mark.parametrize("distorted", [False, True])
+def test_limiter_keeps_mean_and_bounds(ora, distorted):
+    """Random DG2 data: after limiting, the |J|-weighted element mean is unchanged (independent
+    6-point integration of the bilinear map) and the values at every check point (volume and edge
+    Gauss points) lie in [0, 1]; elements already inside the bounds are untouched."""
+    nx, ny, lx, ly = 7, 5, 7e3, 5e3
+    V = inputs.distorted_vertices(nx, ny, lx, ly, 0.28) if distorted else None
+    mesh = Mesh(nx, ny, lx=lx, ly=ly, p=2, ns=6, na=6, verts=V)
+    r = np.random.default_rng(13)
+    c = np.zeros((nx * ny, 6))
+    c[:, 0] = r.uniform(0.05, 0.95, nx * ny)
+    c[:, 1:] = r.uniform(-0.6, 0.6, (nx * ny, 5))
+    c[::3, 1:] *= 1e-3                        # some elements well inside the bounds
+    out = ora.limit(mesh, c, 0.0, 1.0)
+    pts = _check_points()
+    hx, hy = lx / nx, ly / ny
+    for e in range(nx * ny):
+        ix, iy = e % nx, e // nx
+        if V is not None:
+            X = [V[iy + b, ix + a, 0] for b in (0, 1) for a in (0, 1)]; Y = [V[iy + b, ix + a, 1] for b in (0, 1) for a in (0, 1)]
+        else:
+            X = [(ix + a) * hx for b in (0, 1) for a in (0, 1)]; Y = [(iy + b) * hy for b in (0, 1) for a in (0, 1)]
+        assert abs(_phys_mean(out[e], X, Y) - _phys_mean(c[e], X, Y)) < 1e-14
+        vals = [_eval6(out[e], s, t) for s, t in pts]
+        assert min(vals) >= -1e-14 and max(vals) <= 1 + 1e-14
+        if min(_eval6(c[e], s, t) for s, t in pts) >= 0 and max(_eval6(c[e], s, t) for s, t in pts) <= 1:
+            np.testing.assert_array_equal(out[e], c[e])
+
+
+def test_limited_advection_bounds_and_mass(ora):
+    """A discontinuous concentration (1 inside a disc, 0.5 outside, L2-projected into DG2 and limited)
+    in a uniform periodic flow within Zhang-Shu's CFL bound: the unlimited SSP-RK3 step overshoots 1
+    at the check points, the limited one stays in [0, 1] and conserves the total mass exactly
+    (periodic box, the limiter keeps element means)."""
+    nx = ny = 24
+    lx = ly = 24e3
+    mesh = Mesh(nx, ny, lx=lx, ly=ly, p=2, ns=6, na=6, bc=1)
+    xi, wi = np.polynomial.legendre.leggauss(5)
+    q, w = 0.5 * (xi + 1), 0.5 * wi
+    norm = np.array([1, 1 / 12, 1 / 12, 1 / 180, 1 / 180, 1 / 144])
+    A = np.zeros((nx * ny, 6))
+    for e in range(nx * ny):
+        ix, iy = e % nx, e // nx
+        for a in range(5):
+            for b in range(5):
+                x, y = (ix + q[a]) * 1e3, (iy + q[b]) * 1e3
+                f = 1.0 if (x - 12e3) ** 2 + (y - 12e3) ** 2 < (5e3) ** 2 else 0.5
+                for k, g in enumerate(_FAM6):
+                    A[e, k] += w[a] * w[b] * f * g(q[a] - 0.5, q[b] - 0.5) / norm[k]
+    A = ora.limit(mesh, A, 0.0, 1.0)          # bounded initial state (the projection's Gibbs overshoot removed)
+    H = A.copy()
+    shp = mesh.node_shape
+    vx, vy = np.full(shp, 0.3), np.full(shp, 0.2)
+    dt = 200.0                                # (|u|/hx + |v|/hy) dt = 0.1 <= 1/6: Zhang-Shu's CFL for DG2
+    pts = _check_points()
+    ev = lambda C: np.array([[_eval6(C[e], s, t) for s, t in pts] for e in range(nx * ny)])
+    Au, _ = ora.advect(mesh, dt, vx, vy, A, H)
+    Al, Hl = ora.advect_limited(mesh, dt, vx, vy, A, H, 1)
+    assert ev(Au).max() > 1 + 1e-3
+    vl = ev(Al)
+    assert vl.max() <= 1 + 1e-13 and vl.min() >= -1e-13
+    assert abs(Al[:, 0].sum() - A[:, 0].sum()) <= 1e-13 * A[:, 0].sum()
+    assert ev(Hl).min() >= -1e-13 and abs(Hl[:, 0].sum() - H[:, 0].sum()) <= 1e-13 * H[:, 0].sum()
