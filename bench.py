@@ -181,6 +181,8 @@ def main():
                     help="NEXT-3: S and P_g stored in FP32 inside the fused subcycles (arithmetic FP64)")
     ap.add_argument("--fp32-stress", action="store_true",
                     help="NEXT-3: as --fp32-storage plus the stress update (strain, Listing 2, projection) in FP32")
+    ap.add_argument("--limiter", action="store_true",
+                    help="NEXT-4: Zhang-Shu bound-preserving limiter after every advection stage (R#25)")
     ap.add_argument("--moving", action="store_true",
                     help="NEXT-2: regenerate the moving-cyclone forcing on the GPU at every outer step (P:350 protocol)")
     ap.add_argument("--ns", type=int, default=None, choices=[6, 8],
@@ -235,6 +237,8 @@ def main():
         nxsdg.p2p_connect_group(m, rank, world, dist.all_gather_object)
     if args.fp32_storage or args.fp32_stress:
         m.set_option(nxsdg.OPT_PRECISION, 2 if args.fp32_stress else 1)
+    if args.limiter:
+        m.set_option(nxsdg.OPT_LIMITER, 1)
     m.load(st)
     stream = torch.cuda.ExternalStream(m.stream)
     n_el = cfg.nx * cfg.ny   # whole job
@@ -353,6 +357,7 @@ def main():
                        "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el, "alpha": cfg.alpha, "beta": cfg.alpha,
                        "parallelism": f"row strips x{world} ({args.transport} halo)" if world > 1 else "1 GPU",
                        "forcing": "moving cyclone regenerated on the GPU every step" if args.moving else "static (t = 0)",
+                       "limiter": bool(args.limiter),
                        "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},
             "breakdown_ms": {"advect": adv, "prep": prep, "subcycles": sub, "per_subcycle": kernel_ms},
             "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",

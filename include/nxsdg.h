@@ -172,9 +172,13 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_P2P_FUSED_STORES  P2P transport with the TMA kernel: 1 (default) = the fused subcycle kernel stores
  *                           the halo rows (v node rows, S element row) straight into the neighbours' buffers as
  *                           it computes them, the exchange is the flag handshake alone; 0 = copy-engine copies
+ *   NXSDG_OPT_LIMITER       NEXT-4 (DESIGN R#25): 0 (default, the paper's unlimited scheme) | 1 = Zhang-Shu
+ *                           bound-preserving scaling limiter after every SSP-RK stage of nxsdg_advect (A in [0,1],
+ *                           H >= 0 at the volume and edge Gauss points; element means, hence mass, unchanged)
  * INVALID_ARG for an unknown option or value. */
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
-       NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7 };
+       NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,
+       NXSDG_OPT_LIMITER = 8 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

@@ -678,6 +678,71 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect(AdvArgs a) {
 // owned node rows: o = 0.01 (2y/Ly - 1, 1 - 2x/Lx); a = -(W e / r0) exp(-r/r0) R_theta (x - c(t)),
 // c(t) = (Lx/2, Ly/2) + 51.2 km/day t (1, 1), W = 15 m/s, r0 = 100 km, theta = 72 deg.
 // --------------------------------------------------------------------------
+// --------------------------------------------------------------------------
+// NEXT-4 (R#25): Zhang-Shu bound-preserving scaling limiter, applied to an advection stage's output
+// (owned rows): theta from the extremes over the volume and edge Gauss points (the points where the
+// scheme evaluates the tracer), c <- cbar + theta (c - cbar) about the |J|-weighted element mean
+// cbar = c0 + (d1 c1 + d2 c2) / (12 C0)  (|J| = C0 + d1 S + d2 T; d1 = d2 = 0 on the box).
+// A in [0, 1], H >= 0.
+// --------------------------------------------------------------------------
+struct LimArgs {
+    double* A; double* H; const double* verts;   // verts: general quads (single rank), else null
+    int64_t eplane, epitch;
+    int nx, erow_begin, erow_end;
+};
+template <int P, int NA>
+__global__ void k_limit(LimArgs a) {
+    const RefTab& T = c_tab[P - 1];
+    constexpr int NGP = P + 1, NG = NGP * NGP;
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x, lr = a.erow_begin + blockIdx.y;
+    if (ix >= a.nx || lr >= a.erow_end) return;
+    const int64_t e = (int64_t)lr * a.epitch + ix;
+    double d1 = 0.0, d2 = 0.0, C0 = 1.0;
+    if (a.verts) {
+        const double* v00 = a.verts + 2 * ((int64_t)lr * (a.nx + 1) + ix);
+        const double* v01 = v00 + 2 * (a.nx + 1);
+        const double ax = v00[2] - v00[0], ay = v00[3] - v00[1], bx = v01[0] - v00[0], by = v01[1] - v00[1];
+        const double cx = (v01[2] - v01[0]) - ax, cy = (v01[3] - v01[1]) - ay;
+        const double d0 = ax * by - bx * ay;
+        d1 = ax * cy - cx * ay; d2 = cx * by - bx * cy;
+        C0 = d0 + 0.5 * (d1 + d2);
+    }
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+        double* base = f == 0 ? a.A : a.H;
+        const double lo = 0.0, hi = f == 0 ? 1.0 : INFINITY;
+        double c[NA];
+#pragma unroll
+        for (int k = 0; k < NA; ++k) c[k] = base[k * a.eplane + e];
+        double cmin = INFINITY, cmax = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < NA; ++k) v = fma(c[k], T.psi[k][g], v);
+            cmin = fmin(cmin, v); cmax = fmax(cmax, v);
+        }
+#pragma unroll
+        for (int ed = 0; ed < 4; ++ed)
+#pragma unroll
+            for (int q = 0; q < NGP; ++q) {
+                double v = 0.0;
+#pragma unroll
+                for (int k = 0; k < NA; ++k) v = fma(c[k], T.psiedge[ed][k][q], v);
+                cmin = fmin(cmin, v); cmax = fmax(cmax, v);
+            }
+        const double cbar = c[0] + (d1 * c[1] + d2 * c[2]) / (12.0 * C0);
+        double theta = 1.0;
+        if (cmin < lo) theta = fmin(theta, (cbar - lo) / (cbar - cmin));
+        if (cmax > hi) theta = fmin(theta, (hi - cbar) / (cmax - cbar));
+        theta = fmax(0.0, fmin(1.0, theta));
+        if (theta < 1.0) {
+#pragma unroll
+            for (int k = 0; k < NA; ++k) base[k * a.eplane + e] = (k == 0 ? fma(1.0 - theta, cbar, theta * c[0]) : theta * c[k]);
+        }
+    }
+}
+
 struct ForcingArgs {
     double* ox; double* oy; double* ax; double* ay;
     int64_t npitch;

@@ -150,6 +150,7 @@ struct nxsdg_ctx {
     uint32_t p2p_seq = 0;
     bool p2p_ok = false;
     int p2p_fused = 1;               // NXSDG_OPT_P2P_FUSED_STORES
+    int limiter = 0;                 // NXSDG_OPT_LIMITER (NEXT-4, R#25)
     // graphs: key = (n_sub, cv, cs)
     std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
 };
@@ -424,6 +425,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_MAP_MODE:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "map mode 0|1");
             c->map_mode = (int)value; break;
+        case NXSDG_OPT_LIMITER:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "limiter 0|1");
+            c->limiter = (int)value; break;
         case NXSDG_OPT_P2P_FUSED_STORES:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "p2p fused stores 0|1");
             c->p2p_fused = (int)value; break;
@@ -1765,11 +1769,28 @@ static int stage_out_buf(const nxsdg_ctx* c, int stage) {
     return 0;
 }
 
+template <int P, int NA>
+static nxsdg_status limit_t(nxsdg_ctx* c, double* A, double* H) {
+    LimArgs a{};
+    a.A = A; a.H = H; a.verts = c->general ? c->verts : nullptr;
+    a.eplane = c->eplane; a.epitch = c->epitch; a.nx = c->d.nx; a.erow_begin = c->glo; a.erow_end = c->glo + c->nown;
+    dim3 b(128), g((unsigned)((c->d.nx + 127) / 128), (unsigned)c->nown);
+    k_limit<P, NA><<<g, b, 0, c->stream>>>(a);
+    LAUNCHED();
+    return NXSDG_OK;
+}
+
 static nxsdg_status advect_stage(nxsdg_ctx* c, double dt, int stage) {
-    if (c->P == 1) return c->NA == 1 ? advect_t<1, 1>(c, dt, stage) : advect_t<1, 3>(c, dt, stage);
-    if (c->NA == 1) return advect_t<2, 1>(c, dt, stage);
-    if (c->NA == 3) return advect_t<2, 3>(c, dt, stage);
-    return advect_t<2, 6>(c, dt, stage);
+    nxsdg_status s;
+    if (c->P == 1) s = c->NA == 1 ? advect_t<1, 1>(c, dt, stage) : advect_t<1, 3>(c, dt, stage);
+    else if (c->NA == 1) s = advect_t<2, 1>(c, dt, stage);
+    else if (c->NA == 3) s = advect_t<2, 3>(c, dt, stage);
+    else s = advect_t<2, 6>(c, dt, stage);
+    if (s || !c->limiter || c->NA == 1) return s;
+    // NEXT-4 (R#25): bound-preserving limiter on the stage output, before its halo exchange
+    const int ob = stage_out_buf(c, stage);
+    if (c->P == 1) return limit_t<1, 3>(c, c->Asc[ob], c->Hsc[ob]);
+    return c->NA == 3 ? limit_t<2, 3>(c, c->Asc[ob], c->Hsc[ob]) : limit_t<2, 6>(c, c->Asc[ob], c->Hsc[ob]);
 }
 
 // the final stage buffer becomes A, H (pointer swap; ghost rows are refreshed by the next exchange)

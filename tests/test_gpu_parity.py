@@ -158,6 +158,75 @@ def test_advection(nx, ora, na, bc):
         assert abs(got["A"][:, 0].sum() - st["A"][:, 0].sum()) < 1e-12 * abs(st["A"][:, 0]).sum()
 
 
+def _steep_tracers(nxe, nye, na, seed=5):
+    """Seeded tracer coefficients with large slopes: many elements leave [0, 1] at the check points."""
+    r = np.random.default_rng(seed)
+    A = r.uniform(-0.5, 0.5, (nxe * nye, na)); A[:, 0] = r.uniform(0.2, 0.98, nxe * nye)
+    H = r.uniform(-1.0, 1.0, (nxe * nye, na)); H[:, 0] = r.uniform(0.05, 2.0, nxe * nye)
+    return np.ascontiguousarray(A), np.ascontiguousarray(H)
+
+
+@pytest.mark.parametrize("p,ns,na,bc,distorted", [(2, 6, 6, 0, False), (2, 6, 6, 1, False), (2, 6, 3, 0, False),
+                                                  (1, 3, 3, 1, False), (2, 6, 6, 0, True)])
+def test_limited_advection(nx, ora, p, ns, na, bc, distorted):
+    """NEXT-4 (R#25): nxsdg_advect with NXSDG_OPT_LIMITER = 1 (Zhang-Shu limiter after every SSP-RK
+    stage) vs the oracle's ora_advect_limited, on data that triggers the limiter (1e-12)."""
+    nxe, nye, lx, ly = 45, 38, 45e3, 38e3
+    st = case(nxe, nye, p, ns, na, "random", lx, ly)
+    st["A"], st["H"] = _steep_tracers(nxe, nye, na)
+    if bc == 1:
+        for k in ("vx", "vy"):
+            st[k] = np.random.default_rng(3).uniform(-0.1, 0.1, st[k].shape)
+            st[k][-1, :] = st[k][0, :]; st[k][:, -1] = st[k][:, 0]
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.25) if distorted else None
+    dt = 600.0
+    with nx.Mesh(nxe, nye, lx, ly, p, ns, na, bc=bc) as m:
+        if V is not None:
+            m.set_vertices(V)
+        m.set_option(nx.OPT_LIMITER, 1)
+        m.load(st)
+        m.advect(dt)
+        got = m.state(("A", "H"))
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=p, ns=ns, na=na, bc=bc, verts=V)
+    A, H = ora.advect_limited(om, dt, st["vx"], st["vy"], st["A"], st["H"], 1)
+    Au, _ = ora.advect(om, dt, st["vx"], st["vy"], st["A"], st["H"])
+    assert np.abs(Au - A).max() > 1e-3          # the limiter really acted
+    _check(got, {"A": A, "H": H}, st, 1e-12, groups=("A", "H"))
+
+
+def test_limiter_p2p_strips_bitwise(nx):
+    """The limiter is element-local and runs before each stage's halo exchange: 3 P2P ranks in this
+    process give bitwise the single-context result."""
+    nxe, nye, lx, ly = 40, 37, 40e3, 37e3
+    st = case(nxe, nye, 2, 6, 6, "random", lx, ly)
+    st["A"], st["H"] = _steep_tracers(nxe, nye, 6)
+    prm = nx.PhysParams()
+    with nx.Mesh(nxe, nye, lx, ly) as m:
+        m.set_option(nx.OPT_LIMITER, 1)
+        m.load(st); m.advect(prm.dt); m.mevp_substeps(3, begin_step=True)
+        ref = m.state()
+    ms = [nx.Mesh(nxe, nye, lx, ly, rank=r, nranks=3, transport=nx.TRANSPORT_P2P) for r in range(3)]
+    nx.p2p_connect_local(ms)
+    for m in ms:
+        m.set_option(nx.OPT_LIMITER, 1)
+        er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
+        loc = {k: st[k][nr0:nr0 + nrn].copy() for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
+        for k in ("S11", "S12", "S22", "A", "H"):
+            loc[k] = st[k][er0 * nxe:(er0 + ern) * nxe].copy()
+        m.load(loc)
+    for m in ms:
+        m.advect(prm.dt)
+    for m in ms:
+        m.mevp_substeps(3, begin_step=True)
+    for m in ms:
+        m.synchronize()
+    got = {k: np.concatenate([m.read_state(k) for m in ms]) for k in ref}
+    for m in ms:
+        m.destroy()
+    for k in ref:
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+
+
 @pytest.mark.parametrize("bc", [0, 1])
 def test_advection_kernels_agree(nx, bc):
     """Structured CG2/DG2 advection kernel vs the table-driven one (tables from K0)."""
