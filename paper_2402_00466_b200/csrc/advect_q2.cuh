@@ -10,6 +10,7 @@
 // so both sides of every edge use bitwise-identical fluxes.
 #pragma once
 #include "kernels.cuh"
+#include "subcycle_tma.cuh"   // eval_gp: DG2 values at the 3 x 3 Gauss points
 
 namespace nxk {
 
@@ -195,11 +196,36 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_q2(AdvArgs a) {
         L[4] += a.ihy * m0 * (1.0 / 6.0); L[5] -= a.ihy * 0.5 * m1;
         double* out = tr == 0 ? a.Aout : a.Hout;
         const double* c0 = tr == 0 ? c0A : c0H;
+        double nc[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
             const double v = a.a1 * fma(a.dt, L[k] * mr[k], c[k]);
-            out[k * a.eplane + eo] = (a.a0 != 0.0) ? fma(a.a0, c0[k], v) : v;
+            nc[k] = (a.a0 != 0.0) ? fma(a.a0, c0[k], v) : v;
         }
+        if (a.limit) {   // R#25 fused: extremes over the 9 volume and 12 edge Gauss points, scale about the mean
+            double gv[9], ev[4][3];
+            eval_gp<true, true>(nc, gv);
+            trace_s(nc, 1.0, ev[0]); trace_s(nc, -1.0, ev[1]); trace_t(nc, 1.0, ev[2]); trace_t(nc, -1.0, ev[3]);
+            double cmin = gv[0], cmax = gv[0];
+#pragma unroll
+            for (int g = 1; g < 9; ++g) { cmin = fmin(cmin, gv[g]); cmax = fmax(cmax, gv[g]); }
+#pragma unroll
+            for (int ed = 0; ed < 4; ++ed)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) { cmin = fmin(cmin, ev[ed][q]); cmax = fmax(cmax, ev[ed][q]); }
+            const double cbar = nc[0], lo = 0.0, hi = tr == 0 ? 1.0 : INFINITY;
+            double theta = 1.0;
+            if (cmin < lo) theta = fmin(theta, (cbar - lo) / (cbar - cmin));
+            if (cmax > hi) theta = fmin(theta, (hi - cbar) / (cmax - cbar));
+            theta = fmax(0.0, fmin(1.0, theta));
+            if (theta < 1.0) {
+                nc[0] = fma(1.0 - theta, cbar, theta * nc[0]);
+#pragma unroll
+                for (int k = 1; k < 6; ++k) nc[k] *= theta;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) out[k * a.eplane + eo] = nc[k];
     }
 }
 

@@ -509,6 +509,7 @@ struct AdvArgs {
     int has_south, has_north;                 // ghost rows exist below/above (multi-rank)
     int periodic, erows_local;
     double ihx, ihy, dt, a0, a1;
+    int limit;                                // k_advect_q2: fused R#25 limiter on the stage output
 };
 
 template <int NA> struct Cf { double A[NA], H[NA]; };

@@ -1724,6 +1724,9 @@ extern "C" nxsdg_status nxsdg_run_step(nxsdg_ctx* c, nxsdg_step st) {
 }
 
 // ---------------------------------------------------------------- advection
+// the structured CG2/DG2 advection kernel applies the R#25 limiter in its epilogue
+static bool adv_fused_limit(const nxsdg_ctx* c) { return c->limiter && !c->general && c->P == 2 && c->NA == 6 && c->variant == 0; }
+
 template <int P, int NA>
 static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const double* Hin, double* Aout,
                                         double* Hout, double dt, double a0, double a1) {
@@ -1736,6 +1739,7 @@ static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const d
     a.periodic = c->d.bc == NXSDG_BC_PERIODIC; a.erows_local = c->erows_local;
     a.ihx = 1.0 / (c->d.lx / c->d.nx); a.ihy = 1.0 / (c->d.ly / c->d.ny);
     a.dt = dt; a.a0 = a0; a.a1 = a1;
+    a.limit = adv_fused_limit(c);
     dim3 b(32, ADV_ROWS), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + ADV_ROWS - 1) / ADV_ROWS));
     if (c->general) {
         GenAdvArgs ga{a, c->verts, c->d.ny};
@@ -1786,7 +1790,7 @@ static nxsdg_status advect_stage(nxsdg_ctx* c, double dt, int stage) {
     else if (c->NA == 1) s = advect_t<2, 1>(c, dt, stage);
     else if (c->NA == 3) s = advect_t<2, 3>(c, dt, stage);
     else s = advect_t<2, 6>(c, dt, stage);
-    if (s || !c->limiter || c->NA == 1) return s;
+    if (s || !c->limiter || c->NA == 1 || adv_fused_limit(c)) return s;
     // NEXT-4 (R#25): bound-preserving limiter on the stage output, before its halo exchange
     const int ob = stage_out_buf(c, stage);
     if (c->P == 1) return limit_t<1, 3>(c, c->Asc[ob], c->Hsc[ob]);

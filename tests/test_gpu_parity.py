@@ -166,11 +166,13 @@ def _steep_tracers(nxe, nye, na, seed=5):
     return np.ascontiguousarray(A), np.ascontiguousarray(H)
 
 
-@pytest.mark.parametrize("p,ns,na,bc,distorted", [(2, 6, 6, 0, False), (2, 6, 6, 1, False), (2, 6, 3, 0, False),
-                                                  (1, 3, 3, 1, False), (2, 6, 6, 0, True)])
-def test_limited_advection(nx, ora, p, ns, na, bc, distorted):
+@pytest.mark.parametrize("p,ns,na,bc,distorted,variant", [(2, 6, 6, 0, False, 0), (2, 6, 6, 1, False, 0),
+                                                          (2, 6, 6, 0, False, 1), (2, 6, 3, 0, False, 0),
+                                                          (1, 3, 3, 1, False, 0), (2, 6, 6, 0, True, 0)])
+def test_limited_advection(nx, ora, p, ns, na, bc, distorted, variant):
     """NEXT-4 (R#25): nxsdg_advect with NXSDG_OPT_LIMITER = 1 (Zhang-Shu limiter after every SSP-RK
-    stage) vs the oracle's ora_advect_limited, on data that triggers the limiter (1e-12)."""
+    stage) vs the oracle's ora_advect_limited, on data that triggers the limiter (1e-12).  CG2/DG2 box
+    with variant 0: the limiter fused into k_advect_q2's epilogue; otherwise the k_limit pass."""
     nxe, nye, lx, ly = 45, 38, 45e3, 38e3
     st = case(nxe, nye, p, ns, na, "random", lx, ly)
     st["A"], st["H"] = _steep_tracers(nxe, nye, na)
@@ -184,6 +186,7 @@ def test_limited_advection(nx, ora, p, ns, na, bc, distorted):
         if V is not None:
             m.set_vertices(V)
         m.set_option(nx.OPT_LIMITER, 1)
+        m.set_option(nx.OPT_FUSED_KERNEL, variant)
         m.load(st)
         m.advect(dt)
         got = m.state(("A", "H"))
