@@ -233,8 +233,28 @@ def main():
     prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
     st = gen_rank_state(cfg, rank, world)
     m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, device=local, **kw)
+    transport_note = args.transport if world > 1 else None
     if world > 1 and args.transport == "p2p":
-        nxsdg.p2p_connect_group(m, rank, world, dist.all_gather_object)
+        err = ""
+        try:
+            nxsdg.p2p_connect_group(m, rank, world, dist.all_gather_object)
+            if os.environ.get("NXSDG_TEST_P2P_FAIL") and rank == world - 1:   # test knob: exercise the fallback
+                err = "forced by NXSDG_TEST_P2P_FAIL"
+        except nxsdg.NxsdgError as ex:      # no CUDA IPC / peer access on this node
+            err = str(ex)
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not ok.item():                   # every rank falls back together: NCCL transport
+            errs = [None] * world
+            dist.all_gather_object(errs, err)
+            m.destroy()
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(nxsdg.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, device=local, rank=rank,
+                           nranks=world, transport=nxsdg.TRANSPORT_NCCL, nccl_id=bytes(idt.cpu().numpy().tobytes()))
+            transport_note = "nccl (p2p unavailable: " + next(e for e in errs if e)[:160] + ")"
     if args.fp32_storage or args.fp32_stress:
         m.set_option(nxsdg.OPT_PRECISION, 2 if args.fp32_stress else 1)
     if args.limiter:
@@ -355,7 +375,7 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} CG{cfg.p}/DG{cfg.p} (n_S={cfg.ns}, n_A={cfg.na}) warm box + "
                                    f"cyclone forcing; step = advect + prep + {cfg.nsub} fused mEVP subcycles",
                        "nx": cfg.nx, "ny": cfg.ny, "n_sub": cfg.nsub, "elements": n_el, "alpha": cfg.alpha, "beta": cfg.alpha,
-                       "parallelism": f"row strips x{world} ({args.transport} halo)" if world > 1 else "1 GPU",
+                       "parallelism": f"row strips x{world} ({transport_note} halo)" if world > 1 else "1 GPU",
                        "forcing": "moving cyclone regenerated on the GPU every step" if args.moving else "static (t = 0)",
                        "limiter": bool(args.limiter),
                        "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},

@@ -56,3 +56,15 @@ def test_bench_torchrun_two_ranks(transport):
     assert r.returncode == 0 and len(lines) == 1, r.stdout[-2000:] + r.stderr[-3000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
+
+
+def test_bench_p2p_falls_back_to_nccl():
+    """If any rank cannot map its neighbours (no CUDA IPC / peer access), all ranks agree and bench.py
+    runs over NCCL instead, saying so in the JSON line."""
+    r = _torchrun(2, ["bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "C2",
+                      "--e2e-steps", "1", "--no-cpu-baseline"], {"NXSDG_TEST_P2P_FAIL": "1"})
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and len(lines) == 1, r.stdout[-2000:] + r.stderr[-3000:]
+    d = json.loads(lines[0])
+    assert "nccl (p2p unavailable" in d["config"]["parallelism"] and d["value"] > 0, d["config"]
+
