@@ -1,0 +1,64 @@
+"""Fused-kernel options on C4 under SUSTAINED load (the bench's regime: 100-subcycle graphs back to
+back until the power cap has settled), unlike scripts/tune.py's short bursts.  Prints ms per
+subcycle and the median SM clock seen while timing (pynvml)."""
+import sys, os, json, threading, time, statistics
+sys.path.insert(0, os.getcwd())
+import torch
+from paper_2402_00466_b200 import inputs, nxsdg
+
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _h = pynvml.nvmlDeviceGetHandleByIndex(0)
+except Exception:                                  # clocks are context only
+    _h = None
+
+
+def sample_clocks(stop, out):
+    while not stop.is_set():
+        if _h is not None:
+            out.append(pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM))
+        time.sleep(0.02)
+
+
+cfg = inputs.CONFIGS[os.environ.get("CFG", "C4")]
+st = inputs.make_config_case(cfg)
+prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
+m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, int(os.environ.get("NS", "6")), 6, params=prm)
+m.load(st)
+prec = int(os.environ.get("PREC", "0"))
+if prec:
+    m.set_option(nxsdg.OPT_PRECISION, prec)
+bpe = m.bytes_per_element_subcycle
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6545.6
+s = torch.cuda.ExternalStream(m.stream)
+n = 100
+CT = [int(x) for x in os.environ.get("CTAS", "2,3").split(",")]
+STG = [int(x) for x in os.environ.get("STAGES", "2,3").split(",")]
+DY = [int(x) for x in os.environ.get("DYN", "1").split(",")]
+for dyn in DY:
+    for stg in STG:
+        for c in CT:
+            m.set_option(nxsdg.OPT_DYNAMIC, dyn)
+            m.set_option(nxsdg.OPT_CTAS_PER_SM, c)
+            try:
+                m.set_option(nxsdg.OPT_STAGES, stg)
+            except Exception as e:
+                print("skip", stg, e); continue
+            m.mevp_substeps(0, begin_step=True)
+            for _ in range(8):                      # ~1.6 s: let the power cap settle
+                m.mevp_substeps(n, begin_step=False)
+            torch.cuda.synchronize()
+            clk, stop = [], threading.Event()
+            th = threading.Thread(target=sample_clocks, args=(stop, clk)); th.start()
+            t = []
+            for rep in range(4):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s); m.mevp_substeps(n, begin_step=False); e1.record(s); torch.cuda.synchronize()
+                t.append(e0.elapsed_time(e1) / n)
+            stop.set(); th.join()
+            ms = statistics.median(t)
+            gbs = bpe * cfg.nx * cfg.ny / (ms * 1e-3) / 1e9
+            print(json.dumps({"prec": prec, "ctas": c, "stages": stg, "dyn": dyn, "ms_median": ms, "ms_min": min(t),
+                              "alg_GBs": gbs, "frac": gbs / peak,
+                              "sm_mhz": statistics.median(clk) if clk else None}), flush=True)
