@@ -114,6 +114,7 @@ struct nxsdg_ctx {
     int variant = 0;   // fused kernel: 0 = TMA-staged structured (p = 2), 1 = table-driven k_subcycle<P>
     int ctas_per_sm = -1;  // -1 = tuned default on C4: 2 (FP64 S, P_g), 4 (FP32 storage)
     int stages = 2;        // TMA pipeline depth 2..4
+    int const_regs = -1;   // node constants: 0 = fifth TMA box of the stage, 1 = register prefetch, -1 = default
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
@@ -433,7 +434,11 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             c->p2p_fused = (int)value; break;
         case NXSDG_OPT_STAGES:
             if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
+            if (value > 3 && c->precision >= 1) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..3 with FP32 storage");
             c->stages = (int)value; break;
+        case NXSDG_OPT_CONST_STAGING:
+            if (value < -1 || value > 1) return fail(c, NXSDG_ERR_INVALID_ARG, "node-constant staging -1|0|1");
+            c->const_regs = (int)value; break;
         default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
     }
     drop_graphs(c);
@@ -1363,6 +1368,11 @@ static nxsdg_status cvt(nxsdg_ctx* c, const float* src, double* dst, int64_t n) 
 }
 
 static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0 && (!c->general || c->NS == 6); }
+// Defaults of the box kernel, tuned on C4 under sustained load (scripts/tune_sustained.py)
+// FP64 storage: node constants in registers, 4 CTAs/SM (C4: 1.97 ms vs 2.02-2.11 ms per subcycle with the
+// fifth TMA box at 3 or 2 CTAs/SM); FP32 storage keeps the box (its stages are small already: 1.50 vs 1.59 ms)
+static bool const_in_regs(const nxsdg_ctx* c) { return c->const_regs < 0 ? c->precision == 0 : c->const_regs == 1; }
+static int default_ctas(size_t sf_bytes, bool cl) { return cl ? 4 : (sf_bytes == 8 ? 3 : 4); }
 
 // NEXT-1: the fused general-quad subcycle stages the vertex rows and the lumped node masses too
 static nxsdg_status build_gen_maps(nxsdg_ctx* c) {
@@ -1406,26 +1416,54 @@ static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     return NXSDG_OK;
 }
 
-template <bool R, int ST, typename SF, typename CT = double, int NS = 6>
+template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
-    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2Stage<SF, NS>) + sizeof(uint64_t) + sizeof(int4));
+    using Stage = typename K2StageSel<SF, NS, CL>::T;
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + sizeof(uint64_t) + sizeof(int4));
     static bool attr = false;
     if (!attr) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
         attr = true;
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS>, 32 * K2_WARPS, smem));
-    const int cap = c->ctas_per_sm < 0 ? (sizeof(SF) == 8 ? 2 : 4) : c->ctas_per_sm;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL>, 32 * K2_WARPS, smem));
+    const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF, CT, NS><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
+    k_subcycle_tma<R, ST, SF, CT, NS, CL><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
     return NXSDG_OK;
+}
+// stages x replacement pressure x node-constant staging (TMA box | registers)
+template <typename SF, typename CT = double, int NS = 6>
+static nxsdg_status launch_tma_sel(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
+    const bool cl = const_in_regs(c);
+    const int key = (c->stages * 2 + (a.repl ? 1 : 0)) * 2 + (cl ? 1 : 0);
+    switch (key) {
+        case 8: return launch_tma_t<false, 2, SF, CT, NS, false>(c, cv, cs, a);
+        case 9: return launch_tma_t<false, 2, SF, CT, NS, true>(c, cv, cs, a);
+        case 10: return launch_tma_t<true, 2, SF, CT, NS, false>(c, cv, cs, a);
+        case 11: return launch_tma_t<true, 2, SF, CT, NS, true>(c, cv, cs, a);
+        case 12: return launch_tma_t<false, 3, SF, CT, NS, false>(c, cv, cs, a);
+        case 13: return launch_tma_t<false, 3, SF, CT, NS, true>(c, cv, cs, a);
+        case 14: return launch_tma_t<true, 3, SF, CT, NS, false>(c, cv, cs, a);
+        case 15: return launch_tma_t<true, 3, SF, CT, NS, true>(c, cv, cs, a);
+        default: break;
+    }
+    if constexpr (sizeof(SF) == 8) {   // 4 stages: FP64 storage only
+        switch (key) {
+            case 16: return launch_tma_t<false, 4, SF, CT, NS, false>(c, cv, cs, a);
+            case 17: return launch_tma_t<false, 4, SF, CT, NS, true>(c, cv, cs, a);
+            case 18: return launch_tma_t<true, 4, SF, CT, NS, false>(c, cv, cs, a);
+            default: return launch_tma_t<true, 4, SF, CT, NS, true>(c, cv, cs, a);
+        }
+    }
+    return fail(c, NXSDG_ERR_INVALID_ARG, "stages %d with FP32 storage", c->stages);
 }
 
 static nxsdg_status ensure_counters(nxsdg_ctx* c, int n) {
@@ -1462,41 +1500,15 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int 
     if (c->precision == 2) {
         if ((st = build_maps32(c))) return st;
         a.S_out = reinterpret_cast<double*>(c->S32[cs ^ 1]);   // FP32 storage, FP32 stress arithmetic
-        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
-            case 4: return launch_tma_t<false, 2, float, float>(c, cv, cs, a);
-            case 5: return launch_tma_t<true, 2, float, float>(c, cv, cs, a);
-            case 6: return launch_tma_t<false, 3, float, float>(c, cv, cs, a);
-            default: return launch_tma_t<true, 3, float, float>(c, cv, cs, a);
-        }
+        return launch_tma_sel<float, float>(c, cv, cs, a);
     }
     if (c->precision == 1) {
         if ((st = build_maps32(c))) return st;
         a.S_out = reinterpret_cast<double*>(c->S32[cs ^ 1]);   // the kernel stores FP32
-        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
-            case 4: return launch_tma_t<false, 2, float>(c, cv, cs, a);
-            case 5: return launch_tma_t<true, 2, float>(c, cv, cs, a);
-            case 6: return launch_tma_t<false, 3, float>(c, cv, cs, a);
-            default: return launch_tma_t<true, 3, float>(c, cv, cs, a);
-        }
+        return launch_tma_sel<float>(c, cv, cs, a);
     }
-    if (c->NS == 8) {
-        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
-            case 4: return launch_tma_t<false, 2, double, double, 8>(c, cv, cs, a);
-            case 5: return launch_tma_t<true, 2, double, double, 8>(c, cv, cs, a);
-            case 6: return launch_tma_t<false, 3, double, double, 8>(c, cv, cs, a);
-            case 7: return launch_tma_t<true, 3, double, double, 8>(c, cv, cs, a);
-            case 8: return launch_tma_t<false, 4, double, double, 8>(c, cv, cs, a);
-            default: return launch_tma_t<true, 4, double, double, 8>(c, cv, cs, a);
-        }
-    }
-    switch (c->stages * 2 + (a.repl ? 1 : 0)) {
-        case 4: return launch_tma_t<false, 2, double>(c, cv, cs, a);
-        case 5: return launch_tma_t<true, 2, double>(c, cv, cs, a);
-        case 6: return launch_tma_t<false, 3, double>(c, cv, cs, a);
-        case 7: return launch_tma_t<true, 3, double>(c, cv, cs, a);
-        case 8: return launch_tma_t<false, 4, double>(c, cv, cs, a);
-        default: return launch_tma_t<true, 4, double>(c, cv, cs, a);
-    }
+    if (c->NS == 8) return launch_tma_sel<double, double, 8>(c, cv, cs, a);
+    return launch_tma_sel<double>(c, cv, cs, a);
 }
 
 // One fused subcycle launch over the selected chunks (no ping-pong flip).

@@ -41,20 +41,35 @@ template <typename SF> struct K2Cols { static constexpr int E = sizeof(SF) == 8 
 __host__ __device__ constexpr int round128(int b) { return (b + 127) / 128 * 128; }
 
 // One job's shared-memory stage; every TMA destination starts on a 128-B boundary.
+// CL = false: the six node constants are a fifth TMA box of the stage.  CL = true: they are not
+// staged; each lane loads its own 24 doubles straight into registers (coalesced 16-B loads issued
+// before the job's stage is waited for, consumed by the velocity update at its end), which takes
+// 35 % off the stage and lets 4 CTAs (8 warps) share an SM instead of 2.
 template <typename SF, int NS = 6>
-struct __align__(128) K2Stage {
+struct __align__(128) K2StageNC {
     static constexpr int EC = K2Cols<SF>::E;
     alignas(128) SF S[3 * NS][EC];             // planes S11[0..NS), S12[0..NS), S22[0..NS)
     alignas(128) SF Pg[9][EC];
     alignas(128) double vx[3][K2_VCOLS];       // 1584 B
     alignas(128) double vy[3][K2_VCOLS];
+};
+template <typename SF, int NS = 6>
+struct __align__(128) K2Stage : K2StageNC<SF, NS> {
     alignas(128) double C[6][2][K2_CCOLS];     // 5952 B  c1, rx0, ry0, cafo, ox, oy
 };
 static_assert(sizeof(K2Stage<double>) == 16896, "stage layout");
 static_assert(sizeof(K2Stage<double, 8>) == 18432, "stage layout (n_S = 8)");
-template <typename SF, int NS = 6>
+static_assert(sizeof(K2StageNC<double>) == 10880, "stage layout (constants in registers)");
+template <typename SF, int NS, bool CL> struct K2StageSel { using T = K2Stage<SF, NS>; };
+template <typename SF, int NS> struct K2StageSel<SF, NS, true> { using T = K2StageNC<SF, NS>; };
+template <typename SF, int NS = 6, bool CL = false>
 __host__ __device__ constexpr uint32_t k2_tx_bytes() {
-    return (3 * NS + 9) * K2Cols<SF>::E * sizeof(SF) + 2 * 3 * K2_VCOLS * 8 + 6 * 2 * K2_CCOLS * 8;
+    return (3 * NS + 9) * K2Cols<SF>::E * sizeof(SF) + 2 * 3 * K2_VCOLS * 8 + (CL ? 0 : 6 * 2 * K2_CCOLS * 8);
+}
+__device__ __forceinline__ double2 ldg_stream2(const double* p) {   // read once: keep it out of L1
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
 }
 
 struct K2Maps {
@@ -161,6 +176,16 @@ __device__ __forceinline__ void strain_t(const double V[3][3], T (&E)[NS]) {
         E[7] = T(0);
     }
 }
+// E = a Es + b Et over the coefficients, skipping the structural zeros of the d/ds strain (k = 3,
+// and 6 for n_S = 8) and of the d/dt strain (k = 4, and 7)
+template <typename T, int NS>
+__device__ __forceinline__ void combine(const T (&Es)[NS], const T (&Et)[NS], T ca, T cb, T (&E)[NS]) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const bool zs = k == 3 || (NS == 8 && k == 6), zt = k == 4 || (NS == 8 && k == 7);
+        E[k] = zs ? cb * Et[k] : (zt ? ca * Es[k] : fma(ca, Es[k], cb * Et[k]));
+    }
+}
 // values at the 9 Gauss points (g = gy*3 + gx) of sum_k E_k psi_k; HAS3/HAS4 drop known zeros.
 // e(S, T) = A(T) + S B(T) + q(S) Q(T): A = E0 + E2 T + E4 q(T), B = E1 + E5 T (+ E7 q(T)),
 // Q = E3 (+ E6 T) -- the bracketed terms are the n_S = 8 functions (R#24).
@@ -191,7 +216,7 @@ __device__ __forceinline__ void eval_gp(const T (&E)[NS], T e[9]) {
 // S_k <- fac S_k + sc * (R G)_k  (R = M_ref^{-1} psi_k(g) w_g) by 1D moments;
 // n_S = 8: p6 = 2160 sum w q(S) T G, p7 = 2160 sum w S q(T) G, both (100 a / 9) x second moments
 template <typename T, int NS>
-__device__ __forceinline__ void project(const T G[9], double sc, T fac, T (&S)[NS]) {
+__device__ __forceinline__ void proj_coeffs(const T G[9], double sc, T (&p)[NS]) {
     T X0[3], X1[3], X2[3];
 #pragma unroll
     for (int gy = 0; gy < 3; ++gy) {
@@ -200,59 +225,78 @@ __device__ __forceinline__ void project(const T G[9], double sc, T fac, T (&S)[N
         X1[gy] = d;
         X2[gy] = fma(T(-2), m, s);
     }
-    const T p0 = fma(T(5), X0[0] + X0[2], T(8) * X0[1]) * T(sc / 324.0);
-    const T p1 = fma(T(5), X1[0] + X1[2], T(8) * X1[1]) * T(sc * kC / 18.0);
-    const T p2 = (X0[2] - X0[0]) * T(sc * kC / 18.0);
-    const T p3 = fma(T(5), X2[0] + X2[2], T(8) * X2[1]) * T(sc * 10.0 / 54.0);
-    const T p4 = fma(T(-2), X0[1], X0[0] + X0[2]) * T(sc * 10.0 / 54.0);
-    const T p5 = (X1[2] - X1[0]) * T(sc * kC * kC);
-    S[0] = fma(fac, S[0], p0); S[1] = fma(fac, S[1], p1); S[2] = fma(fac, S[2], p2);
-    S[3] = fma(fac, S[3], p3); S[4] = fma(fac, S[4], p4); S[5] = fma(fac, S[5], p5);
+    p[0] = fma(T(5), X0[0] + X0[2], T(8) * X0[1]) * T(sc / 324.0);
+    p[1] = fma(T(5), X1[0] + X1[2], T(8) * X1[1]) * T(sc * kC / 18.0);
+    p[2] = (X0[2] - X0[0]) * T(sc * kC / 18.0);
+    p[3] = fma(T(5), X2[0] + X2[2], T(8) * X2[1]) * T(sc * 10.0 / 54.0);
+    p[4] = fma(T(-2), X0[1], X0[0] + X0[2]) * T(sc * 10.0 / 54.0);
+    p[5] = (X1[2] - X1[0]) * T(sc * kC * kC);
     if constexpr (NS == 8) {
-        const T p6 = (X2[2] - X2[0]) * T(sc * 100.0 * kA / 9.0);
-        const T p7 = fma(T(-2), X1[1], X1[0] + X1[2]) * T(sc * 100.0 * kA / 9.0);
-        S[6] = fma(fac, S[6], p6); S[7] = fma(fac, S[7], p7);
+        p[6] = (X2[2] - X2[0]) * T(sc * 100.0 * kA / 9.0);
+        p[7] = fma(T(-2), X1[1], X1[0] + X1[2]) * T(sc * 100.0 * kA / 9.0);
     }
 }
-// r[jx][jy] += sum_k Ds[j][k] S_k * h  (d/ds part, uses k = 0,1,2,4,5 and 7)
+template <typename T, int NS>
+__device__ __forceinline__ void project(const T G[9], double sc, T fac, T (&S)[NS]) {
+    T p[NS];
+    proj_coeffs(G, sc, p);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) S[k] = fma(fac, S[k], p[k]);
+}
+// The pair (g11, g22) = (a + b, a - b) projected together: S11 <- fac S11 + R a + R b,
+// S22 <- fac S22 + R a - R b, with b's factor 1/2 in its scale (sb = 0.5)
+template <typename T, int NS>
+__device__ __forceinline__ void project_pair(const T Ga[9], const T Gb[9], T fac, T (&S11)[NS], T (&S22)[NS]) {
+    T pa[NS], pb[NS];
+    proj_coeffs(Ga, 1.0, pa);
+    proj_coeffs(Gb, 0.5, pb);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        S11[k] = fma(fac, S11[k], pa[k] + pb[k]);
+        S22[k] = fma(fac, S22[k], pa[k] - pb[k]);
+    }
+}
+// r[jx][jy] += f(jx) f(jy) sum_k Ds[j][k] S_k * h  (d/ds part, uses k = 0,1,2,4,5 and 7), where
+// f(0) = f(2) = 1, f(1) = 1/2 is the lumped-mass ratio of the node type (corner 1/9, edge 2/9,
+// centre 4/9 of |K|: 1/m = -9 f(jx) f(jy) with h = -9/hx), folded into the constants
 template <int NS>
 __device__ __forceinline__ void div_s(const double (&S)[NS], double h, double r[3][3]) {
     const double u = fma(S[4], h * (1.0 / 90.0), S[0] * (h / 6.0)), v = S[2] * (h / 12.0);
-    const double Z0[3] = {u - v, fma(S[0], h * (2.0 / 3.0), -S[4] * (h / 45.0)), u + v};
-    double p = S[1] * (h / 6.0), m = S[1] * (h * 2.0 / 3.0);
-    if constexpr (NS == 8) { p = fma(S[7], h * (1.0 / 90.0), p); m = fma(S[7], -h * (1.0 / 45.0), m); }
+    const double Z0[3] = {u - v, fma(S[0], h * (1.0 / 3.0), -S[4] * (h / 90.0)), u + v};
+    double p = S[1] * (h / 6.0), m = S[1] * (h * 1.0 / 3.0);
+    if constexpr (NS == 8) { p = fma(S[7], h * (1.0 / 90.0), p); m = fma(S[7], -h * (1.0 / 90.0), m); }
     const double w = S[5] * (h / 12.0);
     const double Z1[3] = {p - w, m, p + w};
 #pragma unroll
     for (int jy = 0; jy < 3; ++jy) {
         const double t = Z1[jy] * (1.0 / 3.0);
         r[0][jy] += t - Z0[jy];
-        r[1][jy] += Z1[jy] * (-2.0 / 3.0);
+        r[1][jy] += Z1[jy] * (-1.0 / 3.0);
         r[2][jy] += t + Z0[jy];
     }
 }
-// r[jx][jy] += sum_k Dt[j][k] S_k * h  (d/dt part, uses k = 0,1,2,3,5 and 6)
+// r[jx][jy] += f(jx) f(jy) sum_k Dt[j][k] S_k * h  (d/dt part, uses k = 0,1,2,3,5 and 6)
 template <int NS>
 __device__ __forceinline__ void div_t(const double (&S)[NS], double h, double r[3][3]) {
     const double u = fma(S[3], h * (1.0 / 90.0), S[0] * (h / 6.0)), v = S[1] * (h / 12.0);
-    const double W0[3] = {u - v, fma(S[0], h * (2.0 / 3.0), -S[3] * (h / 45.0)), u + v};
-    double p = S[2] * (h / 6.0), m = S[2] * (h * 2.0 / 3.0);
-    if constexpr (NS == 8) { p = fma(S[6], h * (1.0 / 90.0), p); m = fma(S[6], -h * (1.0 / 45.0), m); }
+    const double W0[3] = {u - v, fma(S[0], h * (1.0 / 3.0), -S[3] * (h / 90.0)), u + v};
+    double p = S[2] * (h / 6.0), m = S[2] * (h * 1.0 / 3.0);
+    if constexpr (NS == 8) { p = fma(S[6], h * (1.0 / 90.0), p); m = fma(S[6], -h * (1.0 / 90.0), m); }
     const double w = S[5] * (h / 12.0);
     const double W1[3] = {p - w, m, p + w};
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx) {
         const double t = W1[jx] * (1.0 / 3.0);
         r[jx][0] += t - W0[jx];
-        r[jx][1] += W1[jx] * (-2.0 / 3.0);
+        r[jx][1] += W1[jx] * (-1.0 / 3.0);
         r[jx][2] += t + W0[jx];
     }
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6>
+template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
-    using Stage = K2Stage<SF, NS>;
+    using Stage = typename K2StageSel<SF, NS, CL>::T;
     constexpr int AL = K2Cols<SF>::ALIGN;
     SF* const S_out = reinterpret_cast<SF*>(a.S_out);   // FP32 buffers in mixed-precision mode
     extern __shared__ __align__(1024) unsigned char k2_smem[];   // no static smem: base stays 1024-B aligned
@@ -300,16 +344,17 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     auto issue = [&](const Cur& c, int s) {
         Stage* t = stg + s;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS>());
+        mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, CL>());
         const int xs = (c.ix0 - 1) & ~(AL - 1);   // 16-B aligned start column (arithmetic: -1 -> -2 / -4)
         tma3(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0);
         tma3(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0);
         tma2(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
         tma2(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
-        tma3(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0);
+        if constexpr (!CL) tma3(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0);
     };
 
     const double ihx = a.ihx, ihy = a.ihy, fac = a.fac, hA = 0.5 * a.ainv;
+    const double mhx = -9.0 * ihx, mhy = -9.0 * ihy;   // -1 / (corner lumped mass / |K|) = -9
     const int64_t npitch = a.npitch, eplane = a.eplane;
     // prologue: jobs 0 .. STAGES-2 in flight; job j lives in stage j % STAGES
     Cur pre;
@@ -343,10 +388,25 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             cur.u = jd.x; cur.lr = jd.y; cur.lr1 = jd.z; cur.ring = jd.w & 1; cur.first = (jd.w & 2) != 0;
             cur.ix0 = (cur.u % a.nstrips) * 31;
         }
+        const int ix = cur.ix0 - 1 + lane, lr = cur.lr;
+        // CL: this lane's node constants [field][jy][q] (only lanes that update nodes; the boundary
+        // column ix = nx is forced to zero below, so it needs none)
+        double cr[6][2][2];
+        if constexpr (CL) {
+            const bool need = lane >= 1 && ix >= 0 && ix < a.nx && !cur.ring;
+            const double* const fld[6] = {a.c1, a.rx0, a.ry0, a.cafo, a.ox, a.oy};
+#pragma unroll
+            for (int f = 0; f < 6; ++f)
+#pragma unroll
+                for (int jy = 0; jy < 2; ++jy) {
+                    double2 v = make_double2(0.0, 0.0);
+                    if (need) v = ldg_stream2(fld[f] + (int64_t)(2 * lr + jy) * npitch + 2 * ix);
+                    cr[f][jy][0] = v.x; cr[f][jy][1] = v.y;
+                }
+        }
         mbar_wait(&bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
         const Stage& t = stg[s];
-        const int ix = cur.ix0 - 1 + lane, lr = cur.lr;
         const int eo = (cur.ix0 - 1) - ((cur.ix0 - 1) & ~(AL - 1));   // lane offset inside the S / P_g box
         if (cur.first) { carx[0] = carx[1] = cary[0] = cary[1] = 0.0; }
 
@@ -359,41 +419,41 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             Vx[jy][0] = a2.x; Vx[jy][1] = a2.y; Vx[jy][2] = t.vx[jy][2 * lane + 2];
             Vy[jy][0] = b2.x; Vy[jy][1] = b2.y; Vy[jy][2] = t.vy[jy][2 * lane + 2];
         }
-        // ---- strain (Table 1 "strain"): DG coefficients, then Gauss-point values
-        CT e11[9], e12[9], e22[9];
+        // ---- strain (Table 1 "strain"): DG coefficients, then Gauss-point values of
+        //      the trace u = e11 + e22, the half difference w = (e11 - e22)/2 and e12, in which
+        //      Hibler's Delta^2 = 1.25 (e11^2 + e22^2) + 1.5 e11 e22 + e12^2 is u^2 + w^2 + e12^2
+        CT eu[9], ew[9], e12[9];
         {
             CT Es[NS], Et[NS], E[NS];
             const CT cihx = (CT)ihx, cihy = (CT)ihy;
+            const CT hx2 = CT(0.5) * cihx, hy2 = CT(0.5) * cihy;
             strain_s(Vx, Es);
-#pragma unroll
-            for (int k = 0; k < NS; ++k) E[k] = cihx * Es[k];
-            eval_gp<false, true>(E, e11);
             strain_t(Vy, Et);
-#pragma unroll
-            for (int k = 0; k < NS; ++k) E[k] = cihy * Et[k];
-            eval_gp<true, false>(E, e22);
+            combine(Es, Et, cihx, cihy, E);
+            eval_gp<true, true>(E, eu);
+            combine(Es, Et, hx2, -hy2, E);
+            eval_gp<true, true>(E, ew);
             strain_t(Vx, Et);
             strain_s(Vy, Es);
-            const CT hx2 = CT(0.5) * cihx, hy2 = CT(0.5) * cihy;
-#pragma unroll
-            for (int k = 0; k < NS; ++k) E[k] = fma(hy2, Et[k], hx2 * Es[k]);
+            combine(Es, Et, hx2, hy2, E);
             eval_gp<true, true>(E, e12);
         }
-        // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in:
-        //      g11 = alpha^{-1} (P/Delta (5/8 e11 + 3/8 e22) - P/2) = ph (rD (1.25 e11 + 0.75 e22) - 1)
-        //      g12 = alpha^{-1} P/Delta e12/4 = (ph rD e12) / 2 (the 1/2 goes into the projection)
+        // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in: with
+        //      pr = alpha^{-1} P / (2 Delta) and sub = alpha^{-1} P / 2 (REPL: P_r / 2, R#4),
+        //      g11 = pr (1.25 e11 + 0.75 e22) - sub = a + b, g22 = a - b, a = pr u - sub, b = pr w / 2;
+        //      g12 = alpha^{-1} P/Delta e12/4 = (pr e12) / 2 (each 1/2 goes into the projection)
         const CT cdmin2 = (CT)a.dmin2, chA = (CT)hA;
 #pragma unroll
         for (int g = 0; g < 9; ++g) {
-            const CT x = e11[g], y = e22[g], z = e12[g];
-            const CT draw2 = fma(z, z, fma(CT(1.5) * x, y, CT(1.25) * fma(x, x, y * y)));
+            const CT u = eu[g], w = ew[g], z = e12[g];
+            const CT draw2 = fma(u, u, fma(w, w, z * z));
             const CT rD = rsqrt_t(draw2 + cdmin2);
             const CT ph = (CT)t.Pg[g][eo + lane] * chA;
             const CT pr = ph * rD;
             // replacement pressure (R#4): P_r/2 = (P/2) Draw/Delta, Draw = draw2 * rsqrt(draw2)
             const CT sub = REPL ? pr * (draw2 > CT(0) ? draw2 * rsqrt_t(draw2) : CT(0)) : ph;
-            e11[g] = fma(pr, fma(CT(1.25), x, CT(0.75) * y), -sub);
-            e22[g] = fma(pr, fma(CT(1.25), y, CT(0.75) * x), -sub);
+            eu[g] = fma(pr, u, -sub);
+            ew[g] = pr * w;
             e12[g] = pr * z;
         }
         CT C11[NS], C12[NS], C22[NS];
@@ -403,9 +463,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             C22[k] = (CT)t.S[2 * NS + k][eo + lane];
         }
         const CT cfac = (CT)fac;
-        project(e11, 1.0, cfac, C11);
+        project_pair(eu, ew, cfac, C11, C22);
         project(e12, 0.5, cfac, C12);
-        project(e22, 1.0, cfac, C22);
         double S11[NS], S12[NS], S22[NS];   // the divergence and velocity stay FP64
 #pragma unroll
         for (int k = 0; k < NS; ++k) { S11[k] = (double)C11[k]; S12[k] = (double)C12[k]; S22[k] = (double)C22[k]; }
@@ -434,8 +493,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j) { rX[i][j] = 0.0; rY[i][j] = 0.0; }
-        div_s(S11, ihx, rX); div_t(S12, ihy, rX);
-        div_s(S12, ihx, rY); div_t(S22, ihy, rY);
+        div_s(S11, mhx, rX); div_t(S12, mhy, rX);      // already divided by the lumped mass
+        div_s(S12, mhx, rY); div_t(S22, mhy, rY);
         // ---- per-node gather (row below, W, E) + velocity update (R#11), branch-free:
         //      all four owned nodes are updated, boundary nodes select 0, stores are predicated
         const bool nvalid = lane >= 1 && ix >= 0 && ix <= a.nx && !cur.ring;
@@ -454,7 +513,6 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             }
         }
         if (nvalid) {
-            const double invm[2][2] = {{-9.0, -4.5}, {-4.5, -2.25}};   // -1 / lumped-mass factor [jy][q]
             const bool brow0 = lr == a.erow_begin && a.bottom_boundary;
 #pragma unroll
             for (int jy = 0; jy < 2; ++jy) {
@@ -463,10 +521,16 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                 for (int q = 0; q < 2; ++q) {
                     const int I = 2 * ix + q;
                     const int cc = 2 * lane - 2 + q;
-                    const double fx = sumx[jy][q] * invm[jy][q], fy = sumy[jy][q] * invm[jy][q];
+                    const double fx = sumx[jy][q], fy = sumy[jy][q];   // F / m (mass folded into div_s/t)
                     const double vxo = Vx[jy][q], vyo = Vy[jy][q];
-                    const double c1 = t.C[0][jy][cc], r0x = t.C[1][jy][cc], r0y = t.C[2][jy][cc];
-                    const double cf = t.C[3][jy][cc], oxv = t.C[4][jy][cc], oyv = t.C[5][jy][cc];
+                    double c1, r0x, r0y, cf, oxv, oyv;
+                    if constexpr (CL) {
+                        c1 = cr[0][jy][q]; r0x = cr[1][jy][q]; r0y = cr[2][jy][q];
+                        cf = cr[3][jy][q]; oxv = cr[4][jy][q]; oyv = cr[5][jy][q];
+                    } else {
+                        c1 = t.C[0][jy][cc]; r0x = t.C[1][jy][cc]; r0y = t.C[2][jy][cc];
+                        cf = t.C[3][jy][cc]; oxv = t.C[4][jy][cc]; oyv = t.C[5][jy][cc];
+                    }
                     const double dx = oxv - vxo, dy = oyv - vyo;
                     const double w2 = fma(dx, dx, dy * dy);
                     const double w = w2 > 0.0 ? w2 * rsqrt_nr(w2) : 0.0;   // |o - v|

@@ -24,7 +24,7 @@ def sample_clocks(stop, out):
 cfg = inputs.CONFIGS[os.environ.get("CFG", "C4")]
 st = inputs.make_config_case(cfg)
 prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
-m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, int(os.environ.get("NS", "6")), 6, params=prm)
+m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, 6, 6, params=prm)
 m.load(st)
 prec = int(os.environ.get("PREC", "0"))
 if prec:
@@ -33,32 +33,29 @@ bpe = m.bytes_per_element_subcycle
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6545.6
 s = torch.cuda.ExternalStream(m.stream)
 n = 100
-CT = [int(x) for x in os.environ.get("CTAS", "2,3").split(",")]
-STG = [int(x) for x in os.environ.get("STAGES", "2,3").split(",")]
-DY = [int(x) for x in os.environ.get("DYN", "1").split(",")]
-for dyn in DY:
-    for stg in STG:
-        for c in CT:
-            m.set_option(nxsdg.OPT_DYNAMIC, dyn)
-            m.set_option(nxsdg.OPT_CTAS_PER_SM, c)
-            try:
-                m.set_option(nxsdg.OPT_STAGES, stg)
-            except Exception as e:
-                print("skip", stg, e); continue
-            m.mevp_substeps(0, begin_step=True)
-            for _ in range(8):                      # ~1.6 s: let the power cap settle
-                m.mevp_substeps(n, begin_step=False)
-            torch.cuda.synchronize()
-            clk, stop = [], threading.Event()
-            th = threading.Thread(target=sample_clocks, args=(stop, clk)); th.start()
-            t = []
-            for rep in range(4):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(s); m.mevp_substeps(n, begin_step=False); e1.record(s); torch.cuda.synchronize()
-                t.append(e0.elapsed_time(e1) / n)
-            stop.set(); th.join()
-            ms = statistics.median(t)
-            gbs = bpe * cfg.nx * cfg.ny / (ms * 1e-3) / 1e9
-            print(json.dumps({"prec": prec, "ctas": c, "stages": stg, "dyn": dyn, "ms_median": ms, "ms_min": min(t),
-                              "alg_GBs": gbs, "frac": gbs / peak,
-                              "sm_mhz": statistics.median(clk) if clk else None}), flush=True)
+# COMBOS = "cl:ctas:stages,..." (cl = NXSDG_OPT_CONST_STAGING), measured REPS times, interleaved
+COMBOS = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("COMBOS", "0:2:2,0:3:2,1:4:2,1:3:2").split(",")]
+REPS = int(os.environ.get("REPS", "2"))
+m.set_option(nxsdg.OPT_DYNAMIC, int(os.environ.get("DYN", "1")))
+for rep in range(REPS):
+    for cl, c, stg in COMBOS:
+        m.set_option(nxsdg.OPT_CONST_STAGING, cl)
+        m.set_option(nxsdg.OPT_CTAS_PER_SM, c)
+        m.set_option(nxsdg.OPT_STAGES, stg)
+        m.mevp_substeps(0, begin_step=True)
+        for _ in range(8):                      # ~1.6 s: let the power cap settle
+            m.mevp_substeps(n, begin_step=False)
+        torch.cuda.synchronize()
+        clk, stop = [], threading.Event()
+        th = threading.Thread(target=sample_clocks, args=(stop, clk)); th.start()
+        t = []
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s); m.mevp_substeps(n, begin_step=False); e1.record(s); torch.cuda.synchronize()
+            t.append(e0.elapsed_time(e1) / n)
+        stop.set(); th.join()
+        ms = statistics.median(t)
+        gbs = bpe * cfg.nx * cfg.ny / (ms * 1e-3) / 1e9
+        print(json.dumps({"prec": prec, "rep": rep, "const_regs": cl, "ctas": c, "stages": stg, "ms_median": ms,
+                          "ms_min": min(t), "alg_GBs": gbs, "frac": gbs / peak,
+                          "sm_mhz": statistics.median(clk) if clk else None}), flush=True)

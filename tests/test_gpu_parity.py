@@ -98,6 +98,30 @@ def test_fused_variants_and_tuning(nx, ora, variant, ty, ctas, stages):
     _check(got, ref, st, 1e-11)
 
 
+@pytest.mark.parametrize("ns,prec", [(6, 0), (8, 0), (6, 1), (6, 2)])
+@pytest.mark.parametrize("shape", [(70, 75), (1, 5), (6, 1), (93, 33)])
+@pytest.mark.parametrize("ctas,stages", [(4, 2), (3, 3), (1, 2)])
+def test_const_staging_bitwise(nx, ora, ns, prec, shape, ctas, stages):
+    """NXSDG_OPT_CONST_STAGING: the node constants prefetched into registers (1) instead of staged as
+    a fifth TMA box (0) change only where the same doubles come from, so the states agree BITWISE,
+    for every storage precision, n_S and grid size; the register variant is also checked against the
+    oracle (FP64 storage)."""
+    nxe, nye = shape
+    lx, ly = 2e3 * nxe, 2e3 * nye
+    st = case(nxe, nye, 2, ns, 6, "warm", lx, ly)
+    base = {nx.OPT_PRECISION: prec} if prec else {}
+    got = {}
+    for cl in (0, 1):
+        opts = dict(base)
+        opts.update({nx.OPT_CONST_STAGING: cl, nx.OPT_CTAS_PER_SM: ctas, nx.OPT_STAGES: stages})
+        got[cl] = _gpu_run(nx, st, nxe, nye, 2, ns, 6, 4, lx, ly, options=opts)
+    for k in got[0]:
+        assert np.array_equal(got[0][k], got[1][k]), k
+    if prec == 0:
+        ref = ora.subcycles(ora_mesh(nxe, nye, 2, ns, 6, lx, ly), ora_params(nx.PhysParams()), 4, st)
+        _check(got[1], ref, st, 1e-11)
+
+
 def test_fused_variants_agree(nx):
     """TMA structured kernel vs table-driven kernel (tables from the K0 kernel): same result
     to rounding after 3 subcycles."""
