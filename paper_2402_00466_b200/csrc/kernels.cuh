@@ -139,7 +139,32 @@ struct SubArgs {
     int up_elem_row;                // local element row whose S goes up (to the neighbour's row 0)
     int dn_node_row, dn_dst_row;    // local node row that goes down, and its row at the neighbour
     int64_t peer_up_eplane;         // the upper neighbour's element plane stride
+    int ntail, qtail;               // persistent kernels: the last ntail selected chunks are split into
+                                    // qtail sub-units each (0 / 1 = off)
+    int l2_hints;                   // box TMA kernel: L2 eviction-policy bits (subcycle_tma.cuh)
 };
+
+// Unit u of a persistent kernel's work list -> strip and element rows [lr0, lr1) (lr0 >= lr1: empty).
+// Whole chunks come first, strip-fastest; the last a.ntail selected chunks follow as a.qtail
+// sub-units each, so the final units handed out are short and the warps finish together
+// (tail split).  Every partition gives bitwise the same result (ring recomputation,
+// fixed-order node sums).
+__device__ __forceinline__ int units_total(const SubArgs& a) {
+    return a.nstrips * (a.nsel + a.ntail * (a.qtail - 1));
+}
+__device__ __forceinline__ void unit_rows(const SubArgs& a, int u, int& strip, int& lr0, int& lr1) {
+    const int nbulk = a.nstrips * (a.nsel - a.ntail);
+    int i, sub = 0, q = 1;
+    if (u < nbulk) {
+        strip = u % a.nstrips; i = u / a.nstrips;
+    } else {
+        const int v = u - nbulk, k = v / a.nstrips;
+        strip = v % a.nstrips; i = a.nsel - a.ntail + k / a.qtail; sub = k % a.qtail; q = a.qtail;
+    }
+    const int c0 = a.erow_begin + (a.chunk0 + i * a.chunk_step) * a.ty, c1 = min(c0 + a.ty, a.erow_end);
+    const int per = (a.ty + q - 1) / q;
+    lr0 = c0 + sub * per; lr1 = min(lr0 + per, c1);
+}
 
 template <int P, int NS_ = Deg<P>::NS>
 __global__ void __launch_bounds__(128) k_subcycle(SubArgs a) {

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -115,6 +116,7 @@ struct nxsdg_ctx {
     int ctas_per_sm = -1;  // -1 = tuned default on C4: 2 (FP64 S, P_g), 4 (FP32 storage)
     int stages = 2;        // TMA pipeline depth 2..4
     int const_regs = -1;   // node constants: 0 = fifth TMA box of the stage, 1 = register prefetch, -1 = default
+    int tail_split = 1;    // persistent kernels: split the last chunks into short sub-units (1) or not (0)
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
@@ -436,6 +438,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
             if (value > 3 && c->precision >= 1) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..3 with FP32 storage");
             c->stages = (int)value; break;
+        case NXSDG_OPT_TAIL_SPLIT:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "tail split 0|1");
+            c->tail_split = (int)value; break;
         case NXSDG_OPT_CONST_STAGING:
             if (value < -1 || value > 1) return fail(c, NXSDG_ERR_INVALID_ARG, "node-constant staging -1|0|1");
             c->const_regs = (int)value; break;
@@ -1285,13 +1290,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// L2 sector promotion of the TMA loads (tuning experiment hook: NXSDG_TMA_L2_PROMOTION = 0 none,
+// 1 64 B, 2 128 B, 3 256 B (default))
+static CUtensorMapL2promotion l2_promotion() {
+    const char* e = getenv("NXSDG_TMA_L2_PROMOTION");
+    const int v = e ? atoi(e) : 3;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 static bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
                    const cuuint32_t* box) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1368,6 +1382,21 @@ static nxsdg_status cvt(nxsdg_ctx* c, const float* src, double* dst, int64_t n) 
 }
 
 static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0 && (!c->general || c->NS == 6); }
+// Tail split of a persistent launch with twarps warps: the last chunks become ~8-row sub-units, enough of
+// them (2 x twarps) that every warp's final unit is short, so the warps finish within ~8 jobs of each
+// other instead of ~ty (the idle tail of a launch is half a unit on average)
+static SubArgs with_tail(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps) {
+    SubArgs a = a0;
+    a.ntail = 0; a.qtail = 1;
+    static const int hints = getenv("NXSDG_L2_HINTS") ? atoi(getenv("NXSDG_L2_HINTS")) : 0;   // experiment hook
+    a.l2_hints = hints;
+    const int q = a.ty / 8;
+    if (!c->tail_split || !a.work_counter || q < 2 || a.nsel < 2) return a;
+    const int64_t need = (2 * twarps + (int64_t)a.nstrips * q - 1) / ((int64_t)a.nstrips * q);
+    a.ntail = (int)std::min<int64_t>(a.nsel, need);
+    a.qtail = q;
+    return a;
+}
 // Defaults of the box kernel, tuned on C4 under sustained load (scripts/tune_sustained.py)
 // FP64 storage: node constants in registers, 4 CTAs/SM (C4: 1.97 ms vs 2.02-2.11 ms per subcycle with the
 // fifth TMA box at 3 or 2 CTAs/SM); FP32 storage keeps the box (its stages are small already: 1.50 vs 1.59 ms)
@@ -1412,7 +1441,8 @@ static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
-    k_subcycle_gen<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->gen_maps[cv][cs], a);
+    k_subcycle_gen<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->gen_maps[cv][cs],
+                                                                       with_tail(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
 
@@ -1436,7 +1466,8 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF, CT, NS, CL><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, a);
+    k_subcycle_tma<R, ST, SF, CT, NS, CL><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
+        mp, with_tail(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
 // stages x replacement pressure x node-constant staging (TMA box | registers)

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
     uint64_t* bar = reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * STAGES * sizeof(Stage)) + wib * STAGES;
     const int twarps = gridDim.x * K2_WARPS;
     const int gw = blockIdx.x * K2_WARPS + wib;
-    const int nunits = a.nstrips * a.nsel;
+    const int nunits = units_total(a);
     if (gw >= nunits) return;
     if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
@@ -74,12 +74,18 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
 
     struct Cur { int u, lr, lr1, ix0; bool ring, first, ok; };
     auto start_unit = [&](int u, Cur& c) {
-        c.ok = u < nunits;
-        if (!c.ok) return;
-        const int strip = u % a.nstrips, chunk = a.chunk0 + (u / a.nstrips) * a.chunk_step;
-        const int lr0 = a.erow_begin + chunk * a.ty;
-        c.u = u; c.lr1 = min(lr0 + a.ty, a.erow_end); c.ix0 = strip * 31;
-        c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
+        for (;;) {                        // skip empty sub-units (ragged last chunk)
+            c.ok = u < nunits;
+            if (!c.ok) return;
+            int strip, lr0, lr1;
+            unit_rows(a, u, strip, lr0, lr1);
+            if (lr0 < lr1) {
+                c.u = u; c.lr1 = lr1; c.ix0 = strip * 31;
+                c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
+                return;
+            }
+            u = a.work_counter ? twarps + atomicAdd(a.work_counter, 1) : u + twarps;
+        }
     };
     auto advance = [&](Cur& c) {
         ++c.lr; c.ring = false; c.first = false;

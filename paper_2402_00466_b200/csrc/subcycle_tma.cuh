@@ -96,6 +96,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         }
     }
 }
+// L2 eviction policies (createpolicy) for the cache-hinted TMA loads / global accesses below
+__device__ __forceinline__ uint64_t l2_policy(int kind) {   // 0 evict_normal, 1 evict_first, 2 evict_last
+    uint64_t p;
+    if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma3h(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;"
+        ::"r"(su32(dst)), "l"((uint64_t)m), "r"(x), "r"(y), "r"(z), "r"(su32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma2h(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(su32(dst)), "l"((uint64_t)m), "r"(x), "r"(y), "r"(su32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double2 ldg_stream2h(const double* p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint2(double* p, double x, double y, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(x), "d"(y), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
@@ -309,8 +342,12 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     }
     const int twarps = gridDim.x * K2_WARPS;
     const int gw = blockIdx.x * K2_WARPS + wib;
-    const int nunits = a.nstrips * a.nsel;
+    const int nunits = units_total(a);
     if (gw >= nunits) return;
+    // L2 policies (a.l2_hints bits: 1 streamed loads S, P_g, node constants evict_first; 2 stores
+    // evict_first; 4 v boxes evict_last)
+    const uint64_t pol_ld = l2_policy(a.l2_hints & 1 ? 1 : 0), pol_st = l2_policy(a.l2_hints & 2 ? 1 : 0);
+    const uint64_t pol_v = l2_policy(a.l2_hints & 4 ? 2 : 0);
     if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -323,12 +360,18 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     // cursor and records each job in the stage's descriptor slot; all lanes read it back.
     struct Cur { int u, lr, lr1, ix0; bool ring, first, ok; };
     auto start_unit = [&](int u, Cur& c) {
-        c.ok = u < nunits;
-        if (!c.ok) return;
-        const int strip = u % a.nstrips, chunk = a.chunk0 + (u / a.nstrips) * a.chunk_step;
-        const int lr0 = a.erow_begin + chunk * a.ty;
-        c.u = u; c.lr1 = min(lr0 + a.ty, a.erow_end); c.ix0 = strip * 31;
-        c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
+        for (;;) {                        // skip empty sub-units (ragged last chunk)
+            c.ok = u < nunits;
+            if (!c.ok) return;
+            int strip, lr0, lr1;
+            unit_rows(a, u, strip, lr0, lr1);
+            if (lr0 < lr1) {
+                c.u = u; c.lr1 = lr1; c.ix0 = strip * 31;
+                c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
+                return;
+            }
+            u = a.work_counter ? twarps + atomicAdd(a.work_counter, 1) : u + twarps;
+        }
     };
     auto advance = [&](Cur& c) {          // lane 0 only
         ++c.lr; c.ring = false; c.first = false;
@@ -346,11 +389,11 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, CL>());
         const int xs = (c.ix0 - 1) & ~(AL - 1);   // 16-B aligned start column (arithmetic: -1 -> -2 / -4)
-        tma3(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0);
-        tma3(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0);
-        tma2(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
-        tma2(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
-        if constexpr (!CL) tma3(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0);
+        tma3h(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0, pol_ld);
+        tma3h(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0, pol_ld);
+        tma2h(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
+        tma2h(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
+        if constexpr (!CL) tma3h(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0, pol_ld);
     };
 
     const double ihx = a.ihx, ihy = a.ihy, fac = a.fac, hA = 0.5 * a.ainv;
@@ -400,7 +443,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
 #pragma unroll
                 for (int jy = 0; jy < 2; ++jy) {
                     double2 v = make_double2(0.0, 0.0);
-                    if (need) v = ldg_stream2(fld[f] + (int64_t)(2 * lr + jy) * npitch + 2 * ix);
+                    if (need) v = ldg_stream2h(fld[f] + (int64_t)(2 * lr + jy) * npitch + 2 * ix, pol_ld);
                     cr[f][jy][0] = v.x; cr[f][jy][1] = v.y;
                 }
         }
@@ -473,9 +516,9 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             const int64_t e = (int64_t)lr * a.epitch + ix;
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
-                S_out[k * eplane + e] = (SF)S11[k];
-                S_out[(NS + k) * eplane + e] = (SF)S12[k];
-                S_out[(2 * NS + k) * eplane + e] = (SF)S22[k];
+                st_hint(S_out + k * eplane + e, (SF)S11[k], pol_st);
+                st_hint(S_out + (NS + k) * eplane + e, (SF)S12[k], pol_st);
+                st_hint(S_out + (2 * NS + k) * eplane + e, (SF)S22[k], pol_st);
             }
             if (a.peer_S_up != nullptr && lr == a.up_elem_row) {   // P2P: the neighbour's ghost element row 0
                 const int64_t pe = a.peer_up_eplane;
@@ -546,8 +589,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                 const int jr = 2 * lr + jy;
                 const int64_t n = (int64_t)jr * npitch + 2 * ix;
                 if (ix < a.nx) {
-                    *reinterpret_cast<double2*>(a.vx_out + n) = make_double2(nvx[0], nvx[1]);
-                    *reinterpret_cast<double2*>(a.vy_out + n) = make_double2(nvy[0], nvy[1]);
+                    st_hint2(a.vx_out + n, nvx[0], nvx[1], pol_st);
+                    st_hint2(a.vy_out + n, nvy[0], nvy[1], pol_st);
                 } else {                                  // ix == nx: only the boundary column 2 nx
                     a.vx_out[n] = 0.0;
                     a.vy_out[n] = 0.0;

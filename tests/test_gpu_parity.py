@@ -122,6 +122,33 @@ def test_const_staging_bitwise(nx, ora, ns, prec, shape, ctas, stages):
         _check(got[1], ref, st, 1e-11)
 
 
+@pytest.mark.parametrize("general", [False, True])
+@pytest.mark.parametrize("shape,ty,ctas", [((70, 75), 16, 1), ((93, 133), 32, 1), ((40, 301), 24, 2), ((5, 9), 16, 1)])
+def test_tail_split_bitwise(nx, ora, general, shape, ty, ctas):
+    """NXSDG_OPT_TAIL_SPLIT re-partitions a launch's last chunks into short sub-units (each with its
+    own ring row); node sums keep their fixed order, so the state is BITWISE that of the unsplit
+    launch, for the box kernel and the fused general-quad kernel; and it matches the oracle."""
+    nxe, nye = shape
+    lx, ly = 2e3 * nxe, 2e3 * nye
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.2) if general else None
+    got = {}
+    for split in (0, 1):
+        with nx.Mesh(nxe, nye, lx, ly, 2, 6, 6) as m:
+            if general:
+                m.set_vertices(V)
+            for k, v in {nx.OPT_TAIL_SPLIT: split, nx.OPT_CHUNK_ROWS: ty, nx.OPT_CTAS_PER_SM: ctas}.items():
+                m.set_option(k, v)
+            m.load(st)
+            m.mevp_substeps(3, begin_step=True)
+            got[split] = m.state()
+    for k in got[0]:
+        assert np.array_equal(got[0][k], got[1][k]), k
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=2, ns=6, na=6, verts=V)
+    ref = ora.subcycles(om, ora_params(nx.PhysParams()), 3, st)
+    _check(got[1], ref, st, 1e-11)
+
+
 def test_fused_variants_agree(nx):
     """TMA structured kernel vs table-driven kernel (tables from the K0 kernel): same result
     to rounding after 3 subcycles."""
