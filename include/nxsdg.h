@@ -167,6 +167,9 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *                           (smaller stages, more CTAs per SM), -1 (default) = tuned choice
  *   NXSDG_OPT_TAIL_SPLIT    persistent fused kernels with the work counter: 1 (default) = the last chunks of
  *                           each launch are split into ~8-row sub-units so the warps finish together; 0 = off
+ *   NXSDG_OPT_L2_POLICY     fused TMA kernels' L2 eviction policies (createpolicy + .L2::cache_hint), bits:
+ *                           1 = streamed loads (S, P_g, node constants) evict_first, 2 = the new S and v
+ *                           stores evict_first, 4 = v boxes evict_last; default 2 (0 = evict_normal)
  *   NXSDG_OPT_DYNAMIC       1 (default): warps claim work units from an atomic counter; 0: static round-robin
  *   NXSDG_OPT_PRECISION     0 (default): FP64 everywhere; 1 (NEXT-3): the fused CG2/DG2 subcycles keep
  *                           S and P_g in FP32 storage (arithmetic and the v state stay FP64); the FP64 S
@@ -183,7 +186,7 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  * INVALID_ARG for an unknown option or value. */
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
        NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,
-       NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10 };
+       NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

@@ -117,6 +117,7 @@ struct nxsdg_ctx {
     int stages = 2;        // TMA pipeline depth 2..4
     int const_regs = -1;   // node constants: 0 = fifth TMA box of the stage, 1 = register prefetch, -1 = default
     int tail_split = 1;    // persistent kernels: split the last chunks into short sub-units (1) or not (0)
+    int l2_policy = 2;     // fused TMA kernels: L2 eviction-policy bits (2 = stores evict_first)
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
@@ -438,6 +439,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
             if (value > 3 && c->precision >= 1) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..3 with FP32 storage");
             c->stages = (int)value; break;
+        case NXSDG_OPT_L2_POLICY:
+            if (value < 0 || value > 7) return fail(c, NXSDG_ERR_INVALID_ARG, "L2 policy bits 0..7");
+            c->l2_policy = (int)value; break;
         case NXSDG_OPT_TAIL_SPLIT:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "tail split 0|1");
             c->tail_split = (int)value; break;
@@ -1385,11 +1389,10 @@ static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0 &&
 // Tail split of a persistent launch with twarps warps: the last chunks become ~8-row sub-units, enough of
 // them (2 x twarps) that every warp's final unit is short, so the warps finish within ~8 jobs of each
 // other instead of ~ty (the idle tail of a launch is half a unit on average)
-static SubArgs with_tail(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps) {
+static SubArgs launch_args(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps) {
     SubArgs a = a0;
     a.ntail = 0; a.qtail = 1;
-    static const int hints = getenv("NXSDG_L2_HINTS") ? atoi(getenv("NXSDG_L2_HINTS")) : 0;   // experiment hook
-    a.l2_hints = hints;
+    a.l2_hints = c->l2_policy;
     const int q = a.ty / 8;
     if (!c->tail_split || !a.work_counter || q < 2 || a.nsel < 2) return a;
     const int64_t need = (2 * twarps + (int64_t)a.nstrips * q - 1) / ((int64_t)a.nstrips * q);
@@ -1442,7 +1445,7 @@ static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     k_subcycle_gen<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->gen_maps[cv][cs],
-                                                                       with_tail(c, a, (int64_t)blocks * K2_WARPS));
+                                                                       launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
 
@@ -1467,7 +1470,7 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
     k_subcycle_tma<R, ST, SF, CT, NS, CL><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
-        mp, with_tail(c, a, (int64_t)blocks * K2_WARPS));
+        mp, launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
 // stages x replacement pressure x node-constant staging (TMA box | registers)

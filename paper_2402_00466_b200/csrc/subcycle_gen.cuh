@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
     const int gw = blockIdx.x * K2_WARPS + wib;
     const int nunits = units_total(a);
     if (gw >= nunits) return;
+    const uint64_t pol_st = l2_policy(a.l2_hints & 2 ? 1 : 0);   // stores: evict_first by default
     if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -237,9 +238,9 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
             const int64_t e = (int64_t)lr * a.epitch + ix;
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
-                a.S_out[k * eplane + e] = S11[k];
-                a.S_out[(6 + k) * eplane + e] = S12[k];
-                a.S_out[(12 + k) * eplane + e] = S22[k];
+                st_hint(a.S_out + k * eplane + e, S11[k], pol_st);
+                st_hint(a.S_out + (6 + k) * eplane + e, S12[k], pol_st);
+                st_hint(a.S_out + (12 + k) * eplane + e, S22[k], pol_st);
             }
         }
         // ---- divergence: r_j = sum_g w sigma . adj(J)^T grad_ref phi_j, separable in (gx, gy)
@@ -335,8 +336,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                 }
                 const int64_t n = (int64_t)(2 * lr + jy) * npitch + 2 * ix;
                 if (ix < a.nx) {
-                    *reinterpret_cast<double2*>(a.vx_out + n) = make_double2(nvx[0], nvx[1]);
-                    *reinterpret_cast<double2*>(a.vy_out + n) = make_double2(nvy[0], nvy[1]);
+                    st_hint2(a.vx_out + n, nvx[0], nvx[1], pol_st);
+                    st_hint2(a.vy_out + n, nvy[0], nvy[1], pol_st);
                 } else {
                     a.vx_out[n] = 0.0;
                     a.vy_out[n] = 0.0;

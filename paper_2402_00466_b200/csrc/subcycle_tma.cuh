@@ -344,8 +344,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     const int gw = blockIdx.x * K2_WARPS + wib;
     const int nunits = units_total(a);
     if (gw >= nunits) return;
-    // L2 policies (a.l2_hints bits: 1 streamed loads S, P_g, node constants evict_first; 2 stores
-    // evict_first; 4 v boxes evict_last)
+    // L2 policies, a.l2_hints = NXSDG_OPT_L2_POLICY bits: 1 streamed loads (S, P_g, node constants)
+    // evict_first; 2 (default) stores evict_first; 4 v boxes evict_last.  The new S and v (208 B per
+    // element, 3.5 GB per C4 launch) are not read again in this launch, so with bit 2 they stop
+    // displacing the lines that are: the neighbouring strips' overlap and the shared v row
     const uint64_t pol_ld = l2_policy(a.l2_hints & 1 ? 1 : 0), pol_st = l2_policy(a.l2_hints & 2 ? 1 : 0);
     const uint64_t pol_v = l2_policy(a.l2_hints & 4 ? 2 : 0);
     if (lane == 0) {

@@ -17,6 +17,8 @@ peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEAS
 m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, 6, 6, params=nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha))
 m.set_vertices(V)
 m.load(st)
+if "L2" in os.environ:   # NXSDG_OPT_L2_POLICY (default 2: evict-first stores)
+    m.set_option(nxsdg.OPT_L2_POLICY, int(os.environ["L2"]))
 s = torch.cuda.ExternalStream(m.stream)
 N = cfg.nx * cfg.ny
 bpe = m.bytes_per_element_subcycle
