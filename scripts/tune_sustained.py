@@ -22,9 +22,13 @@ def sample_clocks(stop, out):
 
 
 cfg = inputs.CONFIGS[os.environ.get("CFG", "C4")]
+NS = int(os.environ.get("NS", "6"))
+if NS != cfg.ns:
+    cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, NS, cfg.na, cfg.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect,
+                        cfg.alpha)
 st = inputs.make_config_case(cfg)
 prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
-m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, 6, 6, params=prm)
+m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, NS, 6, params=prm)
 m.load(st)
 prec = int(os.environ.get("PREC", "0"))
 if prec:
@@ -33,8 +37,9 @@ bpe = m.bytes_per_element_subcycle
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6545.6
 s = torch.cuda.ExternalStream(m.stream)
 n = 100
-# COMBOS = "cl:ctas:stages[:ty[:split[:l2]]],..." (cl = NXSDG_OPT_CONST_STAGING, ty = chunk rows, default 32,
-# split = NXSDG_OPT_TAIL_SPLIT, default 1, l2 = NXSDG_OPT_L2_POLICY, default 2),
+# COMBOS = "cl:ctas:stages[:ty[:split[:l2[:vc]]]],..." (cl = NXSDG_OPT_CONST_STAGING, ty = chunk rows, default 32,
+# split = NXSDG_OPT_TAIL_SPLIT, default 1, l2 = NXSDG_OPT_L2_POLICY, default 2, vc = NXSDG_OPT_V_ROW_CARRY,
+# default 1),
 # measured REPS times, interleaved
 COMBOS = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("COMBOS", "0:2:2,0:3:2,1:4:2,1:3:2").split(",")]
 REPS = int(os.environ.get("REPS", "2"))
@@ -48,6 +53,8 @@ for rep in range(REPS):
         m.set_option(nxsdg.OPT_TAIL_SPLIT, split)
         l2 = combo[5] if len(combo) > 5 else 2
         m.set_option(nxsdg.OPT_L2_POLICY, l2)
+        vc = combo[6] if len(combo) > 6 else 1
+        m.set_option(nxsdg.OPT_V_ROW_CARRY, vc)
         m.set_option(nxsdg.OPT_CONST_STAGING, cl)
         m.set_option(nxsdg.OPT_CTAS_PER_SM, c)
         m.set_option(nxsdg.OPT_STAGES, stg)
@@ -65,6 +72,6 @@ for rep in range(REPS):
         stop.set(); th.join()
         ms = statistics.median(t)
         gbs = bpe * cfg.nx * cfg.ny / (ms * 1e-3) / 1e9
-        print(json.dumps({"prec": prec, "rep": rep, "const_regs": cl, "ctas": c, "stages": stg, "ty": ty, "split": split, "l2": l2, "ms_median": ms,
+        print(json.dumps({"prec": prec, "rep": rep, "const_regs": cl, "ctas": c, "stages": stg, "ty": ty, "split": split, "l2": l2, "vcarry": vc, "ms_median": ms,
                           "ms_min": min(t), "alg_GBs": gbs, "frac": gbs / peak,
                           "sm_mhz": statistics.median(clk) if clk else None}), flush=True)
