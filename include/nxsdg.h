@@ -159,17 +159,22 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *                           1: table-driven register kernel k_subcycle<p> (reference-table variant)
  *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (default 32; one ring row each)
  *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy;
- *                           -1 (default) = tuned: 3 with FP64 S/P_g storage, 4 with FP32 storage or with
- *                           the node constants in registers, 3 for the fused general-quad kernel)
+ *                           -1 (default) = tuned: 4 with the node constants in registers (FP64, n_S = 6),
+ *                           3 (n_S = 6) / 2 (n_S = 8) with them TMA-staged in FP64, 4 with FP32 storage,
+ *                           3 for the fused general-quad kernel)
  *   NXSDG_OPT_STAGES        TMA pipeline depth per warp, 2..4 (default 2; 2..3 with FP32 storage)
  *   NXSDG_OPT_CONST_STAGING box kernel's six node constants (c1, rhs0, cAFo, o): 0 = a fifth TMA box of each
  *                           stage, 1 = each lane prefetches its 24 doubles into registers with 16-B loads
- *                           (smaller stages, more CTAs per SM), -1 (default) = tuned choice
+ *                           (smaller stages, more CTAs per SM), -1 (default) = tuned: 1 for FP64 storage with
+ *                           n_S = 6, else 0
  *   NXSDG_OPT_TAIL_SPLIT    persistent fused kernels with the work counter: 1 (default) = the last chunks of
  *                           each launch are split into ~8-row sub-units so the warps finish together; 0 = off
  *   NXSDG_OPT_L2_POLICY     fused TMA kernels' L2 eviction policies (createpolicy + .L2::cache_hint), bits:
  *                           1 = streamed loads (S, P_g, node constants) evict_first, 2 = the new S and v
  *                           stores evict_first, 4 = v boxes evict_last; default 2 (0 = evict_normal)
+ *   NXSDG_OPT_V_ROW_CARRY   box TMA kernel: 1 (default) = consecutive element rows of a warp's work unit share
+ *                           a v node row, which the next job takes from registers (its TMA boxes load the two
+ *                           new node rows only); 0 = every job loads all three rows
  *   NXSDG_OPT_DYNAMIC       1 (default): warps claim work units from an atomic counter; 0: static round-robin
  *   NXSDG_OPT_PRECISION     0 (default): FP64 everywhere; 1 (NEXT-3): the fused CG2/DG2 subcycles keep
  *                           S and P_g in FP32 storage (arithmetic and the v state stay FP64); the FP64 S
@@ -186,7 +191,8 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  * INVALID_ARG for an unknown option or value. */
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
        NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,
-       NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11 };
+       NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11,
+       NXSDG_OPT_V_ROW_CARRY = 12 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

@@ -142,6 +142,7 @@ struct SubArgs {
     int ntail, qtail;               // persistent kernels: the last ntail selected chunks are split into
                                     // qtail sub-units each (0 / 1 = off)
     int l2_hints;                   // box TMA kernel: L2 eviction-policy bits (subcycle_tma.cuh)
+    int vcarry;                     // box TMA kernel: shared v node row carried in registers (subcycle_tma.cuh)
 };
 
 // Unit u of a persistent kernel's work list -> strip and element rows [lr0, lr1) (lr0 >= lr1: empty).

@@ -118,6 +118,7 @@ struct nxsdg_ctx {
     int const_regs = -1;   // node constants: 0 = fifth TMA box of the stage, 1 = register prefetch, -1 = default
     int tail_split = 1;    // persistent kernels: split the last chunks into short sub-units (1) or not (0)
     int l2_policy = 2;     // fused TMA kernels: L2 eviction-policy bits (2 = stores evict_first)
+    int v_carry = 1;       // box TMA kernel: a unit's next job re-uses the shared v node row from registers
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
@@ -439,6 +440,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value < 2 || value > 4) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..4");
             if (value > 3 && c->precision >= 1) return fail(c, NXSDG_ERR_INVALID_ARG, "stages 2..3 with FP32 storage");
             c->stages = (int)value; break;
+        case NXSDG_OPT_V_ROW_CARRY:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "v row carry 0|1");
+            c->v_carry = (int)value; break;
         case NXSDG_OPT_L2_POLICY:
             if (value < 0 || value > 7) return fail(c, NXSDG_ERR_INVALID_ARG, "L2 policy bits 0..7");
             c->l2_policy = (int)value; break;
@@ -1320,13 +1324,14 @@ static nxsdg_status build_maps(nxsdg_ctx* c) {
     const cuuint64_t ns[2] = {(cuuint64_t)c->npitch * 8, (cuuint64_t)c->nn * 8};
     const cuuint64_t nS = 3 * (cuuint64_t)c->NS;
     const cuuint64_t dS[3] = {nx, er, nS}, dP[3] = {nx, er, 9}, dV[2] = {ncols, nr}, dC[3] = {ncols, nr, 6};
-    const cuuint32_t bS[3] = {K2Cols<double>::E, 1, (cuuint32_t)nS}, bP[3] = {K2Cols<double>::E, 1, 9}, bV[2] = {K2_VCOLS, 3},
+    const cuuint32_t bS[3] = {K2Cols<double>::E, 1, (cuuint32_t)nS}, bP[3] = {K2Cols<double>::E, 1, 9}, bV[2] = {K2_VCOLS, 3}, bV2[2] = {K2_VCOLS, 2},
                      bC[3] = {K2_CCOLS, 2, 6};
     for (int v = 0; v < 2; ++v)
         for (int s = 0; s < 2; ++s) {
             K2Maps& M = c->maps[v][s];
             bool ok = encode(&M.S, c->S[s], 3, dS, es, bS) && encode(&M.Pg, c->Pg, 3, dP, es, bP) &&
                       encode(&M.vx, c->vx[v], 2, dV, ns, bV) && encode(&M.vy, c->vy[v], 2, dV, ns, bV) &&
+                      encode(&M.vx2, c->vx[v], 2, dV, ns, bV2) && encode(&M.vy2, c->vy[v], 2, dV, ns, bV2) &&
                       encode(&M.C, c->nodec, 3, dC, ns, bC);
             if (!ok) return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         }
@@ -1393,6 +1398,7 @@ static SubArgs launch_args(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps
     SubArgs a = a0;
     a.ntail = 0; a.qtail = 1;
     a.l2_hints = c->l2_policy;
+    a.vcarry = c->v_carry;
     const int q = a.ty / 8;
     if (!c->tail_split || !a.work_counter || q < 2 || a.nsel < 2) return a;
     const int64_t need = (2 * twarps + (int64_t)a.nstrips * q - 1) / ((int64_t)a.nstrips * q);
@@ -1401,10 +1407,14 @@ static SubArgs launch_args(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps
     return a;
 }
 // Defaults of the box kernel, tuned on C4 under sustained load (scripts/tune_sustained.py)
-// FP64 storage: node constants in registers, 4 CTAs/SM (C4: 1.97 ms vs 2.02-2.11 ms per subcycle with the
-// fifth TMA box at 3 or 2 CTAs/SM); FP32 storage keeps the box (its stages are small already: 1.50 vs 1.59 ms)
-static bool const_in_regs(const nxsdg_ctx* c) { return c->const_regs < 0 ? c->precision == 0 : c->const_regs == 1; }
-static int default_ctas(size_t sf_bytes, bool cl) { return cl ? 4 : (sf_bytes == 8 ? 3 : 4); }
+// FP64 storage, n_S = 6: node constants in registers, 4 CTAs/SM (C4: 1.87-1.96 ms vs 1.95-2.11 ms per
+// subcycle with the fifth TMA box at 3 or 2 CTAs/SM).  n_S = 8 (18.4 KB stages, 240 registers with the
+// constants in registers): the TMA box at 2 CTAs/SM, 2.12 ms vs 2.22 ms.  FP32 storage keeps the box (its
+// stages are small already: 1.48 vs 1.58 ms).  profiles/tune_sustained_r01.log, tune_l2_policy_r01.log
+static bool const_in_regs(const nxsdg_ctx* c) {
+    return c->const_regs < 0 ? (c->precision == 0 && c->NS == 6) : c->const_regs == 1;
+}
+static int default_ctas(size_t sf_bytes, bool cl, int ns) { return cl ? 4 : (sf_bytes == 8 ? (ns == 8 ? 2 : 3) : 4); }
 
 // NEXT-1: the fused general-quad subcycle stages the vertex rows and the lumped node masses too
 static nxsdg_status build_gen_maps(nxsdg_ctx* c) {
@@ -1463,7 +1473,7 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL>, 32 * K2_WARPS, smem));
-    const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL) : c->ctas_per_sm;
+    const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL, NS) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;

@@ -74,6 +74,7 @@ __device__ __forceinline__ double2 ldg_stream2(const double* p) {   // read once
 
 struct K2Maps {
     CUtensorMap S, Pg, vx, vy, C;    // 5 x 128 B, 64-B aligned
+    CUtensorMap vx2, vy2;            // 2-row v boxes: the new node rows of a unit's continuing job
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -386,15 +387,24 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     auto record = [&](const Cur& c, int st) {   // lane 0
         jobs[st] = make_int4(c.ok ? c.u : -1, c.lr, c.lr1, (c.ring ? 1 : 0) | (c.first ? 2 : 0));
     };
+    // v row carry: a continuing job (not the first of its unit) loads node rows 2lr+1, 2lr+2 into smem
+    // rows 0, 1 and takes row 2lr (the previous job's top row, same lane columns) from registers
+    const bool vcarry = a.vcarry != 0;
     auto issue = [&](const Cur& c, int s) {
         Stage* t = stg + s;
+        const bool cont = vcarry && !c.first;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, CL>());
+        mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, CL>() - (cont ? 2u * K2_VCOLS * 8u : 0u));
         const int xs = (c.ix0 - 1) & ~(AL - 1);   // 16-B aligned start column (arithmetic: -1 -> -2 / -4)
         tma3h(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0, pol_ld);
         tma3h(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0, pol_ld);
-        tma2h(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
-        tma2h(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
+        if (cont) {
+            tma2h(&t->vx[0][0], &maps.vx2, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr + 1, pol_v);
+            tma2h(&t->vy[0][0], &maps.vy2, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr + 1, pol_v);
+        } else {
+            tma2h(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
+            tma2h(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
+        }
         if constexpr (!CL) tma3h(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0, pol_ld);
     };
 
@@ -418,6 +428,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     uint32_t phase = 0;    // bit s = parity of stage s
     int s = 0;
     double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
+    double carVx[3] = {0.0, 0.0, 0.0}, carVy[3] = {0.0, 0.0, 0.0};   // v row carry (node row 2lr of the next job)
     for (;;) {
         const int sp = (s + STAGES - 1) % STAGES;
         if (lane == 0) {
@@ -455,15 +466,25 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         const int eo = (cur.ix0 - 1) - ((cur.ix0 - 1) & ~(AL - 1));   // lane offset inside the S / P_g box
         if (cur.first) { carx[0] = carx[1] = cary[0] = cary[1] = 0.0; }
 
-        // ---- node values of this element (local box columns 2*lane .. 2*lane+2)
+        // ---- node values of this element (local box columns 2*lane .. 2*lane+2); node row 2lr + jy is
+        //      smem row jy - ro (ro = 1 for a continuing job: its row 0 is the carried one)
         double Vx[3][3], Vy[3][3];
+        const int ro = (vcarry && !cur.first) ? 1 : 0;
 #pragma unroll
         for (int jy = 0; jy < 3; ++jy) {
-            const double2 a2 = *reinterpret_cast<const double2*>(&t.vx[jy][2 * lane]);
-            const double2 b2 = *reinterpret_cast<const double2*>(&t.vy[jy][2 * lane]);
-            Vx[jy][0] = a2.x; Vx[jy][1] = a2.y; Vx[jy][2] = t.vx[jy][2 * lane + 2];
-            Vy[jy][0] = b2.x; Vy[jy][1] = b2.y; Vy[jy][2] = t.vy[jy][2 * lane + 2];
+            if (jy == 0 && ro) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) { Vx[0][q] = carVx[q]; Vy[0][q] = carVy[q]; }
+                continue;
+            }
+            const int r = jy - ro;
+            const double2 a2 = *reinterpret_cast<const double2*>(&t.vx[r][2 * lane]);
+            const double2 b2 = *reinterpret_cast<const double2*>(&t.vy[r][2 * lane]);
+            Vx[jy][0] = a2.x; Vx[jy][1] = a2.y; Vx[jy][2] = t.vx[r][2 * lane + 2];
+            Vy[jy][0] = b2.x; Vy[jy][1] = b2.y; Vy[jy][2] = t.vy[r][2 * lane + 2];
         }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { carVx[q] = Vx[2][q]; carVy[q] = Vy[2][q]; }
         // ---- strain (Table 1 "strain"): DG coefficients, then Gauss-point values of
         //      the trace u = e11 + e22, the half difference w = (e11 - e22)/2 and e12, in which
         //      Hibler's Delta^2 = 1.25 (e11^2 + e22^2) + 1.5 e11 e22 + e12^2 is u^2 + w^2 + e12^2

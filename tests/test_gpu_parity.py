@@ -149,6 +149,50 @@ def test_tail_split_bitwise(nx, ora, general, shape, ty, ctas):
     _check(got[1], ref, st, 1e-11)
 
 
+@pytest.mark.parametrize("ns,prec", [(6, 0), (8, 0), (6, 1), (6, 2)])
+@pytest.mark.parametrize("shape,ty", [((70, 75), 32), ((93, 33), 1), ((6, 41), 7), ((40, 64), 16)])
+def test_v_row_carry_bitwise(nx, ora, ns, prec, shape, ty):
+    """NXSDG_OPT_V_ROW_CARRY: a unit's continuing job takes the shared v node row from the previous
+    job's registers and TMA-loads only the two new rows; the node values are the same doubles, so
+    the state is bitwise that of the three-row loads (every precision, n_S, chunk height incl. 1)."""
+    nxe, nye = shape
+    lx, ly = 2e3 * nxe, 2e3 * nye
+    st = case(nxe, nye, 2, ns, 6, "warm", lx, ly)
+    got = {}
+    for carry in (0, 1):
+        opts = {nx.OPT_V_ROW_CARRY: carry, nx.OPT_CHUNK_ROWS: ty}
+        if prec:
+            opts[nx.OPT_PRECISION] = prec
+        got[carry] = _gpu_run(nx, st, nxe, nye, 2, ns, 6, 4, lx, ly, options=opts)
+    for k in got[0]:
+        assert np.array_equal(got[0][k], got[1][k]), k
+    if prec == 0:
+        ref = ora.subcycles(ora_mesh(nxe, nye, 2, ns, 6, lx, ly), ora_params(nx.PhysParams()), 4, st)
+        _check(got[1], ref, st, 1e-11)
+
+
+@pytest.mark.parametrize("general", [False, True])
+def test_l2_policy_bitwise(nx, general):
+    """NXSDG_OPT_L2_POLICY only changes the cache hints of loads and stores: every policy gives the
+    default's state bitwise (box and general-quad fused kernels)."""
+    nxe, nye = 70, 75
+    lx, ly = 2e3 * nxe, 2e3 * nye
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.2) if general else None
+    got = {}
+    for pol in (2, 0, 1, 4, 7):
+        with nx.Mesh(nxe, nye, lx, ly, 2, 6, 6) as m:
+            if general:
+                m.set_vertices(V)
+            m.set_option(nx.OPT_L2_POLICY, pol)
+            m.load(st)
+            m.mevp_substeps(3, begin_step=True)
+            got[pol] = m.state()
+    for pol in (0, 1, 4, 7):
+        for k in got[2]:
+            assert np.array_equal(got[2][k], got[pol][k]), (pol, k)
+
+
 def test_fused_variants_agree(nx):
     """TMA structured kernel vs table-driven kernel (tables from the K0 kernel): same result
     to rounding after 3 subcycles."""
