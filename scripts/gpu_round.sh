@@ -16,3 +16,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_a
     -o gpurun_out/prof_other python bench.py --steps 1 --warmup 0 --nsub 2 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_other.log 2>&1
 echo "ncu other rc=$?" >> gpurun_out/ncu_other.log
 timeout 900 python bench.py --ns 8 --no-cpu-baseline > gpurun_out/bench_ns8.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ns8.log
+timeout 900 python bench.py --fp32-stress --no-cpu-baseline > gpurun_out/bench_fp32.log 2>&1; echo "rc=$?" >> gpurun_out/bench_fp32.log
+timeout 600 python scripts/bench_general.py > gpurun_out/bench_general.log 2>&1; echo "rc=$?" >> gpurun_out/bench_general.log

@@ -21,6 +21,15 @@ for (nxe, nye, p, ns, na) in [(37, 29, 2, 6, 6), (16, 16, 1, 3, 3), (9, 70, 2, 6
             m.set_option(nxsdg.OPT_FUSED_KERNEL, variant)
             m.set_option(nxsdg.OPT_CHUNK_ROWS, 8)
             run(m, st)
+# default TMA path at a 32-row chunk height on a taller box: tail split (8-row sub-units), v row carry,
+# node constants in registers (1) and TMA-staged (0)
+nxe, nye = 40, 140
+st = inputs.make_case(nxe, nye, 2, 6, 6, kind="random", lx=nxe * 1e3, ly=nye * 1e3)
+for cl in (1, 0):
+    with nxsdg.Mesh(nxe, nye, nxe * 1e3, nye * 1e3, 2, 6, 6) as m:
+        m.set_option(nxsdg.OPT_CONST_STAGING, cl)
+        m.set_option(nxsdg.OPT_CTAS_PER_SM, 1)
+        run(m, st)
 # fused general quads
 nxe, nye = 37, 33
 st = inputs.make_case(nxe, nye, 2, 6, 6, kind="random", lx=nxe * 1e3, ly=nye * 1e3)
