@@ -23,6 +23,10 @@ def sample_clocks(stop, out):
 
 cfg = inputs.CONFIGS[os.environ.get("CFG", "C4")]
 NS = int(os.environ.get("NS", "6"))
+if "NY" in os.environ:   # a row strip of the config (e.g. C4 per GPU at 8 GPUs: NY=512), same resolution
+    ny = int(os.environ["NY"])
+    cfg = inputs.Config(cfg.name, cfg.nx, ny, cfg.p, cfg.ns, cfg.na, cfg.nsub, cfg.lx, cfg.ly * ny / cfg.ny, cfg.kind,
+                        cfg.advect, cfg.alpha)
 if NS != cfg.ns:
     cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, NS, cfg.na, cfg.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect,
                         cfg.alpha)
