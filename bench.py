@@ -175,7 +175,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nsub", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=None,
-                    help="pipelined e2e outer steps (default max(10, --steps)); the first forcing upload and the "
+                    help="pipelined e2e outer steps (default max(30, --steps): the paper's 30-outer-step protocol, "
+                         "P:350); the first forcing upload and the "
                          "last velocity readback are not overlapped and stay inside the timed region")
     ap.add_argument("--fp32-storage", action="store_true",
                     help="NEXT-3: S and P_g stored in FP32 inside the fused subcycles (arithmetic FP64)")
@@ -314,7 +315,7 @@ def main():
     achieved = bpe * n_el_rank / (kernel_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak_hbm()
     traffic = ncu_traffic_per_launch() if cfg.ns == 6 and not (args.fp32_storage or args.fp32_stress) else None
-    kernel = KERNEL if cfg.ns == 6 else "k_subcycle<2,8> (table-driven fused strain+stress+divergence+velocity, n_S = 8)"
+    kernel = KERNEL if cfg.ns == 6 else "k_subcycle_tma<..., n_S = 8> (fused strain+stress+divergence+velocity, CG2/DG2)"
 
     # e2e: the same metric through the C ABI with pinned HOST buffers, copies inside the timed region.
     # The model state (v, S, A, H) lives on the device across outer steps; each outer step's external
@@ -322,7 +323,7 @@ def main():
     # pinned host memory, and its result is read back (v, nxsdg_read_state) - DESIGN.md §6.
     e2e = None
     if args.e2e_steps is None:
-        args.e2e_steps = max(10, args.steps)
+        args.e2e_steps = max(30, args.steps)   # the paper's protocol length: 30 outer steps
     if args.e2e_steps > 0:
         fkeys = ("ox", "oy", "ax", "ay")
         pinned = {k: torch.from_numpy(st[k]).pin_memory() for k in fkeys}
