@@ -171,7 +171,8 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *                           each launch are split into ~8-row sub-units so the warps finish together; 0 = off
  *   NXSDG_OPT_L2_POLICY     fused TMA kernels' L2 eviction policies (createpolicy + .L2::cache_hint), bits:
  *                           1 = streamed loads (S, P_g, node constants) evict_first, 2 = the new S and v
- *                           stores evict_first, 4 = v boxes evict_last; default 2 (0 = evict_normal)
+ *                           stores evict_first, 4 = v boxes evict_last (bits 1 and 4: box kernel only);
+ *                           default 2 (0 = evict_normal everywhere)
  *   NXSDG_OPT_V_ROW_CARRY   box TMA kernel: 1 (default) = consecutive element rows of a warp's work unit share
  *                           a v node row, which the next job takes from registers (its TMA boxes load the two
  *                           new node rows only); 0 = every job loads all three rows

@@ -1298,11 +1298,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// L2 sector promotion of the TMA loads (tuning experiment hook: NXSDG_TMA_L2_PROMOTION = 0 none,
-// 1 64 B, 2 128 B, 3 256 B (default))
+// L2 sector promotion of the TMA loads: 128 B.  A box row of the S / P_g boxes is 272 B at a 16-B
+// offset, so 256-B promotion fetches up to 768 B for it and relies on the neighbour strip to use the
+// rest while it is still in L2; at 8 warps/SM that often fails: C4 launch DRAM reads 8.97 GB (256 B)
+// vs 8.53 GB (128 B), sustained 1.910 vs 1.905 ms (profiles/tune_promo_r01.log).  Experiment hook:
+// NXSDG_TMA_L2_PROMOTION = 0 none, 1 64 B, 2 128 B (default), 3 256 B
 static CUtensorMapL2promotion l2_promotion() {
     const char* e = getenv("NXSDG_TMA_L2_PROMOTION");
-    const int v = e ? atoi(e) : 3;
+    const int v = e ? atoi(e) : 2;
     return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
          : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
 }
@@ -1345,7 +1348,7 @@ static bool encode_f32(CUtensorMap* m, const void* base, const cuuint64_t* dims,
     if (!fn) return false;
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
