@@ -1403,7 +1403,7 @@ static SubArgs launch_args(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps
     a.l2_hints = c->l2_policy;
     a.vcarry = c->v_carry;
     const int q = a.ty / 8;
-    if (!c->tail_split || !a.work_counter || q < 2 || a.nsel < 2) return a;
+    if (!c->tail_split || !a.work_counter || q < 2 || a.nsel < 1) return a;
     const int64_t need = (2 * twarps + (int64_t)a.nstrips * q - 1) / ((int64_t)a.nstrips * q);
     a.ntail = (int)std::min<int64_t>(a.nsel, need);
     a.qtail = q;

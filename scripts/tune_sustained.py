@@ -33,6 +33,8 @@ if NS != cfg.ns:
 st = inputs.make_config_case(cfg)
 prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
 m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, NS, 6, params=prm)
+if os.environ.get("GENERAL"):   # distorted quads (NEXT-1): the fused general-quad kernel, 728 B/element
+    m.set_vertices(inputs.distorted_vertices(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 0.25))
 m.load(st)
 prec = int(os.environ.get("PREC", "0"))
 if prec:
