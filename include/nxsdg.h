@@ -161,12 +161,14 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy;
  *                           -1 (default) = tuned: 4 with the node constants in registers (FP64, n_S = 6),
  *                           3 (n_S = 6) / 2 (n_S = 8) with them TMA-staged in FP64, 4 with FP32 storage,
- *                           3 for the fused general-quad kernel)
+ *                           4 / 3 for the fused general-quad kernel with late / boxed constants)
  *   NXSDG_OPT_STAGES        TMA pipeline depth per warp, 2..4 (default 2; 2..3 with FP32 storage)
- *   NXSDG_OPT_CONST_STAGING box kernel's six node constants (c1, rhs0, cAFo, o): 0 = a fifth TMA box of each
- *                           stage, 1 = each lane prefetches its 24 doubles into registers with 16-B loads
- *                           (smaller stages, more CTAs per SM), -1 (default) = tuned: 1 for FP64 storage with
- *                           n_S = 6, else 0
+ *   NXSDG_OPT_CONST_STAGING the fused kernels' six node constants (c1, rhs0, cAFo, o): 0 = a TMA box of each
+ *                           stage; 1 = box kernel: each lane prefetches its 24 doubles into registers with
+ *                           16-B loads, general-quad kernel: a second TMA loads them into the stage's S / P_g
+ *                           region once the stress update has consumed it (both: smaller stages, more CTAs
+ *                           per SM); -1 (default) = tuned: box kernel 1 for FP64 storage with n_S = 6, else 0;
+ *                           general-quad kernel 1
  *   NXSDG_OPT_TAIL_SPLIT    persistent fused kernels with the work counter: 1 (default) = the last chunks of
  *                           each launch are split into ~8-row sub-units so the warps finish together; 0 = off
  *   NXSDG_OPT_L2_POLICY     fused TMA kernels' L2 eviction policies (createpolicy + .L2::cache_hint), bits:

@@ -1417,6 +1417,10 @@ static SubArgs launch_args(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps
 static bool const_in_regs(const nxsdg_ctx* c) {
     return c->const_regs < 0 ? (c->precision == 0 && c->NS == 6) : c->const_regs == 1;
 }
+// general-quad fused kernel: node constants loaded late into the consumed S / P_g region (1, default: 4 CTAs/SM,
+// sustained C4 2.75 ms per subcycle) or as a box of the stage (0: 3 CTAs/SM, 2.88 ms;
+// profiles/tune_gen_late_const_r01.log)
+static bool gen_late_const(const nxsdg_ctx* c) { return c->const_regs < 0 ? true : c->const_regs == 1; }
 static int default_ctas(size_t sf_bytes, bool cl, int ns) { return cl ? 4 : (sf_bytes == 8 ? (ns == 8 ? 2 : 3) : 4); }
 
 // NEXT-1: the fused general-quad subcycle stages the vertex rows and the lumped node masses too
@@ -1441,23 +1445,26 @@ static nxsdg_status build_gen_maps(nxsdg_ctx* c) {
     return NXSDG_OK;
 }
 
-template <bool R, int ST>
+template <bool R, int ST, bool LC = false>
 static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
-    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(K2GenStage) + sizeof(uint64_t) + sizeof(int4));
+    const size_t smem = (size_t)K2_WARPS * ST *
+                        (sizeof(typename K2GenStageSel<LC>::T) + 2 * sizeof(uint64_t) + sizeof(int4));
     static bool attr = false;
     if (!attr) {
-        CU(cudaFuncSetAttribute(k_subcycle_gen<R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaFuncSetAttribute(k_subcycle_gen<R, ST, LC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_gen<R, ST>, 32 * K2_WARPS, smem));
-    const int cap = c->ctas_per_sm < 0 ? 3 : c->ctas_per_sm;   // tuned on C4 (profiles/tune_gen_r01.log)
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_gen<R, ST, LC>, 32 * K2_WARPS, smem));
+    // tuned on C4 (profiles/tune_gen_r01.log, tune_gen_sustained_r01.log): 3 CTAs/SM with the constant box,
+    // 4 with the late constants (smaller stages)
+    const int cap = c->ctas_per_sm < 0 ? (LC ? 4 : 3) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
-    k_subcycle_gen<R, ST><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->gen_maps[cv][cs],
+    k_subcycle_gen<R, ST, LC><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(c->gen_maps[cv][cs],
                                                                        launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
@@ -1537,11 +1544,17 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int 
     a.work_counter = c->dynamic ? c->counters + slot : nullptr;
     if (c->general) {
         if ((st = build_gen_maps(c))) return st;
-        switch (c->stages * 2 + (a.repl ? 1 : 0)) {
-            case 4: return launch_gen_t<false, 2>(c, cv, cs, a);
-            case 5: return launch_gen_t<true, 2>(c, cv, cs, a);
-            case 6: return launch_gen_t<false, 3>(c, cv, cs, a);
-            default: return launch_gen_t<true, 3>(c, cv, cs, a);
+        const bool lc = gen_late_const(c);
+        const int st = std::min(c->stages, 3);   // the general kernel is instantiated for 2 and 3 stages
+        switch ((st * 2 + (a.repl ? 1 : 0)) * 2 + (lc ? 1 : 0)) {
+            case 8: return launch_gen_t<false, 2, false>(c, cv, cs, a);
+            case 9: return launch_gen_t<false, 2, true>(c, cv, cs, a);
+            case 10: return launch_gen_t<true, 2, false>(c, cv, cs, a);
+            case 11: return launch_gen_t<true, 2, true>(c, cv, cs, a);
+            case 12: return launch_gen_t<false, 3, false>(c, cv, cs, a);
+            case 13: return launch_gen_t<false, 3, true>(c, cv, cs, a);
+            case 14: return launch_gen_t<true, 3, false>(c, cv, cs, a);
+            default: return launch_gen_t<true, 3, true>(c, cv, cs, a);
         }
     }
     if (c->precision == 2) {

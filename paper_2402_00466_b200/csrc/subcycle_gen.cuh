@@ -33,6 +33,18 @@ struct __align__(128) K2GenStage {
 __host__ __device__ constexpr uint32_t k2g_tx_bytes() {
     return k2_tx_bytes<double, 6>() + 2 * K2_VCOLS * 8 + 2 * K2_CCOLS * 8;
 }
+// LC ("late constants", NXSDG_OPT_CONST_STAGING = 1 for this kernel): the stage has no node-constant
+// box; once the stress update has consumed S and P_g, lane 0 TMA-loads the job's six node constants
+// into that region (7.5 KB >= 5952 B) on a second mbarrier, and the velocity update waits for it.
+// 13.1 KB stages instead of 19 KB: 4 CTAs (8 warps) per SM fit instead of 3.
+struct __align__(128) K2GenStageLC {
+    K2StageNC<double, 6> b;
+    alignas(128) double X[2][K2_VCOLS];
+    alignas(128) double M[2][K2_CCOLS];
+};
+__host__ __device__ constexpr uint32_t k2g_const_bytes() { return 6 * 2 * K2_CCOLS * 8; }
+template <bool LC> struct K2GenStageSel { using T = K2GenStage; };
+template <> struct K2GenStageSel<true> { using T = K2GenStageLC; };
 
 // q-th 1D Lagrange value / derivative of node j at the Gauss abscissa S_q in {-a, 0, a}:
 //   L0 = 2S^2 - S, L1 = 1 - 4S^2, L2 = 2S^2 + S;  L0' = 4S - 1, L1' = -8S, L2' = 4S + 1  (2a^2 = 0.3)
@@ -55,9 +67,14 @@ __device__ __forceinline__ void moments(const double G[9], double sc, double (&b
     for (int k = 0; k < 6; ++k) b[k] *= mref[k];
 }
 
-template <bool REPL, int STAGES>
+__device__ __forceinline__ const double* gen_const_box(const K2GenStage& t) { return &t.b.C[0][0][0]; }
+__device__ __forceinline__ const double* gen_const_box(const K2GenStageLC& t) { return &t.b.S[0][0]; }
+
+template <bool REPL, int STAGES, bool LC = false>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_constant__ K2GenMaps maps, SubArgs a) {
-    using Stage = K2GenStage;
+    using Stage = typename K2GenStageSel<LC>::T;
+    using NC6 = K2StageNC<double, 6>;
+    static_assert(!LC || offsetof(NC6, vx) >= 6 * 2 * K2_CCOLS * 8, "the constants fit before vx");
     extern __shared__ __align__(1024) unsigned char k2_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     Stage* stg = reinterpret_cast<Stage*>(k2_smem) + wib * STAGES;
@@ -67,8 +84,14 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
     const int nunits = units_total(a);
     if (gw >= nunits) return;
     const uint64_t pol_st = l2_policy(a.l2_hints & 2 ? 1 : 0);   // stores: evict_first by default
+    // LC: one more mbarrier per stage for the late constants, after the job descriptors
+    uint64_t* barC = reinterpret_cast<uint64_t*>(reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) +
+                                                 K2_WARPS * STAGES) + wib * STAGES;
     if (lane == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&bar[s], 1);
+            if constexpr (LC) mbar_init(&barC[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -102,13 +125,13 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
     auto issue = [&](const Cur& c, int s) {
         Stage* t = stg + s;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], k2g_tx_bytes());
+        mbar_expect_tx(&bar[s], k2g_tx_bytes() - (LC ? k2g_const_bytes() : 0u));
         const int xs = (c.ix0 - 1) & ~1;
         tma3(&t->b.S[0][0], &maps.S, &bar[s], xs, c.lr, 0);
         tma3(&t->b.Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0);
         tma2(&t->b.vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
         tma2(&t->b.vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr);
-        tma3(&t->b.C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0);
+        if constexpr (!LC) tma3(&t->b.C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0);
         tma2(&t->X[0][0], &maps.X, &bar[s], 2 * (c.ix0 - 1), c.lr);
         tma2(&t->M[0][0], &maps.M, &bar[s], 2 * c.ix0, 2 * c.lr);
     };
@@ -128,7 +151,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
         }
     }
     __syncwarp();
-    uint32_t phase = 0;
+    uint32_t phase = 0, phaseC = 0;
     int s = 0;
     double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
     for (;;) {
@@ -234,6 +257,17 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
             S12[k] = fma(fac, t.b.S[6 + k][eo + lane], S12[k]);
             S22[k] = fma(fac, t.b.S[12 + k][eo + lane], S22[k]);
         }
+        // LC: S and P_g of this stage are consumed; load the node constants into their place
+        if constexpr (LC) {
+            if (!cur.ring) {
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&barC[s], k2g_const_bytes());
+                    tma3(const_cast<double*>(&t.b.S[0][0]), &maps.C, &barC[s], 2 * cur.ix0, 2 * lr, 0);
+                }
+            }
+        }
         if (!cur.ring && evalid && lane >= 1) {
             const int64_t e = (int64_t)lr * a.epitch + ix;
 #pragma unroll
@@ -307,6 +341,13 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                 sumx[jy][q] = sx; sumy[jy][q] = sy;
             }
         }
+        if constexpr (LC) {
+            if (!cur.ring) {
+                mbar_wait(&barC[s], (phaseC >> s) & 1u);
+                phaseC ^= 1u << s;
+            }
+        }
+        const double (*CC)[2][K2_CCOLS] = reinterpret_cast<const double (*)[2][K2_CCOLS]>(gen_const_box(t));
         if (nvalid) {
             const bool brow0 = lr == a.erow_begin && a.bottom_boundary;
 #pragma unroll
@@ -320,8 +361,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                     const double im = mass > 0.0 ? -rcp_nr(mass) : 0.0;       // F = -r / m
                     const double fx = sumx[jy][q] * im, fy = sumy[jy][q] * im;
                     const double vxo = Vx[jy][q], vyo = Vy[jy][q];
-                    const double c1 = t.b.C[0][jy][cc], r0x = t.b.C[1][jy][cc], r0y = t.b.C[2][jy][cc];
-                    const double cf = t.b.C[3][jy][cc], oxv = t.b.C[4][jy][cc], oyv = t.b.C[5][jy][cc];
+                    const double c1 = CC[0][jy][cc], r0x = CC[1][jy][cc], r0y = CC[2][jy][cc];
+                    const double cf = CC[3][jy][cc], oxv = CC[4][jy][cc], oyv = CC[5][jy][cc];
                     const double dx = oxv - vxo, dy = oyv - vyo;
                     const double w2 = fma(dx, dx, dy * dy);
                     const double w = w2 > 0.0 ? w2 * rsqrt_nr(w2) : 0.0;

@@ -171,6 +171,33 @@ def test_v_row_carry_bitwise(nx, ora, ns, prec, shape, ty):
         _check(got[1], ref, st, 1e-11)
 
 
+@pytest.mark.parametrize("shape,ctas,stages,repl", [((70, 75), 4, 2, 0), ((37, 33), 2, 3, 0), ((93, 41), 0, 2, 1),
+                                                   ((6, 1), 4, 2, 0), ((1, 5), 1, 3, 1)])
+def test_general_late_constants_bitwise(nx, ora, shape, ctas, stages, repl):
+    """Fused general-quad kernel, NXSDG_OPT_CONST_STAGING = 1: the node constants arrive by a second TMA
+    into the consumed S / P_g region instead of a box of the stage; the same doubles reach the velocity
+    update, so the state is bitwise that of the box variant, and it matches the oracle."""
+    nxe, nye = shape
+    lx, ly = 2e3 * nxe, 2e3 * nye
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.25)
+    prm = nx.PhysParams(replacement_pressure=repl)
+    got = {}
+    for lc in (0, 1):
+        with nx.Mesh(nxe, nye, lx, ly, 2, 6, 6, params=prm) as m:
+            m.set_vertices(V)
+            for k, v in {nx.OPT_CONST_STAGING: lc, nx.OPT_CTAS_PER_SM: ctas, nx.OPT_STAGES: stages}.items():
+                m.set_option(k, v)
+            m.load(st)
+            m.mevp_substeps(4, begin_step=True)
+            got[lc] = m.state()
+    for k in got[0]:
+        assert np.array_equal(got[0][k], got[1][k]), k
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=2, ns=6, na=6, verts=V)
+    ref = ora.subcycles(om, ora_params(prm), 4, st)
+    _check(got[1], ref, st, 1e-11)
+
+
 @pytest.mark.parametrize("general", [False, True])
 def test_l2_policy_bitwise(nx, general):
     """NXSDG_OPT_L2_POLICY only changes the cache hints of loads and stores: every policy gives the
