@@ -18,3 +18,7 @@ echo "ncu other rc=$?" >> gpurun_out/ncu_other.log
 timeout 900 python bench.py --ns 8 --no-cpu-baseline > gpurun_out/bench_ns8.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ns8.log
 timeout 900 python bench.py --fp32-stress --no-cpu-baseline > gpurun_out/bench_fp32.log 2>&1; echo "rc=$?" >> gpurun_out/bench_fp32.log
 timeout 600 python scripts/bench_general.py > gpurun_out/bench_general.log 2>&1; echo "rc=$?" >> gpurun_out/bench_general.log
+for tool in memcheck racecheck; do
+  SANITIZE_P2P=1 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log
+done

@@ -198,6 +198,27 @@ def test_general_late_constants_bitwise(nx, ora, shape, ctas, stages, repl):
     _check(got[1], ref, st, 1e-11)
 
 
+@pytest.mark.parametrize("repl", [0, 1])
+def test_general_four_stages_request(nx, ora, repl):
+    """NXSDG_OPT_STAGES = 4 on a distorted mesh: the general-quad kernel exists for 2 and 3 stages and
+    runs 3, with the replacement-pressure flag as set (a 4-stage request once fell through to the
+    replacement-pressure instantiation)."""
+    nxe, nye = 40, 37
+    lx, ly = 2e3 * nxe, 2e3 * nye
+    st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
+    V = inputs.distorted_vertices(nxe, nye, lx, ly, 0.25)
+    prm = nx.PhysParams(replacement_pressure=repl)
+    with nx.Mesh(nxe, nye, lx, ly, 2, 6, 6, params=prm) as m:
+        m.set_vertices(V)
+        m.set_option(nx.OPT_STAGES, 4)
+        m.load(st)
+        m.mevp_substeps(3, begin_step=True)
+        got = m.state()
+    om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=2, ns=6, na=6, verts=V)
+    ref = ora.subcycles(om, ora_params(prm), 3, st)
+    _check(got, ref, st, 1e-11)
+
+
 @pytest.mark.parametrize("general", [False, True])
 def test_l2_policy_bitwise(nx, general):
     """NXSDG_OPT_L2_POLICY only changes the cache hints of loads and stores: every policy gives the
