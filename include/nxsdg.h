@@ -159,16 +159,17 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *                           1: table-driven register kernel k_subcycle<p> (reference-table variant)
  *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (default 32; one ring row each)
  *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy;
- *                           -1 (default) = tuned: 4 with the node constants in registers (FP64, n_S = 6),
+ *                           -1 (default) = tuned: 4 with the node constants in registers or loaded late,
  *                           3 (n_S = 6) / 2 (n_S = 8) with them TMA-staged in FP64, 4 with FP32 storage,
  *                           4 / 3 for the fused general-quad kernel with late / boxed constants)
  *   NXSDG_OPT_STAGES        TMA pipeline depth per warp, 2..4 (default 2; 2..3 with FP32 storage)
  *   NXSDG_OPT_CONST_STAGING the fused kernels' six node constants (c1, rhs0, cAFo, o): 0 = a TMA box of each
  *                           stage; 1 = box kernel: each lane prefetches its 24 doubles into registers with
- *                           16-B loads, general-quad kernel: a second TMA loads them into the stage's S / P_g
- *                           region once the stress update has consumed it (both: smaller stages, more CTAs
- *                           per SM); -1 (default) = tuned: box kernel 1 for FP64 storage with n_S = 6, else 0;
- *                           general-quad kernel 1
+ *                           16-B loads; 2 = box kernel (FP64 storage only, else UNSUPPORTED at the launch):
+ *                           a second TMA loads them into the stage's S / P_g region once the stress update has
+ *                           consumed it; general-quad kernel: 1 and 2 both mean that late TMA (all: smaller
+ *                           stages, more CTAs per SM); -1 (default) = tuned: box kernel 1 (FP64, n_S = 6),
+ *                           2 (FP64, n_S = 8), 0 (FP32 storage); general-quad kernel late
  *   NXSDG_OPT_TAIL_SPLIT    persistent fused kernels with the work counter: 1 (default) = the last chunks of
  *                           each launch are split into ~8-row sub-units so the warps finish together; 0 = off
  *   NXSDG_OPT_L2_POLICY     fused TMA kernels' L2 eviction policies (createpolicy + .L2::cache_hint), bits:

@@ -450,7 +450,7 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "tail split 0|1");
             c->tail_split = (int)value; break;
         case NXSDG_OPT_CONST_STAGING:
-            if (value < -1 || value > 1) return fail(c, NXSDG_ERR_INVALID_ARG, "node-constant staging -1|0|1");
+            if (value < -1 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "node-constant staging -1|0|1|2");
             c->const_regs = (int)value; break;
         default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
     }
@@ -1414,13 +1414,17 @@ static SubArgs launch_args(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps
 // subcycle with the fifth TMA box at 3 or 2 CTAs/SM).  n_S = 8 (18.4 KB stages, 240 registers with the
 // constants in registers): the TMA box at 2 CTAs/SM, 2.12 ms vs 2.22 ms.  FP32 storage keeps the box (its
 // stages are small already: 1.48 vs 1.58 ms).  profiles/tune_sustained_r01.log, tune_l2_policy_r01.log
-static bool const_in_regs(const nxsdg_ctx* c) {
-    return c->const_regs < 0 ? (c->precision == 0 && c->NS == 6) : c->const_regs == 1;
+// n_S = 8: late constants (mode 2) at 4 CTAs/SM, 2.20 ms vs 2.31 ms with the box at 2 CTAs/SM; n_S = 6: the
+// register prefetch (mode 1) stays ahead of mode 2 (1.91 vs 1.99 ms; profiles/tune_box_late_const_r01.log)
+static int const_mode(const nxsdg_ctx* c) {
+    if (c->const_regs >= 0) return c->const_regs;
+    if (c->precision != 0) return 0;
+    return c->NS == 8 ? 2 : 1;
 }
 // general-quad fused kernel: node constants loaded late into the consumed S / P_g region (1, default: 4 CTAs/SM,
 // sustained C4 2.75 ms per subcycle) or as a box of the stage (0: 3 CTAs/SM, 2.88 ms;
 // profiles/tune_gen_late_const_r01.log)
-static bool gen_late_const(const nxsdg_ctx* c) { return c->const_regs < 0 ? true : c->const_regs == 1; }
+static bool gen_late_const(const nxsdg_ctx* c) { return c->const_regs < 0 ? true : c->const_regs >= 1; }
 static int default_ctas(size_t sf_bytes, bool cl, int ns) { return cl ? 4 : (sf_bytes == 8 ? (ns == 8 ? 2 : 3) : 4); }
 
 // NEXT-1: the fused general-quad subcycle stages the vertex rows and the lumped node masses too
@@ -1469,54 +1473,50 @@ static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     return NXSDG_OK;
 }
 
-template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false>
+template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false, bool LC = false>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
-    using Stage = typename K2StageSel<SF, NS, CL>::T;
-    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + sizeof(uint64_t) + sizeof(int4));
+    using Stage = typename K2StageSel<SF, NS, CL || LC>::T;
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + 2 * sizeof(uint64_t) + sizeof(int4));
     static bool attr = false;
     if (!attr) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
         attr = true;
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL>, 32 * K2_WARPS, smem));
-    const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL, NS) : c->ctas_per_sm;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC>, 32 * K2_WARPS,
+                                                     smem));
+    const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL || LC, NS) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
     const int64_t units = (int64_t)a.nstrips * a.nsel;
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF, CT, NS, CL><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
+    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
         mp, launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
 // stages x replacement pressure x node-constant staging (TMA box | registers)
+// stages x replacement pressure x node-constant mode (0 TMA box | 1 registers | 2 late TMA, FP64 only)
+template <typename SF, typename CT, int NS, int ST>
+static nxsdg_status launch_tma_mode(nxsdg_ctx* c, int cv, int cs, const SubArgs& a, int mode) {
+    if (mode == 1) return a.repl ? launch_tma_t<true, ST, SF, CT, NS, true>(c, cv, cs, a)
+                                 : launch_tma_t<false, ST, SF, CT, NS, true>(c, cv, cs, a);
+    if constexpr (sizeof(SF) == 8) {
+        if (mode == 2) return a.repl ? launch_tma_t<true, ST, SF, CT, NS, false, true>(c, cv, cs, a)
+                                     : launch_tma_t<false, ST, SF, CT, NS, false, true>(c, cv, cs, a);
+    }
+    return a.repl ? launch_tma_t<true, ST, SF, CT, NS>(c, cv, cs, a) : launch_tma_t<false, ST, SF, CT, NS>(c, cv, cs, a);
+}
 template <typename SF, typename CT = double, int NS = 6>
 static nxsdg_status launch_tma_sel(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
-    const bool cl = const_in_regs(c);
-    const int key = (c->stages * 2 + (a.repl ? 1 : 0)) * 2 + (cl ? 1 : 0);
-    switch (key) {
-        case 8: return launch_tma_t<false, 2, SF, CT, NS, false>(c, cv, cs, a);
-        case 9: return launch_tma_t<false, 2, SF, CT, NS, true>(c, cv, cs, a);
-        case 10: return launch_tma_t<true, 2, SF, CT, NS, false>(c, cv, cs, a);
-        case 11: return launch_tma_t<true, 2, SF, CT, NS, true>(c, cv, cs, a);
-        case 12: return launch_tma_t<false, 3, SF, CT, NS, false>(c, cv, cs, a);
-        case 13: return launch_tma_t<false, 3, SF, CT, NS, true>(c, cv, cs, a);
-        case 14: return launch_tma_t<true, 3, SF, CT, NS, false>(c, cv, cs, a);
-        case 15: return launch_tma_t<true, 3, SF, CT, NS, true>(c, cv, cs, a);
-        default: break;
-    }
-    if constexpr (sizeof(SF) == 8) {   // 4 stages: FP64 storage only
-        switch (key) {
-            case 16: return launch_tma_t<false, 4, SF, CT, NS, false>(c, cv, cs, a);
-            case 17: return launch_tma_t<false, 4, SF, CT, NS, true>(c, cv, cs, a);
-            case 18: return launch_tma_t<true, 4, SF, CT, NS, false>(c, cv, cs, a);
-            default: return launch_tma_t<true, 4, SF, CT, NS, true>(c, cv, cs, a);
-        }
-    }
+    int mode = const_mode(c);
+    if (sizeof(SF) != 8 && mode == 2) return fail(c, NXSDG_ERR_UNSUPPORTED, "late node constants need FP64 storage");
+    if (c->stages == 2) return launch_tma_mode<SF, CT, NS, 2>(c, cv, cs, a, mode);
+    if (c->stages == 3) return launch_tma_mode<SF, CT, NS, 3>(c, cv, cs, a, mode);
+    if constexpr (sizeof(SF) == 8) return launch_tma_mode<SF, CT, NS, 4>(c, cv, cs, a, mode);
     return fail(c, NXSDG_ERR_INVALID_ARG, "stages %d with FP32 storage", c->stages);
 }
 

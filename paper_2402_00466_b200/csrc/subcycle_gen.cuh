@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
         // LC: S and P_g of this stage are consumed; load the node constants into their place
         if constexpr (LC) {
             if (!cur.ring) {
+                asm volatile("" ::: "memory");   // every lane's reads of the stage are issued before the barrier
                 __syncwarp();
                 if (lane == 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -328,9 +328,15 @@ __device__ __forceinline__ void div_t(const double (&S)[NS], double h, double r[
 }
 
 // ---------------------------------------------------------------- the kernel
-template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false>
+// LC = true (with CL = false, FP64 storage): the constants are not staged with the job; once the stress
+// update has read S and P_g, lane 0 TMA-loads them into the stage's S region (>= 5952 B for FP64) on a
+// second mbarrier, and the velocity update waits for it - small stages without CL's 24 live registers.
+template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
-    using Stage = typename K2StageSel<SF, NS, CL>::T;
+    static_assert(!(CL && LC), "one node-constant mode");
+    static_assert(!LC || sizeof(SF) == 8, "late constants need the FP64 S region");
+    constexpr bool NOBOX = CL || LC;
+    using Stage = typename K2StageSel<SF, NS, NOBOX>::T;
     constexpr int AL = K2Cols<SF>::ALIGN;
     SF* const S_out = reinterpret_cast<SF*>(a.S_out);   // FP32 buffers in mixed-precision mode
     extern __shared__ __align__(1024) unsigned char k2_smem[];   // no static smem: base stays 1024-B aligned
@@ -351,8 +357,14 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     // displacing the lines that are: the neighbouring strips' overlap and the shared v row
     const uint64_t pol_ld = l2_policy(a.l2_hints & 1 ? 1 : 0), pol_st = l2_policy(a.l2_hints & 2 ? 1 : 0);
     const uint64_t pol_v = l2_policy(a.l2_hints & 4 ? 2 : 0);
+    // LC: one more mbarrier per stage for the late constants, after the job descriptors
+    uint64_t* barC = reinterpret_cast<uint64_t*>(reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) +
+                                                 K2_WARPS * STAGES) + wib * STAGES;
     if (lane == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&bar[s], 1);
+            if constexpr (LC) mbar_init(&barC[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -394,7 +406,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         Stage* t = stg + s;
         const bool cont = vcarry && !c.first;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, CL>() - (cont ? 2u * K2_VCOLS * 8u : 0u));
+        mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, NOBOX>() - (cont ? 2u * K2_VCOLS * 8u : 0u));
         const int xs = (c.ix0 - 1) & ~(AL - 1);   // 16-B aligned start column (arithmetic: -1 -> -2 / -4)
         tma3h(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0, pol_ld);
         tma3h(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0, pol_ld);
@@ -405,7 +417,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             tma2h(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
             tma2h(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
         }
-        if constexpr (!CL) tma3h(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0, pol_ld);
+        if constexpr (!NOBOX) tma3h(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0, pol_ld);
     };
 
     const double ihx = a.ihx, ihy = a.ihy, fac = a.fac, hA = 0.5 * a.ainv;
@@ -425,7 +437,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         }
     }
     __syncwarp();
-    uint32_t phase = 0;    // bit s = parity of stage s
+    uint32_t phase = 0, phaseC = 0;    // bit s = parity of stage s (LC: of its constants barrier)
     int s = 0;
     double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
     double carVx[3] = {0.0, 0.0, 0.0}, carVy[3] = {0.0, 0.0, 0.0};   // v row carry (node row 2lr of the next job)
@@ -531,6 +543,17 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         const CT cfac = (CT)fac;
         project_pair(eu, ew, cfac, C11, C22);
         project(e12, 0.5, cfac, C12);
+        if constexpr (LC) {   // S and P_g of this stage are consumed (their values already feed the
+            if (!cur.ring) {  // projection FMAs): the node constants go there
+                asm volatile("" ::: "memory");   // every lane's reads of the stage are issued before the barrier
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&barC[s], 6u * 2u * K2_CCOLS * 8u);
+                    tma3h(const_cast<SF*>(&t.S[0][0]), &maps.C, &barC[s], 2 * cur.ix0, 2 * lr, 0, pol_ld);
+                }
+            }
+        }
         double S11[NS], S12[NS], S22[NS];   // the divergence and velocity stay FP64
 #pragma unroll
         for (int k = 0; k < NS; ++k) { S11[k] = (double)C11[k]; S12[k] = (double)C12[k]; S22[k] = (double)C22[k]; }
@@ -578,6 +601,12 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                 sumx[jy][q] = sx; sumy[jy][q] = sy;
             }
         }
+        if constexpr (LC) {
+            if (!cur.ring) {
+                mbar_wait(&barC[s], (phaseC >> s) & 1u);
+                phaseC ^= 1u << s;
+            }
+        }
         if (nvalid) {
             const bool brow0 = lr == a.erow_begin && a.bottom_boundary;
 #pragma unroll
@@ -593,6 +622,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                     if constexpr (CL) {
                         c1 = cr[0][jy][q]; r0x = cr[1][jy][q]; r0y = cr[2][jy][q];
                         cf = cr[3][jy][q]; oxv = cr[4][jy][q]; oyv = cr[5][jy][q];
+                    } else if constexpr (LC) {
+                        const double (*LCb)[2][K2_CCOLS] = reinterpret_cast<const double (*)[2][K2_CCOLS]>(&t.S[0][0]);
+                        c1 = LCb[0][jy][cc]; r0x = LCb[1][jy][cc]; r0y = LCb[2][jy][cc];
+                        cf = LCb[3][jy][cc]; oxv = LCb[4][jy][cc]; oyv = LCb[5][jy][cc];
                     } else {
                         c1 = t.C[0][jy][cc]; r0x = t.C[1][jy][cc]; r0y = t.C[2][jy][cc];
                         cf = t.C[3][jy][cc]; oxv = t.C[4][jy][cc]; oyv = t.C[5][jy][cc];

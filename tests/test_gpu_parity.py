@@ -102,8 +102,9 @@ def test_fused_variants_and_tuning(nx, ora, variant, ty, ctas, stages):
 @pytest.mark.parametrize("shape", [(70, 75), (1, 5), (6, 1), (93, 33)])
 @pytest.mark.parametrize("ctas,stages", [(4, 2), (3, 3), (1, 2)])
 def test_const_staging_bitwise(nx, ora, ns, prec, shape, ctas, stages):
-    """NXSDG_OPT_CONST_STAGING: the node constants prefetched into registers (1) instead of staged as
-    a fifth TMA box (0) change only where the same doubles come from, so the states agree BITWISE,
+    """NXSDG_OPT_CONST_STAGING: the node constants prefetched into registers (1) or TMA-loaded late into
+    the consumed S region (2) instead of staged as a fifth TMA box (0) change only where the same
+    doubles come from, so the states agree BITWISE,
     for every storage precision, n_S and grid size; the register variant is also checked against the
     oracle (FP64 storage)."""
     nxe, nye = shape
@@ -111,12 +112,14 @@ def test_const_staging_bitwise(nx, ora, ns, prec, shape, ctas, stages):
     st = case(nxe, nye, 2, ns, 6, "warm", lx, ly)
     base = {nx.OPT_PRECISION: prec} if prec else {}
     got = {}
-    for cl in (0, 1):
+    modes = (0, 1, 2) if prec == 0 else (0, 1)   # 2 = late TMA into the consumed S region (FP64 storage)
+    for cl in modes:
         opts = dict(base)
         opts.update({nx.OPT_CONST_STAGING: cl, nx.OPT_CTAS_PER_SM: ctas, nx.OPT_STAGES: stages})
         got[cl] = _gpu_run(nx, st, nxe, nye, 2, ns, 6, 4, lx, ly, options=opts)
-    for k in got[0]:
-        assert np.array_equal(got[0][k], got[1][k]), k
+    for cl in modes[1:]:
+        for k in got[0]:
+            assert np.array_equal(got[0][k], got[cl][k]), (cl, k)
     if prec == 0:
         ref = ora.subcycles(ora_mesh(nxe, nye, 2, ns, 6, lx, ly), ora_params(nx.PhysParams()), 4, st)
         _check(got[1], ref, st, 1e-11)
@@ -812,6 +815,19 @@ def test_ns8_unsupported_combinations(nx):
         assert e.value.status == nx.ERR_UNSUPPORTED
         with pytest.raises(nx.NxsdgError) as e:
             m.set_vertices(np.zeros((9, 9, 2)))
+        assert e.value.status == nx.ERR_UNSUPPORTED
+
+
+def test_late_constants_need_fp64_storage(nx):
+    """NXSDG_OPT_CONST_STAGING = 2 loads the constants into the FP64 S region of the stage; with FP32
+    storage that region is too small: UNSUPPORTED at the launch, not a silent fallback."""
+    st = case(12, 10, 2, 6, 6, "warm", 24e3, 20e3)
+    with nx.Mesh(12, 10, 24e3, 20e3, 2, 6, 6) as m:
+        m.load(st)
+        m.set_option(nx.OPT_PRECISION, 1)
+        m.set_option(nx.OPT_CONST_STAGING, 2)
+        with pytest.raises(nx.NxsdgError) as e:
+            m.mevp_substeps(1, begin_step=True)
         assert e.value.status == nx.ERR_UNSUPPORTED
 
 
