@@ -7,9 +7,9 @@ import ncu_summary as n
 
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for tag, bpe, cfg in (("ns8", 776.0, "C4 4096^2 CG2/DG2 n_S = 8, one fused subcycle launch (bench.py --ns 8 --nsub 10, "
-                                     "6th launch), defaults: node constants TMA-staged, 2 CTAs/SM"),
+                                     "6th launch), defaults: node constants TMA-loaded late into the consumed S region, 4 CTAs/SM"),
                       ("gen", 728.0, "C4-size distorted CG2/DG2 (delta 0.25), one fused general subcycle, defaults "
-                                     "(3 CTAs/SM, tail split, evict-first stores)")):
+                                     "(late node constants, 4 CTAs/SM, tail split, evict-first stores)")):
     rep = os.path.join(root, "gpurun_out", f"prof_{tag}.ncu-rep")
     if not os.path.exists(rep):
         continue
