@@ -139,6 +139,106 @@ def oracle_sample(cfg, nsub, win=160):
                       f"advect + prep + {nsub} subcycles, oracle (plain C FP64, OpenMP)"}
 
 
+def oracle_baseline(cfg, win, nsamples=3):
+    """cpu_baseline: the oracle as it stands, median of nsamples runs on the same window as the reference
+    arm, plus single-thread rates on C1 (whole mesh, 10 subcycles) and a 128^2 window of C2."""
+    import oracle
+    samples = [oracle_sample(cfg, cfg.nsub, win=win) for _ in range(nsamples)]
+    out = {"value": float(np.median([x["value"] for x in samples])), "unit": "element-updates/s",
+           "cores": samples[0]["cores"], "kind": "oracle", "sample": samples[0]["sample"] + f", median of {nsamples}",
+           "samples": [x["value"] for x in samples], "seconds": sum(x["seconds"] for x in samples)}
+    o = oracle.Oracle()
+    n0 = o.threads
+    try:
+        o.L.ora_set_threads(1)
+        one = {}
+        for name, w in (("C1", 16), ("C2", 128)):
+            c = inputs.CONFIGS[name]
+            x = oracle_sample(c, c.nsub, win=w)
+            one[name] = {"value": x["value"], "sample": x["sample"], "seconds": x["seconds"]}
+        out["single_thread"] = one
+    finally:
+        o.L.ora_set_threads(n0)
+    try:
+        with open("/proc/cpuinfo") as f:
+            out["cpu_model"] = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), None)
+    except OSError:
+        pass
+    out["compiler"] = "gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp"
+    return out
+
+
+def window_parity(m, cfg, rank, world, nsub, dist=None, core=12):
+    """Correctness evidence on the bench line: after one outer step (advect + prep + nsub fused
+    subcycles) of the bench configuration, a core x core window - centred on the middle strip interface
+    for N > 1 (the rows there come from two ranks and crossed the halo exchange), on the domain centre
+    for N = 1 - against the oracle run on the window plus its light-cone ring.  Returns
+    the group-normalised relative max errors; the north_star bar is 1e-10 (S, v), 1e-12 (A, H)."""
+    import oracle
+    from paper_2402_00466_b200 import nxsdg
+    p = cfg.p
+    if world > 1:
+        cy = nxsdg.partition(cfg.ny, p, world, world // 2)[0] - core // 2
+    else:
+        cy = cfg.ny // 2 - core // 2
+    cx = cfg.nx // 2 - core // 2
+    mine = {}
+    r0, er = m.elem_row0, m.elem_rows
+    n0, nr = m.node_row0, m.node_rows
+    for k in ("S11", "S12", "S22", "A", "H"):
+        a = m.read_state(k).reshape(er, cfg.nx, -1)
+        for gy in range(max(cy, r0), min(cy + core, r0 + er)):
+            mine[(k, gy)] = a[gy - r0, cx:cx + core].copy()
+    for k in ("vx", "vy"):
+        a = m.read_state(k)
+        for gj in range(max(p * cy, n0), min(p * (cy + core) + 1, n0 + nr)):
+            mine[(k, gj)] = a[gj - n0, p * cx:p * (cx + core) + 1].copy()
+    parts = [mine]
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+    if rank != 0:
+        return None
+    rows = {}
+    for d in parts:
+        rows.update(d)
+    g = {k: np.stack([rows[(k, gy)] for gy in range(cy, cy + core)]).reshape(-1, rows[(k, cy)].shape[-1])
+         for k in ("S11", "S12", "S22", "A", "H")}
+    for k in ("vx", "vy"):
+        g[k] = np.stack([rows[(k, gj)] for gj in range(p * cy, p * (cy + core) + 1)])
+    ring = nsub + 5
+    ix0, iy0 = max(0, cx - ring), max(0, cy - ring)
+    w, h = min(cfg.nx, cx + core + ring) - ix0, min(cfg.ny, cy + core + ring) - iy0
+    sub = inputs.make_config_case(cfg, window=(ix0, iy0, w, h))
+    hx, hy = cfg.lx / cfg.nx, cfg.ly / cfg.ny
+    om = oracle.Mesh(w, h, lx=w * hx, ly=h * hy, p=p, ns=cfg.ns, na=cfg.na)
+    t0 = time.perf_counter()
+    ref = oracle.Oracle().outer_step(om, oracle.Params(alpha=cfg.alpha, beta=cfg.alpha), nsub, sub, do_advect=True)
+    init = inputs.make_config_case(cfg, window=(cx, cy, core, core))
+    ex, ey = cx - ix0, cy - iy0
+    rc = {}
+    for k, a in ref.items():
+        if k in ("vx", "vy"):
+            rc[k] = a[p * ey:p * (ey + core) + 1, p * ex:p * (ex + core) + 1]
+        elif k in g:
+            rc[k] = a.reshape(h, w, -1)[ey:ey + core, ex:ex + core].reshape(-1, a.shape[1])
+
+    def err(keys, inc=False):
+        num = max(float(np.abs((g[k] - init[k] if inc else g[k]) - (rc[k] - init[k] if inc else rc[k])).max())
+                  for k in keys)
+        den = max(float(np.abs(rc[k] - init[k] if inc else rc[k]).max()) for k in keys)
+        return num / den if den > 0 else num
+
+    S, V = ("S11", "S12", "S22"), ("vx", "vy")
+    e = {"S": err(S), "dS": err(S, True), "v": err(V), "dv": err(V, True), "A": err(("A",)), "H": err(("H",))}
+    return {"window": f"{core}x{core} elements at ({cx},{cy})" +
+                      (f", centred on the interface of ranks {world // 2 - 1}/{world // 2}" if world > 1 else
+                       ", domain centre"),
+            "after": f"advect + prep + {nsub} fused subcycles from the initial state",
+            "errors": e, "pass": max(e["S"], e["dS"], e["v"], e["dv"]) <= 1e-10 and max(e["A"], e["H"]) <= 1e-12,
+            "oracle_s": time.perf_counter() - t0}
+
+
 def run_reference(args, cfg):
     rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
     if rank != 0:
@@ -193,7 +293,9 @@ def main():
                          "memory with a device-side flag handshake (CUDA IPC); nccl = ncclSend/ncclRecv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-window", type=int, default=512, help="oracle window per --impl reference step")
-    ap.add_argument("--cpu-window", type=int, default=640, help="oracle window of the cpu_baseline sample")
+    ap.add_argument("--cpu-window", type=int, default=None,
+                    help="oracle window of the cpu_baseline samples (default: --ref-window, the reference arm's)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle window check on the bench line")
     args = ap.parse_args()
     cname = args.config or ("C5" if args.weak else "C4")
     cfg = inputs.CONFIGS[cname]
@@ -260,8 +362,21 @@ def main():
         m.set_option(nxsdg.OPT_PRECISION, 2 if args.fp32_stress else 1)
     if args.limiter:
         m.set_option(nxsdg.OPT_LIMITER, 1)
+    infos = [m.transport_info]
+    if world > 1:
+        infos = [None] * world
+        dist.all_gather_object(infos, m.transport_info)
     m.load(st)
     stream = torch.cuda.ExternalStream(m.stream)
+    parity = None
+    if not args.no_parity and not (args.fp32_storage or args.fp32_stress or args.moving or args.limiter):
+        # correctness evidence on the bench line: one outer step of the bench configuration from the
+        # initial state, an oracle window across the middle strip interface (N > 1) or at the centre
+        m.advect(prm.dt)
+        m.mevp_substeps(cfg.nsub, begin_step=True)
+        m.synchronize()
+        parity = window_parity(m, cfg, rank, world, cfg.nsub, dist if world > 1 else None)
+        m.load(st)
     n_el = cfg.nx * cfg.ny   # whole job
     n_el_rank = m.elem_rows * cfg.nx
 
@@ -360,9 +475,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            s = oracle_sample(cfg, cfg.nsub, win=args.cpu_window)
-            cpu = {"value": s["value"], "unit": "element-updates/s", "cores": s["cores"], "kind": "oracle",
-                   "sample": s["sample"], "seconds": s["seconds"]}
+            cpu = oracle_baseline(cfg, args.cpu_window or args.ref_window)
         except Exception as ex:  # the oracle is a reported baseline, never the product
             cpu = {"value": None, "error": str(ex)}
 
@@ -386,6 +499,8 @@ def main():
                          "algorithmic_bytes_per_launch": bpe * n_el_rank, "bytes_per_element_subcycle": bpe},
             "clocks": clk.summary(),
             "gpu_launches": launches,
+            "ranks": infos,
+            "parity": parity,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

@@ -10,9 +10,11 @@
  *     (advection) step.  One subcycle = strain (Table 1) ->
  *     stress update (Listing 1/2) -> stress divergence
  *      -> velocity update.
- *   Discretisation: structured quadrilateral box mesh, CG velocity
- *   of degree p (Q1|Q2), DG stress with n_S coefficients (3|6), DG tracers
- *   with n_A coefficients (1|3|6), Gauss rule NGP from Listing 2 line 462.
+ *   Discretisation: structured quadrilateral mesh (the box, or general
+ *   quads with the bilinear map of each cell's vertices, nxsdg_set_vertices), CG
+ *   velocity of degree p (Q1|Q2), DG stress with n_S coefficients (3 with Q1; 6
+ *   or 8 with Q2, R#6/R#24), DG tracers with n_A coefficients (1|3|6), Gauss rule
+ *   NGP from Listing 2 line 462.
  *
  * Layouts at the ABI (logical, independent of the device layout):
  *   DG field : (owned element rows) x nx x n doubles, row-major, one element's
@@ -192,11 +194,16 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_LIMITER       NEXT-4 (DESIGN R#25): 0 (default, the paper's unlimited scheme) | 1 = Zhang-Shu
  *                           bound-preserving scaling limiter after every SSP-RK stage of nxsdg_advect (A in [0,1],
  *                           H >= 0 at the volume and edge Gauss points; element means, hence mass, unchanged)
+ *   NXSDG_OPT_MULTIRANK_GRAPH  row-strip ranks (P2P or NCCL transport): 1 (default) = nxsdg_mevp_substeps
+ *                           captures its n fused subcycles - boundary chunks, exchange (peer stores + flag
+ *                           handshake, or NCCL send/recv) on the halo stream, interior chunks, join - in one
+ *                           CUDA graph per (n, ping-pong parity) and replays it (one host crossing per call);
+ *                           0 = the same work issued from the host one subcycle at a time
  * INVALID_ARG for an unknown option or value. */
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
        NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,
        NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11,
-       NXSDG_OPT_V_ROW_CARRY = 12 };
+       NXSDG_OPT_V_ROW_CARRY = 12, NXSDG_OPT_MULTIRANK_GRAPH = 13 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */
@@ -218,8 +225,10 @@ nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* ctx, double t);
  * (ny+1) x (nx+1) x 2 doubles row-major (count = 2 (nx+1)(ny+1)); elements map bilinearly from their
  * four vertices.  In this mode the stress step (Listing 2) uses per-element inverse
  * maps per NXSDG_OPT_MAP_MODE, every nxsdg_run_step step and nxsdg_advect (closed box) run the
- * general-geometry kernels, and nxsdg_mevp_substeps requires NXSDG_UNFUSED (the fused kernels are
- * box-specialised: UNSUPPORTED otherwise).  Single rank only. */
+ * general-geometry kernels, and nxsdg_mevp_substeps runs the fused general-quad subcycle kernel
+ * (geometry recomputed on the fly from the vertices; CG2/DG2 with n_S = 6) or, with NXSDG_UNFUSED, the
+ * unfused general-geometry steps.  Fused subcycles with CG1 or n_S = 8 on a general mesh return
+ * UNSUPPORTED (use NXSDG_UNFUSED).  Single rank only. */
 nxsdg_status nxsdg_set_vertices(nxsdg_ctx* ctx, const double* xy, int64_t count, nxsdg_mem mem);
 
 /* ---- compute ----------------------------------------------------------------- */
@@ -243,10 +252,11 @@ nxsdg_status nxsdg_stream_join(nxsdg_ctx* ctx);
 nxsdg_status nxsdg_nccl_unique_id(void* out128);
 /* P2P transport (SURVEY §8(e) "device-initiated peer stores").  Each halo exchange
  * copies the halo plan's send rows with the copy engine directly into the receive rows of the
- * neighbour's buffers (one 2D copy per message, no staging, no NCCL), then writes the exchange
- * number into the neighbour's flag word (cuStreamWriteValue32, fenced) and makes the context
- * stream wait on the device until both neighbours have written it into ours
- * (cuStreamWaitValue32 >=).  The host never blocks.
+ * neighbour's buffers (one 2D copy per message, no staging, no NCCL), then sets its word of flag
+ * slot (k & 1) in each neighbour to 1 (cuStreamWriteValue32, fenced) and makes the context stream
+ * wait on the device until both neighbours have set ours (cuStreamWaitValue32 ==, with
+ * CU_STREAM_WAIT_VALUE_FLUSH where the device can flush remote writes), then clears it.  Constant
+ * values: the exchange replays inside CUDA graphs.  The host never blocks.
  * nxsdg_p2p_export: an opaque blob (*needed bytes; blob == NULL: size only) with CUDA IPC handles
  *   of this rank's exchanged buffers and flag pair; give it to ranks r-1 and r+1 (e.g. with
  *   torch.distributed all_gather_object).  STATE unless the context uses NXSDG_TRANSPORT_P2P.
@@ -298,6 +308,12 @@ int64_t nxsdg_kernel_launches(const nxsdg_ctx* ctx);
 double nxsdg_bytes_per_element_subcycle(const nxsdg_ctx* ctx);
 /* cudaStream_t the context runs on. */
 void* nxsdg_stream(const nxsdg_ctx* ctx);
+/* One line describing this rank's transport (for the bench's per-rank line): rank, device, transport,
+ * P2P neighbours (device, IPC or in-process), whether the P2P waits flush remote writes, whether the
+ * fused peer stores and the multi-rank subcycle graph are in use (and why not, if capture was refused).
+ * Writes at most cap bytes including the terminating NUL into buf (truncating); returns the full
+ * length (excluding NUL), or -1 for a NULL context. */
+int64_t nxsdg_transport_info(const nxsdg_ctx* ctx, char* buf, int64_t cap);
 
 #ifdef __cplusplus
 }

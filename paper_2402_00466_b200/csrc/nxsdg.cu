@@ -150,14 +150,18 @@ struct nxsdg_ctx {
     // scratch buffers, identically on every rank, so a field's current allocation has the same
     // index on both sides), this rank's two flag words and the neighbours' mapped buffers
     double* orig[kP2PBufs] = {};
-    uint32_t* flags = nullptr;       // [0] written by the lower neighbour, [1] by the upper one
+    uint32_t* flags = nullptr;       // [slot][side]: [2k] written by the lower neighbour, [2k+1] by the upper one
     struct Peer { bool on = false, ipc = false; double* buf[kP2PBufs] = {}; uint32_t* flags = nullptr; Geom g{}; } peer[2];
-    uint32_t p2p_seq = 0;
+    uint32_t p2p_seq = 0;            // P2P exchanges so far; exchange k uses flag slot k & 1
+    unsigned p2p_wait_flags = 0;     // CU_STREAM_WAIT_VALUE_FLUSH where the device can flush remote writes
     bool p2p_ok = false;
+    int mr_graph = 1;                // NXSDG_OPT_MULTIRANK_GRAPH
     int p2p_fused = 1;               // NXSDG_OPT_P2P_FUSED_STORES
     int limiter = 0;                 // NXSDG_OPT_LIMITER (NEXT-4, R#25)
-    // graphs: key = (n_sub, cv, cs)
-    std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+    // graphs: key = (n_sub, cv, cs + 2 precision + 8 P2P-slot parity + 16 multi-rank)
+    struct Graph { cudaGraphExec_t exec; int64_t launches; };
+    std::map<std::tuple<int, int, int>, Graph> graphs;
+    std::string mr_graph_note;       // why multi-rank capture was given up (empty = in use)
 };
 
 static nxsdg_status fail(nxsdg_ctx* c, nxsdg_status s, const char* fmt, ...) {
@@ -226,7 +230,7 @@ static nxsdg_status alloc(nxsdg_ctx* c, double** p, size_t n) {
 static void drop_graphs(nxsdg_ctx* c) {
     if (c->graphs.empty()) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
     c->graphs.clear();
 }
 
@@ -326,8 +330,8 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
         std::copy(o, o + kP2PBufs, c->orig);
     }
     if (d->nranks > 1 && d->transport == NXSDG_TRANSPORT_P2P) {
-        if (cudaMalloc(&c->flags, 2 * sizeof(uint32_t)) != cudaSuccess) return bail(NXSDG_ERR_OOM);
-        if (cudaMemset(c->flags, 0, 2 * sizeof(uint32_t)) != cudaSuccess) return bail(NXSDG_ERR_CUDA);
+        if (cudaMalloc(&c->flags, 4 * sizeof(uint32_t)) != cudaSuccess) return bail(NXSDG_ERR_OOM);
+        if (cudaMemset(c->flags, 0, 4 * sizeof(uint32_t)) != cudaSuccess) return bail(NXSDG_ERR_CUDA);
     }
 #undef AL
     // K0: reference-element tables into __constant__ (all three spaces; tiny)
@@ -452,6 +456,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_CONST_STAGING:
             if (value < -1 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "node-constant staging -1|0|1|2");
             c->const_regs = (int)value; break;
+        case NXSDG_OPT_MULTIRANK_GRAPH:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "multi-rank graph 0|1");
+            c->mr_graph = (int)value; break;
         default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
     }
     drop_graphs(c);
@@ -1020,14 +1027,20 @@ static nxsdg_status halo_loopback_all(std::vector<nxsdg_ctx*>& ctxs, uint32_t wh
 // ---- P2P transport (NXSDG_TRANSPORT_P2P): no NCCL, no staging.  Every send segment of the halo
 // plan is copied by the copy engine straight from this rank's buffer into the matching receive
 // rows of the neighbour's buffer (peer memory over NVLink / NVSwitch: a CUDA IPC mapping across
-// processes, a plain device pointer inside one process), then this rank bumps its word in each
-// neighbour's flag pair (cuStreamWriteValue32, fenced) and its stream waits, on the device, until
-// both neighbours have bumped its own pair to the same exchange number (cuStreamWaitValue32 GEQ).
-// Every rank issues the same sequence of halo calls, so exchange numbers match.  Race freedom:
-// an exchange writes only ghost rows of the buffer the preceding kernel produced, which no kernel
-// of the receiver reads before the receiver's own wait for this exchange; and the sender can only
-// reach its next exchange after waiting for the receiver's signal of this one, which the receiver
-// issues after the kernels that read the previous contents of those ghost rows.
+// processes, a plain device pointer inside one process), then this rank sets its word of slot
+// k & 1 in each neighbour's flags to 1 (cuStreamWriteValue32, which fences the copies and kernel
+// peer stores before it), and its stream waits, on the device, until both neighbours have set its
+// own slot-(k & 1) words to 1 (cuStreamWaitValue32 EQ, with CU_STREAM_WAIT_VALUE_FLUSH where the
+// device supports it, so remote writes that arrived before the flag are visible to the work after
+// the wait even if the device reordered them), then clears them.  Every value is a constant, so
+// the exchange can be captured in a CUDA graph and replayed (the multi-rank subcycle graphs).
+// Every rank issues the same sequence of halo calls, so slots match.  A sender sets slot s again
+// (exchange k + 2) only after waiting for the receiver's exchange-(k + 1) signal, which the receiver
+// writes after clearing slot s (stream order + the write's fence), so no signal is lost.  Race
+// freedom: an exchange writes only ghost rows of the buffer the preceding kernel produced, which
+// no kernel of the receiver reads before the receiver's own wait for this exchange; and the sender
+// can only reach its next exchange after waiting for the receiver's signal of this one, which the
+// receiver issues after the kernels that read the previous contents of those ghost rows.
 typedef CUresult (*PFN_sv32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 struct MemOps { PFN_sv32 write = nullptr, wait = nullptr; };
 static MemOps& memops() {
@@ -1074,13 +1087,19 @@ static nxsdg_status halo_p2p(nxsdg_ctx* c, uint32_t what, cudaStream_t st) {
         nxsdg_status s = copy2d(c, pr.buf[bi] + rv->off0, rv->stride, base + m.off0, m.stride, m.count, m.nseg, st);
         if (s) return s;
     }
-    const uint32_t seq = ++c->p2p_seq;
+    const int slot = (int)(c->p2p_seq++ & 1u) * 2;
     for (int sd = 0; sd < 2; ++sd)   // I am my lower neighbour's upper one (word 1) and vice versa
-        if (c->peer[sd].on && mo.write((CUstream)st, (CUdeviceptr)(c->peer[sd].flags + (sd == 0 ? 1 : 0)), seq, 0) != CUDA_SUCCESS)
+        if (c->peer[sd].on &&
+            mo.write((CUstream)st, (CUdeviceptr)(c->peer[sd].flags + slot + (sd == 0 ? 1 : 0)), 1u, 0) != CUDA_SUCCESS)
             return fail(c, NXSDG_ERR_CUDA, "cuStreamWriteValue32 failed");
-    for (int sd = 0; sd < 2; ++sd)
-        if (c->peer[sd].on && mo.wait((CUstream)st, (CUdeviceptr)(c->flags + sd), seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    for (int sd = 0; sd < 2; ++sd) {
+        if (!c->peer[sd].on) continue;
+        if (mo.wait((CUstream)st, (CUdeviceptr)(c->flags + slot + sd), 1u, CU_STREAM_WAIT_VALUE_EQ | c->p2p_wait_flags) !=
+            CUDA_SUCCESS)
             return fail(c, NXSDG_ERR_CUDA, "cuStreamWaitValue32 failed");
+        if (mo.write((CUstream)st, (CUdeviceptr)(c->flags + slot + sd), 0u, 0) != CUDA_SUCCESS)
+            return fail(c, NXSDG_ERR_CUDA, "cuStreamWriteValue32 (clear) failed");
+    }
     return NXSDG_OK;
 }
 
@@ -1131,6 +1150,12 @@ static void p2p_finish_connect(nxsdg_ctx* c) {
     for (int sd = 0; sd < 2; ++sd)
         if (c->peer[sd].on)
             c->peer[sd].g = make_geom(c->d.nx, c->d.ny, c->P, c->NS, c->NA, c->d.nranks, c->d.rank + (sd == 0 ? -1 : 1));
+    int can_flush = 0;
+    if (cudaDeviceGetAttribute(&can_flush, cudaDevAttrCanFlushRemoteWrites, c->d.device) != cudaSuccess) {
+        cudaGetLastError();
+        can_flush = 0;
+    }
+    c->p2p_wait_flags = can_flush ? (unsigned)CU_STREAM_WAIT_VALUE_FLUSH : 0u;
     c->p2p_ok = ok;
 }
 
@@ -1168,6 +1193,33 @@ extern "C" nxsdg_status nxsdg_p2p_connect(nxsdg_ctx* c, const void* lower, const
     }
     p2p_finish_connect(c);
     return NXSDG_OK;
+}
+
+static bool p2p_fused_stores(const nxsdg_ctx* c);
+extern "C" int64_t nxsdg_transport_info(const nxsdg_ctx* c, char* buf, int64_t cap) {
+    if (!c) return -1;
+    static const char* names[] = {"none", "nccl", "loopback", "p2p"};
+    const int t = c->d.transport >= 0 && c->d.transport < 4 ? c->d.transport : 0;
+    std::string s = "rank " + std::to_string(c->d.rank) + "/" + std::to_string(c->d.nranks) + " device " +
+                    std::to_string(c->d.device) + " transport " + names[t];
+    if (c->d.transport == NXSDG_TRANSPORT_P2P) {
+        for (int sd = 0; sd < 2; ++sd) {
+            s += sd == 0 ? " lower:" : " upper:";
+            if (!c->peer[sd].on) { s += "none"; continue; }
+            s += c->peer[sd].ipc ? "ipc" : "in-process";
+        }
+        s += std::string(" wait_flush=") + (c->p2p_wait_flags ? "1" : "0");
+        s += std::string(" fused_peer_stores=") + (p2p_fused_stores(c) ? "1" : "0");
+    }
+    if (c->d.nranks > 1)
+        s += std::string(" subcycle_graph=") + (c->mr_graph && c->mr_graph_note.empty() ? "1" : "0") +
+             (c->mr_graph_note.empty() ? "" : " (" + c->mr_graph_note + ")");
+    if (buf && cap > 0) {
+        const size_t n = std::min<size_t>(s.size(), (size_t)cap - 1);
+        memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return (int64_t)s.size();
 }
 
 extern "C" nxsdg_status nxsdg_p2p_connect_local(nxsdg_ctx** ctxs, int32_t n) {
@@ -1449,14 +1501,18 @@ static nxsdg_status build_gen_maps(nxsdg_ctx* c) {
     return NXSDG_OK;
 }
 
+// per-device "function attribute already set" flags (ordinals >= 64 set the attribute on every launch)
+static inline bool dev_bit_test(uint64_t m, int dev) { return dev >= 0 && dev < 64 && ((m >> dev) & 1u); }
+static inline void dev_bit_set(uint64_t& m, int dev) { if (dev >= 0 && dev < 64) m |= uint64_t(1) << dev; }
+
 template <bool R, int ST, bool LC = false>
 static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     const size_t smem = (size_t)K2_WARPS * ST *
                         (sizeof(typename K2GenStageSel<LC>::T) + 2 * sizeof(uint64_t) + sizeof(int4));
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr_set = 0;   // the attribute is per device: one bit per ordinal
+    if (!dev_bit_test(attr_set, c->d.device)) {
         CU(cudaFuncSetAttribute(k_subcycle_gen<R, ST, LC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        dev_bit_set(attr_set, c->d.device);
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
@@ -1478,11 +1534,11 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
     using Stage = typename K2StageSel<SF, NS, CL || LC>::T;
     const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + 2 * sizeof(uint64_t) + sizeof(int4));
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr_set = 0;   // the attribute is per device: one bit per ordinal
+    if (!dev_bit_test(attr_set, c->d.device)) {
         CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-        attr = true;
+        dev_bit_set(attr_set, c->d.device);
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
@@ -1522,6 +1578,9 @@ static nxsdg_status launch_tma_sel(nxsdg_ctx* c, int cv, int cs, const SubArgs& 
 
 static nxsdg_status ensure_counters(nxsdg_ctx* c, int n) {
     if (c->ncounters >= n) return NXSDG_OK;
+    // cached graphs captured the old buffer (memset node + kernel argument): drop them (this waits
+    // for any replay still in flight) before the buffer goes away
+    drop_graphs(c);
     if (c->counters) cudaFree(c->counters);
     c->counters = nullptr; c->ncounters = 0;
     CU(cudaMalloc(&c->counters, sizeof(int) * (size_t)std::max(n, 128)));
@@ -1571,10 +1630,11 @@ static nxsdg_status launch_tma(nxsdg_ctx* c, int cv, int cs, int slot = -1, int 
     return launch_tma_sel<double>(c, cv, cs, a);
 }
 
-// One fused subcycle launch over the selected chunks (no ping-pong flip).
-static nxsdg_status launch_subcycle_sel(nxsdg_ctx* c, int sel) {
+// One fused subcycle launch over the selected chunks (no ping-pong flip); slot: the launch's work
+// counter inside a graph (-1: direct launch, the counter is zeroed first).
+static nxsdg_status launch_subcycle_sel(nxsdg_ctx* c, int sel, int slot = -1) {
     if (use_tma(c)) {
-        nxsdg_status st = launch_tma(c, c->cv, c->cs, -1, sel);
+        nxsdg_status st = launch_tma(c, c->cv, c->cs, slot, sel);
         if (st) return st;
     } else {
         SubArgs a = sub_args(c, c->cv, c->cs);
@@ -1590,35 +1650,41 @@ static nxsdg_status launch_subcycle_sel(nxsdg_ctx* c, int sel) {
     return NXSDG_OK;
 }
 
-static nxsdg_status launch_subcycle(nxsdg_ctx* c) {
-    nxsdg_status st = launch_subcycle_sel(c, SEL_ALL);
+static nxsdg_status launch_subcycle(nxsdg_ctx* c, int slot = -1) {
+    nxsdg_status st = launch_subcycle_sel(c, SEL_ALL, slot);
     if (st) return st;
     c->cv ^= 1; c->cs ^= 1;
     return NXSDG_OK;
 }
 
-// Multi-rank NCCL subcycle with overlap: boundary chunks (first and last
-// chunk rows, which produce every row a neighbour needs) -> event -> halo exchange on the
-// halo stream, concurrently the interior chunks on the main stream -> join.
-static nxsdg_status subcycle_overlapped(nxsdg_ctx* c) {
-    nxsdg_status st;
-    if (n_chunks(c) < 3) {
-        if ((st = launch_subcycle(c))) return st;
-        return halo(c, p2p_fused_stores(c) ? 0u : (uint32_t)(NXSDG_HALO_V | NXSDG_HALO_S));
-    }
+static nxsdg_status ensure_halo_stream(nxsdg_ctx* c) {
     if (!c->hstream) {
         CU(cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
     }
-    if ((st = launch_subcycle_sel(c, SEL_BOUNDARY))) return st;
+    return NXSDG_OK;
+}
+
+// Multi-rank subcycle with overlap: boundary chunks (first and last chunk rows,
+// which produce every row a neighbour needs) -> event -> halo exchange on the halo stream,
+// concurrently the interior chunks on the main stream -> join.  Exactly one exchange per subcycle.
+// slot0 >= 0: inside a graph capture, the launches use work-counter slots slot0, slot0 + 1.
+static nxsdg_status subcycle_overlapped(nxsdg_ctx* c, int slot0 = -1) {
+    nxsdg_status st;
+    if (n_chunks(c) < 3) {
+        if ((st = launch_subcycle(c, slot0))) return st;
+        return halo(c, p2p_fused_stores(c) ? 0u : (uint32_t)(NXSDG_HALO_V | NXSDG_HALO_S));
+    }
+    if ((st = ensure_halo_stream(c))) return st;
+    if ((st = launch_subcycle_sel(c, SEL_BOUNDARY, slot0))) return st;
     c->cv ^= 1; c->cs ^= 1;                      // the exchange moves rows of the new state
     CU(cudaEventRecord(c->ev_bnd, c->stream));
     CU(cudaStreamWaitEvent(c->hstream, c->ev_bnd, 0));
     if ((st = halo_on(c, p2p_fused_stores(c) ? 0u : (uint32_t)(NXSDG_HALO_V | NXSDG_HALO_S), c->hstream))) return st;
     CU(cudaEventRecord(c->ev_x, c->hstream));
     c->cv ^= 1; c->cs ^= 1;                      // interior reads the old state
-    if ((st = launch_subcycle_sel(c, SEL_INTERIOR))) return st;
+    if ((st = launch_subcycle_sel(c, SEL_INTERIOR, slot0 < 0 ? -1 : slot0 + 1))) return st;
     c->cv ^= 1; c->cs ^= 1;
     CU(cudaStreamWaitEvent(c->stream, c->ev_x, 0));
     return NXSDG_OK;
@@ -1728,7 +1794,16 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
         }
         CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         int cv = c->cv, cs = c->cs;
-        if (use_tma(c)) CU(cudaMemsetAsync(c->counters, 0, sizeof(int) * (size_t)n, c->stream));
+        if (use_tma(c)) {
+            cudaError_t me = cudaMemsetAsync(c->counters, 0, sizeof(int) * (size_t)n, c->stream);
+            if (me != cudaSuccess) {   // end (and discard) the capture so the stream stays usable
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(c->stream, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                cudaGetLastError();
+                return fail(c, NXSDG_ERR_CUDA, "graph capture memset: %s", cudaGetErrorString(me));
+            }
+        }
         for (int i = 0; i < n; ++i) {
             if (use_tma(c)) {
                 nxsdg_status st = launch_tma(c, cv, cs, i);
@@ -1749,11 +1824,67 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
         e = cudaGraphInstantiate(&ge, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-        it = c->graphs.emplace(key, ge).first;
+        it = c->graphs.emplace(key, nxsdg_ctx::Graph{ge, n}).first;
     }
-    CU(cudaGraphLaunch(it->second, c->stream));
-    c->launches += n;
+    CU(cudaGraphLaunch(it->second.exec, c->stream));
+    c->launches += it->second.launches;
     if (n & 1) { c->cv ^= 1; c->cs ^= 1; }
+    return NXSDG_OK;
+}
+
+// Multi-rank (P2P / NCCL row strips): capture n overlapped subcycles - boundary launch, exchange on
+// the halo stream (fused peer stores + flag handshake, copy-engine peer copies, or NCCL send/recv),
+// interior launch, join - in one CUDA graph and replay it: one host crossing per call instead of
+// ~8 API calls per subcycle.  The P2P handshake uses constant flag values (halo_p2p), so replays
+// are exact; the graph is keyed by the ping-pong parities and the P2P slot parity it starts from.
+// Returns NXSDG_ERR_UNSUPPORTED (state unchanged) if the capture itself is refused, so the caller can
+// issue the subcycles from the host instead.
+static nxsdg_status run_graph_multirank(nxsdg_ctx* c, int n) {
+    const int par = (int)(c->p2p_seq & 1u);
+    auto key = std::make_tuple(n, c->cv, c->cs + 8 * par + 16);
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        nxsdg_status st;
+        if (use_tma(c) && (st = build_maps(c))) return st;
+        if ((st = ensure_counters(c, 2 * n))) return st;
+        if ((st = ensure_halo_stream(c))) return st;
+        if (c->d.transport == NXSDG_TRANSPORT_NCCL && (st = ensure_halo_staging(c))) return st;
+        const int cv0 = c->cv, cs0 = c->cs;
+        const uint32_t seq0 = c->p2p_seq;
+        const int64_t l0 = c->launches;
+        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        cudaError_t me = use_tma(c) ? cudaMemsetAsync(c->counters, 0, sizeof(int) * (size_t)(2 * n), c->stream)
+                                    : cudaSuccess;
+        st = me == cudaSuccess ? NXSDG_OK : NXSDG_ERR_CUDA;
+        for (int i = 0; i < n && !st; ++i) st = subcycle_overlapped(c, 2 * i);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        const int64_t nl = c->launches - l0;
+        c->cv = cv0; c->cs = cs0; c->p2p_seq = seq0; c->launches = l0;   // nothing ran yet
+        if (st || e != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            c->mr_graph_note = st ? c->err : std::string("capture: ") + cudaGetErrorString(e);
+            // an API call refused inside the capture is not a device fault: un-poison; the host-issued
+            // fallback reports any real error again
+            c->err.clear();
+            c->poisoned = false;
+            return NXSDG_ERR_UNSUPPORTED;
+        }
+        cudaGraphExec_t ge;
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            c->mr_graph_note = std::string("instantiate: ") + cudaGetErrorString(e);
+            return NXSDG_ERR_UNSUPPORTED;
+        }
+        it = c->graphs.emplace(key, nxsdg_ctx::Graph{ge, nl}).first;
+    }
+    CU(cudaGraphLaunch(it->second.exec, c->stream));
+    c->launches += it->second.launches;
+    if (n & 1) { c->cv ^= 1; c->cs ^= 1; }
+    if (c->d.transport == NXSDG_TRANSPORT_P2P) c->p2p_seq += (uint32_t)n;
     return NXSDG_OK;
 }
 
@@ -1778,6 +1909,11 @@ extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t fl
         return cvt(c, c->S32[c->cs], c->S[c->cs], nS);
     }
     if (!unfused && c->d.nranks == 1 && n > 0) return run_graph(c, n);
+    if (!unfused && c->d.nranks > 1 && n > 0 && c->mr_graph && c->mr_graph_note.empty() && c->precision == 0 &&
+        c->d.transport != NXSDG_TRANSPORT_LOOPBACK) {
+        s = run_graph_multirank(c, n);
+        if (s != NXSDG_ERR_UNSUPPORTED) return s;   // else: capture refused (noted), issue from the host
+    }
     for (int i = 0; i < n; ++i)
         if ((s = one_subcycle(c, unfused))) return s;
     return NXSDG_OK;

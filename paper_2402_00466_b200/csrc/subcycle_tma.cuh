@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstddef>
 #include <cstdio>
 
 namespace nxk {
@@ -329,12 +330,18 @@ __device__ __forceinline__ void div_t(const double (&S)[NS], double h, double r[
 
 // ---------------------------------------------------------------- the kernel
 // LC = true (with CL = false, FP64 storage): the constants are not staged with the job; once the stress
-// update has read S and P_g, lane 0 TMA-loads them into the stage's S region (>= 5952 B for FP64) on a
-// second mbarrier, and the velocity update waits for it - small stages without CL's 24 live registers.
+// update has read S and P_g, lane 0 TMA-loads them (5952 B) into the stage from the start of its S region
+// on a second mbarrier, and the velocity update waits for it - small stages without CL's 24 live
+// registers.  For n_S = 6 the S region is 4896 B, so the constants also overwrite the start of P_g; both
+// regions have been consumed by then (the static_assert below keeps them clear of the v rows, which the
+// divergence / velocity still read).
 template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
     static_assert(!(CL && LC), "one node-constant mode");
     static_assert(!LC || sizeof(SF) == 8, "late constants need the FP64 S region");
+    using StageNC_ = K2StageNC<SF, NS>;
+    static_assert(!LC || offsetof(StageNC_, vx) >= 6 * 2 * K2_CCOLS * sizeof(double),
+                  "late constants overwrite only the consumed S / P_g regions");
     constexpr bool NOBOX = CL || LC;
     using Stage = typename K2StageSel<SF, NS, NOBOX>::T;
     constexpr int AL = K2Cols<SF>::ALIGN;

@@ -30,7 +30,8 @@ BEGIN_STEP, UNFUSED = 1, 2
 STEPS = {"strain": 0, "stress": 1, "divergence": 2, "velocity": 3}
 TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_P2P = 0, 1, 2, 3
 (OPT_FUSED_KERNEL, OPT_CHUNK_ROWS, OPT_CTAS_PER_SM, OPT_STAGES, OPT_DYNAMIC, OPT_MAP_MODE, OPT_PRECISION,
- OPT_P2P_FUSED_STORES, OPT_LIMITER, OPT_CONST_STAGING, OPT_TAIL_SPLIT, OPT_L2_POLICY, OPT_V_ROW_CARRY) = range(13)
+ OPT_P2P_FUSED_STORES, OPT_LIMITER, OPT_CONST_STAGING, OPT_TAIL_SPLIT, OPT_L2_POLICY, OPT_V_ROW_CARRY,
+ OPT_MULTIRANK_GRAPH) = range(14)
 
 
 class NxsdgError(RuntimeError):
@@ -92,6 +93,7 @@ def _load() -> C.CDLL:
         "nxsdg_p2p_export": ([vp, vp, i64, C.POINTER(i64)], i32),
         "nxsdg_p2p_connect": ([vp, vp, vp], i32),
         "nxsdg_p2p_connect_local": ([C.POINTER(vp), i32], i32),
+        "nxsdg_transport_info": ([vp, C.c_char_p, i64], i64),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -109,6 +111,7 @@ EXPORTED = [
     "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option", "nxsdg_halo_plan",
     "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone", "nxsdg_set_vertices", "nxsdg_stream_join",
     "nxsdg_debug_reference_tables", "nxsdg_p2p_export", "nxsdg_p2p_connect", "nxsdg_p2p_connect_local",
+    "nxsdg_transport_info",
 ]
 HALO_V, HALO_S, HALO_AH, HALO_AH_SCR0, HALO_AH_SCR1 = 1, 2, 4, 8, 16
 HF_VX, HF_VY, HF_S, HF_A, HF_H, HF_A_SCR0, HF_H_SCR0, HF_A_SCR1, HF_H_SCR1 = range(9)
@@ -246,6 +249,12 @@ class Mesh:
     @property
     def bytes_per_element_subcycle(self) -> float:
         return float(lib.nxsdg_bytes_per_element_subcycle(self.h))
+
+    @property
+    def transport_info(self) -> str:
+        buf = C.create_string_buffer(512)
+        lib.nxsdg_transport_info(self.h, buf, len(buf))
+        return buf.value.decode()
 
     def set_option(self, option: int, value: int):
         _chk(self.h, lib.nxsdg_set_option(self.h, int(option), int(value)), "set_option")

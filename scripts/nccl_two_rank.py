@@ -26,6 +26,7 @@ dist.broadcast(t, 0)
 m = nxsdg.Mesh(nxe, nye, lx, ly, rank=rank, nranks=world, transport=nxsdg.TRANSPORT_NCCL,
                nccl_id=bytes(t.numpy()), device=0)
 m.set_option(nxsdg.OPT_CHUNK_ROWS, ty)
+m.set_option(nxsdg.OPT_MULTIRANK_GRAPH, int(os.environ.get("MR_GRAPH", "1")))
 er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
 loc = {k: np.ascontiguousarray(st[k][nr0:nr0 + nrn]) for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
 for k in ("S11", "S12", "S22", "A", "H"):
@@ -33,9 +34,11 @@ for k in ("S11", "S12", "S22", "A", "H"):
 m.load(loc)
 m.advect(prm.dt)
 m.mevp_substeps(7, begin_step=True)
+m.mevp_substeps(4, begin_step=False)
 m.mevp_substeps(3, begin_step=False, unfused=True)
 m.synchronize()
 mine = m.state()
+info = m.transport_info
 parts = [None] * world
 dist.all_gather_object(parts, mine)
 m.destroy()
@@ -43,8 +46,15 @@ if rank == 0:
     got = {k: np.concatenate([p[k] for p in parts]) for k in mine}
     with nxsdg.Mesh(nxe, nye, lx, ly) as ref:
         ref.load(st); ref.advect(prm.dt); ref.mevp_substeps(7, begin_step=True)
-        ref.mevp_substeps(3, begin_step=False, unfused=True)
+        ref.mevp_substeps(4, begin_step=False); ref.mevp_substeps(3, begin_step=False, unfused=True)
         want = ref.state()
+    # the gathered strips against the oracle (advection + 14 subcycles, SURVEY §8(c).5 bar)
+    import oracle
+    ns_ = want["S11"].shape[1]
+    ora = oracle.Oracle().outer_step(oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=2, ns=ns_, na=6), oracle.Params(), 14, st)
+    oerr = max(max(float(np.abs(got[k] - ora[k]).max()) for k in g) / max(float(np.abs(ora[k]).max()) for k in g)
+               for g in (("S11", "S12", "S22"), ("vx", "vy"), ("A",), ("H",)))
     bad = {k: float(np.abs(got[k] - want[k]).max()) for k in want if not np.array_equal(got[k], want[k])}
-    print(json.dumps({"nccl_ranks": world, "chunk_rows": ty, "bitwise_equal": not bad, "max_diff": bad}), flush=True)
+    print(json.dumps({"nccl_ranks": world, "chunk_rows": ty, "bitwise_equal": not bad, "max_diff": bad,
+                      "oracle_err": oerr, "transport": info}), flush=True)
     sys.exit(0 if not bad else 3)

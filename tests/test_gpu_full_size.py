@@ -1,15 +1,29 @@
-"""Full-size parity at BASELINE.json's bench configuration (C4: 4096 x 4096 CG2/DG2,
-one outer step = advection + BEGIN_STEP prep + 100 fused subcycles, exactly the launch
-configuration bench.py times), checked against the oracle on windows; the same for the n_S = 8
-space and for a distorted C4 mesh through the fused general-quad kernel.
+"""Full-size parity at BASELINE.json's configurations, each at its full count, checked against the
+oracle on windows (the paper's "comparing to the CPU version" protocol):
 
-Light cone: one subcycle moves information by at most one element
-(node v -> adjacent elements' strain/stress -> their nodes), each RK stage of the
-advection by one element, the prep's nodal means by one.  So the oracle run on a
-window padded by a ring of n_sub + 3 + 2 elements, with the window's own (wrong)
-boundary conditions on the ring's outside, reproduces the global solution exactly
-in the window's centre.  Windows: the four domain corners (the true boundary is
-inside them), the cyclone centre, and seeded random positions."""
+- C4 (4096^2 CG2/DG2, 125 m): one outer step = advection + BEGIN_STEP prep + 100 fused subcycles,
+  exactly the launch configuration bench.py times ("box"); the same for the n_S = 8 space ("ns8") and
+  for a distorted C4 mesh through the fused general-quad kernel ("general");
+- C4 as 8 row strips of 4096 x 512 (the 8-GPU partition), 8 P2P ranks in one process, each on its own
+  stream, fused peer stores + device flag handshake, the multi-rank subcycle graph ("strips8"):
+  windows centred on each of the 7 strip interfaces against the oracle, and the gathered strips
+  bitwise equal to one context;
+- C3 (2048^2, 250 m) and C5 (8192^2, 62.5 m, the weak-scaling per-GPU size), advection + 100.
+
+Light cone: one subcycle moves information by at most one element (node v -> adjacent
+elements' strain/stress -> their nodes), each RK stage of the advection by one element, the prep's
+nodal means by one.  So the oracle run on a window padded by a ring of n_sub + 3 + 2 elements, with
+the window's own (wrong) boundary conditions on the ring's outside, reproduces the global solution
+exactly in the window's centre.  Windows: the four domain corners (the true boundary is inside them),
+the cyclone centre, seeded random positions; for the strips, the interfaces.
+
+Bar (north_star): relative max-norm error <= 1e-10 on S and v (fields and increments) after the full
+count, <= 1e-12 on the A, H fields.  Unconditional, except for the n_S = 8 space at 125 m, where the
+oracle's own plain and FMA builds already differ by 0.9e-10 ... 2.5e-10 after 100 subcycles
+(DESIGN.md §4): there the bar is max(1e-10, 4 x that floor), computed per window.  Every window's
+errors are printed (they appear in the -m gpu log)."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -18,26 +32,42 @@ from paper_2402_00466_b200 import inputs
 from tests.parity import group_err
 
 pytestmark = pytest.mark.gpu
+CORE = 12
+PARAMS = ["box", "ns8", "general", "strips8", "C3", "C5"]
 
 
-@pytest.fixture(scope="module", params=["box", "ns8", "general"])
-def c4_result(request):
-    """box: the bench path (k_subcycle_tma, n_S = 6).  ns8: the n_S = 8 space (NEXT-4).  general: the
-    C4 mesh with interior vertices moved by up to 0.25 h / 2 and the fused general-quad kernel
-    (NEXT-1, k_subcycle_gen).  Each: advection + prep + 100 fused subcycles at full size."""
-    import dataclasses
+def _cfg(kind):
+    if kind == "C3":
+        return inputs.CONFIGS["C3"]
+    if kind == "C5":
+        return inputs.CONFIGS["C5"]
+    cfg = inputs.CONFIGS["C4"]
+    return dataclasses.replace(cfg, ns=8) if kind == "ns8" else cfg
+
+
+def _load_local(m, st, nxe):
+    er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
+    loc = {k: np.ascontiguousarray(st[k][nr0:nr0 + nrn]) for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
+    for k in ("S11", "S12", "S22", "A", "H"):
+        loc[k] = np.ascontiguousarray(st[k][er0 * nxe:(er0 + ern) * nxe])
+    m.load(loc)
+
+
+@pytest.fixture(scope="module", params=PARAMS)
+def full_result(request):
+    """Each: advection + prep + 100 fused subcycles at full size through the C ABI."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2402_00466_b200 import build
     build.build()
     from paper_2402_00466_b200 import nxsdg
-    cfg = inputs.CONFIGS["C4"]
-    if request.param == "ns8":
-        cfg = dataclasses.replace(cfg, ns=8)
+    kind = request.param
+    cfg = _cfg(kind)
     st = inputs.make_config_case(cfg)
-    V = inputs.distorted_vertices(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 0.25) if request.param == "general" else None
+    V = inputs.distorted_vertices(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 0.25) if kind == "general" else None
     prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
+    extra = {}
     with nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm) as m:
         if V is not None:
             m.set_vertices(V)
@@ -45,7 +75,27 @@ def c4_result(request):
         m.advect(prm.dt)
         m.mevp_substeps(cfg.nsub, begin_step=True)
         got = m.state()
-    return cfg, st, got, V
+    if kind == "strips8":
+        nr = 8
+        ms = [nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, rank=r, nranks=nr,
+                         transport=nxsdg.TRANSPORT_P2P) for r in range(nr)]
+        nxsdg.p2p_connect_local(ms)
+        for m in ms:
+            _load_local(m, st, cfg.nx)
+        for m in ms:
+            m.advect(prm.dt)
+        for m in ms:
+            m.mevp_substeps(cfg.nsub, begin_step=True)
+        for m in ms:
+            m.synchronize()
+        extra["info"] = [m.transport_info for m in ms]
+        strips = {k: np.concatenate([m.read_state(k) for m in ms]) for k in got}
+        extra["row0"] = [m.elem_row0 for m in ms]
+        for m in ms:
+            m.destroy()
+        extra["single"] = got
+        got = strips
+    return kind, cfg, st, got, V, extra
 
 
 def _cut(cfg, arrs, ix0, iy0, w, h):
@@ -60,41 +110,27 @@ def _cut(cfg, arrs, ix0, iy0, w, h):
     return out
 
 
-def _windows(cfg, core=12):
+def _windows(kind, cfg, extra):
     rng = np.random.default_rng(inputs.SEED_BASE + 4)
     nx, ny = cfg.nx, cfg.ny
-    ws = [(0, 0), (nx - core, 0), (0, ny - core), (nx - core, ny - core), (nx // 2 - core // 2, ny // 2 - core // 2)]
-    ws += [(int(rng.integers(0, nx - core)), int(rng.integers(0, ny - core))) for _ in range(3)]
+    if kind == "strips8":   # centred on each strip interface (element row r0 of ranks 1..7)
+        return [(int(rng.integers(0, nx - CORE)), r0 - CORE // 2) for r0 in extra["row0"][1:]]
+    ws = [(0, 0), (nx - CORE, 0), (0, ny - CORE), (nx - CORE, ny - CORE), (nx // 2 - CORE // 2, ny // 2 - CORE // 2)]
+    ws += [(int(rng.integers(0, nx - CORE)), int(rng.integers(0, ny - CORE))) for _ in range(3)]
     return ws
 
 
-@pytest.mark.parametrize("wi", range(8))
-def test_c4_window_parity(c4_result, wi):
-    cfg, st, got, V = c4_result
-    core = 12
+def _window_errors(kind, cfg, st, got, V, cx, cy):
     ring = cfg.nsub + 3 + 2
-    cx, cy = _windows(cfg, core)[wi]
     ix0, iy0 = max(0, cx - ring), max(0, cy - ring)
-    ix1, iy1 = min(cfg.nx, cx + core + ring), min(cfg.ny, cy + core + ring)
+    ix1, iy1 = min(cfg.nx, cx + CORE + ring), min(cfg.ny, cy + CORE + ring)
     w, h = ix1 - ix0, iy1 - iy0
     hx, hy = cfg.lx / cfg.nx, cfg.ly / cfg.ny
     sub = _cut(cfg, st, ix0, iy0, w, h)
     verts = None if V is None else np.ascontiguousarray(V[iy0:iy0 + h + 1, ix0:ix0 + w + 1])
     mesh = oracle.Mesh(w, h, lx=w * hx, ly=h * hy, p=cfg.p, ns=cfg.ns, na=cfg.na, verts=verts)
     oprm = oracle.Params(alpha=cfg.alpha, beta=cfg.alpha)
-    ref = oracle.Oracle().outer_step(mesh, oprm, cfg.nsub, sub, do_advect=True)
-    # compare the core cells: elements [cx, cx+core) x [cy, cy+core), and their nodes
-    g = _cut(cfg, got, cx, cy, core, core)
-    loc = {k: v for k, v in ref.items() if k in got}
     p = cfg.p
-    rc = {}
-    for k, a in loc.items():
-        if a.ndim == 2 and a.shape == (p * h + 1, p * w + 1):
-            rc[k] = a[p * (cy - iy0):p * (cy - iy0 + core) + 1, p * (cx - ix0):p * (cx - ix0 + core) + 1]
-        else:
-            n = a.shape[1]
-            rc[k] = a.reshape(h, w, n)[cy - iy0:cy - iy0 + core, cx - ix0:cx - ix0 + core].reshape(-1, n)
-    init = _cut(cfg, st, cx, cy, core, core)
 
     def core_of(res):
         out = {}
@@ -102,25 +138,51 @@ def test_c4_window_parity(c4_result, wi):
             if k not in got:
                 continue
             if a.ndim == 2 and a.shape == (p * h + 1, p * w + 1):
-                out[k] = a[p * (cy - iy0):p * (cy - iy0 + core) + 1, p * (cx - ix0):p * (cx - ix0 + core) + 1]
+                out[k] = a[p * (cy - iy0):p * (cy - iy0 + CORE) + 1, p * (cx - ix0):p * (cx - ix0 + CORE) + 1]
             else:
-                out[k] = a.reshape(h, w, a.shape[1])[cy - iy0:cy - iy0 + core, cx - ix0:cx - ix0 + core].reshape(-1, a.shape[1])
+                out[k] = a.reshape(h, w, a.shape[1])[cy - iy0:cy - iy0 + CORE, cx - ix0:cx - ix0 + CORE].reshape(-1, a.shape[1])
         return out
 
-    for grp in (("S11", "S12", "S22"), ("vx", "vy")):
-        e = group_err(g, rc, grp)
-        de = group_err({k: g[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp)
-        bar = 1e-10
-        if max(e, de) > bar:
-            # self-consistency bound: after 100 subcycles at 125 m the oracle's own
-            # plain and FMA builds can already differ by ~1e-10 (n_S = 8); the GPU must then be
-            # within 4x of that floor on this window
-            fm = core_of(oracle.Oracle("fma").outer_step(mesh, oprm, cfg.nsub, sub, do_advect=True))
-            floor = max(group_err(fm, rc, grp), group_err({k: fm[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp))
-            bar = max(bar, 4 * floor)
-        assert e <= bar and de <= bar, (grp, e, de, bar, (cx, cy))
-    # A, H: fields only.  One advection step at 125 m changes the high coefficients by
-    # ~1e-11 of the field while the DG volume and edge terms cancel to ~11 digits, so
-    # their increments carry no parity information.
-    for grp in (("A",), ("H",)):
-        assert group_err(g, rc, grp) <= 1e-12, (grp, group_err(g, rc, grp), (cx, cy))
+    rc = core_of(oracle.Oracle().outer_step(mesh, oprm, cfg.nsub, sub, do_advect=True))
+    g = _cut(cfg, got, cx, cy, CORE, CORE)
+    init = _cut(cfg, st, cx, cy, CORE, CORE)
+    err = {}
+    for name, grp in (("S", ("S11", "S12", "S22")), ("v", ("vx", "vy"))):
+        err[name] = group_err(g, rc, grp)
+        err["d" + name] = group_err({k: g[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp)
+    for name in ("A", "H"):
+        err[name] = group_err(g, rc, (name,))
+    bar = 1e-10
+    if kind == "ns8" and max(err["S"], err["dS"], err["v"], err["dv"]) > bar:
+        fm = core_of(oracle.Oracle("fma").outer_step(mesh, oprm, cfg.nsub, sub, do_advect=True))
+        floor = 0.0
+        for grp in (("S11", "S12", "S22"), ("vx", "vy")):
+            floor = max(floor, group_err(fm, rc, grp),
+                        group_err({k: fm[k] - init[k] for k in grp}, {k: rc[k] - init[k] for k in grp}, grp))
+        err["floor"] = floor
+        bar = max(bar, 4 * floor)
+    err["bar"] = bar
+    return err
+
+
+def test_full_size_window_parity(full_result, capsys):
+    kind, cfg, st, got, V, extra = full_result
+    rows, bad = [], []
+    for (cx, cy) in _windows(kind, cfg, extra):
+        e = _window_errors(kind, cfg, st, got, V, cx, cy)
+        rows.append(f"  {kind:8s} ({cx:5d},{cy:5d})  " + "  ".join(f"{k}={v:.1e}" for k, v in e.items()))
+        # S, v fields and increments at the bar; A, H fields at 1e-12.  One advection step at these
+        # resolutions changes the high coefficients by ~1e-11 of the field while the DG volume and edge
+        # terms cancel to ~11 digits, so the A, H increments carry no parity information.
+        if max(e["S"], e["dS"], e["v"], e["dv"]) > e["bar"] or max(e["A"], e["H"]) > 1e-12:
+            bad.append((cx, cy, e))
+    with capsys.disabled():
+        print(f"\nfull-size parity {kind} ({cfg.nx}x{cfg.ny}, n_S={cfg.ns}, advect + {cfg.nsub} subcycles, "
+              f"alpha=beta={cfg.alpha:g}):")
+        print("\n".join(rows))
+        if kind == "strips8":
+            print("  " + "\n  ".join(extra["info"]))
+    assert not bad, bad
+    if kind == "strips8":   # the 8-strip partition is bitwise the single context
+        for k, a in extra["single"].items():
+            np.testing.assert_array_equal(got[k], a, err_msg=k)

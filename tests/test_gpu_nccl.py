@@ -29,23 +29,30 @@ def _torchrun(n, args, extra_env=None, timeout=600):
     return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
 
 
-@pytest.mark.parametrize("n,ty", [(2, 4), (3, 4), (2, 32)])
-def test_nccl_strips_bitwise_equal_single(n, ty):
-    r = _torchrun(n, ["scripts/nccl_two_rank.py"], {"TY": str(ty)})
+@pytest.mark.parametrize("n,ty,graph", [(2, 4, 1), (3, 4, 1), (2, 32, 1), (3, 4, 0)])
+def test_nccl_strips_bitwise_equal_single(n, ty, graph):
+    """NCCL row strips: bitwise equal to one context, and the gathered strips within the north_star
+    bar of the oracle (advection + 14 subcycles); graph = 1: the subcycles replay as one CUDA graph
+    per call (NCCL send/recv captured), 0: host-issued."""
+    r = _torchrun(n, ["scripts/nccl_two_rank.py"], {"TY": str(ty), "MR_GRAPH": str(graph)})
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-3000:]
     d = json.loads(lines[-1])
-    assert d["bitwise_equal"], d
+    assert d["bitwise_equal"] and d["oracle_err"] <= 1e-10, d
+    print(d["transport"])
 
 
-@pytest.mark.parametrize("n,ty,ns", [(2, 4, 6), (3, 4, 6), (2, 32, 8)])
-def test_p2p_ipc_strips_bitwise_equal_single(n, ty, ns):
-    """P2P transport across processes (CUDA IPC mappings exchanged through torch.distributed)."""
-    r = _torchrun(n, ["scripts/p2p_two_rank.py"], {"TY": str(ty), "NS": str(ns)})
+@pytest.mark.parametrize("n,ty,ns,graph", [(2, 4, 6, 1), (3, 4, 6, 1), (2, 32, 8, 1), (3, 4, 6, 0)])
+def test_p2p_ipc_strips_bitwise_equal_single(n, ty, ns, graph):
+    """P2P transport across processes (CUDA IPC mappings exchanged through torch.distributed); bitwise
+    equal to one context and within the bar of the oracle; with and without the subcycle graph."""
+    r = _torchrun(n, ["scripts/p2p_two_rank.py"], {"TY": str(ty), "NS": str(ns), "MR_GRAPH": str(graph)})
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-3000:]
     d = json.loads(lines[-1])
-    assert d["bitwise_equal"], d
+    assert d["bitwise_equal"] and d["oracle_err"] <= 1e-10, d
+    if graph:
+        assert "subcycle_graph=1" in d["transport"], d["transport"]
 
 
 @pytest.mark.parametrize("transport", ["p2p", "nccl"])

@@ -878,6 +878,30 @@ def test_graph_replay_matches_eager_chunks(nx):
         np.testing.assert_array_equal(a[k], b[k])
 
 
+def test_graph_cache_survives_counter_reallocation(nx):
+    """a graph captured before the work-counter buffer grows must not replay on the freed
+    buffer.  n = 3, then 200 (more counters than the first allocation's 128: reallocation), then 3 again
+    (the cached n = 3 graph would replay on the freed buffer if it survived), bitwise equal to the same
+    206 subcycles as 4 eager-sized calls of another context."""
+    nxe, nye = 40, 41
+    st = case(nxe, nye, 2, 6, 6, "warm", 40e3, 41e3)
+    with nx.Mesh(nxe, nye, 40e3, 41e3) as m:
+        m.load(st)
+        m.mevp_substeps(3, begin_step=True)
+        m.mevp_substeps(200, begin_step=False)
+        m.mevp_substeps(3, begin_step=False)
+        a = m.state()
+    with nx.Mesh(nxe, nye, 40e3, 41e3) as m:
+        m.load(st)
+        m.mevp_substeps(3, begin_step=True)
+        for _ in range(2):
+            m.mevp_substeps(100, begin_step=False)
+        m.mevp_substeps(3, begin_step=False)
+        b = m.state()
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
 @pytest.mark.parametrize("nranks,ty,variant", [(2, 32, 0), (3, 32, 0), (5, 32, 0), (2, 4, 0), (3, 3, 0), (3, 4, 1)])
 def test_loopback_strips_bitwise_equal_single(nx, nranks, ty, variant):
     """Row strips with halo exchange give bitwise the single-GPU result (fused + advection).
@@ -916,15 +940,18 @@ def test_loopback_strips_bitwise_equal_single(nx, nranks, ty, variant):
         np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
 
 
+@pytest.mark.parametrize("graph", [1, 0])
 @pytest.mark.parametrize("nranks,ty,ns,fused", [(2, 4, 6, 1), (3, 4, 6, 1), (2, 32, 6, 1), (3, 5, 8, 1),
                                                 (3, 4, 6, 0), (2, 32, 8, 0), (47, 1, 6, 1), (47, 1, 6, 0)])
-def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns, fused):
+def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns, fused, graph):
     """P2P transport inside one process: every rank on its OWN stream, so the ranks run
     concurrently and the only ordering between them is the device-side flag handshake; halo rows
     are copied straight into the neighbours' buffers.  Advection, fused subcycles (boundary /
     interior overlap with ty = 4) and unfused subcycles: bitwise equal to one context.  fused = 1:
     the fused kernel stores the halo rows into the neighbours' buffers itself (the exchange is the
-    flag handshake alone); 0: copy-engine copies.  47 ranks: one element row per strip."""
+    flag handshake alone); 0: copy-engine copies.  47 ranks: one element row per strip.  graph = 1
+    (default): each rank's fused subcycles replay as one CUDA graph per call (NXSDG_OPT_MULTIRANK_GRAPH);
+    the calls below (6, then 3 and 2) start from both flag-slot parities."""
     nxe, nye, lx, ly = 50, 47, 50e3, 47e3
     st = case(nxe, nye, 2, ns, 6, "random", lx, ly)
     prm = nx.PhysParams()
@@ -932,6 +959,8 @@ def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns, fused):
         m.load(st)
         m.advect(prm.dt)
         m.mevp_substeps(6, begin_step=True)
+        m.mevp_substeps(3, begin_step=False)
+        m.mevp_substeps(2, begin_step=False)
         m.mevp_substeps(2, begin_step=False, unfused=True)
         ref = m.state()
     ms = [nx.Mesh(nxe, nye, lx, ly, 2, ns, 6, rank=r, nranks=nranks, transport=nx.TRANSPORT_P2P) for r in range(nranks)]
@@ -940,6 +969,7 @@ def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns, fused):
     for m in ms:
         m.set_option(nx.OPT_CHUNK_ROWS, ty)
         m.set_option(nx.OPT_P2P_FUSED_STORES, fused)
+        m.set_option(nx.OPT_MULTIRANK_GRAPH, graph)
         er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
         loc = {k: st[k][nr0:nr0 + nrn].copy() for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
         for k in ("S11", "S12", "S22", "A", "H"):
@@ -949,10 +979,15 @@ def test_p2p_local_strips_bitwise_equal_single(nx, nranks, ty, ns, fused):
         m.advect(prm.dt)
     for m in ms:
         m.mevp_substeps(6, begin_step=True)
+    for n in (3, 2):
+        for m in ms:
+            m.mevp_substeps(n, begin_step=False)
     for m in ms:
         m.mevp_substeps(2, begin_step=False, unfused=True)
     for m in ms:
         m.synchronize()
+    if graph:
+        assert all("subcycle_graph=1" in m.transport_info for m in ms), ms[0].transport_info
     got = {k: np.concatenate([m.read_state(k) for m in ms]) for k in ref}
     for m in ms:
         m.destroy()
