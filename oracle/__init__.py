@@ -44,7 +44,7 @@ class OraMesh(C.Structure):
     _fields_ = [
         ("nx", C.c_int), ("ny", C.c_int), ("lx", C.c_double), ("ly", C.c_double),
         ("p", C.c_int), ("ns", C.c_int), ("na", C.c_int), ("bc", C.c_int),
-        ("verts", C.POINTER(C.c_double)),
+        ("verts", C.POINTER(C.c_double)), ("radius", C.c_double), ("lat0", C.c_double),
     ]
 
 
@@ -88,13 +88,16 @@ class Mesh:
     na: int = 6
     bc: int = 0
     verts: np.ndarray | None = None   # (ny+1, nx+1, 2) vertex coordinates; None = box
+    radius: float = 0.0               # > 0: lon-lat mesh on the sphere (R#26); lx, ly in radians
+    lat0: float = 0.0                 # southern edge latitude [rad] (sphere)
 
     def c(self) -> OraMesh:
         vp = None
         if self.verts is not None:
             self._vkeep = np.ascontiguousarray(self.verts, dtype=np.float64)
             vp = self._vkeep.ctypes.data_as(_P)
-        return OraMesh(self.nx, self.ny, self.lx, self.ly, self.p, self.ns, self.na, self.bc, vp)
+        return OraMesh(self.nx, self.ny, self.lx, self.ly, self.p, self.ns, self.na, self.bc, vp,
+                       float(self.radius), float(self.lat0))
 
     @property
     def n_elem(self) -> int:

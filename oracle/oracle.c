@@ -149,8 +149,34 @@ static void element_vertices(const ora_mesh* m, int ix, int iy, double X[4], dou
     }
 }
 
-/* |J| of the bilinear map at (s,t); fills J^{-1} row-major ([ds/dx ds/dy; dt/dx dt/dy]). */
+/* Spherical lat-lon mesh (R#26): element (ix, iy) covers longitudes ix dlon + s dlon and
+ * latitudes lat0 + (iy + t) dlat.  In the local orthonormal east-north frame the map's Jacobian is
+ * diag(R cos(lat) dlon, R dlat); physical vector components are (east, north). */
+static int is_sphere(const ora_mesh* m) { return m->radius > 0.0 && !m->verts; }
+static double sph_lat(const ora_mesh* m, int iy, double t) { return m->lat0 + (iy + t) * (m->ly / m->ny); }
+
+/* The metric (Christoffel) coefficient tan(lat) / R of the orthonormal frame on the sphere at (iy, t);
+ * 0 on plane meshes.  It enters the strain rate of a vector field,
+ *   eps11 = (1/(R cos lat)) du/dlon - v tan(lat)/R,  eps22 = (1/R) dv/dlat,
+ *   eps12 = 1/2 [(1/(R cos lat)) dv/dlon + (1/R) du/dlat + u tan(lat)/R],
+ * and, as its adjoint, the weak stress divergence (R#26). */
+static double metric_tan(const ora_mesh* m, int iy, double t) {
+    if (!is_sphere(m)) return 0.0;
+    return tan(sph_lat(m, iy, t)) / m->radius;
+}
+
+/* |J| of the bilinear map at (s,t); fills J^{-1} row-major ([ds/dx ds/dy; dt/dx dt/dy]).
+ * On the sphere: |J| = R^2 cos(lat) dlon dlat, J^{-1} = diag(1 / (R cos(lat) dlon), 1 / (R dlat)). */
 double ora_element_jacobian(const ora_mesh* m, int ix, int iy, double s, double t, double Jinv[4]) {
+    if (is_sphere(m)) {
+        double dlon = m->lx / m->nx, dlat = m->ly / m->ny, R = m->radius, c = cos(sph_lat(m, iy, t));
+        (void)ix; (void)s;
+        if (Jinv) {
+            Jinv[0] = 1.0 / (R * c * dlon); Jinv[1] = 0.0;
+            Jinv[2] = 0.0;                  Jinv[3] = 1.0 / (R * dlat);
+        }
+        return R * R * c * dlon * dlat;
+    }
     double X[4], Y[4];
     element_vertices(m, ix, iy, X, Y);
     double phi[4], ds[4], dt[4];
@@ -168,8 +194,16 @@ double ora_element_jacobian(const ora_mesh* m, int ix, int iy, double s, double 
     return det;
 }
 
-/* Tangent vector of the element map along s (col 0) or t (col 1). */
+/* Tangent vector of the element map along s (col 0) or t (col 1); on the sphere in the local
+ * east-north frame: (R cos(lat) dlon, 0) and (0, R dlat). */
 static void element_tangent(const ora_mesh* m, int ix, int iy, double s, double t, int col, double* T) {
+    if (is_sphere(m)) {
+        double dlon = m->lx / m->nx, dlat = m->ly / m->ny, R = m->radius;
+        (void)ix; (void)s;
+        if (col == 0) { T[0] = R * cos(sph_lat(m, iy, t)) * dlon; T[1] = 0.0; }
+        else { T[0] = 0.0; T[1] = R * dlat; }
+        return;
+    }
     double X[4], Y[4];
     element_vertices(m, ix, iy, X, Y);
     double phi[4], ds[4], dt[4];
@@ -242,6 +276,9 @@ static int solve_mass(int n, const double* M, double* b) {
 
 static int check_mesh(const ora_mesh* m) {
     if (!m || m->nx < 1 || m->ny < 1 || !(m->lx > 0) || !(m->ly > 0)) return -1;
+    if (m->radius < 0.0 || (m->radius > 0.0 && (m->verts || fabs(m->lat0) >= 1.5707963267948966 ||
+                                                fabs(m->lat0 + m->ly) >= 1.5707963267948966)))
+        return -1;
     if (m->p == 1 && m->ns != 3) return -2;
     if (m->p == 2 && m->ns != 6 && m->ns != 8) return -2;
     if (m->p != 1 && m->p != 2) return -2;
@@ -259,7 +296,8 @@ static long elem_node(const ora_mesh* m, int ix, int iy, int j) {
 }
 
 /* O4 strain (Table 1 "strain"; R#9): E_c = M_K^{-1} sum_g w_g |J_g| psi(g) eps_c(g),
- * eps11 = d vx/dx, eps22 = d vy/dy, eps12 = (d vx/dy + d vy/dx)/2 from the CG field. */
+ * eps11 = d vx/dx, eps22 = d vy/dy, eps12 = (d vx/dy + d vy/dx)/2 from the CG field; on the sphere
+ * (R#26) with the metric terms -vy tan(lat)/R in eps11 and +vx tan(lat)/(2R) in eps12. */
 int ora_strain(const ora_mesh* m, const double* vx, const double* vy,
                double* E11, double* E12, double* E22) {
     int rc = check_mesh(m); if (rc) return rc;
@@ -288,7 +326,7 @@ int ora_strain(const ora_mesh* m, const double* vx, const double* vy,
                 double detJ = ora_element_jacobian(m, ix, iy, s, t, Jinv);
                 double phi[MAXCG], dps[MAXCG], dpt[MAXCG];
                 ora_cg_basis(m->p, s, t, phi, dps, dpt);
-                double dvxdx = 0, dvxdy = 0, dvydx = 0, dvydy = 0;
+                double dvxdx = 0, dvxdy = 0, dvydx = 0, dvydy = 0, ugx = 0, ugy = 0;
                 for (int j = 0; j < ncg; ++j) {
                     double gxj, gyj;
                     phys_grad(Jinv, dps[j], dpt[j], &gxj, &gyj);
@@ -296,8 +334,12 @@ int ora_strain(const ora_mesh* m, const double* vx, const double* vy,
                     double ux = vx[n] - cx, uy = vy[n] - cy;
                     dvxdx += ux * gxj; dvxdy += ux * gyj;
                     dvydx += uy * gxj; dvydy += uy * gyj;
+                    ugx += phi[j] * ux; ugy += phi[j] * uy;
                 }
-                double eps11 = dvxdx, eps22 = dvydy, eps12 = 0.5 * (dvxdy + dvydx);
+                /* sphere (R#26): the metric terms of the orthonormal frame, with v at the point */
+                double kt = metric_tan(m, iy, t);
+                double vgx = cx + ugx, vgy = cy + ugy;
+                double eps11 = dvxdx - kt * vgy, eps22 = dvydy, eps12 = 0.5 * (dvxdy + dvydx + kt * vgx);
                 double psi[MAXN];
                 ora_dg_basis(ns, s, t, psi);
                 for (int k = 0; k < ns; ++k) {
@@ -395,7 +437,8 @@ int ora_stress(const ora_mesh* m, const ora_params* prm,
  *   F^x_j = - sum_{K ∋ j} sum_g w_g |J_g| [sigma11 dphi_j/dx + sigma12 dphi_j/dy]
  *   F^y_j = - sum_{K ∋ j} sum_g w_g |J_g| [sigma12 dphi_j/dx + sigma22 dphi_j/dy]
  * sigma_c(g) = sum_k S_c,k psi_k(g).  Element contributions first, then a
- * per-node gather over the adjacent elements. */
+ * per-node gather over the adjacent elements.  On the sphere (R#26) the adjoint of the strain's
+ * metric terms: + sigma12 phi_j tan(lat)/R in F^x, - sigma11 phi_j tan(lat)/R in F^y. */
 int ora_divergence(const ora_mesh* m, const double* S11, const double* S12, const double* S22,
                    double* Fx, double* Fy) {
     int rc = check_mesh(m); if (rc) return rc;
@@ -425,11 +468,12 @@ int ora_divergence(const ora_mesh* m, const double* S11, const double* S12, cons
                 }
                 double phi[MAXCG], dps[MAXCG], dpt[MAXCG];
                 ora_cg_basis(p, s, t, phi, dps, dpt);
+                double kt = metric_tan(m, iy, t);   /* sphere: the adjoint of the strain's metric terms */
                 for (int j = 0; j < ncg; ++j) {
                     double gxj, gyj;
                     phys_grad(Jinv, dps[j], dpt[j], &gxj, &gyj);
-                    lx[j] -= w * detJ * (s11 * gxj + s12 * gyj);
-                    ly[j] -= w * detJ * (s12 * gxj + s22 * gyj);
+                    lx[j] -= w * detJ * (s11 * gxj + s12 * gyj + s12 * phi[j] * kt);
+                    ly[j] -= w * detJ * (s12 * gxj + s22 * gyj - s11 * phi[j] * kt);
                 }
             }
         for (int j = 0; j < ncg; ++j) { rx[e * ncg + j] = lx[j]; ry[e * ncg + j] = ly[j]; }

@@ -33,6 +33,10 @@ typedef struct {
     const double* verts; /* NULL: axis-aligned box x_{a,b} = (a hx, b hy).  Else (ny+1) x (nx+1) x 2
                             vertex coordinates, row-major: a general (distorted) quad mesh with the
                             bilinear element map of its four vertices (R#23) */
+    double radius;   /* > 0 (verts NULL): longitude-latitude mesh on the sphere of this radius [m]
+                        ("quadrilateral meshes in spherical coordinates"; R#26): lx, ly are
+                        the angular extents in longitude and latitude [rad], lat0 the southern edge */
+    double lat0;     /* [rad], |lat0|, |lat0 + ly| < pi/2 */
 } ora_mesh;
 
 typedef struct {

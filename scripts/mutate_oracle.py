@@ -43,7 +43,8 @@ MUTANTS = [
     ("stress_delta_weight", "Delta with 1.25 e11 e22 instead of 1.5",
      "+ 1.50 * e11[g] * e22[g]", "+ 1.25 * e11[g] * e22[g]"),
     ("divergence_transposed", "F^y with sigma22 d/dx + sigma12 d/dy (transposed operand)",
-     "ly[j] -= w * detJ * (s12 * gxj + s22 * gyj);", "ly[j] -= w * detJ * (s22 * gxj + s12 * gyj);"),
+     "ly[j] -= w * detJ * (s12 * gxj + s22 * gyj - s11 * phi[j] * kt);",
+     "ly[j] -= w * detJ * (s22 * gxj + s12 * gyj - s11 * phi[j] * kt);"),
     ("coriolis_sign", "Coriolis term with the wrong sign in x",
      "+ mm * prm->f_c * (vyo - oy[n])", "+ mm * prm->f_c * (oy[n] - vyo)"),
     ("rk3_weights", "SSP-RK3 second stage 1/2, 1/2 instead of 3/4, 1/4",
@@ -97,6 +98,22 @@ MUTANTS = [
      "An[n] * (Fa * amag * ax[n] + Fo * w * ox[n])", "An[n] * (Fa * ax[n] + Fo * w * ox[n])"),
     ("advect_volume_sign", "advection volume term with the wrong sign",
      "b[k] += w * detJ * cv * (ux * gxk + uy * gyk);", "b[k] -= w * detJ * cv * (ux * gxk + uy * gyk);"),
+    # --- sphere (R#26)
+    ("sph_strain_metric_sign", "sphere: eps11 metric term with the wrong sign",
+     "double eps11 = dvxdx - kt * vgy", "double eps11 = dvxdx + kt * vgy"),
+    ("sph_strain_metric_dropped", "sphere: eps12 without its metric term",
+     "eps12 = 0.5 * (dvxdy + dvydx + kt * vgx)", "eps12 = 0.5 * (dvxdy + dvydx)"),
+    ("sph_divergence_metric_dropped", "sphere: F^x without the metric term",
+     "lx[j] -= w * detJ * (s11 * gxj + s12 * gyj + s12 * phi[j] * kt);", "lx[j] -= w * detJ * (s11 * gxj + s12 * gyj);"),
+    ("sph_jacobian_no_cos", "sphere: |J| without cos(lat)",
+     "return R * R * c * dlon * dlat;", "return R * R * dlon * dlat;"),
+    ("sph_parallel_edge_no_cos", "sphere: parallel-arc edge length without cos(lat)",
+     "if (col == 0) { T[0] = R * cos(sph_lat(m, iy, t)) * dlon; T[1] = 0.0; }",
+     "if (col == 0) { T[0] = R * dlon; T[1] = 0.0; }"),
+    ("sph_metric_at_centre", "sphere: metric evaluated at the element-centre latitude",
+     "return tan(sph_lat(m, iy, t)) / m->radius;", "return tan(sph_lat(m, iy, 0.5)) / m->radius;"),
+    ("sph_dlon_dlat_swapped", "sphere: J^-1 with dlat in the longitude entry",
+     "Jinv[0] = 1.0 / (R * c * dlon); Jinv[1] = 0.0;", "Jinv[0] = 1.0 / (R * c * dlat); Jinv[1] = 0.0;"),
     ("strain_vy_typo", "strain reads vx where vy is meant",
      "double ux = vx[n] - cx, uy = vy[n] - cy;", "double ux = vx[n] - cx, uy = vx[n] - cy;"),
 ]

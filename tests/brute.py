@@ -13,6 +13,10 @@ pieces on purpose, so that a slip in the oracle's own building blocks cannot can
 - geometry: the bilinear map written out from the vertex array, gradients through the adjugate
   (|J| J^-T, so every weak form is polynomial), edge normals x length from the straight edge's end
   vertices (no tangent evaluation, no normalisation);
+- sphere (R#26): the lon-lat element's metric written from the spherical line element
+  ds^2 = R^2 cos^2(lat) dlon^2 + R^2 dlat^2 (|J| = R^2 cos(lat) dlon dlat, adjugate diag(R dlat,
+  R cos(lat) dlon)), the frame's metric term tan(lat)/R, edge normals x length from the edge's arc
+  lengths; every integral with the method's rule (the integrands are not polynomials);
 - operators: global matrices assembled by scatter over elements (strain G, divergence D),
   the nodal mean of the DG->CG prep by scatter-and-count, the velocity update in vector form
   with the Coriolis term as the rotation (v - o) x k.
@@ -64,10 +68,16 @@ def ngp_of(ns):
 
 # ------------------------------------------------------------------ mesh
 class BMesh:
-    """nx x ny quads; ``verts`` (ny+1, nx+1, 2) or None for the box."""
+    """nx x ny quads; ``verts`` (ny+1, nx+1, 2) or None for the box; radius > 0: lon-lat mesh on the
+    sphere (lx, ly angular extents [rad], lat0 the southern edge)."""
 
-    def __init__(self, nx, ny, lx, ly, p, ns, na, bc=0, verts=None):
+    def __init__(self, nx, ny, lx, ly, p, ns, na, bc=0, verts=None, radius=0.0, lat0=0.0):
         self.nx, self.ny, self.lx, self.ly, self.p, self.ns, self.na, self.bc = nx, ny, lx, ly, p, ns, na, bc
+        self.radius, self.lat0 = radius, lat0
+        self.sphere = radius > 0
+        # the quadrature of integrals the method evaluates exactly on plane meshes (8 points: exact for
+        # the polynomial integrands) or, on the sphere, with its own rule
+        self.kq = ngp_of(ns) if self.sphere else 8
         if verts is None:
             X, Y = np.meshgrid(np.arange(nx + 1) * (lx / nx), np.arange(ny + 1) * (ly / ny))
             verts = np.stack([X, Y], axis=-1)
@@ -88,8 +98,19 @@ class BMesh:
         q = self.V[iy:iy + 2, ix:ix + 2].copy()
         return q - q[0, 0]
 
+    def lat(self, iy, t):
+        return self.lat0 + (iy + t) * self.ly / self.ny
+
+    def kt(self, iy, t):
+        """metric term tan(lat) / R of the sphere's orthonormal frame (0 on plane meshes)"""
+        return np.tan(self.lat(iy, t)) / self.radius if self.sphere else 0.0
+
     def jac(self, ix, iy, s, t):
         """(|J|, adj) with adj = |J| J^-T, so grad f = adj @ (f_s, f_t) / |J|."""
+        if self.sphere:
+            R, dl, dp = self.radius, self.lx / self.nx, self.ly / self.ny
+            c = np.cos(self.lat(iy, t))
+            return R * R * c * dl * dp, np.array([[R * dp, 0.0], [0.0, R * c * dl]])
         q = self.corners(ix, iy)
         xs = (1 - t) * (q[0, 1] - q[0, 0]) + t * (q[1, 1] - q[1, 0])      # d(x, y)/ds
         xt = (1 - s) * (q[1, 0] - q[0, 0]) + s * (q[1, 1] - q[0, 1])      # d(x, y)/dt
@@ -111,7 +132,8 @@ class BMesh:
         return I == 0 or J == 0 or I == self.NX - 1 or J == self.NY - 1
 
 
-def elem_mass(m: BMesh, ix, iy, n, k=8):
+def elem_mass(m: BMesh, ix, iy, n, k=None):
+    k = m.kq if k is None else k
     x, w = gauss(k)
     M = np.zeros((n, n))
     for a in range(k):
@@ -124,27 +146,32 @@ def elem_mass(m: BMesh, ix, iy, n, k=8):
 
 # ------------------------------------------------------------------ assembled operators
 def strain_matrices(m: BMesh):
-    """Global G11, G12x, G12y, G22 (ne*ns x nn): E11 = G11 vx, E22 = G22 vy,
-    E12 = G12x vx + G12y vy -- the |J|-weighted L2 projection of sym grad v_h (R#9), 8-point rule
-    (exact: |J| eps is a polynomial of degree <= 2 ngp - 1 per variable on bilinear elements)."""
+    """Global G11, G11y, G12x, G12y, G22 (ne*ns x nn): E11 = G11 vx + G11y vy, E22 = G22 vy,
+    E12 = G12x vx + G12y vy -- the |J|-weighted L2 projection of sym grad v_h (R#9) with the sphere's
+    metric terms (R#26: -v tan/R in eps11, +u tan/(2R) in eps12; G11y = 0 on plane meshes); 8-point
+    rule on plane meshes (exact: |J| eps is a polynomial of degree <= 2 ngp - 1 per variable on
+    bilinear elements), the method's rule on the sphere."""
     ns, ne, nn, p = m.ns, m.ne, m.nn, m.p
-    G = {k: np.zeros((ne * ns, nn)) for k in ("11", "12x", "12y", "22")}
-    x, w = gauss(8)
+    G = {k: np.zeros((ne * ns, nn)) for k in ("11", "11y", "12x", "12y", "22")}
+    kq = m.kq
+    x, w = gauss(kq)
     for iy in range(m.ny):
         for ix in range(m.nx):
             e = iy * m.nx + ix
             Minv = np.linalg.inv(elem_mass(m, ix, iy, ns))
             loc = {k: np.zeros((ns, (p + 1) ** 2)) for k in G}
-            for a in range(8):
-                for b in range(8):
+            for a in range(kq):
+                for b in range(kq):
                     s, t = x[a], x[b]
-                    _, adj = m.jac(ix, iy, s, t)
-                    _, ds, dt = m.cg(s, t)
+                    det, adj = m.jac(ix, iy, s, t)
+                    phi, ds, dt = m.cg(s, t)
                     g = adj @ np.stack([ds.ravel(), dt.ravel()])     # |J| grad phi_j, (2, ncg)
                     f = w[a] * w[b] * psi(ns, s, t)
+                    kt = det * m.kt(iy, t) * phi.ravel()              # |J| tan/R phi_j
                     loc["11"] += np.outer(f, g[0])
+                    loc["11y"] -= np.outer(f, kt)
                     loc["22"] += np.outer(f, g[1])
-                    loc["12x"] += 0.5 * np.outer(f, g[1])
+                    loc["12x"] += 0.5 * (np.outer(f, g[1]) + np.outer(f, kt))
                     loc["12y"] += 0.5 * np.outer(f, g[0])
             cols = [m.node(ix, iy, jx, jy) for jy in range(p + 1) for jx in range(p + 1)]
             for k in G:
@@ -153,35 +180,41 @@ def strain_matrices(m: BMesh):
 
 
 def divergence_matrices(m: BMesh):
-    """Global D1x, D2x (nn x ne*ns) etc.: F^x = -(D_x S11 + D_y S12), F^y = -(D_x S12 + D_y S22)
-    with D_x[j, (e,k)] = int_K psi_k d phi_j/dx (R#10), 8-point rule (polynomial integrand, exact)."""
+    """Global D_x, D_y, K (nn x ne*ns): F^x = -(D_x S11 + D_y S12 + K S12), F^y = -(D_x S12 + D_y S22
+    - K S11) with D_x[j, (e,k)] = int_K psi_k d phi_j/dx (R#10) and K[j, (e,k)] = int_K psi_k phi_j
+    tan(lat)/R (the sphere's metric term, R#26; 0 on plane meshes): the adjoint of strain_matrices."""
     ns, ne, nn, p = m.ns, m.ne, m.nn, m.p
-    Dx = np.zeros((nn, ne * ns)); Dy = np.zeros((nn, ne * ns))
-    x, w = gauss(8)
+    Dx = np.zeros((nn, ne * ns)); Dy = np.zeros((nn, ne * ns)); K = np.zeros((nn, ne * ns))
+    kq = m.kq
+    x, w = gauss(kq)
     for iy in range(m.ny):
         for ix in range(m.nx):
             e = iy * m.nx + ix
             rows = [m.node(ix, iy, jx, jy) for jy in range(p + 1) for jx in range(p + 1)]
-            for a in range(8):
-                for b in range(8):
+            for a in range(kq):
+                for b in range(kq):
                     s, t = x[a], x[b]
-                    _, adj = m.jac(ix, iy, s, t)
-                    _, ds, dt = m.cg(s, t)
+                    det, adj = m.jac(ix, iy, s, t)
+                    phi, ds, dt = m.cg(s, t)
                     g = adj @ np.stack([ds.ravel(), dt.ravel()])
                     f = w[a] * w[b] * psi(ns, s, t)
-                    Dx[np.ix_(rows, range(e * ns, (e + 1) * ns))] += np.outer(g[0], f)
-                    Dy[np.ix_(rows, range(e * ns, (e + 1) * ns))] += np.outer(g[1], f)
-    return Dx, Dy
+                    cols = range(e * ns, (e + 1) * ns)
+                    Dx[np.ix_(rows, cols)] += np.outer(g[0], f)
+                    Dy[np.ix_(rows, cols)] += np.outer(g[1], f)
+                    K[np.ix_(rows, cols)] += np.outer(det * m.kt(iy, t) * phi.ravel(), f)
+    return Dx, Dy, K
 
 
 def lumped_mass(m: BMesh):
-    """m_j = int phi_j over the mesh (8-point rule, exact for Q_p times a bilinear |J|)."""
+    """m_j = int phi_j over the mesh (8-point rule, exact for Q_p times a bilinear |J|; the method's
+    rule on the sphere)."""
     out = np.zeros(m.nn)
-    x, w = gauss(8)
+    kq = m.kq
+    x, w = gauss(kq)
     for iy in range(m.ny):
         for ix in range(m.nx):
-            for a in range(8):
-                for b in range(8):
+            for a in range(kq):
+                for b in range(kq):
                     det, _ = m.jac(ix, iy, x[a], x[b])
                     phi, _, _ = m.cg(x[a], x[b])
                     for jy in range(m.p + 1):
@@ -259,7 +292,7 @@ def velocity(m: BMesh, prm, Fx, Fy, mass, Hn, An, vn, o, a, v):
 def subcycles(m: BMesh, prm, nsub, st):
     """n subcycles by assembled global operators: E = G v, S <- stress, F = -D S, v <- velocity."""
     G = strain_matrices(m)
-    Dx, Dy = divergence_matrices(m)
+    Dx, Dy, K = divergence_matrices(m)
     mass = lumped_mass(m)
     Hn, An = prep(m, st["H"], st["A"])
     ns = m.ns
@@ -269,13 +302,13 @@ def subcycles(m: BMesh, prm, nsub, st):
     a = np.stack([st["ax"].ravel(), st["ay"].ravel()], axis=1)
     S = [st[k].copy() for k in ("S11", "S12", "S22")]
     for _ in range(nsub):
-        E11 = (G["11"] @ v[:, 0]).reshape(-1, ns)
+        E11 = (G["11"] @ v[:, 0] + G["11y"] @ v[:, 1]).reshape(-1, ns)
         E22 = (G["22"] @ v[:, 1]).reshape(-1, ns)
         E12 = (G["12x"] @ v[:, 0] + G["12y"] @ v[:, 1]).reshape(-1, ns)
         S = stress(m, prm, E11, E12, E22, st["H"], st["A"], *S)
         s11, s12, s22 = (x.ravel() for x in S)
-        Fx = -(Dx @ s11 + Dy @ s12)
-        Fy = -(Dx @ s12 + Dy @ s22)
+        Fx = -(Dx @ s11 + Dy @ s12 + K @ s12)
+        Fy = -(Dx @ s12 + Dy @ s22 - K @ s11)
         v = velocity(m, prm, Fx, Fy, mass, Hn, An, vn, o, a, v)
     shp = (m.NY, m.NX)
     return dict(vx=v[:, 0].reshape(shp), vy=v[:, 1].reshape(shp), S11=S[0], S12=S[1], S22=S[2])
@@ -285,7 +318,14 @@ def subcycles(m: BMesh, prm, nsub, st):
 def _edge(m: BMesh, ix, iy, edge):
     """(points on the edge as functions of r, neighbour's matching points, N = outward normal x length).
     edge 0 east, 1 west, 2 north, 3 south.  The edge is straight (bilinear map), so N is its end-vertex
-    difference rotated a quarter turn outwards."""
+    difference rotated a quarter turn outwards.  On the sphere the edges are a meridian arc (length
+    R dlat, normal +-east) and a parallel arc (R cos(lat) dlon, normal +-north)."""
+    if m.sphere:
+        R, dl, dp = m.radius, m.lx / m.nx, m.ly / m.ny
+        return [((lambda r: (1.0, r)), (lambda r: (0.0, r)), np.array([R * dp, 0.0]), (ix + 1, iy)),
+                ((lambda r: (0.0, r)), (lambda r: (1.0, r)), np.array([-R * dp, 0.0]), (ix - 1, iy)),
+                ((lambda r: (r, 1.0)), (lambda r: (r, 0.0)), np.array([0.0, R * np.cos(m.lat(iy, 1.0)) * dl]), (ix, iy + 1)),
+                ((lambda r: (r, 0.0)), (lambda r: (r, 1.0)), np.array([0.0, -R * np.cos(m.lat(iy, 0.0)) * dl]), (ix, iy - 1))][edge]
     q = m.corners(ix, iy)
     if edge == 0:
         d = q[1, 1] - q[0, 1]; N = np.array([d[1], -d[0]])

@@ -25,7 +25,19 @@ from oracle import Mesh, Params
 from paper_2402_00466_b200 import inputs
 
 
+R_EARTH = 6371e3
+LAT0 = math.radians(60.0)
+
+
+def _sphere_pair(nx, ny, p, ns, na, dlon=0.05, dlat=0.04, lat0=LAT0, bc=0, radius=R_EARTH):
+    """lon-lat patch of nx x ny elements, each dlon x dlat [rad], southern edge lat0 (R#26)."""
+    return (Mesh(nx, ny, lx=nx * dlon, ly=ny * dlat, p=p, ns=ns, na=na, bc=bc, radius=radius, lat0=lat0),
+            brute.BMesh(nx, ny, nx * dlon, ny * dlat, p, ns, na, bc=bc, radius=radius, lat0=lat0))
+
+
 def _pair(nx, ny, p, ns, na, lx, ly, distorted, bc=0, delta=0.28, seed=None):
+    if distorted == "sphere":
+        return _sphere_pair(nx, ny, p, ns, na, bc=bc)
     V = None
     if distorted:
         V = inputs.distorted_vertices(nx, ny, lx, ly, delta, **({} if seed is None else {"seed": seed}))
@@ -179,7 +191,7 @@ def test_distorted_strain_brute_force(ora, p, ns):
     vx = r.uniform(-0.2, 0.2, mesh.node_shape); vy = r.uniform(-0.2, 0.2, mesh.node_shape)
     E11, E12, E22 = ora.strain(mesh, vx, vy)
     G = brute.strain_matrices(bm)
-    ref = ((G["11"] @ vx.ravel()).reshape(-1, ns), (G["12x"] @ vx.ravel() + G["12y"] @ vy.ravel()).reshape(-1, ns),
+    ref = ((G["11"] @ vx.ravel() + G["11y"] @ vy.ravel()).reshape(-1, ns), (G["12x"] @ vx.ravel() + G["12y"] @ vy.ravel()).reshape(-1, ns),
            (G["22"] @ vy.ravel()).reshape(-1, ns))
     scale = max(np.abs(x).max() for x in ref)
     for g, x in zip((E11, E12, E22), ref):
@@ -193,9 +205,9 @@ def test_distorted_divergence_brute_force(ora, p, ns):
     r = np.random.default_rng(6)
     S = [r.uniform(-1e4, 1e4, (12, ns)) for _ in range(3)]
     Fx, Fy = ora.divergence(mesh, *S)
-    Dx, Dy = brute.divergence_matrices(bm)
+    Dx, Dy, K = brute.divergence_matrices(bm)
     s11, s12, s22 = (x.ravel() for x in S)
-    rx, ry = -(Dx @ s11 + Dy @ s12), -(Dx @ s12 + Dy @ s22)
+    rx, ry = -(Dx @ s11 + Dy @ s12 + K @ s12), -(Dx @ s12 + Dy @ s22 - K @ s11)
     scale = max(np.abs(rx).max(), np.abs(ry).max())
     assert np.abs(Fx.ravel() - rx).max() < 1e-12 * scale and np.abs(Fy.ravel() - ry).max() < 1e-12 * scale
 
@@ -284,11 +296,11 @@ def test_box_advection_operator_brute_force(ora):
 # ---------------------------------------------------------------- whole subcycle, assembled operators
 @pytest.mark.parametrize("n", [2, 3, 4])
 @pytest.mark.parametrize("p,ns,na", [(1, 3, 3), (2, 6, 6), (2, 8, 6)])
-@pytest.mark.parametrize("distorted", [False, True])
+@pytest.mark.parametrize("distorted", [False, True, "sphere"])
 def test_whole_subcycle_assembled_operators(ora, n, p, ns, na, distorted):
     """n x n meshes, 3 subcycles (strain -> stress -> divergence -> velocity)
     computed with globally assembled operators (tests/brute.py) vs the element-loop oracle, on seeded
-    random data (clamps active, S^0 != 0)."""
+    random data (clamps active, S^0 != 0); box, distorted quads (R#23) and the lon-lat sphere (R#26)."""
     lx = ly = n * 1e3
     mesh, bm = _pair(n, n, p, ns, na, lx, ly, distorted=distorted, seed=inputs.SEED_BASE + n)
     st = inputs.make_case(n, n, p, ns, na, kind="random", lx=lx, ly=ly, seed=inputs.SEED_BASE + 10 * n + p)
@@ -328,3 +340,142 @@ def test_replacement_pressure_scales_the_plastic_stress(ora):
     # zero strain rate: zero stress (the defining property of the replacement pressure)
     z = ora.stress(mesh, Params(alpha=1.0, replacement_pressure=1), *Z, H, A, *Z)
     assert max(np.abs(x).max() for x in z) == 0.0
+
+
+# ---------------------------------------------------------------- sphere (NEXT-4, R#26)
+def test_sphere_element_areas_closed_form(ora):
+    """The Gauss integral of |J| over a lon-lat element approximates its exact spherical area
+    R^2 dlon (sin lat1 - sin lat0) within the 3-point rule's error bound (|err| <= dlat^7 / 2016000 x
+    |cos^(6)| x R^2 dlon ~ 1e-16 relative here), per element and in total."""
+    mesh, _ = _sphere_pair(4, 5, 2, 6, 6)
+    x, w = ora.gauss(3)
+    tot = 0.0
+    for iy in range(5):
+        la, lb = LAT0 + iy * 0.04, LAT0 + (iy + 1) * 0.04
+        exact = R_EARTH**2 * 0.05 * (math.sin(lb) - math.sin(la))
+        for ix in range(4):
+            area = sum(w[a] * w[b] * ora.jacobian(mesh, ix, iy, x[a], x[b])[0] for a in range(3) for b in range(3))
+            assert abs(area - exact) < 1e-13 * exact
+            tot += area
+    exact_tot = R_EARTH**2 * 0.2 * (math.sin(LAT0 + 0.2) - math.sin(LAT0))
+    assert abs(tot - exact_tot) < 1e-13 * exact_tot
+    m = ora.lumped_mass(mesh)
+    assert abs(m.sum() - tot) < 1e-12 * tot
+
+
+def test_sphere_reduces_to_the_box_near_the_equator(ora):
+    """Special case: a patch at the equator on a sphere of radius 1e12 m with the box's physical sizes
+    (dlon = hx / R, dlat = hy / R) is the plane box up to O((L/R)^2) ~ 1e-17: one outer step (advection +
+    3 subcycles) agrees with the box oracle to rounding.  Catches a swapped dlon / dlat, a missing R or
+    cos in the sphere's metric."""
+    nx, ny, hx, hy = 5, 4, 1.2e3, 0.9e3
+    R = 1e12
+    st = inputs.make_case(nx, ny, 2, 6, 6, kind="random", lx=nx * hx, ly=ny * hy)
+    box = ora.outer_step(Mesh(nx, ny, lx=nx * hx, ly=ny * hy), Params(), 3, st)
+    sph = ora.outer_step(Mesh(nx, ny, lx=nx * hx / R, ly=ny * hy / R, radius=R, lat0=-0.5 * ny * hy / R),
+                         Params(), 3, st)
+    for grp in (("S11", "S12", "S22"), ("vx", "vy"), ("A",), ("H",)):
+        num = max(np.abs(box[k] - sph[k]).max() for k in grp)
+        den = max(np.abs(box[k]).max() for k in grp)
+        assert num <= 1e-12 * den, (grp, num / den)
+
+
+@pytest.mark.parametrize("p,ns,na", [(1, 3, 3), (2, 6, 6), (2, 6, 1)])
+def test_sphere_zonal_flow_preserves_constant(ora, p, ns, na):
+    """A constant tracer in any zonal flow u(lat), v = 0 (divergence-free on the sphere:
+    div v = (1/(R cos lat)) du/dlon = 0) is a steady state at every interior element: the volume term's
+    longitude integral of d(psi)/ds is exact and the meridian-edge fluxes use the same latitude points,
+    so they cancel to rounding.  Needs the sphere's edge lengths / normals and |J|."""
+    mesh, _ = _sphere_pair(5, 4, p, ns, na)
+    NY, NX = mesh.node_shape
+    r = np.random.default_rng(3)
+    u_row = r.uniform(-0.2, 0.2, NY)
+    vx = np.repeat(u_row[:, None], NX, axis=1); vy = np.zeros((NY, NX))
+    c = np.zeros((20, na)); c[:, 0] = 0.7
+    rhs = ora.advect_rhs(mesh, vx, vy, c).reshape(4, 5, na)
+    assert np.abs(rhs[1:-1, 1:-1]).max() < 1e-13 * 0.2 / (R_EARTH * 0.04)
+
+
+def test_sphere_rigid_rotation_has_no_strain(ora):
+    """A rigid rotation about the polar axis, u = w R cos(lat), v = 0, has zero strain rate on the
+    sphere - only because of the metric term: (1/R) du/dlat + u tan(lat)/R = w (-sin + cos tan) = 0.
+    Its CG2 interpolant differs from cos by O(dlat^3), so the DG strain is bounded by ~ w dlat^2;
+    without the metric term E12 would be -w sin(lat)/2 ~ 0.45 w."""
+    mesh, _ = _sphere_pair(6, 5, 2, 6, 6)
+    NY, NX = mesh.node_shape
+    om = 1e-6
+    lat = LAT0 + np.arange(NY) * 0.02
+    vx = np.repeat((om * R_EARTH * np.cos(lat))[:, None], NX, axis=1); vy = np.zeros((NY, NX))
+    E11, E12, E22 = ora.strain(mesh, vx, vy)
+    for E in (E11, E12, E22):
+        assert np.abs(E).max() < 5e-3 * om
+    # the same field on the plane (no metric term) is strained: the term is what cancels it
+    flat = Mesh(6, 5, lx=6 * 0.05 * R_EARTH * math.cos(LAT0), ly=5 * 0.04 * R_EARTH)
+    assert np.abs(ora.strain(flat, vx, vy)[1][:, 0]).max() > 0.3 * om
+
+
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
+def test_sphere_strain_divergence_adjointness(ora, p, ns):
+    """Weak-form identity on the sphere: sum_j v_j . F_j = -sum_K (S11 M_K E11 + 2 S12 M_K E12 +
+    S22 M_K E22) with M_K the cos(lat)-weighted DG mass of an independent rule (the method's 3-point
+    rule: the projection is the discrete L2 projection of that rule, so the identity is exact).  A sign
+    or a missing factor of the metric term in either the strain or the divergence breaks it."""
+    mesh, bm = _sphere_pair(4, 3, p, ns, min(ns, 6))
+    r = np.random.default_rng(8)
+    vx = r.uniform(-1, 1, mesh.node_shape); vy = r.uniform(-1, 1, mesh.node_shape)
+    S = [r.uniform(-1, 1, (12, ns)) for _ in range(3)]
+    E11, E12, E22 = ora.strain(mesh, vx, vy)
+    Fx, Fy = ora.divergence(mesh, *S)
+    lhs = (vx * Fx + vy * Fy).sum()
+    rhs = 0.0
+    for iy in range(3):
+        for ix in range(4):
+            e = iy * 4 + ix
+            M = brute.elem_mass(bm, ix, iy, ns)
+            rhs -= S[0][e] @ M @ E11[e] + 2 * S[1][e] @ M @ E12[e] + S[2][e] @ M @ E22[e]
+    assert abs(lhs - rhs) < 1e-12 * max(abs(lhs), 1.0) * 10
+
+
+@pytest.mark.parametrize("p,ns", [(1, 3), (2, 6), (2, 8)])
+def test_sphere_strain_and_divergence_brute_force(ora, p, ns):
+    """O4 / O6 on the sphere against the assembled brute-force operators (metric from the line
+    element, tan(lat)/R terms, the method's rule)."""
+    mesh, bm = _sphere_pair(4, 3, p, ns, min(ns, 6))
+    r = np.random.default_rng(5)
+    vx = r.uniform(-0.2, 0.2, mesh.node_shape); vy = r.uniform(-0.2, 0.2, mesh.node_shape)
+    E11, E12, E22 = ora.strain(mesh, vx, vy)
+    G = brute.strain_matrices(bm)
+    ref = ((G["11"] @ vx.ravel() + G["11y"] @ vy.ravel()).reshape(-1, ns),
+           (G["12x"] @ vx.ravel() + G["12y"] @ vy.ravel()).reshape(-1, ns), (G["22"] @ vy.ravel()).reshape(-1, ns))
+    scale = max(np.abs(x).max() for x in ref)
+    for g, x in zip((E11, E12, E22), ref):
+        assert np.abs(g - x).max() < 1e-12 * scale
+    S = [r.uniform(-1e4, 1e4, (12, ns)) for _ in range(3)]
+    Fx, Fy = ora.divergence(mesh, *S)
+    Dx, Dy, K = brute.divergence_matrices(bm)
+    s11, s12, s22 = (x.ravel() for x in S)
+    rx, ry = -(Dx @ s11 + Dy @ s12 + K @ s12), -(Dx @ s12 + Dy @ s22 - K @ s11)
+    sc = max(np.abs(rx).max(), np.abs(ry).max())
+    assert np.abs(Fx.ravel() - rx).max() < 1e-12 * sc and np.abs(Fy.ravel() - ry).max() < 1e-12 * sc
+    np.testing.assert_allclose(ora.lumped_mass(mesh).ravel(), brute.lumped_mass(bm), rtol=1e-13)
+
+
+@pytest.mark.parametrize("p,ns,na,bc", [(1, 3, 3, 0), (2, 6, 6, 0), (2, 6, 6, 1), (2, 6, 1, 0)])
+def test_sphere_advection_operator_brute_force(ora, p, ns, na, bc):
+    """O11 on the sphere against the brute force (meridian / parallel arc normals and lengths,
+    cos(lat)-weighted mass), closed and periodic; and closed-box conservation of sum_K int_K c dA."""
+    mesh, bm = _sphere_pair(4, 4, p, ns, na, bc=bc)
+    r = np.random.default_rng(31)
+    vx = r.uniform(-0.1, 0.1, mesh.node_shape); vy = r.uniform(-0.1, 0.1, mesh.node_shape)
+    if bc == 1:
+        for v in (vx, vy):
+            v[-1, :] = v[0, :]; v[:, -1] = v[:, 0]
+    else:
+        for v in (vx, vy):
+            v[0, :] = v[-1, :] = v[:, 0] = v[:, -1] = 0.0
+    c = r.uniform(-0.3, 0.3, (16, na)); c[:, 0] = r.uniform(0.3, 1.0, 16)
+    got = ora.advect_rhs(mesh, vx, vy, c)
+    assert _rel(got, brute.advect_rhs(bm, vx, vy, c)) < 1e-12
+    if bc == 0:
+        d = [(brute.elem_mass(bm, e % 4, e // 4, na) @ got[e])[0] for e in range(16)]
+        assert abs(sum(d)) < 1e-13 * sum(abs(x) for x in d)
