@@ -194,6 +194,12 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_LIMITER       NEXT-4 (DESIGN R#25): 0 (default, the paper's unlimited scheme) | 1 = Zhang-Shu
  *                           bound-preserving scaling limiter after every SSP-RK stage of nxsdg_advect (A in [0,1],
  *                           H >= 0 at the volume and edge Gauss points; element means, hence mass, unchanged)
+ *   NXSDG_OPT_ADVECT_KERNEL 0 (default) = the persistent TMA-staged structured advection k_advect_tma for the
+ *                           closed-box CG2/DG2 pair without limiter (bitwise = k_advect_q2); 1 = k_advect_q2
+ *   NXSDG_OPT_ADVECT_STAGES shared-memory row slots per warp of k_advect_tma: 4 (default) | 5
+ *   NXSDG_OPT_FUSE_PREP_PG  single rank with k_advect_tma: 1 (default) = the last advection stage also writes the
+ *                           outer-step prep's P at the Gauss points of the new A, H (bitwise what the prep would
+ *                           compute); 0 = the prep computes it at BEGIN_STEP
  *   NXSDG_OPT_MULTIRANK_GRAPH  row-strip ranks (P2P or NCCL transport): 1 (default) = nxsdg_mevp_substeps
  *                           captures its n fused subcycles - boundary chunks, exchange (peer stores + flag
  *                           handshake, or NCCL send/recv) on the halo stream, interior chunks, join - in one
@@ -203,7 +209,8 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
        NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,
        NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11,
-       NXSDG_OPT_V_ROW_CARRY = 12, NXSDG_OPT_MULTIRANK_GRAPH = 13 };
+       NXSDG_OPT_V_ROW_CARRY = 12, NXSDG_OPT_MULTIRANK_GRAPH = 13, NXSDG_OPT_ADVECT_KERNEL = 14,
+       NXSDG_OPT_ADVECT_STAGES = 15, NXSDG_OPT_FUSE_PREP_PG = 16 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */
@@ -230,6 +237,18 @@ nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* ctx, double t);
  * unfused general-geometry steps.  Fused subcycles with CG1 or n_S = 8 on a general mesh return
  * UNSUPPORTED (use NXSDG_UNFUSED).  Single rank only. */
 nxsdg_status nxsdg_set_vertices(nxsdg_ctx* ctx, const double* xy, int64_t count, nxsdg_mem mem);
+
+/* NEXT-4 ("quadrilateral meshes in spherical coordinates"; R#26): switch the
+ * context to a longitude-latitude mesh on the sphere of `radius` [m]: element (ix, iy) spans longitudes
+ * [ix, ix + 1] x lon_extent / nx and latitudes lat0 + [iy, iy + 1] x lat_extent / ny [rad] (the mesh
+ * descriptor's lx, ly are then unused).  Velocities are the physical (east, north) components; the strain
+ * rate carries the frame's metric terms (eps11 -= v tan(lat)/R, eps12 += u tan(lat)/(2R)), the stress
+ * divergence their adjoint, every integral the weight |J| = R^2 cos(lat) dlon dlat (3-point Gauss rule),
+ * the advection the meridian / parallel arc lengths.  Supported: CG2 / DG2 (n_S = n_A = 6), FP64, the fused
+ * TMA subcycle kernel and the structured advection (single rank or row strips); UNSUPPORTED otherwise
+ * (other degrees, general quads, FP32 storage, unfused / debug steps, the limiter).  INVALID_ARG unless
+ * radius, extents > 0 and both edge latitudes lie inside (-pi/2, pi/2). */
+nxsdg_status nxsdg_set_sphere(nxsdg_ctx* ctx, double radius, double lat0, double lon_extent, double lat_extent);
 
 /* ---- compute ----------------------------------------------------------------- */
 /* n_sub mEVP subcycles.  flags: NXSDG_BEGIN_STEP, NXSDG_UNFUSED.

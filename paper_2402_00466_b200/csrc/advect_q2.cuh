@@ -78,6 +78,11 @@ __device__ __forceinline__ void gp_vals(const double c[6], double e[3][3]) {
     }
 }
 
+// SPH (NEXT-4, R#26): lon-lat sphere rows - the volume integrand carries |J| / (R^2 dlon dlat) = cos(lat)
+// with the gradient's 1/(R cos dlon), 1/(R dlat) (a.ihx, a.ihy), the parallel-arc edges their cos(lat)
+// (the same node-row value on both sides of an edge, so fluxes still cancel bitwise), and the update
+// applies the row's block inverse of the cos-weighted DG mass (row table of nxsdg.cu).
+template <bool SPH = false>
 __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_q2(AdvArgs a) {
     __shared__ double sFA[ADV_ROWS][32][3], sFH[ADV_ROWS][32][3];
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -160,6 +165,10 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_q2(AdvArgs a) {
     }
     const double mr[6] = {1.0, 12.0, 12.0, 180.0, 180.0, 144.0};   // 1 / reference mass
     const int64_t eo = (int64_t)lr * a.epitch + ix;
+    const double* __restrict__ srow = SPH ? a.sph_rows + (int64_t)lr * kSphRow : nullptr;
+    // volume factors (folded into the integrand on the sphere) and north / south edge factors
+    const double vsx = SPH ? 1.0 : a.ihx, vsy = SPH ? 1.0 : a.ihy;
+    const double eny = SPH ? a.ihy * __ldg(srow + SPH_COS_N) : a.ihy, esy = SPH ? a.ihy * __ldg(srow + SPH_COS_S) : a.ihy;
 #pragma unroll
     for (int tr = 0; tr < 2; ++tr) {
         const double* c = tr == 0 ? me.A : me.H;
@@ -168,19 +177,24 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_q2(AdvArgs a) {
         double cg[3][3], Gx[3][3], Gy[3][3];
         gp_vals(c, cg);
 #pragma unroll
-        for (int gy = 0; gy < 3; ++gy)
+        for (int gy = 0; gy < 3; ++gy) {
+            const double fx = SPH ? a.ihx : 1.0, fy = SPH ? a.ihy * __ldg(srow + SPH_COS + gy) : 1.0;
 #pragma unroll
-            for (int g = 0; g < 3; ++g) { Gx[gy][g] = cg[gy][g] * gvx[gy][g]; Gy[gy][g] = cg[gy][g] * gvy[gy][g]; }
+            for (int g = 0; g < 3; ++g) {
+                Gx[gy][g] = SPH ? cg[gy][g] * gvx[gy][g] * fx : cg[gy][g] * gvx[gy][g];
+                Gy[gy][g] = SPH ? cg[gy][g] * gvy[gy][g] * fy : cg[gy][g] * gvy[gy][g];
+            }
+        }
         double x00, x10, x01, y00, y10, y01;
         vol_mom(Gx, x00, x10, x01);
         vol_mom(Gy, y00, y10, y01);
         double L[6];
         L[0] = 0.0;
-        L[1] = a.ihx * x00;
-        L[2] = a.ihy * y00;
-        L[3] = 2.0 * a.ihx * x10;
-        L[4] = 2.0 * a.ihy * y01;
-        L[5] = fma(a.ihx, x01, a.ihy * y10);
+        L[1] = vsx * x00;
+        L[2] = vsy * y00;
+        L[3] = 2.0 * vsx * x10;
+        L[4] = 2.0 * vsy * y01;
+        L[5] = fma(vsx, x01, vsy * y10);
         double m0, m1, m2;
         edge_mom(Fe, m0, m1, m2);   // east, outward +x
         L[0] -= a.ihx * m0; L[1] -= a.ihx * 0.5 * m0; L[2] -= a.ihx * m1; L[3] -= a.ihx * m0 * (1.0 / 6.0);
@@ -189,17 +203,25 @@ __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_q2(AdvArgs a) {
         L[0] += a.ihx * m0; L[1] -= a.ihx * 0.5 * m0; L[2] += a.ihx * m1; L[3] += a.ihx * m0 * (1.0 / 6.0);
         L[4] += a.ihx * m2; L[5] -= a.ihx * 0.5 * m1;
         edge_mom(Fn, m0, m1, m2);   // north, outward +y
-        L[0] -= a.ihy * m0; L[1] -= a.ihy * m1; L[2] -= a.ihy * 0.5 * m0; L[3] -= a.ihy * m2;
-        L[4] -= a.ihy * m0 * (1.0 / 6.0); L[5] -= a.ihy * 0.5 * m1;
+        L[0] -= eny * m0; L[1] -= eny * m1; L[2] -= eny * 0.5 * m0; L[3] -= eny * m2;
+        L[4] -= eny * m0 * (1.0 / 6.0); L[5] -= eny * 0.5 * m1;
         edge_mom(Fs, m0, m1, m2);   // south, outward -y
-        L[0] += a.ihy * m0; L[1] += a.ihy * m1; L[2] -= a.ihy * 0.5 * m0; L[3] += a.ihy * m2;
-        L[4] += a.ihy * m0 * (1.0 / 6.0); L[5] -= a.ihy * 0.5 * m1;
+        L[0] += esy * m0; L[1] += esy * m1; L[2] -= esy * 0.5 * m0; L[3] += esy * m2;
+        L[4] += esy * m0 * (1.0 / 6.0); L[5] -= esy * 0.5 * m1;
         double* out = tr == 0 ? a.Aout : a.Hout;
         const double* c0 = tr == 0 ? c0A : c0H;
-        double nc[6];
+        double nc[6], Ld[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) Ld[k] = L[k] * mr[k];
+        if constexpr (SPH) {   // the row's cos-weighted mass: block inverse (modes {0,2,4}, {1,5}, {3})
+            double p[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) p[k] = Ld[k];
+            sph_apply_q(srow, p, Ld);
+        }
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-            const double v = a.a1 * fma(a.dt, L[k] * mr[k], c[k]);
+            const double v = a.a1 * fma(a.dt, Ld[k], c[k]);
             nc[k] = (a.a0 != 0.0) ? fma(a.a0, c0[k], v) : v;
         }
         if (a.limit) {   // R#25 fused: extremes over the 9 volume and 12 edge Gauss points, scale about the mean

@@ -1,0 +1,245 @@
+// K4, persistent TMA-staged form of the structured CG2/DG2 advection stage (Eq. (1),
+// P:102-106, upwind DG).  The arithmetic is k_advect_q2's, call for call (same traces, fluxes,
+// moments and update, so the results are bitwise those of k_advect_q2); what changes is how the data
+// reaches the registers, the part that kept k_advect_q2 at ~60 % of HBM (16 % warps active, every
+// element loading its east and north neighbours' coefficients again through L1/L2):
+//
+//   - a warp owns a strip of 31 element columns (+ lane 0 = the ring column ix0 - 1, whose east flux
+//     is lane 1's west flux) and marches up a chunk of element rows;
+//   - every row of the chunk, plus one ring row below and one above, is loaded ONCE by TMA into a
+//     ring of shared-memory slots: the A and H coefficients of 34 columns (the strip + both neighbours)
+//     and the two node rows of v the row adds (2k+1, 2k+2; the row below supplies node row 2k);
+//   - a row is processed when the row above has landed: east neighbours come from the slot, west
+//     fluxes by shuffle, south / north fluxes from the slots of the rows below / above (each interior
+//     horizontal edge is evaluated by the two rows sharing it with the same function on the same
+//     inputs: bitwise-identical fluxes, mass conserved to the rounding of the sums);
+//   - the RK combine input c0 (stages 2, 3) is prefetched into registers before the wait.
+// Closed box (boundary edges carry no flux; out-of-range rows / columns arrive zero-filled by TMA and are
+// masked by `open`); periodic meshes, the limiter and the sphere use k_advect_q2.
+#pragma once
+#include "advect_q2.cuh"
+#include "prep_q2.cuh"
+
+namespace nxk {
+
+constexpr int ADV_TMA_WARPS = 2;
+constexpr int ADV_COLS = 34;                   // FP64 box: 16-B aligned start (ix0 - 1) & ~1, covers ix0 + 31
+
+struct __align__(128) AdvSlot {
+    alignas(128) double A[6][ADV_COLS];        // 1632 B
+    alignas(128) double H[6][ADV_COLS];
+    alignas(128) double vx[2][K2_VCOLS];       // node rows 2k+1, 2k+2; 1056 B
+    alignas(128) double vy[2][K2_VCOLS];
+};
+constexpr uint32_t kAdvTx = 2u * 6u * ADV_COLS * 8u + 2u * 2u * K2_VCOLS * 8u;
+
+struct AdvMaps {
+    CUtensorMap A, H;     // 3D {nx, erows_local, 6}, box {34, 1, 6}: the stage input planes
+    CUtensorMap vx, vy;   // 2D node grid, box {66, 2}
+};
+
+struct AdvTmaArgs {
+    AdvArgs a;
+    int nstrips, ty, nchunks;
+};
+
+template <int STAGES>
+__global__ void __launch_bounds__(32 * ADV_TMA_WARPS, 3) k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
+    static_assert(STAGES >= 4, "rows k-1, k, k+1 in use while k+2 loads");
+    constexpr int P = STAGES - 3;                  // positions in flight beyond the three a job uses
+    const AdvArgs& a = ta.a;
+    extern __shared__ __align__(1024) unsigned char adv_smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    AdvSlot* slot = reinterpret_cast<AdvSlot*>(adv_smem) + wib * STAGES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(adv_smem + ADV_TMA_WARPS * STAGES * sizeof(AdvSlot)) + wib * STAGES;
+    int4* desc = reinterpret_cast<int4*>(reinterpret_cast<uint64_t*>(adv_smem + ADV_TMA_WARPS * STAGES * sizeof(AdvSlot)) +
+                                         ADV_TMA_WARPS * STAGES) + wib * STAGES;
+    const int twarps = gridDim.x * ADV_TMA_WARPS, gw = blockIdx.x * ADV_TMA_WARPS + wib;
+    const int nunits = ta.nstrips * ta.nchunks;
+    if (gw >= nunits) return;
+    if (lane == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    // load cursor (lane 0): the warp's units gw, gw + twarps, ...; each unit contributes the rows
+    // lr0 - 1 .. lr1 (ring below, the chunk, ring above); desc = (unit, row, job?, 0)
+    struct Cur { int u, k, lr0, lr1; bool ok; };
+    auto unit_start = [&](int u, Cur& c) {
+        c.ok = u < nunits;
+        if (!c.ok) return;
+        const int chunk = u / ta.nstrips;
+        c.u = u;
+        c.lr0 = a.erow_begin + chunk * ta.ty;
+        c.lr1 = min(c.lr0 + ta.ty, a.erow_end);
+        c.k = c.lr0 - 1;
+    };
+    auto step = [&](Cur& c) {
+        if (++c.k > c.lr1) unit_start(c.u + twarps, c);
+    };
+    auto issue = [&](const Cur& c, int s) {
+        desc[s] = make_int4(c.ok ? c.u : -1, c.k, (c.ok && c.k >= c.lr0 && c.k < c.lr1) ? 1 : 0, 0);
+        if (!c.ok) return;
+        AdvSlot* t = slot + s;
+        const int ix0 = (c.u % ta.nstrips) * 31;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], kAdvTx);
+        const int xs = (ix0 - 1) & ~1;
+        tma3(&t->A[0][0], &maps.A, &bar[s], xs, c.k, 0);
+        tma3(&t->H[0][0], &maps.H, &bar[s], xs, c.k, 0);
+        tma2(&t->vx[0][0], &maps.vx, &bar[s], 2 * (ix0 - 1), 2 * c.k + 1);
+        tma2(&t->vy[0][0], &maps.vy, &bar[s], 2 * (ix0 - 1), 2 * c.k + 1);
+    };
+    Cur cur;
+    if (lane == 0) {
+        unit_start(gw, cur);
+        for (int q = 0; q <= P; ++q) {       // positions 0 .. P
+            issue(cur, q);
+            if (cur.ok) step(cur);
+        }
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    auto wait_slot = [&](int s) {
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+    };
+    const int4 d0 = desc[0];
+    if (d0.x < 0) return;
+    wait_slot(0);
+    const double mr[6] = {1.0, 12.0, 12.0, 180.0, 180.0, 144.0};
+    for (int i = 0;; ++i) {
+        const int sL = (i + STAGES - 1) % STAGES, sM = i % STAGES, sU = (i + 1) % STAGES;
+        const int4 dM = desc[sM];
+        if (dM.x < 0) break;
+        if (lane == 0) {                       // position i + 1 + P into the slot of position i - 2 (done)
+            issue(cur, (i + 1 + P) % STAGES);
+            if (cur.ok) step(cur);
+        }
+        const int4 dU = desc[sU];              // issued at iteration i - P or in the prologue
+        if (dU.x >= 0) wait_slot(sU);          // position i+1 belongs to the same unit when i is a job
+        if (dM.z) {                            // a job: element row r = dM.y of strip dM.x % nstrips
+            const int r = dM.y;
+            const int ix0 = (dM.x % ta.nstrips) * 31, ix = ix0 - 1 + lane;
+            const int eo = (ix0 - 1) - ((ix0 - 1) & ~1);
+            const bool valid = lane >= 1 && ix < a.nx;
+            const int ixc = ix < 0 ? 0 : (ix >= a.nx ? a.nx - 1 : ix);
+            const int64_t e = (int64_t)r * a.epitch + ixc;
+            double c0A[6], c0H[6];
+            if (a.a0 != 0.0) {
+#pragma unroll
+                for (int k = 0; k < 6; ++k) { c0A[k] = a.A0[k * a.eplane + e]; c0H[k] = a.H0[k * a.eplane + e]; }
+            }
+            const AdvSlot& L = slot[sL];
+            const AdvSlot& M = slot[sM];
+            const AdvSlot& U = slot[sU];
+            Cf<6> me, nb;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) { me.A[k] = M.A[k][eo + lane]; me.H[k] = M.H[k][eo + lane]; }
+            double ux[3][3], uy[3][3];   // node rows 2r (row below's slot), 2r+1, 2r+2
+#pragma unroll
+            for (int jx = 0; jx < 3; ++jx) {
+                ux[0][jx] = L.vx[1][2 * lane + jx]; uy[0][jx] = L.vy[1][2 * lane + jx];
+                ux[1][jx] = M.vx[0][2 * lane + jx]; uy[1][jx] = M.vy[0][2 * lane + jx];
+                ux[2][jx] = M.vx[1][2 * lane + jx]; uy[2][jx] = M.vy[1][2 * lane + jx];
+            }
+            double FeA[3], FeH[3], FnA[3], FnH[3], FwA[3], FwH[3], FsA[3], FsH[3];
+            {   // east edge (closed box: no flux through x = Lx)
+#pragma unroll
+                for (int k = 0; k < 6; ++k) { nb.A[k] = M.A[k][eo + lane + 1]; nb.H[k] = M.H[k][eo + lane + 1]; }
+                double vn[3]; q2_interp3(ux[0][2], ux[1][2], ux[2][2], vn);
+                q2_edge(true, me, nb, vn, ix >= 0 && ix + 1 < a.nx, FeA, FeH);
+            }
+            {   // north edge: the row above (ghost / next row, or none at the global top)
+#pragma unroll
+                for (int k = 0; k < 6; ++k) { nb.A[k] = U.A[k][eo + lane]; nb.H[k] = U.H[k][eo + lane]; }
+                double vn[3]; q2_interp3(uy[2][0], uy[2][1], uy[2][2], vn);
+                q2_edge(false, me, nb, vn, r + 1 < a.erow_end || a.has_north, FnA, FnH);
+            }
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                FwA[q] = __shfl_up_sync(0xffffffffu, FeA[q], 1);
+                FwH[q] = __shfl_up_sync(0xffffffffu, FeH[q], 1);
+            }
+            {   // south edge: the row below
+#pragma unroll
+                for (int k = 0; k < 6; ++k) { nb.A[k] = L.A[k][eo + lane]; nb.H[k] = L.H[k][eo + lane]; }
+                double vn[3]; q2_interp3(uy[0][0], uy[0][1], uy[0][2], vn);
+                q2_edge(false, nb, me, vn, r > a.erow_begin || a.has_south, FsA, FsH);
+            }
+            // ---- volume term and update: k_advect_q2's code
+            double gvx[3][3], gvy[3][3];
+            {
+                double X[3][3], Y[3][3];
+#pragma unroll
+                for (int jy = 0; jy < 3; ++jy) { q2_interp3(ux[jy][0], ux[jy][1], ux[jy][2], X[jy]); q2_interp3(uy[jy][0], uy[jy][1], uy[jy][2], Y[jy]); }
+#pragma unroll
+                for (int g = 0; g < 3; ++g) {
+                    double o[3];
+                    q2_interp3(X[0][g], X[1][g], X[2][g], o); gvx[0][g] = o[0]; gvx[1][g] = o[1]; gvx[2][g] = o[2];
+                    q2_interp3(Y[0][g], Y[1][g], Y[2][g], o); gvy[0][g] = o[0]; gvy[1][g] = o[1]; gvy[2][g] = o[2];
+                }
+            }
+            const int64_t eo_g = (int64_t)r * a.epitch + ix;
+            double ncv[2][6];
+#pragma unroll
+            for (int tr = 0; tr < 2; ++tr) {
+                const double* c = tr == 0 ? me.A : me.H;
+                const double* Fe = tr == 0 ? FeA : FeH; const double* Fw = tr == 0 ? FwA : FwH;
+                const double* Fn = tr == 0 ? FnA : FnH; const double* Fs = tr == 0 ? FsA : FsH;
+                double cg[3][3], Gx[3][3], Gy[3][3];
+                gp_vals(c, cg);
+#pragma unroll
+                for (int gy = 0; gy < 3; ++gy)
+#pragma unroll
+                    for (int g = 0; g < 3; ++g) { Gx[gy][g] = cg[gy][g] * gvx[gy][g]; Gy[gy][g] = cg[gy][g] * gvy[gy][g]; }
+                double x00, x10, x01, y00, y10, y01;
+                vol_mom(Gx, x00, x10, x01);
+                vol_mom(Gy, y00, y10, y01);
+                double Lk[6];
+                Lk[0] = 0.0;
+                Lk[1] = a.ihx * x00;
+                Lk[2] = a.ihy * y00;
+                Lk[3] = 2.0 * a.ihx * x10;
+                Lk[4] = 2.0 * a.ihy * y01;
+                Lk[5] = fma(a.ihx, x01, a.ihy * y10);
+                double m0, m1, m2;
+                edge_mom(Fe, m0, m1, m2);
+                Lk[0] -= a.ihx * m0; Lk[1] -= a.ihx * 0.5 * m0; Lk[2] -= a.ihx * m1; Lk[3] -= a.ihx * m0 * (1.0 / 6.0);
+                Lk[4] -= a.ihx * m2; Lk[5] -= a.ihx * 0.5 * m1;
+                edge_mom(Fw, m0, m1, m2);
+                Lk[0] += a.ihx * m0; Lk[1] -= a.ihx * 0.5 * m0; Lk[2] += a.ihx * m1; Lk[3] += a.ihx * m0 * (1.0 / 6.0);
+                Lk[4] += a.ihx * m2; Lk[5] -= a.ihx * 0.5 * m1;
+                edge_mom(Fn, m0, m1, m2);
+                Lk[0] -= a.ihy * m0; Lk[1] -= a.ihy * m1; Lk[2] -= a.ihy * 0.5 * m0; Lk[3] -= a.ihy * m2;
+                Lk[4] -= a.ihy * m0 * (1.0 / 6.0); Lk[5] -= a.ihy * 0.5 * m1;
+                edge_mom(Fs, m0, m1, m2);
+                Lk[0] += a.ihy * m0; Lk[1] += a.ihy * m1; Lk[2] -= a.ihy * 0.5 * m0; Lk[3] += a.ihy * m2;
+                Lk[4] += a.ihy * m0 * (1.0 / 6.0); Lk[5] -= a.ihy * 0.5 * m1;
+                const double* c0 = tr == 0 ? c0A : c0H;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const double v = a.a1 * fma(a.dt, Lk[k] * mr[k], c[k]);
+                    ncv[tr][k] = (a.a0 != 0.0) ? fma(a.a0, c0[k], v) : v;
+                }
+            }
+            if (valid) {
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    a.Aout[k * a.eplane + eo_g] = ncv[0][k];
+                    a.Hout[k * a.eplane + eo_g] = ncv[1][k];
+                }
+                if (a.Pg != nullptr) {   // last stage, single rank: the outer-step prep's P at the Gauss
+                    double P[9];         // points of the new A, H (R#17 / Listing 2), bitwise = k_prep_elems_q2
+                    pg_q2(ncv[1], ncv[0], a.Pstar, a.C_conc, P);
+#pragma unroll
+                    for (int g = 0; g < 9; ++g) a.Pg[g * a.eplane + eo_g] = P[g];
+                }
+            }
+        }
+        __syncwarp();   // every lane is done with slot sL before iteration i + 1 refills it
+    }
+}
+
+}  // namespace nxk

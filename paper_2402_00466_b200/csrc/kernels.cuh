@@ -143,7 +143,13 @@ struct SubArgs {
                                     // qtail sub-units each (0 / 1 = off)
     int l2_hints;                   // box TMA kernel: L2 eviction-policy bits (subcycle_tma.cuh)
     int vcarry;                     // box TMA kernel: shared v node row carried in registers (subcycle_tma.cuh)
+    // NEXT-4 sphere (R#26; box TMA kernel instantiated with SPH): per local element row geometry table
+    // (kSphRow doubles, nxsdg.cu sphere_tables); ihx = 1 / (R dlon), ihy = 1 / (R dlat) then
+    const double* __restrict__ sph_rows;
 };
+// sphere row table layout (doubles per local element row)
+constexpr int kSphRow = 32;
+enum { SPH_COS = 0, SPH_SINR = 3, SPH_QA = 6, SPH_QB = 15, SPH_QC = 19, SPH_IMU = 20, SPH_COS_S = 26, SPH_COS_N = 27 };
 
 // Unit u of a persistent kernel's work list -> strip and element rows [lr0, lr1) (lr0 >= lr1: empty).
 // Whole chunks come first, strip-fastest; the last a.ntail selected chunks follow as a.qtail
@@ -536,6 +542,8 @@ struct AdvArgs {
     int periodic, erows_local;
     double ihx, ihy, dt, a0, a1;
     int limit;                                // k_advect_q2: fused R#25 limiter on the stage output
+    const double* sph_rows;                   // k_advect_q2<true>: sphere row tables (R#26), ihx = 1/(R dlon)
+    double* Pg; double Pstar, C_conc;         // k_advect_tma, last stage: also write P at the Gauss points
 };
 
 template <int NA> struct Cf { double A[NA], H[NA]; };

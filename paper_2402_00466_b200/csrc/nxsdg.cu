@@ -25,6 +25,8 @@
 #include "subcycle_tma.cuh"
 #include "subcycle_gen.cuh"
 #include "advect_q2.cuh"
+#include "advect_tma.cuh"
+#include "prep_q2.cuh"
 #include "general_quads.cuh"
 #include "general_steps.cuh"
 
@@ -119,6 +121,12 @@ struct nxsdg_ctx {
     int tail_split = 1;    // persistent kernels: split the last chunks into short sub-units (1) or not (0)
     int l2_policy = 2;     // fused TMA kernels: L2 eviction-policy bits (2 = stores evict_first)
     int v_carry = 1;       // box TMA kernel: a unit's next job re-uses the shared v node row from registers
+    int adv_kernel = 0;    // NXSDG_OPT_ADVECT_KERNEL: 0 = TMA-staged k_advect_tma where it applies, 1 = k_advect_q2
+    int adv_stages = 4;    // NXSDG_OPT_ADVECT_STAGES: slots per warp of k_advect_tma (4 | 5)
+    int adv_ty = 32;       // element rows per k_advect_tma work unit
+    int fuse_pg = 1;       // NXSDG_OPT_FUSE_PREP_PG: the last k_advect_tma stage also writes P_g (single rank)
+    bool pg_fresh = false; // P_g already holds P of the current A, H (written by the last advection stage)
+    bool adv_last = false; // the advection stage being launched is the last one
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
     int dynamic = 1;       // TMA kernel work distribution: 1 = atomic counter, 0 = static round-robin
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
@@ -131,6 +139,10 @@ struct nxsdg_ctx {
     double* vsnap[2] = {nullptr, nullptr};
     bool fpending = false;
     bool general = false, gmaps_ready = false;
+    // NEXT-4 sphere (R#26): lon-lat mesh of radius R, southern edge lat0, element size dlon x dlat [rad]
+    bool sphere = false;
+    double sph_R = 0.0, sph_lat0 = 0.0, sph_dlon = 0.0, sph_dlat = 0.0;
+    double* sph_rows = nullptr;      // kSphRow doubles per local element row
     double* mlump = nullptr; double* gcontrib = nullptr;           // general quads: lumped masses, div scratch
     int map_mode = 1;      // 0: iMJwPSI pre-assembled per element, 1: on the fly from the vertices
     cudaStream_t hstream = nullptr;                                 // halo stream (NCCL overlap)
@@ -254,6 +266,7 @@ static void free_all(nxsdg_ctx* c) {
     if (c->Pg32) { cudaFree(c->Pg32); c->Pg32 = nullptr; }
     if (c->hstage_send) { cudaFree(c->hstage_send); c->hstage_send = nullptr; }
     if (c->verts) { cudaFree(c->verts); c->verts = nullptr; }
+    if (c->sph_rows) { cudaFree(c->sph_rows); c->sph_rows = nullptr; }
     for (int k = 0; k < 4; ++k) if (c->fstage[k]) { cudaFree(c->fstage[k]); c->fstage[k] = nullptr; }
     for (int k = 0; k < 2; ++k) {
         if (c->vsnap[k]) { cudaFree(c->vsnap[k]); c->vsnap[k] = nullptr; }
@@ -406,6 +419,7 @@ extern "C" nxsdg_status nxsdg_set_params(nxsdg_ctx* c, const nxsdg_params* p) {
     if (s) return s;
     c->prm = *p;
     c->prepped = false;
+    c->pg_fresh = false;   // P depends on P*, C
     drop_graphs(c);   // captured launch arguments are stale
     return NXSDG_OK;
 }
@@ -427,8 +441,8 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             c->dynamic = (int)value; break;
         case NXSDG_OPT_PRECISION:
             if (value < 0 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "precision 0|1|2");
-            if (value >= 1 && (c->P != 2 || c->NS != 6 || c->d.nranks != 1 || c->general))
-                return fail(c, NXSDG_ERR_UNSUPPORTED, "FP32 storage: CG2/DG2 (n_S = 6), single rank");
+            if (value >= 1 && (c->P != 2 || c->NS != 6 || c->d.nranks != 1 || c->general || c->sphere))
+                return fail(c, NXSDG_ERR_UNSUPPORTED, "FP32 storage: CG2/DG2 (n_S = 6), single rank, plane box");
             if (value >= 1 && c->stages > 3) c->stages = 3;
             c->precision = (int)value; c->pg32_ok = false; break;
         case NXSDG_OPT_MAP_MODE:
@@ -456,11 +470,21 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_CONST_STAGING:
             if (value < -1 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "node-constant staging -1|0|1|2");
             c->const_regs = (int)value; break;
+        case NXSDG_OPT_ADVECT_KERNEL:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "advect kernel 0|1");
+            c->adv_kernel = (int)value; break;
+        case NXSDG_OPT_ADVECT_STAGES:
+            if (value != 4 && value != 5) return fail(c, NXSDG_ERR_INVALID_ARG, "advect stages 4|5");
+            c->adv_stages = (int)value; break;
+        case NXSDG_OPT_FUSE_PREP_PG:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "fuse prep P_g 0|1");
+            c->fuse_pg = (int)value; break;
         case NXSDG_OPT_MULTIRANK_GRAPH:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "multi-rank graph 0|1");
             c->mr_graph = (int)value; break;
         default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
     }
+    c->pg_fresh = false;
     drop_graphs(c);
     return NXSDG_OK;
 }
@@ -557,6 +581,7 @@ extern "C" nxsdg_status nxsdg_write_state(nxsdg_ctx* c, nxsdg_field f, const dou
         if (s) return s;
     }
     c->prepped = false;
+    c->pg_fresh = false;
     return NXSDG_OK;
 }
 
@@ -749,6 +774,7 @@ extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64
     if (c->d.nranks != 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads are single-rank");
     if (c->NS == 8) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: n_S = 3 | 6");
     if (c->precision != 0) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: FP64 storage only");
+    if (c->sphere) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads or the sphere, not both");
     const int64_t need = 2 * (int64_t)(c->d.nx + 1) * (c->d.ny + 1);
     if (count != need) return fail(c, NXSDG_ERR_INVALID_ARG, "count %lld != %lld", (long long)count, (long long)need);
     if (!c->verts) CU(cudaMalloc(&c->verts, need * sizeof(double)));
@@ -770,6 +796,100 @@ extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64
     else k_gen_lumped<2><<<g, b, 0, c->stream>>>(a);
     LAUNCHED();
     return NXSDG_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-4: spherical lon-lat mesh (R#26)
+// Per local element row (latitudes lat0 + (gr + t) dlat, gr the global row) the fused subcycle and the
+// advection need: cos(lat) and sin(lat)/R at the 3 Gauss latitudes; the blocks Q = M_row^{-1} M_ref of
+// the row's DG mass M_K = R^2 dlon dlat M_row, M_row = int int psi_a psi_b cos(lat) with the 3-point rule,
+// block-diagonal in the S-degree of the centred Legendre modes (S-parts orthogonal): modes {0, 2, 4} =
+// 1 x {1, T, T^2 - 1/12} -> C^{-1} diag(1, 1/12, 1/180), {1, 5} = S x {1, T} -> C2^{-1} diag(1, 1/12),
+// {3} -> 1 / C00, where C_ij = sum_g w_g P_i(T_g) P_j(T_g) cos(lat_g); the reciprocal lumped masses
+// 1 / mu of the three node rows 2 gr + jy for even / odd node columns (m_j = R^2 dlon dlat mu_j,
+// mu = (1/3 | 2/3) x sum over the touching element rows of sum_g w_g L_jy(t_g) cos(lat_g)); and
+// cos(lat) of the row's south / north edge (from the node-row latitude, so a shared edge gets the
+// bitwise-same factor on both sides).
+static void solve3(const double A[3][3], double X[3][3]) {   // X = A^{-1} (symmetric positive definite)
+    const double d = A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1]) - A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0]) +
+                     A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+    X[0][0] = (A[1][1] * A[2][2] - A[1][2] * A[2][1]) / d; X[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) / d;
+    X[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) / d; X[1][0] = (A[1][2] * A[2][0] - A[1][0] * A[2][2]) / d;
+    X[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) / d; X[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) / d;
+    X[2][0] = (A[1][0] * A[2][1] - A[1][1] * A[2][0]) / d; X[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) / d;
+    X[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) / d;
+}
+
+static nxsdg_status sphere_tables(nxsdg_ctx* c) {
+    const double ka = 0.38729833462074170, gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+    const double tg[3] = {0.5 - ka, 0.5, 0.5 + ka};
+    const double L[3][3] = {{0.3 + ka, 0.4, 0.3 - ka}, {0.0, 1.0, 0.0}, {0.3 - ka, 0.4, 0.3 + ka}};   // L_jy(t_g) [g][jy]
+    const int ny = c->d.ny;
+    auto lat = [&](int64_t gr, double t) { return c->sph_lat0 + ((double)gr + t) * c->sph_dlat; };
+    // T(gr, jy) = sum_g w_g L_jy(t_g) cos(lat_g) of element row gr
+    auto trow = [&](int64_t gr, int jy) {
+        double acc = 0.0;
+        for (int g = 0; g < 3; ++g) acc += gw[g] * L[g][jy] * cos(lat(gr, tg[g]));
+        return acc;
+    };
+    std::vector<double> tab((size_t)c->erows_local * kSphRow, 0.0);
+    for (int lr = 0; lr < c->erows_local; ++lr) {
+        const int64_t gr = c->r0 + (lr - c->glo);
+        double* row = &tab[(size_t)lr * kSphRow];
+        double C[3][3] = {};
+        for (int g = 0; g < 3; ++g) {
+            const double la = lat(gr, tg[g]), cg = cos(la), T = tg[g] - 0.5;
+            const double P[3] = {1.0, T, T * T - 1.0 / 12.0};
+            row[SPH_COS + g] = cg;
+            row[SPH_SINR + g] = sin(la) / c->sph_R;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) C[i][j] += gw[g] * P[i] * P[j] * cg;
+        }
+        double Ci[3][3];
+        solve3(C, Ci);
+        const double mref[3] = {1.0, 1.0 / 12.0, 1.0 / 180.0};
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) row[SPH_QA + 3 * i + j] = Ci[i][j] * mref[j];
+        const double d2 = C[0][0] * C[1][1] - C[0][1] * C[1][0];
+        const double C2i[2][2] = {{C[1][1] / d2, -C[0][1] / d2}, {-C[1][0] / d2, C[0][0] / d2}};
+        const double mref2[2] = {1.0, 1.0 / 12.0};
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) row[SPH_QB + 2 * i + j] = C2i[i][j] * mref2[j];
+        row[SPH_QC] = 1.0 / C[0][0];
+        for (int jy = 0; jy < 3; ++jy) {   // node row J = 2 gr + jy, global element rows touching it
+            const int64_t J = 2 * gr + jy;
+            double T = 0.0;
+            if (J % 2) T = trow(gr, 1);
+            else {
+                const int64_t r = J / 2;
+                if (r - 1 >= 0 && r - 1 < ny) T += trow(r - 1, 2);
+                if (r >= 0 && r < ny) T += trow(r, 0);
+            }
+            row[SPH_IMU + 2 * jy + 0] = T > 0.0 ? 3.0 / T : 0.0;          // even column: 2 x 1/6
+            row[SPH_IMU + 2 * jy + 1] = T > 0.0 ? 1.5 / T : 0.0;          // odd column: 2/3
+        }
+        row[SPH_COS_S] = cos(c->sph_lat0 + (double)gr * c->sph_dlat);
+        row[SPH_COS_N] = cos(c->sph_lat0 + (double)(gr + 1) * c->sph_dlat);
+    }
+    if (!c->sph_rows) CU(cudaMalloc(&c->sph_rows, tab.size() * sizeof(double)));
+    CU(cudaMemcpyAsync(c->sph_rows, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return NXSDG_OK;
+}
+
+extern "C" nxsdg_status nxsdg_set_sphere(nxsdg_ctx* c, double radius, double lat0, double lon_extent, double lat_extent) {
+    GUARD(c);
+    const double half_pi = 1.5707963267948966;
+    if (!(radius > 0.0) || !(lon_extent > 0.0) || !(lat_extent > 0.0) || !(fabs(lat0) < half_pi) ||
+        !(fabs(lat0 + lat_extent) < half_pi))
+        return fail(c, NXSDG_ERR_INVALID_ARG, "sphere: radius, extents > 0 and latitudes inside (-pi/2, pi/2)");
+    if (c->P != 2 || c->NS != 6 || c->NA != 6 || c->general || c->precision != 0)
+        return fail(c, NXSDG_ERR_UNSUPPORTED, "sphere: CG2 / DG2 (n_S = n_A = 6), FP64, box mesh");
+    c->sphere = true;
+    c->sph_R = radius; c->sph_lat0 = lat0;
+    c->sph_dlon = lon_extent / c->d.nx; c->sph_dlat = lat_extent / c->d.ny;
+    drop_graphs(c);
+    c->prepped = false;
+    return sphere_tables(c);
 }
 
 static GenArgs gen_args(nxsdg_ctx* c) {
@@ -1280,6 +1400,19 @@ static nxsdg_status launch_prep(nxsdg_ctx* c) {
 }
 
 static nxsdg_status dispatch_prep(nxsdg_ctx* c) {
+    if (c->P == 2 && c->NA == 6) {   // structured (prep_q2.cuh); P_g only if the advection did not write it
+        PrepArgs a = prep_args(c);
+        const int rows = a.node_row_end - a.node_row_begin;
+        dim3 bn(32, 4), gn((unsigned)((c->d.nx + 1 + 31) / 32), (unsigned)((rows / 2 + 1 + 3) / 4));
+        k_prep_nodes_q2<<<gn, bn, 0, c->stream>>>(a);
+        LAUNCHED();
+        if (!c->pg_fresh) {
+            dim3 be(128), ge((unsigned)((c->d.nx + 127) / 128), (unsigned)c->erows_local);
+            k_prep_elems_q2<<<ge, be, 0, c->stream>>>(a);
+            LAUNCHED();
+        }
+        return NXSDG_OK;
+    }
     if (c->P == 1) return c->NA == 1 ? launch_prep<1, 1>(c) : launch_prep<1, 3>(c);
     if (c->NA == 1) return launch_prep<2, 1>(c);
     if (c->NA == 3) return launch_prep<2, 3>(c);
@@ -1306,6 +1439,10 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     a.top_boundary = c->r1 == c->d.ny;
     const double hx = c->d.lx / c->d.nx, hy = c->d.ly / c->d.ny;
     a.ihx = 1.0 / hx; a.ihy = 1.0 / hy;
+    if (c->sphere) {   // R#26: the row tables carry the latitude dependence
+        a.ihx = 1.0 / (c->sph_R * c->sph_dlon); a.ihy = 1.0 / (c->sph_R * c->sph_dlat);
+        a.sph_rows = c->sph_rows;
+    }
     a.ainv = 1.0 / c->prm.alpha; a.fac = 1.0 - a.ainv;
     a.dmin2 = c->prm.DeltaMin * c->prm.DeltaMin;
     a.beta = c->prm.beta; a.b1 = 1.0 + c->prm.beta; a.kc = c->prm.dt * c->prm.f_c;
@@ -1529,20 +1666,20 @@ static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     return NXSDG_OK;
 }
 
-template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false, bool LC = false>
+template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false, bool LC = false, bool SPH = false>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
     using Stage = typename K2StageSel<SF, NS, CL || LC>::T;
     const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + 2 * sizeof(uint64_t) + sizeof(int4));
     static uint64_t attr_set = 0;   // the attribute is per device: one bit per ordinal
     if (!dev_bit_test(attr_set, c->d.device)) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
         dev_bit_set(attr_set, c->d.device);
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC>, 32 * K2_WARPS,
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH>, 32 * K2_WARPS,
                                                      smem));
     const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL || LC, NS) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
@@ -1550,7 +1687,7 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
+    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
         mp, launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
@@ -1568,6 +1705,14 @@ static nxsdg_status launch_tma_mode(nxsdg_ctx* c, int cv, int cs, const SubArgs&
 }
 template <typename SF, typename CT = double, int NS = 6>
 static nxsdg_status launch_tma_sel(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
+    if constexpr (sizeof(SF) == 8 && sizeof(CT) == 8 && NS == 6) {
+        if (c->sphere) {   // R#26: node constants in registers, 2 or 3 stages
+            if (c->stages >= 3) return a.repl ? launch_tma_t<true, 3, SF, CT, 6, true, false, true>(c, cv, cs, a)
+                                              : launch_tma_t<false, 3, SF, CT, 6, true, false, true>(c, cv, cs, a);
+            return a.repl ? launch_tma_t<true, 2, SF, CT, 6, true, false, true>(c, cv, cs, a)
+                          : launch_tma_t<false, 2, SF, CT, 6, true, false, true>(c, cv, cs, a);
+        }
+    }
     int mode = const_mode(c);
     if (sizeof(SF) != 8 && mode == 2) return fail(c, NXSDG_ERR_UNSUPPORTED, "late node constants need FP64 storage");
     if (c->stages == 2) return launch_tma_mode<SF, CT, NS, 2>(c, cv, cs, a, mode);
@@ -1754,6 +1899,8 @@ static nxsdg_status check_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
     if (c->general && !(flags & NXSDG_UNFUSED) && n > 0 && !use_tma(c))
         return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: the fused subcycle needs CG2/DG2 and the TMA kernel; "
                                               "use NXSDG_UNFUSED");
+    if (c->sphere && n > 0 && ((flags & NXSDG_UNFUSED) || !use_tma(c) || c->precision != 0))
+        return fail(c, NXSDG_ERR_UNSUPPORTED, "sphere: fused FP64 TMA subcycles only");
     if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
     if (!(flags & NXSDG_BEGIN_STEP) && !c->prepped) return fail(c, NXSDG_ERR_STATE, "first call of an outer step needs NXSDG_BEGIN_STEP");
     return NXSDG_OK;
@@ -1925,6 +2072,7 @@ extern "C" nxsdg_status nxsdg_run_step(nxsdg_ctx* c, nxsdg_step st) {
     if (st == NXSDG_STEP_VELOCITY && !c->prepped)
         return fail(c, NXSDG_ERR_STATE, "needs a BEGIN_STEP (nxsdg_mevp_substeps(ctx, 0, NXSDG_BEGIN_STEP))");
     if (c->d.nranks > 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "debug steps are single-rank");
+    if (c->sphere) return fail(c, NXSDG_ERR_UNSUPPORTED, "sphere: no unfused debug steps");
     nxsdg_status s = ensure_debug_buffers(c);
     if (s) return s;
     if (c->general) return st == NXSDG_STEP_STRESS ? general_stress(c) : general_step(c, st);
@@ -1934,6 +2082,51 @@ extern "C" nxsdg_status nxsdg_run_step(nxsdg_ctx* c, nxsdg_step st) {
 // ---------------------------------------------------------------- advection
 // the structured CG2/DG2 advection kernel applies the R#25 limiter in its epilogue
 static bool adv_fused_limit(const nxsdg_ctx* c) { return c->limiter && !c->general && c->P == 2 && c->NA == 6 && c->variant == 0; }
+
+// k_advect_tma applies to the configs' structured closed-box CG2/DG2 pair (no limiter, no sphere)
+static bool use_adv_tma(const nxsdg_ctx* c) {
+    return c->P == 2 && c->NA == 6 && c->variant == 0 && c->adv_kernel == 0 && !c->general && !c->sphere &&
+           !c->limiter && c->d.bc == NXSDG_BC_CLOSED;
+}
+// single rank: the last k_advect_tma stage writes P_g for the new A, H (the ghost rows of a strip need
+// their neighbour's new A, H, so row strips keep the separate P_g pass after the BEGIN_STEP exchange)
+static bool fuse_pg(const nxsdg_ctx* c) { return c->fuse_pg && c->d.nranks == 1 && use_adv_tma(c); }
+
+template <int ST>
+static nxsdg_status launch_adv_tma_t(nxsdg_ctx* c, const AdvMaps& mp, const AdvTmaArgs& ta) {
+    const size_t smem = (size_t)ADV_TMA_WARPS * ST * (sizeof(AdvSlot) + sizeof(uint64_t) + sizeof(int4));
+    static uint64_t attr_set = 0;
+    if (!dev_bit_test(attr_set, c->d.device)) {
+        CU(cudaFuncSetAttribute(k_advect_tma<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dev_bit_set(attr_set, c->d.device);
+    }
+    int nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_advect_tma<ST>, 32 * ADV_TMA_WARPS, smem));
+    const int64_t units = (int64_t)ta.nstrips * ta.nchunks;
+    const int64_t want = (units + ADV_TMA_WARPS - 1) / ADV_TMA_WARPS;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
+    k_advect_tma<ST><<<blocks, 32 * ADV_TMA_WARPS, smem, c->stream>>>(mp, ta);
+    return NXSDG_OK;
+}
+
+static nxsdg_status launch_adv_tma(nxsdg_ctx* c, const AdvArgs& a) {
+    AdvMaps mp;
+    const cuuint64_t nx = c->d.nx, er = c->erows_local, ncols = 2 * (cuuint64_t)c->d.nx + 1, nr = c->nrows_local;
+    const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 8, (cuuint64_t)c->eplane * 8};
+    const cuuint64_t ns[2] = {(cuuint64_t)c->npitch * 8, (cuuint64_t)c->nn * 8};
+    const cuuint64_t dA[3] = {nx, er, 6}, dV[2] = {ncols, nr};
+    const cuuint32_t bA[3] = {ADV_COLS, 1, 6}, bV[2] = {K2_VCOLS, 2};
+    if (!encode(&mp.A, a.Ain, 3, dA, es, bA) || !encode(&mp.H, a.Hin, 3, dA, es, bA) ||
+        !encode(&mp.vx, a.vx, 2, dV, ns, bV) || !encode(&mp.vy, a.vy, 2, dV, ns, bV))
+        return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled (advection) failed");
+    AdvTmaArgs ta{};
+    ta.a = a;
+    ta.nstrips = (c->d.nx + 1 + 30) / 31;
+    ta.ty = c->adv_ty;
+    ta.nchunks = (c->nown + ta.ty - 1) / ta.ty;
+    return c->adv_stages == 5 ? launch_adv_tma_t<5>(c, mp, ta) : launch_adv_tma_t<4>(c, mp, ta);
+}
 
 template <int P, int NA>
 static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const double* Hin, double* Aout,
@@ -1946,13 +2139,22 @@ static nxsdg_status launch_advect_stage(nxsdg_ctx* c, const double* Ain, const d
     a.has_south = c->glo; a.has_north = c->ghi;
     a.periodic = c->d.bc == NXSDG_BC_PERIODIC; a.erows_local = c->erows_local;
     a.ihx = 1.0 / (c->d.lx / c->d.nx); a.ihy = 1.0 / (c->d.ly / c->d.ny);
+    if (c->sphere) {
+        a.ihx = 1.0 / (c->sph_R * c->sph_dlon); a.ihy = 1.0 / (c->sph_R * c->sph_dlat);
+        a.sph_rows = c->sph_rows;
+    }
     a.dt = dt; a.a0 = a0; a.a1 = a1;
     a.limit = adv_fused_limit(c);
+    if (c->adv_last && fuse_pg(c)) { a.Pg = c->Pg; a.Pstar = c->prm.Pstar; a.C_conc = c->prm.C_conc; }
     dim3 b(32, ADV_ROWS), g((unsigned)((c->d.nx + 31) / 32), (unsigned)((c->nown + ADV_ROWS - 1) / ADV_ROWS));
     if (c->general) {
         GenAdvArgs ga{a, c->verts, c->d.ny};
         k_advect_gen<P, NA><<<g, b, 0, c->stream>>>(ga);
-    } else if (P == 2 && NA == 6 && c->variant == 0) k_advect_q2<<<g, b, 0, c->stream>>>(a);   // structured
+    } else if (P == 2 && NA == 6 && use_adv_tma(c)) {   // persistent TMA-staged form (advect_tma.cuh)
+        nxsdg_status st = launch_adv_tma(c, a);
+        if (st) return st;
+    } else if (P == 2 && NA == 6 && c->sphere) k_advect_q2<true><<<g, b, 0, c->stream>>>(a);   // R#26
+    else if (P == 2 && NA == 6 && c->variant == 0) k_advect_q2<false><<<g, b, 0, c->stream>>>(a);   // structured
     else k_advect<P, NA><<<g, b, 0, c->stream>>>(a);
     LAUNCHED();
     return NXSDG_OK;
@@ -1994,6 +2196,7 @@ static nxsdg_status limit_t(nxsdg_ctx* c, double* A, double* H) {
 
 static nxsdg_status advect_stage(nxsdg_ctx* c, double dt, int stage) {
     nxsdg_status s;
+    c->adv_last = stage == n_stages(c) - 1;
     if (c->P == 1) s = c->NA == 1 ? advect_t<1, 1>(c, dt, stage) : advect_t<1, 3>(c, dt, stage);
     else if (c->NA == 1) s = advect_t<2, 1>(c, dt, stage);
     else if (c->NA == 3) s = advect_t<2, 3>(c, dt, stage);
@@ -2011,12 +2214,15 @@ static nxsdg_status advect_finish(nxsdg_ctx* c) {
     std::swap(c->A, c->Asc[last]);
     std::swap(c->H, c->Hsc[last]);
     c->prepped = false;
+    c->pg_fresh = fuse_pg(c);   // the last stage wrote P of the new A, H
     return NXSDG_OK;
 }
 
 extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
     GUARD(c);
     if (!(dt >= 0.0)) return fail(c, NXSDG_ERR_INVALID_ARG, "dt < 0");
+    if (c->sphere && c->limiter) return fail(c, NXSDG_ERR_UNSUPPORTED, "sphere: no limiter (R#25 uses the box mean)");
+    c->pg_fresh = false;
     if (c->general && c->d.bc != NXSDG_BC_CLOSED) return fail(c, NXSDG_ERR_UNSUPPORTED, "general quads: closed box only");
     if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_LOOPBACK)
         return fail(c, NXSDG_ERR_STATE, "loopback ranks advect through nxsdg_group_advect");

@@ -1,0 +1,117 @@
+// Outer-step prep (row a1; Listing 2, R#17) for the configs' CG2 / DG2 pair (n_A = 6),
+// structured: the table-driven k_prep_nodes<2, 6> / k_prep_elems<2, 6> of kernels.cuh looked the DG
+// basis up in __constant__ with a per-thread node index (divergent constant-cache accesses, 4 gathers of
+// 12 coefficients per node); here the DG2 values at the Q2 node positions (S, T in {-1/2, 0, 1/2}) are
+// folded into the code, one thread updates the 2 x 2 nodes an element owns from the 4 elements around
+// them, and the per-node arithmetic is k_prep_nodes' own (same sums in the same order: bitwise equal).
+// The P at the Gauss points (pg_q2) is shared with the last advection stage, which produces it for
+// the new A, H while they are still in registers.
+#pragma once
+#include "advect_q2.cuh"
+
+namespace nxk {
+
+// DG2 value at local node (jx, jy) (s, t = jx/2, jy/2): sum_k c_k psi_k, the k order of k_prep_nodes
+template <int JX, int JY>
+__device__ __forceinline__ double dg2_node(const double* c) {
+    constexpr double S = 0.5 * JX - 0.5, T = 0.5 * JY - 0.5;
+    const double psi[6] = {1.0, S, T, S * S - 1.0 / 12.0, T * T - 1.0 / 12.0, S * T};
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) v += c[k] * psi[k];
+    return v;
+}
+
+// P = P* h exp(-C (1 - a)) at the 9 Gauss points, h = max(0, H), a = clamp(A, 0, 1) (Listing 2)
+__device__ __forceinline__ void pg_q2(const double h[6], const double c[6], double Pstar, double C, double P[9]) {
+    double hg[3][3], ag[3][3];
+    gp_vals(h, hg);
+    gp_vals(c, ag);
+#pragma unroll
+    for (int gy = 0; gy < 3; ++gy)
+#pragma unroll
+        for (int gx = 0; gx < 3; ++gx) {
+            const double hv = fmax(hg[gy][gx], 0.0), av = fmin(fmax(ag[gy][gx], 0.0), 1.0);
+            P[gy * 3 + gx] = Pstar * hv * exp(-C * (1.0 - av));
+        }
+}
+
+__global__ void k_prep_elems_q2(PrepArgs a) {
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x, lr = blockIdx.y;
+    if (ix >= a.nx || lr >= a.erows_local) return;
+    const int64_t e = (int64_t)lr * a.epitch + ix;
+    double h[6], c[6], P[9];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { h[k] = a.H[k * a.eplane + e]; c[k] = a.A[k * a.eplane + e]; }
+    pg_q2(h, c, a.Pstar, a.C_conc, P);
+#pragma unroll
+    for (int g = 0; g < 9; ++g) a.Pg[g * a.eplane + e] = P[g];
+}
+
+// thread (ix, pr): nodes (2 ix + q, 2 pr + jy), q, jy in {0, 1}, from elements (ix - 1 | ix, pr - 1 | pr)
+__global__ void k_prep_nodes_q2(PrepArgs a) {
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pr = blockIdx.y * blockDim.y + threadIdx.y + (a.node_row_begin >> 1);
+    if (ix > a.nx || 2 * pr >= a.node_row_end) return;
+    // the 4 elements around the nodes [dy][dx]: dy = 0 the row below (pr - 1), dx = 0 the west one (ix - 1)
+    double hE[2][2][6], aE[2][2][6];
+    bool ok[2][2];
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+            const int ex = ix - 1 + dx, ey = pr - 1 + dy;
+            ok[dy][dx] = ex >= 0 && ex < a.nx && ey >= 0 && ey < a.elem_rows_with_nodes;
+            const int64_t e = (int64_t)(ok[dy][dx] ? ey : 0) * a.epitch + (ok[dy][dx] ? ex : 0);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                hE[dy][dx][k] = ok[dy][dx] ? a.H[k * a.eplane + e] : 0.0;
+                aE[dy][dx][k] = ok[dy][dx] ? a.A[k * a.eplane + e] : 0.0;
+            }
+        }
+#pragma unroll
+    for (int jy = 0; jy < 2; ++jy) {
+        const int jr = 2 * pr + jy;
+        if (jr < a.node_row_begin || jr >= a.node_row_end) continue;
+        double Hn[2], An[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            double hs = 0.0, as = 0.0;
+            int cnt = 0;
+            // k_prep_nodes' order: SW, SE, NW, NE (the node's local position in each)
+            if (jy == 0 && q == 0) {
+                if (ok[0][0]) { hs += dg2_node<2, 2>(hE[0][0]); as += dg2_node<2, 2>(aE[0][0]); ++cnt; }
+                if (ok[0][1]) { hs += dg2_node<0, 2>(hE[0][1]); as += dg2_node<0, 2>(aE[0][1]); ++cnt; }
+                if (ok[1][0]) { hs += dg2_node<2, 0>(hE[1][0]); as += dg2_node<2, 0>(aE[1][0]); ++cnt; }
+                if (ok[1][1]) { hs += dg2_node<0, 0>(hE[1][1]); as += dg2_node<0, 0>(aE[1][1]); ++cnt; }
+            } else if (jy == 0) {
+                if (ok[0][1]) { hs += dg2_node<1, 2>(hE[0][1]); as += dg2_node<1, 2>(aE[0][1]); ++cnt; }
+                if (ok[1][1]) { hs += dg2_node<1, 0>(hE[1][1]); as += dg2_node<1, 0>(aE[1][1]); ++cnt; }
+            } else if (q == 0) {
+                if (ok[1][0]) { hs += dg2_node<2, 1>(hE[1][0]); as += dg2_node<2, 1>(aE[1][0]); ++cnt; }
+                if (ok[1][1]) { hs += dg2_node<0, 1>(hE[1][1]); as += dg2_node<0, 1>(aE[1][1]); ++cnt; }
+            } else {
+                if (ok[1][1]) { hs += dg2_node<1, 1>(hE[1][1]); as += dg2_node<1, 1>(aE[1][1]); ++cnt; }
+            }
+            Hn[q] = cnt ? fmax(hs / cnt, 1e-4) : 1e-4;
+            An[q] = cnt ? fmin(fmax(as / cnt, 0.0), 1.0) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int I = 2 * ix + q;
+            if (I > 2 * a.nx) continue;
+            const int64_t n = (int64_t)jr * a.npitch + I;
+            const double m = a.rho_ice * Hn[q];
+            const double c1 = m / a.dt;
+            const double axv = a.ax[n], ayv = a.ay[n];
+            const double amag = sqrt(axv * axv + ayv * ayv);
+            const double drag = An[q] * a.Fa * amag;
+            a.c1[n] = c1;
+            a.rx0[n] = c1 * a.vx[n] + drag * axv - m * a.f_c * a.oy[n];
+            a.ry0[n] = c1 * a.vy[n] + drag * ayv + m * a.f_c * a.ox[n];
+            a.cafo[n] = An[q] * a.Fo;
+        }
+    }
+}
+
+}  // namespace nxk

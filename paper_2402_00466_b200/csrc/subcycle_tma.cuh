@@ -328,6 +328,147 @@ __device__ __forceinline__ void div_t(const double (&S)[NS], double h, double r[
     }
 }
 
+// ---------------------------------------------------------------- sphere (NEXT-4, R#26)
+// On a lon-lat element the metric varies with latitude only, i.e. with t: in the orthonormal east-north
+// frame |J| = R^2 cos(lat) dlon dlat, J^-1 = diag(1 / (R cos(lat) dlon), 1 / (R dlat)), and the frame's
+// metric term tan(lat)/R enters the strain (eps11 -= v tan/R, eps12 += u tan/(2R)) and, as its adjoint,
+// the divergence.  So the fused kernel evaluates the strain pointwise at the 3 x 3 Gauss points (gy =
+// latitude row), projects |J| eps / (R^2 dlon dlat) = cos(lat) eps with the box moments and the row's
+// cos-weighted DG mass, whose inverse is block-diagonal in the S-degree of the centred Legendre modes
+// ({0, 2, 4}, {1, 5}, {3}: the per-row blocks Q = M_row^{-1} M_ref of the row table), and contracts the
+// divergence with the 1D Lagrange values / derivatives at the Gauss abscissae.  Row tables: nxsdg.cu.
+__device__ __forceinline__ void q2_gauss3(double n0, double n1, double n2, double out[3]) {
+    const double s = n0 + n2, d = n0 - n2, m = fma(0.3, s, 0.4 * n1);
+    out[0] = fma(kA, d, m); out[1] = n1; out[2] = fma(-kA, d, m);
+}
+// the Q2 field V[jy][jx] at the 9 Gauss points (g = gy*3 + gx)
+__device__ __forceinline__ void q2_at_gauss(const double V[3][3], double out[9]) {
+    double X[3][3];
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) q2_gauss3(V[jy][0], V[jy][1], V[jy][2], X[jy]);
+#pragma unroll
+    for (int gx = 0; gx < 3; ++gx) {
+        double o[3];
+        q2_gauss3(X[0][gx], X[1][gx], X[2][gx], o);
+        out[gx] = o[0]; out[3 + gx] = o[1]; out[6 + gx] = o[2];
+    }
+}
+// exact pointwise d/ds, d/dt of a Q2 field at the Gauss points: the derivative lies in the n_S = 8
+// space (R#24), whose strain coefficients are exact
+__device__ __forceinline__ void q2_ds_at_gauss(const double V[3][3], double out[9]) {
+    double E[8];
+    strain_s<double, 8>(V, E);
+    eval_gp<true, true>(E, out);
+}
+__device__ __forceinline__ void q2_dt_at_gauss(const double V[3][3], double out[9]) {
+    double E[8];
+    strain_t<double, 8>(V, E);
+    eval_gp<true, true>(E, out);
+}
+// E = Q p with the row's blocks (p: the box moments M_ref^{-1} sum_g w_g psi(g) G(g))
+__device__ __forceinline__ void sph_apply_q(const double* __restrict__ row, const double (&p)[6], double (&E)[6]) {
+    const double* QA = row + SPH_QA;
+    const double* QB = row + SPH_QB;
+    E[0] = fma(__ldg(QA + 0), p[0], fma(__ldg(QA + 1), p[2], __ldg(QA + 2) * p[4]));
+    E[2] = fma(__ldg(QA + 3), p[0], fma(__ldg(QA + 4), p[2], __ldg(QA + 5) * p[4]));
+    E[4] = fma(__ldg(QA + 6), p[0], fma(__ldg(QA + 7), p[2], __ldg(QA + 8) * p[4]));
+    E[1] = fma(__ldg(QB + 0), p[1], __ldg(QB + 1) * p[5]);
+    E[5] = fma(__ldg(QB + 2), p[1], __ldg(QB + 3) * p[5]);
+    E[3] = __ldg(row + SPH_QC) * p[3];
+}
+// DG strain of v on a sphere row, evaluated at the Gauss points as the trace u = e11 + e22, the half
+// difference w = (e11 - e22)/2 and e12 (the box kernel's variables); ihx = 1 / (R dlon), ihy = 1 / (R dlat)
+__device__ __forceinline__ void sph_strain(const double Vx[3][3], const double Vy[3][3], const double* __restrict__ row,
+                                           double ihx, double ihy, double eu[9], double ew[9], double e12[9]) {
+    double dsx[9], dtx[9], dsy[9], dty[9], vxg[9], vyg[9];
+    q2_ds_at_gauss(Vx, dsx); q2_dt_at_gauss(Vx, dtx);
+    q2_ds_at_gauss(Vy, dsy); q2_dt_at_gauss(Vy, dty);
+    q2_at_gauss(Vx, vxg); q2_at_gauss(Vy, vyg);
+    double Gu[9], Gw[9], Gz[9];
+#pragma unroll
+    for (int g = 0; g < 9; ++g) {   // cos(lat) eps = |J| eps / (R^2 dlon dlat)
+        const double c = __ldg(row + SPH_COS + g / 3), sr = __ldg(row + SPH_SINR + g / 3), ct = c * ihy;
+        const double g11 = fma(ihx, dsx[g], -sr * vyg[g]);
+        const double g22 = ct * dty[g];
+        Gu[g] = g11 + g22;
+        Gw[g] = 0.5 * (g11 - g22);
+        Gz[g] = 0.5 * fma(ct, dtx[g], fma(ihx, dsy[g], sr * vxg[g]));
+    }
+    double p[6], E[6];
+    proj_coeffs(Gu, 1.0, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, eu);
+    proj_coeffs(Gw, 1.0, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, ew);
+    proj_coeffs(Gz, 1.0, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, e12);
+}
+// S11 <- fac S11 + Q (Ra + Rb), S22 <- fac S22 + Q (Ra - Rb), S12 <- fac S12 + Q Rz, with the Gauss-point
+// values weighted by cos(lat) (|J_g| / (R^2 dlon dlat)); b's and z's factor 1/2 in the moments' scale
+__device__ __forceinline__ void sph_project(double Ga[9], double Gb[9], double Gz[9], const double* __restrict__ row,
+                                            double fac, double (&S11)[6], double (&S12)[6], double (&S22)[6]) {
+#pragma unroll
+    for (int g = 0; g < 9; ++g) {
+        const double c = __ldg(row + SPH_COS + g / 3);
+        Ga[g] *= c; Gb[g] *= c; Gz[g] *= c;
+    }
+    double p[6], qa[6], qb[6], qz[6];
+    proj_coeffs(Ga, 1.0, p); sph_apply_q(row, p, qa);
+    proj_coeffs(Gb, 0.5, p); sph_apply_q(row, p, qb);
+    proj_coeffs(Gz, 0.5, p); sph_apply_q(row, p, qz);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        S11[k] = fma(fac, S11[k], qa[k] + qb[k]);
+        S22[k] = fma(fac, S22[k], qa[k] - qb[k]);
+        S12[k] = fma(fac, S12[k], qz[k]);
+    }
+}
+// F / m at this element's nodes r[jx][jy] (as div_s / div_t produce them): the weak form with the metric,
+//   F^x_j = -sum_g w_g |J_g| [s11 dphi_j/dx + s12 dphi_j/dy + s12 phi_j tan/R]
+//   F^y_j = -sum_g w_g |J_g| [s12 dphi_j/dx + s22 dphi_j/dy - s11 phi_j tan/R]
+// over the lumped mass m_j = R^2 dlon dlat mu_j (1/mu per node row and column parity in the row table)
+__device__ __forceinline__ void sph_divergence(const double (&S11)[6], const double (&S12)[6], const double (&S22)[6],
+                                               const double* __restrict__ row, double ihx, double ihy,
+                                               double rX[3][3], double rY[3][3]) {
+    double s11[9], s12[9], s22[9];
+    eval_gp<true, true>(S11, s11); eval_gp<true, true>(S12, s12); eval_gp<true, true>(S22, s22);
+    const double w[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+    const double L[3][3] = {{0.3 + kA, 0.4, 0.3 - kA}, {0.0, 1.0, 0.0}, {0.3 - kA, 0.4, 0.3 + kA}};   // [g][j]
+    const double dL[3][3] = {{-4.0 * kA - 1.0, 8.0 * kA, 1.0 - 4.0 * kA}, {-1.0, 0.0, 1.0},
+                             {4.0 * kA - 1.0, -8.0 * kA, 4.0 * kA + 1.0}};
+#pragma unroll
+    for (int gy = 0; gy < 3; ++gy) {
+        double X1[3], X2[3], Y1[3], Y2[3], Y3[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            X1[j] = 0.0; X2[j] = 0.0; Y2[j] = 0.0; Y3[j] = 0.0;
+#pragma unroll
+            for (int gx = 0; gx < 3; ++gx) {
+                const int g = gy * 3 + gx;
+                X1[j] = fma(w[gx] * dL[gx][j], s11[g], X1[j]);
+                X2[j] = fma(w[gx] * L[gx][j], s12[g], X2[j]);
+                Y2[j] = fma(w[gx] * L[gx][j], s22[g], Y2[j]);
+                Y3[j] = fma(w[gx] * L[gx][j], s11[g], Y3[j]);
+            }
+            Y1[j] = 0.0;
+#pragma unroll
+            for (int gx = 0; gx < 3; ++gx) Y1[j] = fma(w[gx] * dL[gx][j], s12[gy * 3 + gx], Y1[j]);
+        }
+        const double c = __ldg(row + SPH_COS + gy), sr = __ldg(row + SPH_SINR + gy);
+        const double fs = w[gy] * ihx, ft = w[gy] * ihy * c, fm = w[gy] * sr;
+#pragma unroll
+        for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+            for (int jy = 0; jy < 3; ++jy) {
+                rX[jx][jy] = fma(fs * L[gy][jy], X1[jx], fma(fma(ft, dL[gy][jy], fm * L[gy][jy]), X2[jx], rX[jx][jy]));
+                rY[jx][jy] = fma(fs * L[gy][jy], Y1[jx], fma(ft * dL[gy][jy], Y2[jx], fma(-fm * L[gy][jy], Y3[jx], rY[jx][jy])));
+            }
+    }
+#pragma unroll
+    for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+            const double im = -__ldg(row + SPH_IMU + 2 * jy + (jx & 1));
+            rX[jx][jy] *= im; rY[jx][jy] *= im;
+        }
+}
+
 // ---------------------------------------------------------------- the kernel
 // LC = true (with CL = false, FP64 storage): the constants are not staged with the job; once the stress
 // update has read S and P_g, lane 0 TMA-loads them (5952 B) into the stage from the start of its S region
@@ -335,9 +476,10 @@ __device__ __forceinline__ void div_t(const double (&S)[NS], double h, double r[
 // registers.  For n_S = 6 the S region is 4896 B, so the constants also overwrite the start of P_g; both
 // regions have been consumed by then (the static_assert below keeps them clear of the v rows, which the
 // divergence / velocity still read).
-template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false>
+template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false, bool SPH = false>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
     static_assert(!(CL && LC), "one node-constant mode");
+    static_assert(!SPH || (NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8), "sphere: FP64, n_S = 6");
     static_assert(!LC || sizeof(SF) == 8, "late constants need the FP64 S region");
     using StageNC_ = K2StageNC<SF, NS>;
     static_assert(!LC || offsetof(StageNC_, vx) >= 6 * 2 * K2_CCOLS * sizeof(double),
@@ -508,7 +650,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         //      the trace u = e11 + e22, the half difference w = (e11 - e22)/2 and e12, in which
         //      Hibler's Delta^2 = 1.25 (e11^2 + e22^2) + 1.5 e11 e22 + e12^2 is u^2 + w^2 + e12^2
         CT eu[9], ew[9], e12[9];
-        {
+        const double* __restrict__ srow = SPH ? a.sph_rows + (int64_t)lr * kSphRow : nullptr;
+        if constexpr (SPH) {
+            sph_strain(Vx, Vy, srow, ihx, ihy, eu, ew, e12);
+        } else {
             CT Es[NS], Et[NS], E[NS];
             const CT cihx = (CT)ihx, cihy = (CT)ihy;
             const CT hx2 = CT(0.5) * cihx, hy2 = CT(0.5) * cihy;
@@ -548,8 +693,12 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             C22[k] = (CT)t.S[2 * NS + k][eo + lane];
         }
         const CT cfac = (CT)fac;
-        project_pair(eu, ew, cfac, C11, C22);
-        project(e12, 0.5, cfac, C12);
+        if constexpr (SPH) {
+            sph_project(eu, ew, e12, srow, fac, C11, C12, C22);
+        } else {
+            project_pair(eu, ew, cfac, C11, C22);
+            project(e12, 0.5, cfac, C12);
+        }
         if constexpr (LC) {   // S and P_g of this stage are consumed (their values already feed the
             if (!cur.ring) {  // projection FMAs): the node constants go there
                 asm volatile("" ::: "memory");   // every lane's reads of the stage are issued before the barrier
@@ -589,8 +738,12 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j) { rX[i][j] = 0.0; rY[i][j] = 0.0; }
-        div_s(S11, mhx, rX); div_t(S12, mhy, rX);      // already divided by the lumped mass
-        div_s(S12, mhx, rY); div_t(S22, mhy, rY);
+        if constexpr (SPH) {
+            sph_divergence(S11, S12, S22, srow, ihx, ihy, rX, rY);
+        } else {
+            div_s(S11, mhx, rX); div_t(S12, mhy, rX);      // already divided by the lumped mass
+            div_s(S12, mhx, rY); div_t(S22, mhy, rY);
+        }
         // ---- per-node gather (row below, W, E) + velocity update (R#11), branch-free:
         //      all four owned nodes are updated, boundary nodes select 0, stores are predicated
         const bool nvalid = lane >= 1 && ix >= 0 && ix <= a.nx && !cur.ring;

@@ -31,7 +31,7 @@ STEPS = {"strain": 0, "stress": 1, "divergence": 2, "velocity": 3}
 TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_P2P = 0, 1, 2, 3
 (OPT_FUSED_KERNEL, OPT_CHUNK_ROWS, OPT_CTAS_PER_SM, OPT_STAGES, OPT_DYNAMIC, OPT_MAP_MODE, OPT_PRECISION,
  OPT_P2P_FUSED_STORES, OPT_LIMITER, OPT_CONST_STAGING, OPT_TAIL_SPLIT, OPT_L2_POLICY, OPT_V_ROW_CARRY,
- OPT_MULTIRANK_GRAPH) = range(14)
+ OPT_MULTIRANK_GRAPH, OPT_ADVECT_KERNEL, OPT_ADVECT_STAGES, OPT_FUSE_PREP_PG) = range(17)
 
 
 class NxsdgError(RuntimeError):
@@ -94,6 +94,7 @@ def _load() -> C.CDLL:
         "nxsdg_p2p_connect": ([vp, vp, vp], i32),
         "nxsdg_p2p_connect_local": ([C.POINTER(vp), i32], i32),
         "nxsdg_transport_info": ([vp, C.c_char_p, i64], i64),
+        "nxsdg_set_sphere": ([vp, dbl, dbl, dbl, dbl], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -111,7 +112,7 @@ EXPORTED = [
     "nxsdg_bytes_per_element_subcycle", "nxsdg_stream", "nxsdg_set_option", "nxsdg_halo_plan",
     "nxsdg_local_geometry", "nxsdg_set_forcing_cyclone", "nxsdg_set_vertices", "nxsdg_stream_join",
     "nxsdg_debug_reference_tables", "nxsdg_p2p_export", "nxsdg_p2p_connect", "nxsdg_p2p_connect_local",
-    "nxsdg_transport_info",
+    "nxsdg_transport_info", "nxsdg_set_sphere",
 ]
 HALO_V, HALO_S, HALO_AH, HALO_AH_SCR0, HALO_AH_SCR1 = 1, 2, 4, 8, 16
 HF_VX, HF_VY, HF_S, HF_A, HF_H, HF_A_SCR0, HF_H_SCR0, HF_A_SCR1, HF_H_SCR1 = range(9)
@@ -319,6 +320,11 @@ class Mesh:
 
     def stream_join(self):
         _chk(self.h, lib.nxsdg_stream_join(self.h), "stream_join")
+
+    def set_sphere(self, radius: float, lat0: float, lon_extent: float, lat_extent: float):
+        """NEXT-4 (R#26): lon-lat mesh on the sphere (angles in radians)."""
+        _chk(self.h, lib.nxsdg_set_sphere(self.h, float(radius), float(lat0), float(lon_extent), float(lat_extent)),
+             "set_sphere")
 
     def set_vertices(self, xy):
         p, n, mem = _ptr_mem(xy)

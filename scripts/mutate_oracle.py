@@ -79,7 +79,7 @@ MUTANTS = [
     ("limiter_drops_mean", "limiter scales c without restoring the mean",
      "ce[0] += (1.0 - theta) * cbar;", "ce[0] += 0.0 * cbar;"),
     ("strain_e12_no_half", "eps12 = dvx/dy + dvy/dx (engineering shear)",
-     "eps12 = 0.5 * (dvxdy + dvydx)", "eps12 = (dvxdy + dvydx)"),
+     "eps12 = 0.5 * (dvxdy + dvydx + kt * vgx)", "eps12 = (dvxdy + dvydx + kt * vgx)"),
     ("stress_relaxation_factor", "S <- (1 - 1/alpha^2) S + ...",
      "double fac = 1.0 - alphaInv;", "double fac = 1.0 - alphaInv * alphaInv;"),
     ("jinv_cofactor_sign", "J^-1 off-diagonal with the wrong sign",

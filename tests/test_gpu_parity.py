@@ -878,6 +878,52 @@ def test_graph_replay_matches_eager_chunks(nx):
         np.testing.assert_array_equal(a[k], b[k])
 
 
+@pytest.mark.parametrize("shape", [(70, 75), (31, 33), (1, 5), (6, 1), (130, 97), (32, 64)])
+@pytest.mark.parametrize("stages", [4, 5])
+def test_advect_tma_bitwise_equals_q2(nx, shape, stages):
+    """The persistent TMA-staged advection (k_advect_tma, the default for the closed-box CG2/DG2 pair) does
+    k_advect_q2's arithmetic call for call: three SSP-RK3 stages (and the prep that follows) bitwise equal
+    across strip / chunk boundaries, ragged edges and degenerate shapes."""
+    nxe, nye = shape
+    st = case(nxe, nye, 2, 6, 6, "random", nxe * 1e3, nye * 1e3)
+    out = []
+    for kern in (0, 1):
+        with nx.Mesh(nxe, nye, nxe * 1e3, nye * 1e3) as m:
+            m.set_option(nx.OPT_ADVECT_KERNEL, kern)
+            m.set_option(nx.OPT_ADVECT_STAGES, stages)
+            m.load(st)
+            for _ in range(2):
+                m.advect(3000.0)
+            m.mevp_substeps(2, begin_step=True)
+            out.append(m.state())
+    for k in out[0]:
+        np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
+
+
+def test_fused_prep_pg_bitwise(nx):
+    """The last advection stage writing P at the Gauss points (NXSDG_OPT_FUSE_PREP_PG, single rank) gives
+    bitwise the outer steps of the separate prep pass, including a BEGIN_STEP after a state write (which
+    must drop the fused P_g) and a parameter change of P*."""
+    nxe, nye = 70, 45
+    st = case(nxe, nye, 2, 6, 6, "warm", 140e3, 90e3)
+    out = []
+    for fuse in (1, 0):
+        with nx.Mesh(nxe, nye, 140e3, 90e3) as m:
+            m.set_option(nx.OPT_FUSE_PREP_PG, fuse)
+            m.load(st)
+            m.advect(120.0)
+            m.mevp_substeps(5, begin_step=True)
+            m.advect(120.0)
+            m.write_state("H", st["H"])          # P_g of the advected H is stale now
+            m.mevp_substeps(5, begin_step=True)
+            m.advect(120.0)
+            m.set_params(nx.PhysParams(Pstar=30000.0))
+            m.mevp_substeps(5, begin_step=True)
+            out.append(m.state())
+    for k in out[0]:
+        np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
+
+
 def test_graph_cache_survives_counter_reallocation(nx):
     """a graph captured before the work-counter buffer grows must not replay on the freed
     buffer.  n = 3, then 200 (more counters than the first allocation's 128: reallocation), then 3 again
