@@ -141,7 +141,7 @@ def oracle_sample(cfg, nsub, win=160):
 
 def oracle_baseline(cfg, win, nsamples=3):
     """cpu_baseline: the oracle as it stands, median of nsamples runs on the same window as the reference
-    arm, plus single-thread rates on C1 (whole mesh, 10 subcycles) and a 128^2 window of C2."""
+    arm, plus single-thread rates on C1 (whole mesh, 10 subcycles) and a 96^2 window of C2."""
     import oracle
     samples = [oracle_sample(cfg, cfg.nsub, win=win) for _ in range(nsamples)]
     out = {"value": float(np.median([x["value"] for x in samples])), "unit": "element-updates/s",
@@ -152,7 +152,7 @@ def oracle_baseline(cfg, win, nsamples=3):
     try:
         o.L.ora_set_threads(1)
         one = {}
-        for name, w in (("C1", 16), ("C2", 128)):
+        for name, w in (("C1", 16), ("C2", 96)):
             c = inputs.CONFIGS[name]
             x = oracle_sample(c, c.nsub, win=w)
             one[name] = {"value": x["value"], "sample": x["sample"], "seconds": x["seconds"]}

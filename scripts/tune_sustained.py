@@ -45,7 +45,7 @@ s = torch.cuda.ExternalStream(m.stream)
 n = 100
 # COMBOS = "cl:ctas:stages[:ty[:split[:l2[:vc]]]],..." (cl = NXSDG_OPT_CONST_STAGING, ty = chunk rows, default 32,
 # split = NXSDG_OPT_TAIL_SPLIT, default 1, l2 = NXSDG_OPT_L2_POLICY, default 2, vc = NXSDG_OPT_V_ROW_CARRY,
-# default 1),
+# default 1, pair = NXSDG_OPT_PAIR_STRIPS, default 0),
 # measured REPS times, interleaved
 COMBOS = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("COMBOS", "0:2:2,0:3:2,1:4:2,1:3:2").split(",")]
 REPS = int(os.environ.get("REPS", "2"))
@@ -61,6 +61,8 @@ for rep in range(REPS):
         m.set_option(nxsdg.OPT_L2_POLICY, l2)
         vc = combo[6] if len(combo) > 6 else 1
         m.set_option(nxsdg.OPT_V_ROW_CARRY, vc)
+        pair = combo[7] if len(combo) > 7 else 0
+        m.set_option(nxsdg.OPT_PAIR_STRIPS, pair)
         m.set_option(nxsdg.OPT_CONST_STAGING, cl)
         m.set_option(nxsdg.OPT_CTAS_PER_SM, c)
         m.set_option(nxsdg.OPT_STAGES, stg)
@@ -78,6 +80,6 @@ for rep in range(REPS):
         stop.set(); th.join()
         ms = statistics.median(t)
         gbs = bpe * cfg.nx * cfg.ny / (ms * 1e-3) / 1e9
-        print(json.dumps({"prec": prec, "rep": rep, "const_regs": cl, "ctas": c, "stages": stg, "ty": ty, "split": split, "l2": l2, "vcarry": vc, "ms_median": ms,
+        print(json.dumps({"prec": prec, "rep": rep, "const_regs": cl, "ctas": c, "stages": stg, "ty": ty, "split": split, "l2": l2, "vcarry": vc, "pair": pair, "ms_median": ms,
                           "ms_min": min(t), "alg_GBs": gbs, "frac": gbs / peak,
                           "sm_mhz": statistics.median(clk) if clk else None}), flush=True)

@@ -900,6 +900,25 @@ def test_advect_tma_bitwise_equals_q2(nx, shape, stages):
         np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
 
 
+@pytest.mark.parametrize("ty", [32, 5])
+def test_pair_strips_bitwise(nx, ty):
+    """NXSDG_OPT_PAIR_STRIPS (the CTA's two warps claim adjacent strips together) changes only which warp
+    computes which unit: bitwise the independent claims, on ragged meshes with odd strip counts, tail
+    sub-units and empty ragged units (ty = 5)."""
+    nxe, nye = 130, 97
+    st = case(nxe, nye, 2, 6, 6, "random", nxe * 1e3, nye * 1e3)
+    out = []
+    for pair in (1, 0):
+        with nx.Mesh(nxe, nye, nxe * 1e3, nye * 1e3) as m:
+            m.set_option(nx.OPT_PAIR_STRIPS, pair)
+            m.set_option(nx.OPT_CHUNK_ROWS, ty)
+            m.load(st)
+            m.mevp_substeps(7, begin_step=True)
+            out.append(m.state())
+    for k in out[0]:
+        np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
+
+
 def test_fused_prep_pg_bitwise(nx):
     """The last advection stage writing P at the Gauss points (NXSDG_OPT_FUSE_PREP_PG, single rank) gives
     bitwise the outer steps of the separate prep pass, including a BEGIN_STEP after a state write (which
