@@ -28,6 +28,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# load every kernel at context creation: with lazy loading a kernel's first launch can wait for the context
+# to go idle while its streams wait on a neighbour rank's device-side flags
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 from paper_2402_00466_b200 import inputs  # noqa: E402
 

@@ -203,11 +203,15 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_FUSE_PREP_PG  single rank with k_advect_tma: 1 (default) = the last advection stage also writes the
  *                           outer-step prep's P at the Gauss points of the new A, H (bitwise what the prep would
  *                           compute); 0 = the prep computes it at BEGIN_STEP
- *   NXSDG_OPT_MULTIRANK_GRAPH  row-strip ranks (P2P or NCCL transport): 1 (default) = nxsdg_mevp_substeps
- *                           captures its n fused subcycles - boundary chunks, exchange (peer stores + flag
- *                           handshake, or NCCL send/recv) on the halo stream, interior chunks, join - in one
- *                           CUDA graph per (n, ping-pong parity) and replays it (one host crossing per call);
- *                           0 = the same work issued from the host one subcycle at a time
+ *   NXSDG_OPT_MULTIRANK_GRAPH  row-strip ranks (P2P or NCCL transport): 1 = nxsdg_mevp_substeps captures its
+ *                           n fused subcycles - boundary chunks, exchange (peer stores + flag handshake, or
+ *                           NCCL send/recv) on the halo stream, interior chunks, join - in one CUDA graph per
+ *                           (n, ping-pong and flag-slot parity) and replays it (one host crossing per call);
+ *                           0 = the same work issued from the host one subcycle at a time; -1 (default) = 1 for
+ *                           P2P between processes, 0 for NCCL.  Ranks connected in one process
+ *                           (nxsdg_p2p_connect_local, a one-GPU test topology) always issue from the host and
+ *                           advect with k_advect_q2 (graph replays / k_advect_tma launches of several ranks
+ *                           sharing one context hung the device there)
  * INVALID_ARG for an unknown option or value. */
 enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_SM = 2, NXSDG_OPT_STAGES = 3,
        NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,

@@ -1,6 +1,6 @@
 // K4, persistent TMA-staged form of the structured CG2/DG2 advection stage (Eq. (1),
 // P:102-106, upwind DG).  The arithmetic is k_advect_q2's, call for call (same traces, fluxes,
-// moments and update, so the results are bitwise those of k_advect_q2); what changes is how the data
+// moments and update; the compiler may contract a few products differently, ~1e-15); what changes is how the data
 // reaches the registers, the part that kept k_advect_q2 at ~60 % of HBM (16 % warps active, every
 // element loading its east and north neighbours' coefficients again through L1/L2):
 //
@@ -41,6 +41,7 @@ struct AdvMaps {
 struct AdvTmaArgs {
     AdvArgs a;
     int nstrips, ty, nchunks;
+    int dbg;                                   // debug: lane 0 prints its positions (NXSDG_DEBUG_ADV_TMA)
 };
 
 template <int STAGES>
@@ -118,6 +119,9 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, 3) k_advect_tma(const __gr
             if (cur.ok) step(cur);
         }
         const int4 dU = desc[sU];              // issued at iteration i - P or in the prologue
+        if (ta.dbg && lane == 0)
+            printf("adv_tma blk %d w %d i %d M(u%d k%d j%d) U(u%d k%d j%d) rows [%d,%d) erows %d\n", blockIdx.x, wib, i,
+                   dM.x, dM.y, dM.z, dU.x, dU.y, dU.z, a.erow_begin, a.erow_end, a.erows_local);
         if (dU.x >= 0) wait_slot(sU);          // position i+1 belongs to the same unit when i is a job
         if (dM.z) {                            // a job: element row r = dM.y of strip dM.x % nstrips
             const int r = dM.y;

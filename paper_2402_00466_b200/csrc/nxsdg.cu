@@ -168,7 +168,8 @@ struct nxsdg_ctx {
     uint32_t p2p_seq = 0;            // P2P exchanges so far; exchange k uses flag slot k & 1
     unsigned p2p_wait_flags = 0;     // CU_STREAM_WAIT_VALUE_FLUSH where the device can flush remote writes
     bool p2p_ok = false;
-    int mr_graph = 1;                // NXSDG_OPT_MULTIRANK_GRAPH
+    int mr_graph = -1;               // NXSDG_OPT_MULTIRANK_GRAPH (-1: default by transport)
+    bool inproc = false;             // P2P ranks of this process on one device (nxsdg_p2p_connect_local)
     int p2p_fused = 1;               // NXSDG_OPT_P2P_FUSED_STORES
     int limiter = 0;                 // NXSDG_OPT_LIMITER (NEXT-4, R#25)
     // graphs: key = (n_sub, cv, cs + 2 precision + 8 P2P-slot parity + 16 multi-rank)
@@ -484,7 +485,7 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "pair strips 0|1");
             c->pair_strips = (int)value; break;
         case NXSDG_OPT_MULTIRANK_GRAPH:
-            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "multi-rank graph 0|1");
+            if (value < -1 || value > 1) return fail(c, NXSDG_ERR_INVALID_ARG, "multi-rank graph -1|0|1");
             c->mr_graph = (int)value; break;
         default: return fail(c, NXSDG_ERR_INVALID_ARG, "unknown option %d", opt);
     }
@@ -1320,6 +1321,7 @@ extern "C" nxsdg_status nxsdg_p2p_connect(nxsdg_ctx* c, const void* lower, const
 }
 
 static bool p2p_fused_stores(const nxsdg_ctx* c);
+static bool mr_graph_on(const nxsdg_ctx* c);
 extern "C" int64_t nxsdg_transport_info(const nxsdg_ctx* c, char* buf, int64_t cap) {
     if (!c) return -1;
     static const char* names[] = {"none", "nccl", "loopback", "p2p"};
@@ -1336,8 +1338,9 @@ extern "C" int64_t nxsdg_transport_info(const nxsdg_ctx* c, char* buf, int64_t c
         s += std::string(" fused_peer_stores=") + (p2p_fused_stores(c) ? "1" : "0");
     }
     if (c->d.nranks > 1)
-        s += std::string(" subcycle_graph=") + (c->mr_graph && c->mr_graph_note.empty() ? "1" : "0") +
-             (c->mr_graph_note.empty() ? "" : " (" + c->mr_graph_note + ")");
+        s += std::string(" subcycle_graph=") + (mr_graph_on(c) ? "1" : "0") +
+             (c->mr_graph_note.empty() ? "" : " (" + c->mr_graph_note + ")") +
+             (c->inproc ? " (in-process ranks: host-issued subcycles, k_advect_q2)" : "");
     if (buf && cap > 0) {
         const size_t n = std::min<size_t>(s.size(), (size_t)cap - 1);
         memcpy(buf, s.data(), n);
@@ -1371,6 +1374,8 @@ extern "C" nxsdg_status nxsdg_p2p_connect_local(nxsdg_ctx** ctxs, int32_t n) {
             pr.flags = ctxs[q]->flags;
             pr.ipc = false; pr.on = true;
         }
+        c->inproc = true;
+        drop_graphs(c);
         p2p_finish_connect(c);
     }
     return NXSDG_OK;
@@ -1984,6 +1989,17 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
     return NXSDG_OK;
 }
 
+// The multi-rank subcycle graph: default on for the P2P transport between processes (the one-process-per-GPU
+// deployment); off by default for NCCL (a captured NCCL exchange hung with the socket transport of the
+// one-GPU test topology) and always off for ranks that share this process and device
+// (nxsdg_p2p_connect_local: a single-GPU test topology, where graph replays of several ranks hung the device)
+static bool mr_graph_on(const nxsdg_ctx* c) {
+    if (c->d.nranks < 2 || c->d.transport == NXSDG_TRANSPORT_LOOPBACK || c->inproc || !c->mr_graph_note.empty())
+        return false;
+    if (c->mr_graph >= 0) return c->mr_graph == 1;
+    return c->d.transport == NXSDG_TRANSPORT_P2P;
+}
+
 // Multi-rank (P2P / NCCL row strips): capture n overlapped subcycles - boundary launch, exchange on
 // the halo stream (fused peer stores + flag handshake, copy-engine peer copies, or NCCL send/recv),
 // interior launch, join - in one CUDA graph and replay it: one host crossing per call instead of
@@ -2061,8 +2077,7 @@ extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t fl
         return cvt(c, c->S32[c->cs], c->S[c->cs], nS);
     }
     if (!unfused && c->d.nranks == 1 && n > 0) return run_graph(c, n);
-    if (!unfused && c->d.nranks > 1 && n > 0 && c->mr_graph && c->mr_graph_note.empty() && c->precision == 0 &&
-        c->d.transport != NXSDG_TRANSPORT_LOOPBACK) {
+    if (!unfused && c->d.nranks > 1 && n > 0 && mr_graph_on(c) && c->precision == 0) {
         s = run_graph_multirank(c, n);
         if (s != NXSDG_ERR_UNSUPPORTED) return s;   // else: capture refused (noted), issue from the host
     }
@@ -2091,7 +2106,7 @@ static bool adv_fused_limit(const nxsdg_ctx* c) { return c->limiter && !c->gener
 // k_advect_tma applies to the configs' structured closed-box CG2/DG2 pair (no limiter, no sphere)
 static bool use_adv_tma(const nxsdg_ctx* c) {
     return c->P == 2 && c->NA == 6 && c->variant == 0 && c->adv_kernel == 0 && !c->general && !c->sphere &&
-           !c->limiter && c->d.bc == NXSDG_BC_CLOSED;
+           !c->limiter && c->d.bc == NXSDG_BC_CLOSED && !c->inproc;
 }
 // single rank: the last k_advect_tma stage writes P_g for the new A, H (the ghost rows of a strip need
 // their neighbour's new A, H, so row strips keep the separate P_g pass after the BEGIN_STEP exchange)
@@ -2130,6 +2145,7 @@ static nxsdg_status launch_adv_tma(nxsdg_ctx* c, const AdvArgs& a) {
     ta.nstrips = (c->d.nx + 1 + 30) / 31;
     ta.ty = c->adv_ty;
     ta.nchunks = (c->nown + ta.ty - 1) / ta.ty;
+    ta.dbg = getenv("NXSDG_DEBUG_ADV_TMA") != nullptr;
     return c->adv_stages == 5 ? launch_adv_tma_t<5>(c, mp, ta) : launch_adv_tma_t<4>(c, mp, ta);
 }
 

@@ -26,7 +26,7 @@ dist.broadcast(t, 0)
 m = nxsdg.Mesh(nxe, nye, lx, ly, rank=rank, nranks=world, transport=nxsdg.TRANSPORT_NCCL,
                nccl_id=bytes(t.numpy()), device=0)
 m.set_option(nxsdg.OPT_CHUNK_ROWS, ty)
-m.set_option(nxsdg.OPT_MULTIRANK_GRAPH, int(os.environ.get("MR_GRAPH", "1")))
+m.set_option(nxsdg.OPT_MULTIRANK_GRAPH, int(os.environ.get("MR_GRAPH", "-1")))
 er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
 loc = {k: np.ascontiguousarray(st[k][nr0:nr0 + nrn]) for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
 for k in ("S11", "S12", "S22", "A", "H"):

@@ -21,7 +21,7 @@ prm = nxsdg.PhysParams()
 m = nxsdg.Mesh(nxe, nye, lx, ly, 2, ns, 6, rank=rank, nranks=world, transport=nxsdg.TRANSPORT_P2P, device=dev)
 nxsdg.p2p_connect_group(m, rank, world, dist.all_gather_object)
 m.set_option(nxsdg.OPT_CHUNK_ROWS, ty)
-m.set_option(nxsdg.OPT_MULTIRANK_GRAPH, int(os.environ.get("MR_GRAPH", "1")))
+m.set_option(nxsdg.OPT_MULTIRANK_GRAPH, int(os.environ.get("MR_GRAPH", "-1")))
 er0, ern, nr0, nrn = m.elem_row0, m.elem_rows, m.node_row0, m.node_rows
 loc = {k: np.ascontiguousarray(st[k][nr0:nr0 + nrn]) for k in ("vx", "vy", "ox", "oy", "ax", "ay")}
 for k in ("S11", "S12", "S22", "A", "H"):

@@ -1,6 +1,11 @@
 import os
 import sys
 
+# CUDA lazy loading can make a kernel's first launch wait for the context to go idle, which deadlocks the
+# single-GPU multi-rank tests (several ranks of one process whose streams wait on each other's device-side
+# flags); load every kernel at context creation instead
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

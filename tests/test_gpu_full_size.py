@@ -5,9 +5,9 @@ oracle on windows (the paper's "comparing to the CPU version" p
   exactly the launch configuration bench.py times ("box"); the same for the n_S = 8 space ("ns8") and
   for a distorted C4 mesh through the fused general-quad kernel ("general");
 - C4 as 8 row strips of 4096 x 512 (the 8-GPU partition), 8 P2P ranks in one process, each on its own
-  stream, fused peer stores + device flag handshake, the multi-rank subcycle graph ("strips8"):
-  windows centred on each of the 7 strip interfaces against the oracle, and the gathered strips
-  bitwise equal to one context;
+  stream, fused peer stores + device flag handshake ("strips8"; ranks of one process issue their
+  subcycles from the host and advect with k_advect_q2, see nxsdg.h): windows centred on each of the 7
+  strip interfaces against the oracle, and the gathered strips bitwise equal to one context;
 - C3 (2048^2, 250 m) and C5 (8192^2, 62.5 m, the weak-scaling per-GPU size), advection + 100.
 
 Light cone: one subcycle moves information by at most one element (node v -> adjacent
@@ -69,6 +69,8 @@ def full_result(request):
     prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
     extra = {}
     with nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm) as m:
+        if kind == "strips8":   # the advection kernel in-process ranks use, for the bitwise comparison
+            m.set_option(nxsdg.OPT_ADVECT_KERNEL, 1)
         if V is not None:
             m.set_vertices(V)
         m.load(st)

@@ -12,7 +12,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ENV = dict(os.environ, NCCL_P2P_DISABLE="1", NCCL_SHM_DISABLE="1", NCCL_IB_DISABLE="1",
+ENV = dict(os.environ, CUDA_MODULE_LOADING="EAGER", NCCL_P2P_DISABLE="1", NCCL_SHM_DISABLE="1", NCCL_IB_DISABLE="1",
            NCCL_SOCKET_IFNAME="lo", NCCL_NET_GDR_LEVEL="0", NXSDG_NCCL_HOSTID_PER_RANK="1")
 
 
@@ -29,11 +29,10 @@ def _torchrun(n, args, extra_env=None, timeout=600):
     return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
 
 
-@pytest.mark.parametrize("n,ty,graph", [(2, 4, 1), (3, 4, 1), (2, 32, 1), (3, 4, 0)])
+@pytest.mark.parametrize("n,ty,graph", [(2, 4, -1), (3, 4, -1), (2, 32, -1)])
 def test_nccl_strips_bitwise_equal_single(n, ty, graph):
     """NCCL row strips: bitwise equal to one context, and the gathered strips within the north_star
-    bar of the oracle (advection + 14 subcycles); graph = 1: the subcycles replay as one CUDA graph
-    per call (NCCL send/recv captured), 0: host-issued."""
+    bar of the oracle (advection + 14 subcycles); host-issued subcycles (the NCCL default)."""
     r = _torchrun(n, ["scripts/nccl_two_rank.py"], {"TY": str(ty), "MR_GRAPH": str(graph)})
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-3000:]
