@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, 3) k_advect_tma(const __gr
     if (d0.x < 0) return;
     wait_slot(0);
     const double mr[6] = {1.0, 12.0, 12.0, 180.0, 180.0, 144.0};
+    // the north flux of a job is the south flux of the unit's next job (same edge, same function, same
+    // inputs): carried in registers instead of evaluated twice; the unit's first job evaluates its own
+    int prev_unit = -1;
+    double cNA[3] = {0.0, 0.0, 0.0}, cNH[3] = {0.0, 0.0, 0.0};
     for (int i = 0;; ++i) {
         const int sL = (i + STAGES - 1) % STAGES, sM = i % STAGES, sU = (i + 1) % STAGES;
         const int4 dM = desc[sM];
@@ -166,12 +170,18 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, 3) k_advect_tma(const __gr
                 FwA[q] = __shfl_up_sync(0xffffffffu, FeA[q], 1);
                 FwH[q] = __shfl_up_sync(0xffffffffu, FeH[q], 1);
             }
-            {   // south edge: the row below
+            if (prev_unit == dM.x) {   // the previous job was the row below in this unit: its north flux
+#pragma unroll
+                for (int q = 0; q < 3; ++q) { FsA[q] = cNA[q]; FsH[q] = cNH[q]; }
+            } else {   // south edge: the row below (ring row of the unit)
 #pragma unroll
                 for (int k = 0; k < 6; ++k) { nb.A[k] = L.A[k][eo + lane]; nb.H[k] = L.H[k][eo + lane]; }
                 double vn[3]; q2_interp3(uy[0][0], uy[0][1], uy[0][2], vn);
                 q2_edge(false, nb, me, vn, r > a.erow_begin || a.has_south, FsA, FsH);
             }
+#pragma unroll
+            for (int q = 0; q < 3; ++q) { cNA[q] = FnA[q]; cNH[q] = FnH[q]; }
+            prev_unit = dM.x;
             // ---- volume term and update: k_advect_q2's code
             double gvx[3][3], gvy[3][3];
             {

@@ -435,14 +435,15 @@ def test_paper_protocol_30_outer_steps_drift(nx, ora, capsys):
     """NEXT-2, the paper's timing protocol: 30 x (advect + 100 subcycles) = 3000 stress
     updates (1 h at dt = 120 s), the cyclone moving with the GPU-regenerated forcing, and an alpha /
     beta change after 15 outer steps through nxsdg_set_params (a parameter schedule).  Long-horizon
-    parity drift against the oracle after every outer step.  The dynamics amplify FP64 rounding by
-    ~2x per outer step here: the oracle's own plain and FMA builds drift apart the same way
-    (DESIGN.md §4), so the bar at step k is max(1e-10, 10 x that self-consistency floor at step k)
-    -- the GPU must stay as close to the oracle as two correct FP64 evaluations are to each other."""
+    parity against the oracle after EVERY outer step at the north_star bar 1e-10.  alpha = beta = 25000
+    (R#13): at 1500 (alpha beta = 2.3e6 < the stability estimate gamma ~ 9e6 at 2 km) the mEVP
+    iteration amplified rounding ~2x per outer step and the velocity grew (the oracle's own plain and
+    FMA builds drifted to 6e-2 by step 30); at 25000 and 1e5 their floor stays at 1e-11 ... 5e-11 for
+    all 30 steps and |v| stays put (scripts/drift_alpha.py, profiles/drift_alpha_r02.log)."""
     nxe, nye = 40, 36
     lx, ly = nxe * 2e3, nye * 2e3
     st = case(nxe, nye, 2, 6, 6, "warm", lx, ly)
-    prm = nx.PhysParams()
+    prm = nx.PhysParams(alpha=25000.0, beta=25000.0)
     X, Y = np.meshgrid(np.arange(2 * nxe + 1) * (lx / nxe / 2), np.arange(2 * nye + 1) * (ly / nye / 2))
     ref = {k: v.copy() for k, v in st.items()}
     ref_fma = {k: v.copy() for k, v in st.items()}
@@ -453,7 +454,7 @@ def test_paper_protocol_30_outer_steps_drift(nx, ora, capsys):
         m.load(st)
         for k in range(30):
             if k == 15:
-                prm = nx.PhysParams(alpha=3000.0, beta=3000.0)
+                prm = nx.PhysParams(alpha=50000.0, beta=50000.0)
                 m.set_params(prm)
             t = k * prm.dt
             m.set_forcing_cyclone(t)
@@ -471,7 +472,7 @@ def test_paper_protocol_30_outer_steps_drift(nx, ora, capsys):
     with capsys.disabled():
         print("\n30-outer-step drift GPU vs oracle:", " ".join(f"{d:.1e}" for d in drift))
         print("oracle plain vs FMA floor:       ", " ".join(f"{d:.1e}" for d in floor))
-    bad = [(k, d, f) for k, (d, f) in enumerate(zip(drift, floor)) if d > max(TOLN, 10 * f)]
+    bad = [(k, d, f) for k, (d, f) in enumerate(zip(drift, floor)) if d > TOLN]
     assert not bad, bad
 
 
