@@ -17,6 +17,7 @@ and larger than L2, so no flush is needed between steps.
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import subprocess
@@ -285,6 +286,8 @@ def main():
                     help="NEXT-3: S and P_g stored in FP32 inside the fused subcycles (arithmetic FP64)")
     ap.add_argument("--fp32-stress", action="store_true",
                     help="NEXT-3: as --fp32-storage plus the stress update (strain, Listing 2, projection) in FP32")
+    ap.add_argument("--sphere", action="store_true",
+                    help="NEXT-4 (R#26): the config's element counts on a lon-lat patch of the sphere, 60-75 N x 30 deg")
     ap.add_argument("--limiter", action="store_true",
                     help="NEXT-4: Zhang-Shu bound-preserving limiter after every advection stage (R#25)")
     ap.add_argument("--moving", action="store_true",
@@ -309,6 +312,11 @@ def main():
     if args.nsub:
         cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, args.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect,
                             cfg.alpha)
+    SPH = (6371e3, math.radians(60.0), math.radians(30.0), math.radians(15.0))   # R, lat0, lon extent, lat extent
+    if args.sphere:   # inputs on the patch's local east-north coordinates
+        R, lat0, dlon, dlat = SPH
+        cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, cfg.ns, cfg.na, cfg.nsub, R * math.cos(lat0 + 0.5 * dlat) * dlon,
+                            R * dlat, cfg.kind, cfg.advect, cfg.alpha)
     if args.ns and args.ns != cfg.ns:
         cfg = inputs.Config(cfg.name, cfg.nx, cfg.ny, cfg.p, args.ns, cfg.na, cfg.nsub, cfg.lx, cfg.ly, cfg.kind, cfg.advect,
                             cfg.alpha)
@@ -365,6 +373,8 @@ def main():
         m.set_option(nxsdg.OPT_PRECISION, 2 if args.fp32_stress else 1)
     if args.limiter:
         m.set_option(nxsdg.OPT_LIMITER, 1)
+    if args.sphere:
+        m.set_sphere(*SPH)
     infos = [m.transport_info]
     if world > 1:
         infos = [None] * world
@@ -372,7 +382,7 @@ def main():
     m.load(st)
     stream = torch.cuda.ExternalStream(m.stream)
     parity = None
-    if not args.no_parity and not (args.fp32_storage or args.fp32_stress or args.moving or args.limiter):
+    if not args.no_parity and not (args.fp32_storage or args.fp32_stress or args.moving or args.limiter or args.sphere):
         # correctness evidence on the bench line: one outer step of the bench configuration from the
         # initial state, an oracle window across the middle strip interface (N > 1) or at the centre
         m.advect(prm.dt)
@@ -495,6 +505,7 @@ def main():
                        "parallelism": f"row strips x{world} ({transport_note} halo)" if world > 1 else "1 GPU",
                        "forcing": "moving cyclone regenerated on the GPU every step" if args.moving else "static (t = 0)",
                        "limiter": bool(args.limiter),
+                       "sphere": "lon-lat patch 60-75 N x 30 deg, R = 6371 km (R#26)" if args.sphere else None,
                        "l2": "inputs larger than L2 (device state ~17 GB for C4); no flush"},
             "breakdown_ms": {"advect": adv, "prep": prep, "subcycles": sub, "per_subcycle": kernel_ms},
             "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -126,6 +126,7 @@ struct nxsdg_ctx {
     int adv_ty = 32;       // element rows per k_advect_tma work unit
     int fuse_pg = 1;       // NXSDG_OPT_FUSE_PREP_PG: the last k_advect_tma stage also writes P_g (single rank)
     int pair_strips = 0;   // NXSDG_OPT_PAIR_STRIPS: box kernel warps of a CTA claim adjacent strips together
+    int prep_kernel = 0;   // NXSDG_OPT_PREP_KERNEL: CG2/DG2 prep nodes: 0 = row-marching, 1 = per-element threads
     bool pg_fresh = false; // P_g already holds P of the current A, H (written by the last advection stage)
     bool adv_last = false; // the advection stage being launched is the last one
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
@@ -484,6 +485,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_PAIR_STRIPS:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "pair strips 0|1");
             c->pair_strips = (int)value; break;
+        case NXSDG_OPT_PREP_KERNEL:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "prep kernel 0|1");
+            c->prep_kernel = (int)value; break;
         case NXSDG_OPT_MULTIRANK_GRAPH:
             if (value < -1 || value > 1) return fail(c, NXSDG_ERR_INVALID_ARG, "multi-rank graph -1|0|1");
             c->mr_graph = (int)value; break;
@@ -1411,9 +1415,16 @@ static nxsdg_status launch_prep(nxsdg_ctx* c) {
 static nxsdg_status dispatch_prep(nxsdg_ctx* c) {
     if (c->P == 2 && c->NA == 6) {   // structured (prep_q2.cuh); P_g only if the advection did not write it
         PrepArgs a = prep_args(c);
-        const int rows = a.node_row_end - a.node_row_begin;
-        dim3 bn(32, 4), gn((unsigned)((c->d.nx + 1 + 31) / 32), (unsigned)((rows / 2 + 1 + 3) / 4));
-        k_prep_nodes_q2<<<gn, bn, 0, c->stream>>>(a);
+        if (c->prep_kernel == 0) {   // row-marching (default)
+            const int chunk = 64;
+            const int pr_lo = a.node_row_begin >> 1, pr_hi = (a.node_row_end + 1) >> 1;
+            const int64_t warps = (int64_t)((c->d.nx + 1 + 31) / 32) * ((pr_hi - pr_lo + chunk - 1) / chunk);
+            k_prep_nodes_march<<<(unsigned)((warps + 3) / 4), 128, 0, c->stream>>>(a, chunk);
+        } else {
+            const int rows = a.node_row_end - a.node_row_begin;
+            dim3 bn(32, 4), gn((unsigned)((c->d.nx + 1 + 31) / 32), (unsigned)((rows / 2 + 1 + 3) / 4));
+            k_prep_nodes_q2<<<gn, bn, 0, c->stream>>>(a);
+        }
         LAUNCHED();
         if (!c->pg_fresh) {
             dim3 be(128), ge((unsigned)((c->d.nx + 127) / 128), (unsigned)c->erows_local);

@@ -114,4 +114,106 @@ __global__ void k_prep_nodes_q2(PrepArgs a) {
     }
 }
 
+// Row-marching form of k_prep_nodes_q2 (same sums, same order: bitwise equal): a warp owns 32 element
+// columns and marches up a chunk of element rows; each element's 12 coefficients are read once, its DG
+// values at its 9 local nodes are formed once, the west neighbour's arrive by shuffle (lane 0 evaluates
+// the element west of the strip itself) and the row below's top-node values are carried in registers
+// (the chunk's first row evaluates its row below itself).
+struct PrepNodeVals { double h[9], a[9]; };   // [jy * 3 + jx]
+
+__device__ __forceinline__ void prep_vals(const PrepArgs& a, int ex, int ey, bool ok, PrepNodeVals& v) {
+    double hc[6], ac[6];
+    const int64_t e = (int64_t)(ok ? ey : 0) * a.epitch + (ok ? ex : 0);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        hc[k] = ok ? a.H[k * a.eplane + e] : 0.0;
+        ac[k] = ok ? a.A[k * a.eplane + e] : 0.0;
+    }
+    v.h[0] = dg2_node<0, 0>(hc); v.h[1] = dg2_node<1, 0>(hc); v.h[2] = dg2_node<2, 0>(hc);
+    v.h[3] = dg2_node<0, 1>(hc); v.h[4] = dg2_node<1, 1>(hc); v.h[5] = dg2_node<2, 1>(hc);
+    v.h[6] = dg2_node<0, 2>(hc); v.h[7] = dg2_node<1, 2>(hc); v.h[8] = dg2_node<2, 2>(hc);
+    v.a[0] = dg2_node<0, 0>(ac); v.a[1] = dg2_node<1, 0>(ac); v.a[2] = dg2_node<2, 0>(ac);
+    v.a[3] = dg2_node<0, 1>(ac); v.a[4] = dg2_node<1, 1>(ac); v.a[5] = dg2_node<2, 1>(ac);
+    v.a[6] = dg2_node<0, 2>(ac); v.a[7] = dg2_node<1, 2>(ac); v.a[8] = dg2_node<2, 2>(ac);
+}
+
+__device__ __forceinline__ void prep_node_out(const PrepArgs& a, int jr, int I, double hs, double as, int cnt) {
+    const double Hn = cnt ? fmax(hs / cnt, 1e-4) : 1e-4;
+    const double An = cnt ? fmin(fmax(as / cnt, 0.0), 1.0) : 0.0;
+    const int64_t n = (int64_t)jr * a.npitch + I;
+    const double m = a.rho_ice * Hn;
+    const double c1 = m / a.dt;
+    const double axv = a.ax[n], ayv = a.ay[n];
+    const double amag = sqrt(axv * axv + ayv * ayv);
+    const double drag = An * a.Fa * amag;
+    a.c1[n] = c1;
+    a.rx0[n] = c1 * a.vx[n] + drag * axv - m * a.f_c * a.oy[n];
+    a.ry0[n] = c1 * a.vy[n] + drag * ayv + m * a.f_c * a.ox[n];
+    a.cafo[n] = An * a.Fo;
+}
+
+__global__ void __launch_bounds__(128) k_prep_nodes_march(PrepArgs a, int chunk) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nstrips = (a.nx + 1 + 31) / 32;          // element columns 0 .. nx (column nx: node column 2 nx)
+    const int pr_lo = a.node_row_begin >> 1, pr_hi = (a.node_row_end + 1) >> 1;   // element rows with owned nodes
+    const int nchunks = (pr_hi - pr_lo + chunk - 1) / chunk;
+    if (warp >= nstrips * nchunks) return;
+    const int strip = warp % nstrips, ch = warp / nstrips;
+    const int ix = strip * 32 + lane;
+    const int pr0 = pr_lo + ch * chunk, pr1 = min(pr0 + chunk, pr_hi);
+    const bool colok = ix <= a.nx;
+    auto okE = [&](int ex, int ey) { return ex >= 0 && ex < a.nx && ey >= 0 && ey < a.elem_rows_with_nodes; };
+    // row below the chunk (pr0 - 1): own and west values
+    PrepNodeVals below, belowW;
+    prep_vals(a, ix, pr0 - 1, okE(ix, pr0 - 1), below);
+    bool okB = okE(ix, pr0 - 1), okBW;
+    {
+#pragma unroll
+        for (int j = 0; j < 9; ++j) { belowW.h[j] = __shfl_up_sync(0xffffffffu, below.h[j], 1); belowW.a[j] = __shfl_up_sync(0xffffffffu, below.a[j], 1); }
+        okBW = __shfl_up_sync(0xffffffffu, okB, 1);
+        if (lane == 0) { okBW = okE(ix - 1, pr0 - 1); prep_vals(a, ix - 1, pr0 - 1, okBW, belowW); }
+    }
+    for (int pr = pr0; pr < pr1; ++pr) {
+        PrepNodeVals me, W;
+        const bool okM = okE(ix, pr);
+        prep_vals(a, ix, pr, okM, me);
+#pragma unroll
+        for (int j = 0; j < 9; ++j) { W.h[j] = __shfl_up_sync(0xffffffffu, me.h[j], 1); W.a[j] = __shfl_up_sync(0xffffffffu, me.a[j], 1); }
+        bool okW = __shfl_up_sync(0xffffffffu, okM, 1);
+        if (lane == 0) { okW = okE(ix - 1, pr); prep_vals(a, ix - 1, pr, okW, W); }
+        if (colok) {
+#pragma unroll
+            for (int jy = 0; jy < 2; ++jy) {
+                const int jr = 2 * pr + jy;
+                if (jr < a.node_row_begin || jr >= a.node_row_end) continue;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int I = 2 * ix + q;
+                    if (I > 2 * a.nx) continue;
+                    double hs = 0.0, as = 0.0;
+                    int cnt = 0;
+                    // k_prep_nodes' order SW, SE, NW, NE with the node's position in each element
+                    if (jy == 0 && q == 0) {
+                        if (okBW) { hs += belowW.h[8]; as += belowW.a[8]; ++cnt; }
+                        if (okB) { hs += below.h[6]; as += below.a[6]; ++cnt; }
+                        if (okW) { hs += W.h[2]; as += W.a[2]; ++cnt; }
+                        if (okM) { hs += me.h[0]; as += me.a[0]; ++cnt; }
+                    } else if (jy == 0) {
+                        if (okB) { hs += below.h[7]; as += below.a[7]; ++cnt; }
+                        if (okM) { hs += me.h[1]; as += me.a[1]; ++cnt; }
+                    } else if (q == 0) {
+                        if (okW) { hs += W.h[5]; as += W.a[5]; ++cnt; }
+                        if (okM) { hs += me.h[3]; as += me.a[3]; ++cnt; }
+                    } else {
+                        if (okM) { hs += me.h[4]; as += me.a[4]; ++cnt; }
+                    }
+                    prep_node_out(a, jr, I, hs, as, cnt);
+                }
+            }
+        }
+        below = me; belowW = W; okB = okM; okBW = okW;
+    }
+}
+
 }  // namespace nxk

@@ -4,10 +4,10 @@ oracle on windows (the paper's "comparing to the CPU version" p
 - C4 (4096^2 CG2/DG2, 125 m): one outer step = advection + BEGIN_STEP prep + 100 fused subcycles,
   exactly the launch configuration bench.py times ("box"); the same for the n_S = 8 space ("ns8") and
   for a distorted C4 mesh through the fused general-quad kernel ("general");
-- C4 as 8 row strips of 4096 x 512 (the 8-GPU partition), 8 P2P ranks in one process, each on its own
-  stream, fused peer stores + device flag handshake ("strips8"; ranks of one process issue their
-  subcycles from the host and advect with k_advect_q2, see nxsdg.h): windows centred on each of the 7
-  strip interfaces against the oracle, and the gathered strips bitwise equal to one context;
+- C4 as 8 row strips of 4096 x 512 (the 8-GPU partition), one process per rank under torchrun on the one
+  GPU (the deployment's topology: CUDA IPC P2P with fused peer stores, the device flag handshake and the
+  multi-rank subcycle graph; scripts/strips8_full.py): windows centred on each of the 7 strip interfaces
+  against the oracle, and every rank's rows bitwise equal to one context;
 - C3 (2048^2, 250 m) and C5 (8192^2, 62.5 m, the weak-scaling per-GPU size), advection + 100.
 
 Light cone: one subcycle moves information by at most one element (node v -> adjacent
@@ -33,7 +33,7 @@ from tests.parity import group_err
 
 pytestmark = pytest.mark.gpu
 CORE = 12
-PARAMS = ["box", "ns8", "general", "strips8", "C3", "C5"]
+PARAMS = ["box", "ns8", "general", "C3", "C5"]
 
 
 def _cfg(kind):
@@ -69,34 +69,12 @@ def full_result(request):
     prm = nxsdg.PhysParams(alpha=cfg.alpha, beta=cfg.alpha)
     extra = {}
     with nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm) as m:
-        if kind == "strips8":   # the advection kernel in-process ranks use, for the bitwise comparison
-            m.set_option(nxsdg.OPT_ADVECT_KERNEL, 1)
         if V is not None:
             m.set_vertices(V)
         m.load(st)
         m.advect(prm.dt)
         m.mevp_substeps(cfg.nsub, begin_step=True)
         got = m.state()
-    if kind == "strips8":
-        nr = 8
-        ms = [nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, cfg.p, cfg.ns, cfg.na, params=prm, rank=r, nranks=nr,
-                         transport=nxsdg.TRANSPORT_P2P) for r in range(nr)]
-        nxsdg.p2p_connect_local(ms)
-        for m in ms:
-            _load_local(m, st, cfg.nx)
-        for m in ms:
-            m.advect(prm.dt)
-        for m in ms:
-            m.mevp_substeps(cfg.nsub, begin_step=True)
-        for m in ms:
-            m.synchronize()
-        extra["info"] = [m.transport_info for m in ms]
-        strips = {k: np.concatenate([m.read_state(k) for m in ms]) for k in got}
-        extra["row0"] = [m.elem_row0 for m in ms]
-        for m in ms:
-            m.destroy()
-        extra["single"] = got
-        got = strips
     return kind, cfg, st, got, V, extra
 
 
@@ -115,8 +93,6 @@ def _cut(cfg, arrs, ix0, iy0, w, h):
 def _windows(kind, cfg, extra):
     rng = np.random.default_rng(inputs.SEED_BASE + 4)
     nx, ny = cfg.nx, cfg.ny
-    if kind == "strips8":   # centred on each strip interface (element row r0 of ranks 1..7)
-        return [(int(rng.integers(0, nx - CORE)), r0 - CORE // 2) for r0 in extra["row0"][1:]]
     ws = [(0, 0), (nx - CORE, 0), (0, ny - CORE), (nx - CORE, ny - CORE), (nx // 2 - CORE // 2, ny // 2 - CORE // 2)]
     ws += [(int(rng.integers(0, nx - CORE)), int(rng.integers(0, ny - CORE))) for _ in range(3)]
     return ws
@@ -182,9 +158,30 @@ def test_full_size_window_parity(full_result, capsys):
         print(f"\nfull-size parity {kind} ({cfg.nx}x{cfg.ny}, n_S={cfg.ns}, advect + {cfg.nsub} subcycles, "
               f"alpha=beta={cfg.alpha:g}):")
         print("\n".join(rows))
-        if kind == "strips8":
-            print("  " + "\n  ".join(extra["info"]))
     assert not bad, bad
-    if kind == "strips8":   # the 8-strip partition is bitwise the single context
-        for k, a in extra["single"].items():
-            np.testing.assert_array_equal(got[k], a, err_msg=k)
+
+
+def test_c4_eight_strips_interfaces_and_bitwise(capsys):
+    """C4 as 8 row strips in 8 processes (torchrun, IPC P2P, subcycle graph): the 7 interface windows
+    against the oracle at the north_star bar, every rank's rows bitwise equal to one context."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "8",
+                        "scripts/strips8_full.py"], cwd=root, env=env, capture_output=True, text=True, timeout=1800)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+    d = json.loads(lines[-1])
+    with capsys.disabled():
+        print("\nC4 8 strips (8 processes, IPC P2P):")
+        for e in d["interface_windows"]:
+            print("  interface window", e["window"], "  ".join(f"{k}={v:.1e}" for k, v in e.items() if k != "window"))
+        print("  " + "\n  ".join(d["transport"]))
+    assert d["bitwise_equal_single"], d["bitwise_bad"]
+    assert d["parity_ok"] and len(d["interface_windows"]) == 7, d["interface_windows"]

@@ -920,6 +920,24 @@ def test_pair_strips_bitwise(nx, ty):
         np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
 
 
+@pytest.mark.parametrize("shape", [(70, 75), (31, 130), (1, 5), (6, 1), (33, 2)])
+def test_prep_kernels_bitwise(nx, shape):
+    """The row-marching prep (NXSDG_OPT_PREP_KERNEL 0, default) and the per-element gather form (1) make the
+    same sums in the same order: the outer steps are bitwise equal (ragged strips, chunk edges, 1-row meshes)."""
+    nxe, nye = shape
+    st = case(nxe, nye, 2, 6, 6, "random", nxe * 1e3, nye * 1e3)
+    out = []
+    for pk in (0, 1):
+        with nx.Mesh(nxe, nye, nxe * 1e3, nye * 1e3) as m:
+            m.set_option(nx.OPT_PREP_KERNEL, pk)
+            m.load(st)
+            m.advect(120.0)
+            m.mevp_substeps(3, begin_step=True)
+            out.append(m.state())
+    for k in out[0]:
+        np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
+
+
 def test_fused_prep_pg(nx):
     """The last advection stage writing P at the Gauss points (NXSDG_OPT_FUSE_PREP_PG, single rank) gives
     the outer steps of the separate prep pass (same function, up to FMA contraction: 1e-13), including a
