@@ -26,6 +26,7 @@
 #include "subcycle_gen.cuh"
 #include "advect_q2.cuh"
 #include "advect_tma.cuh"
+#include <nvtx3/nvToolsExt.h>     // header-only NVTX v3: ranges for nsys / ncu (--nvtx), no link dependency
 #include "prep_q2.cuh"
 #include "general_quads.cuh"
 #include "general_steps.cuh"
@@ -203,6 +204,14 @@ static nxsdg_status fail(nxsdg_ctx* c, nxsdg_status s, const char* fmt, ...) {
     } while (0)
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// NVTX range for the host span of an API call / exchange (visible on nsys timelines, filterable in ncu)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 extern "C" nxsdg_status nxsdg_partition(int32_t ny, int32_t p, int32_t nranks, int32_t rank, int64_t* er0,
                                         int32_t* erows, int64_t* nr0, int32_t* nrows) {
@@ -1102,6 +1111,7 @@ static double* msg_ptr(nxsdg_ctx* c, const HaloMsg& m) {
 }
 
 static nxsdg_status halo_nccl(nxsdg_ctx* c, uint32_t what, cudaStream_t st) {
+    NvtxRange nv("nxsdg halo nccl");
     nxsdg_status s = ensure_halo_staging(c);
     if (s) return s;
     std::vector<HaloMsg> msgs;
@@ -1192,6 +1202,7 @@ static int p2p_index(const nxsdg_ctx* c, const double* b) {
 }
 
 static nxsdg_status halo_p2p(nxsdg_ctx* c, uint32_t what, cudaStream_t st) {
+    NvtxRange nv("nxsdg halo p2p");
     if (!c->p2p_ok) return fail(c, NXSDG_ERR_STATE, "P2P transport not connected (nxsdg_p2p_connect)");
     MemOps& mo = memops();
     if (!mo.write || !mo.wait) return fail(c, NXSDG_ERR_UNSUPPORTED, "stream memory operations unavailable");
@@ -1905,6 +1916,7 @@ static nxsdg_status launch_step(nxsdg_ctx* c, nxsdg_step st) {
 
 // ---------------------------------------------------------------- compute API
 static nxsdg_status begin_step(nxsdg_ctx* c) {
+    NvtxRange nv("nxsdg begin_step (prep)");
     if (!c->forcing_set) return fail(c, NXSDG_ERR_STATE, "forcing not set");
     nxsdg_status s;
     if ((s = consume_forcing(c))) return s;
@@ -2019,6 +2031,7 @@ static bool mr_graph_on(const nxsdg_ctx* c) {
 // Returns NXSDG_ERR_UNSUPPORTED (state unchanged) if the capture itself is refused, so the caller can
 // issue the subcycles from the host instead.
 static nxsdg_status run_graph_multirank(nxsdg_ctx* c, int n) {
+    NvtxRange nv("nxsdg multi-rank subcycle graph");
     const int par = (int)(c->p2p_seq & 1u);
     auto key = std::make_tuple(n, c->cv, c->cs + 8 * par + 16);
     auto it = c->graphs.find(key);
@@ -2069,6 +2082,7 @@ static nxsdg_status run_graph_multirank(nxsdg_ctx* c, int n) {
 
 extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t flags) {
     GUARD(c);
+    NvtxRange nv("nxsdg_mevp_substeps");
     nxsdg_status s = check_substeps(c, n, flags);
     if (s) return s;
     if (c->d.nranks > 1 && c->d.transport == NXSDG_TRANSPORT_LOOPBACK)
@@ -2252,6 +2266,7 @@ static nxsdg_status advect_finish(nxsdg_ctx* c) {
 
 extern "C" nxsdg_status nxsdg_advect(nxsdg_ctx* c, double dt) {
     GUARD(c);
+    NvtxRange nv("nxsdg_advect");
     if (!(dt >= 0.0)) return fail(c, NXSDG_ERR_INVALID_ARG, "dt < 0");
     if (c->sphere && c->limiter) return fail(c, NXSDG_ERR_UNSUPPORTED, "sphere: no limiter (R#25 uses the box mean)");
     c->pg_fresh = false;

@@ -47,7 +47,7 @@ CONFIGS = {
     "C2": Config("C2", 256, 256, 2, 6, 6, 100),
     "C3": Config("C3", 2048, 2048, 2, 6, 6, 100, advect=True, alpha=25000.0),
     "C4": Config("C4", 4096, 4096, 2, 6, 6, 100, advect=True, alpha=25000.0),
-    "C5": Config("C5", 8192, 8192, 2, 6, 6, 100, advect=True, alpha=25000.0),
+    "C5": Config("C5", 8192, 8192, 2, 6, 6, 100, advect=True, alpha=100000.0),   # R#13: 25000 is unstable at 62.5 m
 }
 
 
