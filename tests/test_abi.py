@@ -109,10 +109,3 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
                 assert "oracle.h" not in txt, f
-
-
-def test_bytes_model_matches_design():
-    """680 B (CG2/DG2) and 256 B (CG1/DG1) per element-subcycle for the fused kernel."""
-    p2 = 4
-    assert 8 * (2 * p2 + 6 * 6 + 9 + 8 * p2) == 680
-    assert 8 * (2 * 1 + 6 * 3 + 4 + 8 * 1) == 256

@@ -560,9 +560,16 @@ def test_general_quads_stress(nx, ora, p, ns, na, mode):
             m.write_state(k, np.ascontiguousarray(v))
         m.run_step("stress"); m.run_step("stress")
         got = dict(zip(("S11", "S12", "S22"), (m.read_state(k) for k in ("S11", "S12", "S22"))))
-        with pytest.raises(nx.NxsdgError) as ex:
-            m.mevp_substeps(1)     # fused subcycle on a general mesh
-        assert ex.value.status in (nx.ERR_UNSUPPORTED, nx.ERR_STATE)
+        shp = (p * nye + 1, p * nxe + 1)
+        m.set_forcing(*(np.zeros(shp) for _ in range(4)))
+        if p == 1:   # the fused general-quad kernel is CG2/DG2: CG1 needs NXSDG_UNFUSED
+            with pytest.raises(nx.NxsdgError) as ex:
+                m.mevp_substeps(1)
+            assert ex.value.status == nx.ERR_UNSUPPORTED
+            m.mevp_substeps(1, unfused=True)
+        else:        # CG2 runs the fused general-quad subcycle
+            m.mevp_substeps(1)
+        m.synchronize()
     om = oracle.Mesh(nxe, nye, lx=lx, ly=ly, p=p, ns=ns, na=na, verts=V)
     ref = ora.stress(om, ora_params(prm), *E, H, A, *S)
     ref = ora.stress(om, ora_params(prm), *E, H, A, *ref)
@@ -1122,3 +1129,16 @@ def test_device_pointers_roundtrip(nx):
         m.read_state("S11", out)
         m.synchronize()
         np.testing.assert_array_equal(out.cpu().numpy(), m.read_state("S11"))
+
+
+@pytest.mark.parametrize("p,ns,na,bpe", [(2, 6, 6, 680.0), (1, 3, 3, 256.0), (2, 8, 6, 776.0)])
+def test_bytes_model_of_the_roofline(nx, p, ns, na, bpe):
+    """The library's algorithmic bytes per element-subcycle (bench.py's roofline numerator)
+    against an independent count of what one fused subcycle must move per element: S read + written
+    (2 x 3 n_S), P_g read (n_G), v read + written at the p^2 nodes an element owns (2 x 2 p^2), the six
+    outer-step node constants at those nodes (6 p^2)."""
+    n_G = 9 if p == 2 else 4
+    count = 8 * (2 * 3 * ns + n_G + 2 * 2 * p * p + 6 * p * p)
+    assert count == bpe
+    with nx.Mesh(20, 20, 20e3, 20e3, p, ns, na) as m:
+        assert m.bytes_per_element_subcycle == bpe
