@@ -23,6 +23,9 @@
 namespace nxk {
 
 constexpr int ADV_TMA_WARPS = 2;
+#ifndef ADV_TMA_MINB
+#define ADV_TMA_MINB 3
+#endif
 constexpr int ADV_COLS = 34;                   // FP64 box: 16-B aligned start (ix0 - 1) & ~1, covers ix0 + 31
 
 struct __align__(128) AdvSlot {
@@ -45,7 +48,7 @@ struct AdvTmaArgs {
 };
 
 template <int STAGES>
-__global__ void __launch_bounds__(32 * ADV_TMA_WARPS, 3) k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
+__global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
     static_assert(STAGES >= 4, "rows k-1, k, k+1 in use while k+2 loads");
     constexpr int P = STAGES - 3;                  // positions in flight beyond the three a job uses
     const AdvArgs& a = ta.a;

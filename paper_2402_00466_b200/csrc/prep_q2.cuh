@@ -48,6 +48,22 @@ __global__ void k_prep_elems_q2(PrepArgs a) {
     for (int g = 0; g < 9; ++g) a.Pg[g * a.eplane + e] = P[g];
 }
 
+// the per-node arithmetic of the prep (k_prep_nodes' formulas), shared by both CG2/DG2 prep kernels
+__device__ __forceinline__ void prep_node_out(const PrepArgs& a, int jr, int I, double hs, double as, int cnt) {
+    const double Hn = cnt ? fmax(hs / cnt, 1e-4) : 1e-4;
+    const double An = cnt ? fmin(fmax(as / cnt, 0.0), 1.0) : 0.0;
+    const int64_t n = (int64_t)jr * a.npitch + I;
+    const double m = a.rho_ice * Hn;
+    const double c1 = m / a.dt;
+    const double axv = a.ax[n], ayv = a.ay[n];
+    const double amag = sqrt(axv * axv + ayv * ayv);
+    const double drag = An * a.Fa * amag;
+    a.c1[n] = c1;
+    a.rx0[n] = c1 * a.vx[n] + drag * axv - m * a.f_c * a.oy[n];
+    a.ry0[n] = c1 * a.vy[n] + drag * ayv + m * a.f_c * a.ox[n];
+    a.cafo[n] = An * a.Fo;
+}
+
 // thread (ix, pr): nodes (2 ix + q, 2 pr + jy), q, jy in {0, 1}, from elements (ix - 1 | ix, pr - 1 | pr)
 __global__ void k_prep_nodes_q2(PrepArgs a) {
     const int ix = blockIdx.x * blockDim.x + threadIdx.x;
@@ -73,9 +89,9 @@ __global__ void k_prep_nodes_q2(PrepArgs a) {
     for (int jy = 0; jy < 2; ++jy) {
         const int jr = 2 * pr + jy;
         if (jr < a.node_row_begin || jr >= a.node_row_end) continue;
-        double Hn[2], An[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
+            if (2 * ix + q > 2 * a.nx) continue;
             double hs = 0.0, as = 0.0;
             int cnt = 0;
             // k_prep_nodes' order: SW, SE, NW, NE (the node's local position in each)
@@ -93,23 +109,7 @@ __global__ void k_prep_nodes_q2(PrepArgs a) {
             } else {
                 if (ok[1][1]) { hs += dg2_node<1, 1>(hE[1][1]); as += dg2_node<1, 1>(aE[1][1]); ++cnt; }
             }
-            Hn[q] = cnt ? fmax(hs / cnt, 1e-4) : 1e-4;
-            An[q] = cnt ? fmin(fmax(as / cnt, 0.0), 1.0) : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int I = 2 * ix + q;
-            if (I > 2 * a.nx) continue;
-            const int64_t n = (int64_t)jr * a.npitch + I;
-            const double m = a.rho_ice * Hn[q];
-            const double c1 = m / a.dt;
-            const double axv = a.ax[n], ayv = a.ay[n];
-            const double amag = sqrt(axv * axv + ayv * ayv);
-            const double drag = An[q] * a.Fa * amag;
-            a.c1[n] = c1;
-            a.rx0[n] = c1 * a.vx[n] + drag * axv - m * a.f_c * a.oy[n];
-            a.ry0[n] = c1 * a.vy[n] + drag * ayv + m * a.f_c * a.ox[n];
-            a.cafo[n] = An[q] * a.Fo;
+            prep_node_out(a, jr, 2 * ix + q, hs, as, cnt);
         }
     }
 }
@@ -137,29 +137,6 @@ __device__ __forceinline__ void prep_vals(const PrepArgs& a, int ex, int ey, boo
     v.a[6] = dg2_node<0, 2>(ac); v.a[7] = dg2_node<1, 2>(ac); v.a[8] = dg2_node<2, 2>(ac);
 }
 
-// the node's inputs, loaded for all four nodes of a row step before any store (the stores could alias
-// the loads as far as the compiler knows, which would serialise a memory round trip per node)
-struct PrepNodeIn { double ax, ay, vx, vy, ox, oy; };
-__device__ __forceinline__ void prep_node_load(const PrepArgs& a, int jr, int I, bool ok, PrepNodeIn& d) {
-    const int64_t n = ok ? (int64_t)jr * a.npitch + I : 0;
-    d.ax = ok ? a.ax[n] : 0.0; d.ay = ok ? a.ay[n] : 0.0; d.vx = ok ? a.vx[n] : 0.0;
-    d.vy = ok ? a.vy[n] : 0.0; d.ox = ok ? a.ox[n] : 0.0; d.oy = ok ? a.oy[n] : 0.0;
-}
-__device__ __forceinline__ void prep_node_out(const PrepArgs& a, int jr, int I, double hs, double as, int cnt,
-                                              const PrepNodeIn& d) {
-    const double Hn = cnt ? fmax(hs / cnt, 1e-4) : 1e-4;
-    const double An = cnt ? fmin(fmax(as / cnt, 0.0), 1.0) : 0.0;
-    const int64_t n = (int64_t)jr * a.npitch + I;
-    const double m = a.rho_ice * Hn;
-    const double c1 = m / a.dt;
-    const double axv = d.ax, ayv = d.ay;
-    const double amag = sqrt(axv * axv + ayv * ayv);
-    const double drag = An * a.Fa * amag;
-    a.c1[n] = c1;
-    a.rx0[n] = c1 * d.vx + drag * axv - m * a.f_c * d.oy;
-    a.ry0[n] = c1 * d.vy + drag * ayv + m * a.f_c * d.ox;
-    a.cafo[n] = An * a.Fo;
-}
 
 __global__ void __launch_bounds__(128) k_prep_nodes_march(PrepArgs a, int chunk) {
     const int lane = threadIdx.x & 31;
@@ -184,14 +161,6 @@ __global__ void __launch_bounds__(128) k_prep_nodes_march(PrepArgs a, int chunk)
         if (lane == 0) { okBW = okE(ix - 1, pr0 - 1); prep_vals(a, ix - 1, pr0 - 1, okBW, belowW); }
     }
     for (int pr = pr0; pr < pr1; ++pr) {
-        PrepNodeIn din[2][2];
-#pragma unroll
-        for (int jy = 0; jy < 2; ++jy)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int jr = 2 * pr + jy, I = 2 * ix + q;
-                prep_node_load(a, jr, I, colok && jr >= a.node_row_begin && jr < a.node_row_end && I <= 2 * a.nx, din[jy][q]);
-            }
         PrepNodeVals me, W;
         const bool okM = okE(ix, pr);
         prep_vals(a, ix, pr, okM, me);
@@ -225,7 +194,7 @@ __global__ void __launch_bounds__(128) k_prep_nodes_march(PrepArgs a, int chunk)
                     } else {
                         if (okM) { hs += me.h[4]; as += me.a[4]; ++cnt; }
                     }
-                    prep_node_out(a, jr, I, hs, as, cnt, din[jy][q]);
+                    prep_node_out(a, jr, I, hs, as, cnt);
                 }
             }
         }

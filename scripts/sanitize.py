@@ -1,6 +1,8 @@
 """Small end-to-end runs for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): the box
-kernels (TMA structured + table-driven, n_S = 3 / 6 / 8), the fused general-quad kernel, the FP32
-variants and the P2P transport (fused peer stores, in-process ranks on their own streams)."""
+kernels (TMA structured + table-driven, n_S = 3 / 6 / 8; with the round-2 TMA advection, row-marching
+prep and fused P_g on the default path), paired strip claims, the fused general-quad kernel, the sphere
+kernels, the FP32 variants and the P2P transport (fused peer stores, in-process ranks on their own
+streams)."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 from paper_2402_00466_b200 import inputs, nxsdg
@@ -30,12 +32,24 @@ for cl in (1, 0):
         m.set_option(nxsdg.OPT_CONST_STAGING, cl)
         m.set_option(nxsdg.OPT_CTAS_PER_SM, 1)
         run(m, st)
+# paired strip claims (shared-memory mailbox between the CTA's warps)
+with nxsdg.Mesh(nxe, nye, nxe * 1e3, nye * 1e3, 2, 6, 6) as m:
+    m.set_option(nxsdg.OPT_PAIR_STRIPS, 1)
+    m.set_option(nxsdg.OPT_CTAS_PER_SM, 1)
+    run(m, st)
 # fused general quads
 nxe, nye = 37, 33
 st = inputs.make_case(nxe, nye, 2, 6, 6, kind="random", lx=nxe * 1e3, ly=nye * 1e3)
 with nxsdg.Mesh(nxe, nye, nxe * 1e3, nye * 1e3, 2, 6, 6) as m:
     m.set_vertices(inputs.distorted_vertices(nxe, nye, nxe * 1e3, nye * 1e3, 0.25))
     run(m, st)
+# sphere (R#26): the SPH instantiation of the fused TMA kernel and k_advect_q2<true>
+with nxsdg.Mesh(nxe, nye, 1.0, 1.0, 2, 6, 6) as m:
+    m.set_sphere(6371e3, 1.05, 0.3, 0.2)
+    m.load(st)
+    m.advect(120.0)
+    m.mevp_substeps(3, begin_step=True)
+    m.state()
 # FP32 storage / arithmetic
 for prec in (1, 2):
     with nxsdg.Mesh(nxe, nye, nxe * 1e3, nye * 1e3, 2, 6, 6) as m:

@@ -18,10 +18,12 @@ exactly in the window's centre.  Windows: the four domain corners (the true boun
 the cyclone centre, seeded random positions; for the strips, the interfaces.
 
 Bar (north_star): relative max-norm error <= 1e-10 on S and v (fields and increments) after the full
-count, <= 1e-12 on the A, H fields.  Unconditional, except for the n_S = 8 space at 125 m, where the
-oracle's own plain and FMA builds already differ by 0.9e-10 ... 2.5e-10 after 100 subcycles
-(DESIGN.md §4): there the bar is max(1e-10, 4 x that floor), computed per window.  Every window's
-errors are printed (they appear in the -m gpu log)."""
+count, <= 1e-12 on the A, H fields.  Unconditional for C3 and C4 (box and general quads), but not where
+two equally valid FP64 evaluations of the method already disagree by more: for the n_S = 8 space at
+125 m and for C5 at 62.5 m the oracle's own plain and FMA builds differ by 0.9e-10 ... 2.5e-10 in S after
+one outer step at some windows (R#13; raising alpha does not reduce it at 62.5 m:
+scripts/floor_alpha.py), so there the bar is max(1e-10, 4 x that floor), computed per window.  Every
+window's errors are printed (they appear in the -m gpu log)."""
 import dataclasses
 
 import numpy as np
@@ -131,7 +133,7 @@ def _window_errors(kind, cfg, st, got, V, cx, cy):
     for name in ("A", "H"):
         err[name] = group_err(g, rc, (name,))
     bar = 1e-10
-    if kind == "ns8" and max(err["S"], err["dS"], err["v"], err["dv"]) > bar:
+    if kind in ("ns8", "C5") and max(err["S"], err["dS"], err["v"], err["dv"]) > bar:
         fm = core_of(oracle.Oracle("fma").outer_step(mesh, oprm, cfg.nsub, sub, do_advect=True))
         floor = 0.0
         for grp in (("S11", "S12", "S22"), ("vx", "vy")):
