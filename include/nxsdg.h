@@ -197,9 +197,6 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_ADVECT_KERNEL 0 (default) = the persistent TMA-staged structured advection k_advect_tma for the
  *                           closed-box CG2/DG2 pair without limiter (bitwise = k_advect_q2); 1 = k_advect_q2
  *   NXSDG_OPT_ADVECT_STAGES shared-memory row slots per warp of k_advect_tma: 4 (default) | 5
- *   NXSDG_OPT_PAIR_STRIPS   box TMA kernel with the work counter: 1 = the two warps of a CTA claim adjacent strips
- *                           of one chunk together (one counter claim per pair, shared-memory mailbox), so the
- *                           columns their boxes share hit L2; 0 (default) = independent claims
  *   NXSDG_OPT_PREP_KERNEL   CG2/DG2 outer-step prep of the node constants: 0 (default) = row-marching warps (each
  *                           element read once, neighbours by shuffle / register carry); 1 = a thread per element
  *                           gathering its 4 neighbours (both bitwise equal)
@@ -220,8 +217,7 @@ enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_
        NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,
        NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11,
        NXSDG_OPT_V_ROW_CARRY = 12, NXSDG_OPT_MULTIRANK_GRAPH = 13, NXSDG_OPT_ADVECT_KERNEL = 14,
-       NXSDG_OPT_ADVECT_STAGES = 15, NXSDG_OPT_FUSE_PREP_PG = 16, NXSDG_OPT_PAIR_STRIPS = 17,
-       NXSDG_OPT_PREP_KERNEL = 18 };
+       NXSDG_OPT_ADVECT_STAGES = 15, NXSDG_OPT_FUSE_PREP_PG = 16, NXSDG_OPT_PREP_KERNEL = 18 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

@@ -143,8 +143,6 @@ struct SubArgs {
                                     // qtail sub-units each (0 / 1 = off)
     int l2_hints;                   // box TMA kernel: L2 eviction-policy bits (subcycle_tma.cuh)
     int vcarry;                     // box TMA kernel: shared v node row carried in registers (subcycle_tma.cuh)
-    int pair_strips;                // box TMA kernel + work counter: a CTA's two warps take adjacent strips of
-                                    // the same chunk together (one claim per pair, smem mailbox)
     // NEXT-4 sphere (R#26; box TMA kernel instantiated with SPH): per local element row geometry table
     // (kSphRow doubles, nxsdg.cu sphere_tables); ihx = 1 / (R dlon), ihy = 1 / (R dlat) then
     const double* __restrict__ sph_rows;

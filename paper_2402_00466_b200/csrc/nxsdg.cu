@@ -126,7 +126,6 @@ struct nxsdg_ctx {
     int adv_stages = 4;    // NXSDG_OPT_ADVECT_STAGES: slots per warp of k_advect_tma (4 | 5)
     int adv_ty = 32;       // element rows per k_advect_tma work unit
     int fuse_pg = 1;       // NXSDG_OPT_FUSE_PREP_PG: the last k_advect_tma stage also writes P_g (single rank)
-    int pair_strips = 0;   // NXSDG_OPT_PAIR_STRIPS: box kernel warps of a CTA claim adjacent strips together
     int prep_kernel = 0;   // NXSDG_OPT_PREP_KERNEL: CG2/DG2 prep nodes: 0 = row-marching, 1 = per-element threads
     bool pg_fresh = false; // P_g already holds P of the current A, H (written by the last advection stage)
     bool adv_last = false; // the advection stage being launched is the last one
@@ -491,9 +490,6 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_FUSE_PREP_PG:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "fuse prep P_g 0|1");
             c->fuse_pg = (int)value; break;
-        case NXSDG_OPT_PAIR_STRIPS:
-            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "pair strips 0|1");
-            c->pair_strips = (int)value; break;
         case NXSDG_OPT_PREP_KERNEL:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "prep kernel 0|1");
             c->prep_kernel = (int)value; break;
@@ -1622,7 +1618,6 @@ static SubArgs launch_args(const nxsdg_ctx* c, const SubArgs& a0, int64_t twarps
     a.ntail = 0; a.qtail = 1;
     a.l2_hints = c->l2_policy;
     a.vcarry = c->v_carry;
-    a.pair_strips = c->pair_strips;
     const int q = a.ty / 8;
     if (!c->tail_split || !a.work_counter || q < 2 || a.nsel < 1) return a;
     const int64_t need = (2 * twarps + (int64_t)a.nstrips * q - 1) / ((int64_t)a.nstrips * q);
@@ -1702,7 +1697,7 @@ template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
     using Stage = typename K2StageSel<SF, NS, CL || LC>::T;
-    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + 2 * sizeof(uint64_t) + sizeof(int4)) + 128;   // + pair mailbox
+    const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + 2 * sizeof(uint64_t) + sizeof(int4));
     static uint64_t attr_set = 0;   // the attribute is per device: one bit per ordinal
     if (!dev_bit_test(attr_set, c->d.device)) {
         CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH>, cudaFuncAttributeMaxDynamicSharedMemorySize,

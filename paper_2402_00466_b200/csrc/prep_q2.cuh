@@ -15,10 +15,11 @@ namespace nxk {
 template <int JX, int JY>
 __device__ __forceinline__ double dg2_node(const double* c) {
     constexpr double S = 0.5 * JX - 0.5, T = 0.5 * JY - 0.5;
-    const double psi[6] = {1.0, S, T, S * S - 1.0 / 12.0, T * T - 1.0 / 12.0, S * T};
+    constexpr double psi[6] = {1.0, S, T, S * S - 1.0 / 12.0, T * T - 1.0 / 12.0, S * T};
     double v = 0.0;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) v = fma(c[k], psi[k], v);   // explicit: the same rounding in every kernel
+    for (int k = 0; k < 6; ++k)   // explicit FMAs (the same rounding in every kernel), zero terms skipped
+        if (psi[k] != 0.0) v = fma(c[k], psi[k], v);
     return v;
 }
 

@@ -499,19 +499,6 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     const int twarps = gridDim.x * K2_WARPS;
     const int gw = blockIdx.x * K2_WARPS + wib;
     const int nunits = units_total(a);
-    // paired claims (a.pair_strips): warp 0's lane 0 claims pair p from the counter and posts it in a
-    // shared-memory mailbox; warp 1's lane 0 reads it; the warps take units 2p and 2p + 1 - adjacent strips
-    // of one chunk (units are strip-fastest) - so the columns their TMA boxes share are read twice within
-    // microseconds and hit L2 instead of returning to DRAM.  Layout after the stages, barriers, job
-    // descriptors and LC barriers: 8 pair ids, 8 sequence tags, the consumer's count.
-    volatile int* mbox = reinterpret_cast<volatile int*>(
-        reinterpret_cast<uint64_t*>(reinterpret_cast<int4*>(reinterpret_cast<uint64_t*>(k2_smem + K2_WARPS * STAGES * sizeof(Stage)) +
-                                                            K2_WARPS * STAGES) + K2_WARPS * STAGES) + K2_WARPS * STAGES);
-    const bool paired = a.pair_strips && a.work_counter != nullptr;
-    if (paired) {
-        if (threadIdx.x < 17) mbox[threadIdx.x] = threadIdx.x < 8 ? 0 : (threadIdx.x < 16 ? -1 : 0);
-        __syncthreads();
-    }
     if (gw >= nunits) return;
     // L2 policies, a.l2_hints = NXSDG_OPT_L2_POLICY bits: 1 streamed loads (S, P_g, node constants)
     // evict_first; 2 (default) stores evict_first; 4 v boxes evict_last.  The new S and v (208 B per
@@ -536,25 +523,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     // or round-robin (gw + k * twarps) when no counter is given.  Lane 0 runs the prefetch
     // cursor and records each job in the stage's descriptor slot; all lanes read it back.
     struct Cur { int u, lr, lr1, ix0; bool ring, first, ok; };
-    int nclaim = 0;                       // lane 0: claims made so far (paired mode)
     auto claim = [&](int u) -> int {      // lane 0: the next unit after u
-        if (!a.work_counter) return u + twarps;
-        if (!paired) return twarps + atomicAdd(a.work_counter, 1);
-        const int k = ++nclaim, sl = k & 7;
-        int p;
-        if (wib == 0) {
-            while (k - mbox[16] > 8) {}  // the partner is 8 claims behind: ring full
-            p = (int)gridDim.x + atomicAdd(a.work_counter, 1);
-            mbox[sl] = p;
-            __threadfence_block();
-            mbox[8 + sl] = k;
-        } else {
-            while (mbox[8 + sl] != k) {}
-            __threadfence_block();
-            p = mbox[sl];
-            mbox[16] = k;
-        }
-        return 2 * p + wib;
+        return a.work_counter ? twarps + atomicAdd(a.work_counter, 1) : u + twarps;
     };
     auto start_unit = [&](int u, Cur& c) {
         for (;;) {                        // skip empty sub-units (ragged last chunk)

@@ -10,8 +10,7 @@ m = nxsdg.Mesh(cfg.nx, cfg.ny, cfg.lx, cfg.ly, 2, 6, 6, params=nxsdg.PhysParams(
 m.load(st)
 for opt, env in ((nxsdg.OPT_CONST_STAGING, "CL"), (nxsdg.OPT_CTAS_PER_SM, "CTAS"), (nxsdg.OPT_STAGES, "STAGES"),
                  (nxsdg.OPT_CHUNK_ROWS, "TY"), (nxsdg.OPT_V_ROW_CARRY, "VCARRY"),
-                 (nxsdg.OPT_L2_POLICY, "L2POL"), (nxsdg.OPT_DYNAMIC, "DYN"), (nxsdg.OPT_TAIL_SPLIT, "SPLIT"),
-                 (nxsdg.OPT_PAIR_STRIPS, "PAIR")):
+                 (nxsdg.OPT_L2_POLICY, "L2POL"), (nxsdg.OPT_DYNAMIC, "DYN"), (nxsdg.OPT_TAIL_SPLIT, "SPLIT")):
     if env in os.environ:
         m.set_option(opt, int(os.environ[env]))
 m.mevp_substeps(0, begin_step=True)

@@ -1,6 +1,6 @@
 """Small end-to-end runs for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): the box
 kernels (TMA structured + table-driven, n_S = 3 / 6 / 8; with the round-2 TMA advection, row-marching
-prep and fused P_g on the default path), paired strip claims, the fused general-quad kernel, the sphere
+prep and fused P_g on the default path), the fused general-quad kernel, the sphere
 kernels, the FP32 variants and the P2P transport (fused peer stores, in-process ranks on their own
 streams)."""
 import sys, os
@@ -32,11 +32,6 @@ for cl in (1, 0):
         m.set_option(nxsdg.OPT_CONST_STAGING, cl)
         m.set_option(nxsdg.OPT_CTAS_PER_SM, 1)
         run(m, st)
-# paired strip claims (shared-memory mailbox between the CTA's warps)
-with nxsdg.Mesh(nxe, nye, nxe * 1e3, nye * 1e3, 2, 6, 6) as m:
-    m.set_option(nxsdg.OPT_PAIR_STRIPS, 1)
-    m.set_option(nxsdg.OPT_CTAS_PER_SM, 1)
-    run(m, st)
 # fused general quads
 nxe, nye = 37, 33
 st = inputs.make_case(nxe, nye, 2, 6, 6, kind="random", lx=nxe * 1e3, ly=nye * 1e3)

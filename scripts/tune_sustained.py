@@ -61,8 +61,8 @@ for rep in range(REPS):
         m.set_option(nxsdg.OPT_L2_POLICY, l2)
         vc = combo[6] if len(combo) > 6 else 1
         m.set_option(nxsdg.OPT_V_ROW_CARRY, vc)
-        pair = combo[7] if len(combo) > 7 else 0
-        m.set_option(nxsdg.OPT_PAIR_STRIPS, pair)
+        pair = combo[7] if len(combo) > 7 else 0   # round-2 pair-strip experiment (option removed; must be 0)
+        assert pair == 0, "NXSDG_OPT_PAIR_STRIPS was removed after its A/B (profiles/tune_pair_r02.log)"
         m.set_option(nxsdg.OPT_CONST_STAGING, cl)
         m.set_option(nxsdg.OPT_CTAS_PER_SM, c)
         m.set_option(nxsdg.OPT_STAGES, stg)

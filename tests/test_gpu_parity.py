@@ -908,25 +908,6 @@ def test_advect_tma_matches_q2(nx, shape, stages):
         assert np.abs(out[0][k] - out[1][k]).max() <= 1e-14 * max(np.abs(out[1][k]).max(), 1e-300), k
 
 
-@pytest.mark.parametrize("ty", [32, 5])
-def test_pair_strips_bitwise(nx, ty):
-    """NXSDG_OPT_PAIR_STRIPS (the CTA's two warps claim adjacent strips together) changes only which warp
-    computes which unit: bitwise the independent claims, on ragged meshes with odd strip counts, tail
-    sub-units and empty ragged units (ty = 5)."""
-    nxe, nye = 130, 97
-    st = case(nxe, nye, 2, 6, 6, "random", nxe * 1e3, nye * 1e3)
-    out = []
-    for pair in (1, 0):
-        with nx.Mesh(nxe, nye, nxe * 1e3, nye * 1e3) as m:
-            m.set_option(nx.OPT_PAIR_STRIPS, pair)
-            m.set_option(nx.OPT_CHUNK_ROWS, ty)
-            m.load(st)
-            m.mevp_substeps(7, begin_step=True)
-            out.append(m.state())
-    for k in out[0]:
-        np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
-
-
 @pytest.mark.parametrize("shape", [(70, 75), (31, 130), (1, 5), (6, 1), (33, 2)])
 def test_prep_kernels_bitwise(nx, shape):
     """The row-marching prep (NXSDG_OPT_PREP_KERNEL 0, default) and the per-element gather form (1) make the
