@@ -10,7 +10,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnxsdg.so")
 SOURCES = ["nxsdg.cu"]
-DEPS = ["nxsdg.cu", "kernels.cuh", "tables.cuh", "subcycle_tma.cuh", "subcycle_gen.cuh", "advect_q2.cuh", "general_quads.cuh", "general_steps.cuh"]
+DEPS = ["nxsdg.cu", "kernels.cuh", "tables.cuh", "subcycle_tma.cuh", "subcycle_gen.cuh", "advect_q2.cuh", "general_quads.cuh", "general_steps.cuh",
+        "advect_tma.cuh", "prep_q2.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
 

@@ -129,19 +129,20 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma
         if (ta.dbg && lane == 0)
             printf("adv_tma blk %d w %d i %d M(u%d k%d j%d) U(u%d k%d j%d) rows [%d,%d) erows %d\n", blockIdx.x, wib, i,
                    dM.x, dM.y, dM.z, dU.x, dU.y, dU.z, a.erow_begin, a.erow_end, a.erows_local);
+        // the RK combine input c0 (stages 2, 3) of a job: issued before the slot wait so the loads overlap it
+        double c0A[6], c0H[6];
+        if (dM.z && a.a0 != 0.0) {
+            const int ix = (dM.x % ta.nstrips) * 31 - 1 + lane;
+            const int64_t e = (int64_t)dM.y * a.epitch + (ix < 0 ? 0 : (ix >= a.nx ? a.nx - 1 : ix));
+#pragma unroll
+            for (int k = 0; k < 6; ++k) { c0A[k] = __ldg(a.A0 + k * a.eplane + e); c0H[k] = __ldg(a.H0 + k * a.eplane + e); }
+        }
         if (dU.x >= 0) wait_slot(sU);          // position i+1 belongs to the same unit when i is a job
         if (dM.z) {                            // a job: element row r = dM.y of strip dM.x % nstrips
             const int r = dM.y;
             const int ix0 = (dM.x % ta.nstrips) * 31, ix = ix0 - 1 + lane;
             const int eo = (ix0 - 1) - ((ix0 - 1) & ~1);
             const bool valid = lane >= 1 && ix < a.nx;
-            const int ixc = ix < 0 ? 0 : (ix >= a.nx ? a.nx - 1 : ix);
-            const int64_t e = (int64_t)r * a.epitch + ixc;
-            double c0A[6], c0H[6];
-            if (a.a0 != 0.0) {
-#pragma unroll
-                for (int k = 0; k < 6; ++k) { c0A[k] = a.A0[k * a.eplane + e]; c0H[k] = a.H0[k * a.eplane + e]; }
-            }
             const AdvSlot& L = slot[sL];
             const AdvSlot& M = slot[sM];
             const AdvSlot& U = slot[sU];

@@ -1425,7 +1425,7 @@ static nxsdg_status dispatch_prep(nxsdg_ctx* c) {
         if (c->prep_kernel == 0) {   // row-marching (default)
             const int chunk = 64;
             const int pr_lo = a.node_row_begin >> 1, pr_hi = (a.node_row_end + 1) >> 1;
-            const int64_t warps = (int64_t)((c->d.nx + 1 + 31) / 32) * ((pr_hi - pr_lo + chunk - 1) / chunk);
+            const int64_t warps = (int64_t)prep_march_strips(c->d.nx) * ((pr_hi - pr_lo + chunk - 1) / chunk);
             k_prep_nodes_march<<<(unsigned)((warps + 3) / 4), 128, 0, c->stream>>>(a, chunk);
         } else {
             const int rows = a.node_row_end - a.node_row_begin;

@@ -50,19 +50,27 @@ __global__ void k_prep_elems_q2(PrepArgs a) {
 }
 
 // the per-node arithmetic of the prep (k_prep_nodes' formulas), shared by both CG2/DG2 prep kernels
-__device__ __forceinline__ void prep_node_out(const PrepArgs& a, int jr, int I, double hs, double as, int cnt) {
+struct PrepNodeOut { double c1, rx0, ry0, cafo; };
+__device__ __forceinline__ PrepNodeOut prep_node_calc(const PrepArgs& a, double hs, double as, int cnt, double axv,
+                                                      double ayv, double vxv, double vyv, double oxv, double oyv) {
     const double Hn = cnt ? fmax(hs / cnt, 1e-4) : 1e-4;
     const double An = cnt ? fmin(fmax(as / cnt, 0.0), 1.0) : 0.0;
-    const int64_t n = (int64_t)jr * a.npitch + I;
     const double m = a.rho_ice * Hn;
     const double c1 = m / a.dt;
-    const double axv = a.ax[n], ayv = a.ay[n];
-    const double amag = sqrt(axv * axv + ayv * ayv);
+    const double amag = sqrt(fma(axv, axv, ayv * ayv));
     const double drag = An * a.Fa * amag;
-    a.c1[n] = c1;
-    a.rx0[n] = c1 * a.vx[n] + drag * axv - m * a.f_c * a.oy[n];
-    a.ry0[n] = c1 * a.vy[n] + drag * ayv + m * a.f_c * a.ox[n];
-    a.cafo[n] = An * a.Fo;
+    const double mf = m * a.f_c;
+    PrepNodeOut o;                                   // explicit FMAs: the same rounding in every prep kernel
+    o.c1 = c1;
+    o.rx0 = fma(c1, vxv, fma(drag, axv, -mf * oyv));
+    o.ry0 = fma(c1, vyv, fma(drag, ayv, mf * oxv));
+    o.cafo = An * a.Fo;
+    return o;
+}
+__device__ __forceinline__ void prep_node_out(const PrepArgs& a, int jr, int I, double hs, double as, int cnt) {
+    const int64_t n = (int64_t)jr * a.npitch + I;
+    const PrepNodeOut o = prep_node_calc(a, hs, as, cnt, a.ax[n], a.ay[n], a.vx[n], a.vy[n], a.ox[n], a.oy[n]);
+    a.c1[n] = o.c1; a.rx0[n] = o.rx0; a.ry0[n] = o.ry0; a.cafo[n] = o.cafo;
 }
 
 // thread (ix, pr): nodes (2 ix + q, 2 pr + jy), q, jy in {0, 1}, from elements (ix - 1 | ix, pr - 1 | pr)
@@ -115,88 +123,124 @@ __global__ void k_prep_nodes_q2(PrepArgs a) {
     }
 }
 
-// Row-marching form of k_prep_nodes_q2 (same sums, same order: bitwise equal): a warp owns 32 element
-// columns and marches up a chunk of element rows; each element's 12 coefficients are read once, its DG
-// values at its 9 local nodes are formed once, the west neighbour's arrive by shuffle (lane 0 evaluates
-// the element west of the strip itself) and the row below's top-node values are carried in registers
-// (the chunk's first row evaluates its row below itself).
+// Row-marching form of k_prep_nodes_q2 (same sums, same order: bitwise equal): a warp owns a strip of 31
+// element columns plus a ring lane (lane 0 = the column west of the strip, which only supplies its values)
+// and marches up a chunk of element rows; each element's 12 coefficients are read once, its DG values at
+// its 9 local nodes are formed once, the west neighbour's arrive by shuffle and the row below's top-node
+// values are carried in registers (the chunk's first row evaluates its row below itself).  Per row every
+// load the row needs - the element's coefficients and the 2 x 2 nodes' six inputs as 16-B pairs - is
+// issued in one batch before any of it is used: one memory latency per row (ncu showed the first form,
+// with separate coefficient, west-element and node-input phases, long-scoreboard bound at 42 % occupancy).
 struct PrepNodeVals { double h[9], a[9]; };   // [jy * 3 + jx]
+struct PrepCoef { double h[6], a[6]; };
 
-__device__ __forceinline__ void prep_vals(const PrepArgs& a, int ex, int ey, bool ok, PrepNodeVals& v) {
-    double hc[6], ac[6];
+__device__ __forceinline__ void prep_coef(const PrepArgs& a, int ex, int ey, bool ok, PrepCoef& c) {
     const int64_t e = (int64_t)(ok ? ey : 0) * a.epitch + (ok ? ex : 0);
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-        hc[k] = ok ? a.H[k * a.eplane + e] : 0.0;
-        ac[k] = ok ? a.A[k * a.eplane + e] : 0.0;
+        c.h[k] = ok ? __ldg(a.H + k * a.eplane + e) : 0.0;
+        c.a[k] = ok ? __ldg(a.A + k * a.eplane + e) : 0.0;
     }
-    v.h[0] = dg2_node<0, 0>(hc); v.h[1] = dg2_node<1, 0>(hc); v.h[2] = dg2_node<2, 0>(hc);
-    v.h[3] = dg2_node<0, 1>(hc); v.h[4] = dg2_node<1, 1>(hc); v.h[5] = dg2_node<2, 1>(hc);
-    v.h[6] = dg2_node<0, 2>(hc); v.h[7] = dg2_node<1, 2>(hc); v.h[8] = dg2_node<2, 2>(hc);
-    v.a[0] = dg2_node<0, 0>(ac); v.a[1] = dg2_node<1, 0>(ac); v.a[2] = dg2_node<2, 0>(ac);
-    v.a[3] = dg2_node<0, 1>(ac); v.a[4] = dg2_node<1, 1>(ac); v.a[5] = dg2_node<2, 1>(ac);
-    v.a[6] = dg2_node<0, 2>(ac); v.a[7] = dg2_node<1, 2>(ac); v.a[8] = dg2_node<2, 2>(ac);
+}
+__device__ __forceinline__ void prep_vals(const PrepCoef& c, PrepNodeVals& v) {
+    v.h[0] = dg2_node<0, 0>(c.h); v.h[1] = dg2_node<1, 0>(c.h); v.h[2] = dg2_node<2, 0>(c.h);
+    v.h[3] = dg2_node<0, 1>(c.h); v.h[4] = dg2_node<1, 1>(c.h); v.h[5] = dg2_node<2, 1>(c.h);
+    v.h[6] = dg2_node<0, 2>(c.h); v.h[7] = dg2_node<1, 2>(c.h); v.h[8] = dg2_node<2, 2>(c.h);
+    v.a[0] = dg2_node<0, 0>(c.a); v.a[1] = dg2_node<1, 0>(c.a); v.a[2] = dg2_node<2, 0>(c.a);
+    v.a[3] = dg2_node<0, 1>(c.a); v.a[4] = dg2_node<1, 1>(c.a); v.a[5] = dg2_node<2, 1>(c.a);
+    v.a[6] = dg2_node<0, 2>(c.a); v.a[7] = dg2_node<1, 2>(c.a); v.a[8] = dg2_node<2, 2>(c.a);
+}
+// the six inputs of a lane's node pair (2 ix, 2 ix + 1) on one node row (the pair is 16-B aligned: npitch is
+// even; at ix = nx the second node is row padding, loaded but never used)
+struct PrepNodeIn { double2 ax, ay, vx, vy, ox, oy; };
+__device__ __forceinline__ void prep_in(const PrepArgs& a, int64_t n, bool ok, PrepNodeIn& p) {
+    const double2 z = make_double2(0.0, 0.0);
+    p.ax = ok ? __ldg(reinterpret_cast<const double2*>(a.ax + n)) : z;
+    p.ay = ok ? __ldg(reinterpret_cast<const double2*>(a.ay + n)) : z;
+    p.vx = ok ? __ldg(reinterpret_cast<const double2*>(a.vx + n)) : z;
+    p.vy = ok ? __ldg(reinterpret_cast<const double2*>(a.vy + n)) : z;
+    p.ox = ok ? __ldg(reinterpret_cast<const double2*>(a.ox + n)) : z;
+    p.oy = ok ? __ldg(reinterpret_cast<const double2*>(a.oy + n)) : z;
 }
 
+__host__ __device__ constexpr int prep_march_strips(int nx) { return (nx + 1 + 30) / 31; }
 
 __global__ void __launch_bounds__(128) k_prep_nodes_march(PrepArgs a, int chunk) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nstrips = (a.nx + 1 + 31) / 32;          // element columns 0 .. nx (column nx: node column 2 nx)
+    const int nstrips = prep_march_strips(a.nx);       // element columns 0 .. nx (column nx: node column 2 nx)
     const int pr_lo = a.node_row_begin >> 1, pr_hi = (a.node_row_end + 1) >> 1;   // element rows with owned nodes
     const int nchunks = (pr_hi - pr_lo + chunk - 1) / chunk;
     if (warp >= nstrips * nchunks) return;
     const int strip = warp % nstrips, ch = warp / nstrips;
-    const int ix = strip * 32 + lane;
+    const int ix = strip * 31 - 1 + lane;              // lane 0: the ring column west of the strip
     const int pr0 = pr_lo + ch * chunk, pr1 = min(pr0 + chunk, pr_hi);
-    const bool colok = ix <= a.nx;
+    const bool colok = lane >= 1 && ix <= a.nx;
     auto okE = [&](int ex, int ey) { return ex >= 0 && ex < a.nx && ey >= 0 && ey < a.elem_rows_with_nodes; };
-    // row below the chunk (pr0 - 1): own and west values
+    // row below the chunk (pr0 - 1): own values, the west ones by shuffle
     PrepNodeVals below, belowW;
-    prep_vals(a, ix, pr0 - 1, okE(ix, pr0 - 1), below);
     bool okB = okE(ix, pr0 - 1), okBW;
     {
+        PrepCoef cb;
+        prep_coef(a, ix, pr0 - 1, okB, cb);
+        prep_vals(cb, below);
 #pragma unroll
         for (int j = 0; j < 9; ++j) { belowW.h[j] = __shfl_up_sync(0xffffffffu, below.h[j], 1); belowW.a[j] = __shfl_up_sync(0xffffffffu, below.a[j], 1); }
         okBW = __shfl_up_sync(0xffffffffu, okB, 1);
-        if (lane == 0) { okBW = okE(ix - 1, pr0 - 1); prep_vals(a, ix - 1, pr0 - 1, okBW, belowW); }
     }
     for (int pr = pr0; pr < pr1; ++pr) {
-        PrepNodeVals me, W;
         const bool okM = okE(ix, pr);
-        prep_vals(a, ix, pr, okM, me);
+        PrepCoef cM;
+        prep_coef(a, ix, pr, okM, cM);
+        PrepNodeIn in[2];
+        bool rowok[2];
+#pragma unroll
+        for (int jy = 0; jy < 2; ++jy) {
+            const int jr = 2 * pr + jy;
+            rowok[jy] = colok && jr >= a.node_row_begin && jr < a.node_row_end;
+            prep_in(a, (int64_t)jr * a.npitch + 2 * ix, rowok[jy], in[jy]);
+        }
+        PrepNodeVals me, W;
+        prep_vals(cM, me);
 #pragma unroll
         for (int j = 0; j < 9; ++j) { W.h[j] = __shfl_up_sync(0xffffffffu, me.h[j], 1); W.a[j] = __shfl_up_sync(0xffffffffu, me.a[j], 1); }
-        bool okW = __shfl_up_sync(0xffffffffu, okM, 1);
-        if (lane == 0) { okW = okE(ix - 1, pr); prep_vals(a, ix - 1, pr, okW, W); }
-        if (colok) {
+        const bool okW = __shfl_up_sync(0xffffffffu, okM, 1);
 #pragma unroll
-            for (int jy = 0; jy < 2; ++jy) {
-                const int jr = 2 * pr + jy;
-                if (jr < a.node_row_begin || jr >= a.node_row_end) continue;
+        for (int jy = 0; jy < 2; ++jy) {
+            if (!rowok[jy]) continue;
+            const int jr = 2 * pr + jy;
+            PrepNodeOut o[2];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int I = 2 * ix + q;
-                    if (I > 2 * a.nx) continue;
-                    double hs = 0.0, as = 0.0;
-                    int cnt = 0;
-                    // k_prep_nodes' order SW, SE, NW, NE with the node's position in each element
-                    if (jy == 0 && q == 0) {
-                        if (okBW) { hs += belowW.h[8]; as += belowW.a[8]; ++cnt; }
-                        if (okB) { hs += below.h[6]; as += below.a[6]; ++cnt; }
-                        if (okW) { hs += W.h[2]; as += W.a[2]; ++cnt; }
-                        if (okM) { hs += me.h[0]; as += me.a[0]; ++cnt; }
-                    } else if (jy == 0) {
-                        if (okB) { hs += below.h[7]; as += below.a[7]; ++cnt; }
-                        if (okM) { hs += me.h[1]; as += me.a[1]; ++cnt; }
-                    } else if (q == 0) {
-                        if (okW) { hs += W.h[5]; as += W.a[5]; ++cnt; }
-                        if (okM) { hs += me.h[3]; as += me.a[3]; ++cnt; }
-                    } else {
-                        if (okM) { hs += me.h[4]; as += me.a[4]; ++cnt; }
-                    }
-                    prep_node_out(a, jr, I, hs, as, cnt);
+            for (int q = 0; q < 2; ++q) {
+                double hs = 0.0, as = 0.0;
+                int cnt = 0;
+                // k_prep_nodes' order SW, SE, NW, NE with the node's position in each element
+                if (jy == 0 && q == 0) {
+                    if (okBW) { hs += belowW.h[8]; as += belowW.a[8]; ++cnt; }
+                    if (okB) { hs += below.h[6]; as += below.a[6]; ++cnt; }
+                    if (okW) { hs += W.h[2]; as += W.a[2]; ++cnt; }
+                    if (okM) { hs += me.h[0]; as += me.a[0]; ++cnt; }
+                } else if (jy == 0) {
+                    if (okB) { hs += below.h[7]; as += below.a[7]; ++cnt; }
+                    if (okM) { hs += me.h[1]; as += me.a[1]; ++cnt; }
+                } else if (q == 0) {
+                    if (okW) { hs += W.h[5]; as += W.a[5]; ++cnt; }
+                    if (okM) { hs += me.h[3]; as += me.a[3]; ++cnt; }
+                } else {
+                    if (okM) { hs += me.h[4]; as += me.a[4]; ++cnt; }
                 }
+                const PrepNodeIn& p = in[jy];
+                o[q] = q == 0 ? prep_node_calc(a, hs, as, cnt, p.ax.x, p.ay.x, p.vx.x, p.vy.x, p.ox.x, p.oy.x)
+                              : prep_node_calc(a, hs, as, cnt, p.ax.y, p.ay.y, p.vx.y, p.vy.y, p.ox.y, p.oy.y);
+            }
+            const int64_t n = (int64_t)jr * a.npitch + 2 * ix;
+            if (ix < a.nx) {
+                *reinterpret_cast<double2*>(a.c1 + n) = make_double2(o[0].c1, o[1].c1);
+                *reinterpret_cast<double2*>(a.rx0 + n) = make_double2(o[0].rx0, o[1].rx0);
+                *reinterpret_cast<double2*>(a.ry0 + n) = make_double2(o[0].ry0, o[1].ry0);
+                *reinterpret_cast<double2*>(a.cafo + n) = make_double2(o[0].cafo, o[1].cafo);
+            } else {                                    // ix = nx: node column 2 nx only
+                a.c1[n] = o[0].c1; a.rx0[n] = o[0].rx0; a.ry0[n] = o[0].ry0; a.cafo[n] = o[0].cafo;
             }
         }
         below = me; belowW = W; okB = okM; okBW = okW;

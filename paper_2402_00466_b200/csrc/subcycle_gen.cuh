@@ -57,14 +57,72 @@ __device__ __forceinline__ double lag_d(int j, int q) {
     return j == 0 ? fma(4.0, s, -1.0) : (j == 1 ? -8.0 * s : fma(4.0, s, 1.0));
 }
 
-// b = M_ref (R G) scaled back to plain moments sum_g w psi_k G_g (project() divides by M_ref)
-__device__ __forceinline__ void moments(const double G[9], double sc, double (&b)[6]) {
-    const double mref[6] = {1.0, 1.0 / 12.0, 1.0 / 12.0, 1.0 / 180.0, 1.0 / 180.0, 1.0 / 144.0};
+// Raw Gauss sums of the six P2 moments: the plain moment sum_g w psi_k G_g is tau_k q_k (tau_k = M_ref,k x
+// the box projection's scale of proj_coeffs), so the scales fold into the mass solve below.
+__device__ __forceinline__ void proj_raw(const double G[9], double (&q)[6]) {
+    double X0[3], X1[3], X2[3];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) b[k] = 0.0;
-    project(G, sc, 0.0, b);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) b[k] *= mref[k];
+    for (int gy = 0; gy < 3; ++gy) {
+        const double s = G[gy * 3] + G[gy * 3 + 2], d = G[gy * 3 + 2] - G[gy * 3], m = G[gy * 3 + 1];
+        X0[gy] = fma(5.0, s, 8.0 * m);
+        X1[gy] = d;
+        X2[gy] = fma(-2.0, m, s);
+    }
+    q[0] = fma(5.0, X0[0] + X0[2], 8.0 * X0[1]);
+    q[1] = fma(5.0, X1[0] + X1[2], 8.0 * X1[1]);
+    q[2] = X0[2] - X0[0];
+    q[3] = fma(5.0, X2[0] + X2[2], 8.0 * X2[1]);
+    q[4] = fma(-2.0, X0[1], X0[0] + X0[2]);
+    q[5] = X1[2] - X1[0];
+}
+constexpr double kTau0 = 1.0 / 324.0, kTau1 = (1.0 / 12.0) * (kC / 18.0), kTau2 = kTau1;
+constexpr double kTau3 = (1.0 / 180.0) * (10.0 / 54.0), kTau4 = kTau3, kTau5 = (1.0 / 144.0) * (kC * kC);
+
+// Sparse LDL^T of M_K = c0 D + d1 M_S + d2 M_T (general_quads.cuh): its off-diagonal pattern is (1,0), (2,0),
+// (3,1), (5,1), (4,2), (5,2); eliminated in the order 3, 4, 0, 1, 2, 5 it fills only (2,1), so a solve
+// costs 7 + 7 FMAs and 6 products instead of the dense Cholesky's 2 x 15 FMAs and 12 products, and the
+// factor needs 4 reciprocals (1/c0 serves the pivots c0/180, c0/180, c0).  The moment scales tau are
+// folded in: with y_i = tau_i yh_i the forward pass runs on the raw sums q (g_ij = l_ij tau_j / tau_i) and
+// the pivots become rho_i = tau_i / p_i.  Same matrix as the oracle's M_i, another elimination order.
+struct MassLDL6 {
+    double l13, l10, l24, l20, l21, l51, l52;    // unit lower factor (backward substitution)
+    double g13, g10, g24, g20, g21, g51, g52;    // forward coefficients on the raw sums
+    double rho[6];
+};
+__device__ __forceinline__ void mass_ldl6(double c0, double d1, double d2, MassLDL6& F) {
+    const double ic = rcp_nr(c0);
+    F.l13 = d1 * ic; F.l24 = d2 * ic;                       // pivots 3, 4: c0 / 180; m31 = d1 / 180, m42 = d2 / 180
+    F.l10 = F.l13 * (1.0 / 12.0); F.l20 = F.l24 * (1.0 / 12.0);   // pivot 0: c0; m10 = d1 / 12, m20 = d2 / 12
+    const double m21 = -(d1 * F.l20) * (1.0 / 12.0);       // fill: -m10 m20 / c0
+    const double p1 = fma(-d1 * (1.0 / 80.0), F.l13, c0 * (1.0 / 12.0));   // c0/12 - m31^2/p3 - m10^2/p0
+    const double ip1 = rcp_nr(p1);
+    F.l21 = m21 * ip1;
+    const double m51 = d2 * (1.0 / 144.0);
+    F.l51 = m51 * ip1;
+    const double p2 = fma(-F.l21, m21, fma(-d2 * (1.0 / 80.0), F.l24, c0 * (1.0 / 12.0)));
+    const double ip2 = rcp_nr(p2);
+    const double m52 = fma(-F.l21, m51, d1 * (1.0 / 144.0));
+    F.l52 = m52 * ip2;
+    const double p5 = fma(-F.l52, m52, fma(-F.l51, m51, c0 * (1.0 / 144.0)));
+    const double ip5 = rcp_nr(p5);
+    F.g13 = F.l13 * (kTau3 / kTau1); F.g10 = F.l10 * (kTau0 / kTau1);
+    F.g24 = F.l24 * (kTau4 / kTau2); F.g20 = F.l20 * (kTau0 / kTau2);
+    F.g21 = F.l21 * (kTau1 / kTau2); F.g51 = F.l51 * (kTau1 / kTau5); F.g52 = F.l52 * (kTau2 / kTau5);
+    F.rho[0] = kTau0 * ic; F.rho[3] = (180.0 * kTau3) * ic; F.rho[4] = (180.0 * kTau4) * ic;
+    F.rho[1] = kTau1 * ip1; F.rho[2] = kTau2 * ip2; F.rho[5] = kTau5 * ip5;
+}
+// x = M_K^{-1} (sc tau (.) q)
+__device__ __forceinline__ void ldl6_solve(const MassLDL6& F, const double (&q)[6], double sc, double (&x)[6]) {
+    const double y1 = fma(-F.g10, q[0], fma(-F.g13, q[3], q[1]));
+    const double y2 = fma(-F.g21, y1, fma(-F.g20, q[0], fma(-F.g24, q[4], q[2])));
+    const double y5 = fma(-F.g52, y2, fma(-F.g51, y1, q[5]));
+    const double x5 = (sc * F.rho[5]) * y5;
+    const double x2 = fma(-F.l52, x5, (sc * F.rho[2]) * y2);
+    const double x1 = fma(-F.l51, x5, fma(-F.l21, x2, (sc * F.rho[1]) * y1));
+    x[0] = fma(-F.l20, x2, fma(-F.l10, x1, (sc * F.rho[0]) * q[0]));
+    x[4] = fma(-F.l24, x2, (sc * F.rho[4]) * q[4]);
+    x[3] = fma(-F.l13, x1, (sc * F.rho[3]) * q[3]);
+    x[1] = x1; x[2] = x2; x[5] = x5;
 }
 
 __device__ __forceinline__ const double* gen_const_box(const K2GenStage& t) { return &t.b.C[0][0][0]; }
@@ -190,8 +248,8 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
         }
         const double d0 = ax_ * by_ - bx_ * ay_, d1 = ax_ * cy_ - cx_ * ay_, d2 = cx_ * by_ - bx_ * cy_;
         const double c0 = d0 + 0.5 * (d1 + d2);
-        double L[21];
-        gen_mass_chol_n<6>(c0, d1, d2, L);
+        MassLDL6 F;
+        mass_ldl6(c0, d1, d2, F);
         // J columns at the Gauss point (gx, gy): x_s = ax + cx t, x_t = bx + cx s, y_s = ay + cy t, y_t = by + cy s
         auto jac = [&](int gx, int gy, double& xs, double& xt, double& ys, double& yt) {
             const double sg = 0.5 + (gx - 1) * kA, tg = 0.5 + (gy - 1) * kA;
@@ -229,9 +287,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                     e22[g] = fma(xs, Dty[g], -xt * Dsy[g]);                                   // |J| d vy / dy
                     e12[g] = 0.5 * (fma(xs, Dtx[g], -xt * Dsx[g]) + fma(yt, Dsy[g], -ys * Dty[g]));
                 }
-            double E11[6], E12[6], E22[6];
-            moments(e11, 1.0, E11); moments(e12, 1.0, E12); moments(e22, 1.0, E22);
-            chol_solve<6>(L, E11); chol_solve<6>(L, E12); chol_solve<6>(L, E22);
+            double E11[6], E12[6], E22[6], q[6];
+            proj_raw(e11, q); ldl6_solve(F, q, 1.0, E11);
+            proj_raw(e12, q); ldl6_solve(F, q, 1.0, E12);
+            proj_raw(e22, q); ldl6_solve(F, q, 1.0, E22);
             eval_gp<true, true>(E11, e11); eval_gp<true, true>(E12, e12); eval_gp<true, true>(E22, e22);
         }
         // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in as in the box kernel
@@ -249,8 +308,12 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
             e12[g] = jd * (pr * z);
         }
         double S11[6], S12[6], S22[6];
-        moments(e11, 1.0, S11); moments(e12, 0.5, S12); moments(e22, 1.0, S22);
-        chol_solve<6>(L, S11); chol_solve<6>(L, S12); chol_solve<6>(L, S22);
+        {
+            double q[6];
+            proj_raw(e11, q); ldl6_solve(F, q, 1.0, S11);
+            proj_raw(e12, q); ldl6_solve(F, q, 0.5, S12);
+            proj_raw(e22, q); ldl6_solve(F, q, 1.0, S22);
+        }
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
             S11[k] = fma(fac, t.b.S[k][eo + lane], S11[k]);
@@ -292,11 +355,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                     const int g = gy * 3 + gx;
                     double xs, xt, ys, yt;
                     jac(gx, gy, xs, xt, ys, yt);
-                    const double w = w1[gx] * w1[gy];
-                    AX[g] = w * fma(s11[g], yt, -s12[g] * xt);     // coefficient of d phi / ds
-                    BX[g] = w * fma(s12[g], xs, -s11[g] * ys);     // coefficient of d phi / dt
-                    AY[g] = w * fma(s12[g], yt, -s22[g] * xt);
-                    BY[g] = w * fma(s22[g], xs, -s12[g] * ys);
+                    AX[g] = fma(s11[g], yt, -s12[g] * xt);     // coefficient of d phi / ds (weights below)
+                    BX[g] = fma(s12[g], xs, -s11[g] * ys);     // coefficient of d phi / dt
+                    AY[g] = fma(s12[g], yt, -s22[g] * xt);
+                    BY[g] = fma(s22[g], xs, -s12[g] * ys);
                 }
 #pragma unroll
             for (int jx = 0; jx < 3; ++jx) {
@@ -306,7 +368,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                     double pax = 0.0, pbx = 0.0, pay = 0.0, pby = 0.0;
 #pragma unroll
                     for (int gx = 0; gx < 3; ++gx) {
-                        const double dl = lag_d(jx, gx), lv = lag_v(jx, gx);
+                        const double dl = w1[gx] * lag_d(jx, gx), lv = w1[gx] * lag_v(jx, gx);   // constants
                         pax = fma(AX[gy * 3 + gx], dl, pax); pbx = fma(BX[gy * 3 + gx], lv, pbx);
                         pay = fma(AY[gy * 3 + gx], dl, pay); pby = fma(BY[gy * 3 + gx], lv, pby);
                     }
@@ -317,7 +379,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                     double sx = 0.0, sy = 0.0;
 #pragma unroll
                     for (int gy = 0; gy < 3; ++gy) {
-                        const double lv = lag_v(jy, gy), dl = lag_d(jy, gy);
+                        const double lv = w1[gy] * lag_v(jy, gy), dl = w1[gy] * lag_d(jy, gy);
                         sx = fma(uAX[gy], lv, fma(uBX[gy], dl, sx));
                         sy = fma(uAY[gy], lv, fma(uBY[gy], dl, sy));
                     }

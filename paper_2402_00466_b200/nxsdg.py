@@ -18,6 +18,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libnxsdg.so")
+# A/B experiments only (scripts/): load another build of the same ABI, e.g. the previous commit's kernels
+if os.environ.get("NXSDG_LIB_AB"):
+    LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ["NXSDG_LIB_AB"]))
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_STATE, ERR_CUDA, ERR_NCCL, ERR_OOM = range(7)
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "STATE", 4: "CUDA", 5: "NCCL", 6: "OOM"}
