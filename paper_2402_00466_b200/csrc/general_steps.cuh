@@ -35,6 +35,7 @@ struct GenStepArgs {
     const double* vx_in; const double* vy_in; double* vx_out; double* vy_out;
     double* S; double* E; double* Fx; double* Fy; double* contrib;   // contrib: 2*NCG planes
     double* mlump;
+    double* imlump;                         // -1 / m (0 where m <= 0): the fused subcycle's F / m factor
     const double* H; const double* A;
     const double* c1; const double* rx0; const double* ry0; const double* cafo; const double* ox; const double* oy;
     int64_t eplane, epitch, npitch;
@@ -69,6 +70,7 @@ __global__ void k_gen_lumped(GenStepArgs a) {
                 }
         }
     a.mlump[(int64_t)J * a.npitch + I] = m;
+    if (a.imlump) a.imlump[(int64_t)J * a.npitch + I] = m > 0.0 ? -rcp_nr(m) : 0.0;   // the fused kernel's factor
 }
 
 // strain: E_c = M_K^{-1} sum_g w_g |J_g| psi(g) eps_c(g), with w |J| eps from adj(J) (R#9)

@@ -28,7 +28,7 @@ struct K2GenMaps {
 struct __align__(128) K2GenStage {
     K2Stage<double, 6> b;
     alignas(128) double X[2][K2_VCOLS];    // vertex rows lr, lr+1: 33 vertices x (x, y)
-    alignas(128) double M[2][K2_CCOLS];    // lumped masses of node rows 2 lr, 2 lr + 1 (owned columns)
+    alignas(128) double M[2][K2_CCOLS];    // -1 / lumped mass of node rows 2 lr, 2 lr + 1 (owned columns)
 };
 __host__ __device__ constexpr uint32_t k2g_tx_bytes() {
     return k2_tx_bytes<double, 6>() + 2 * K2_VCOLS * 8 + 2 * K2_CCOLS * 8;
@@ -46,37 +46,42 @@ __host__ __device__ constexpr uint32_t k2g_const_bytes() { return 6 * 2 * K2_CCO
 template <bool LC> struct K2GenStageSel { using T = K2GenStage; };
 template <> struct K2GenStageSel<true> { using T = K2GenStageLC; };
 
-// q-th 1D Lagrange value / derivative of node j at the Gauss abscissa S_q in {-a, 0, a}:
-//   L0 = 2S^2 - S, L1 = 1 - 4S^2, L2 = 2S^2 + S;  L0' = 4S - 1, L1' = -8S, L2' = 4S + 1  (2a^2 = 0.3)
-__device__ __forceinline__ double lag_v(int j, int q) {
-    const double s = (q - 1) * kA;
-    return j == 0 ? fma(2.0 * s, s, -s) : (j == 1 ? fma(-4.0 * s, s, 1.0) : fma(2.0 * s, s, s));
-}
-__device__ __forceinline__ double lag_d(int j, int q) {
-    const double s = (q - 1) * kA;
-    return j == 0 ? fma(4.0, s, -1.0) : (j == 1 ? -8.0 * s : fma(4.0, s, 1.0));
-}
-
 // Raw Gauss sums of the six P2 moments: the plain moment sum_g w psi_k G_g is tau_k q_k (tau_k = M_ref,k x
-// the box projection's scale of proj_coeffs), so the scales fold into the mass solve below.
+// the box projection's scale of proj_coeffs, with the 1D sums 5 G(-a) + 8 G(0) + 5 G(a) taken as
+// G(-a) + 1.6 G(0) + G(a)), so the scales fold into the mass solve below.
 __device__ __forceinline__ void proj_raw(const double G[9], double (&q)[6]) {
     double X0[3], X1[3], X2[3];
 #pragma unroll
     for (int gy = 0; gy < 3; ++gy) {
         const double s = G[gy * 3] + G[gy * 3 + 2], d = G[gy * 3 + 2] - G[gy * 3], m = G[gy * 3 + 1];
-        X0[gy] = fma(5.0, s, 8.0 * m);
+        X0[gy] = fma(1.6, m, s);
         X1[gy] = d;
         X2[gy] = fma(-2.0, m, s);
     }
-    q[0] = fma(5.0, X0[0] + X0[2], 8.0 * X0[1]);
-    q[1] = fma(5.0, X1[0] + X1[2], 8.0 * X1[1]);
+    const double s0 = X0[0] + X0[2];
+    q[0] = fma(1.6, X0[1], s0);
+    q[1] = fma(1.6, X1[1], X1[0] + X1[2]);
     q[2] = X0[2] - X0[0];
-    q[3] = fma(5.0, X2[0] + X2[2], 8.0 * X2[1]);
-    q[4] = fma(-2.0, X0[1], X0[0] + X0[2]);
+    q[3] = fma(1.6, X2[1], X2[0] + X2[2]);
+    q[4] = fma(-2.0, X0[1], s0);
     q[5] = X1[2] - X1[0];
 }
-constexpr double kTau0 = 1.0 / 324.0, kTau1 = (1.0 / 12.0) * (kC / 18.0), kTau2 = kTau1;
-constexpr double kTau3 = (1.0 / 180.0) * (10.0 / 54.0), kTau4 = kTau3, kTau5 = (1.0 / 144.0) * (kC * kC);
+constexpr double kTau0 = 25.0 / 324.0, kTau1 = 5.0 * (1.0 / 12.0) * (kC / 18.0), kTau2 = kTau1;
+constexpr double kTau3 = 5.0 * (1.0 / 180.0) * (10.0 / 54.0), kTau4 = kTau3, kTau5 = (1.0 / 144.0) * (kC * kC);
+
+// 1D contractions over the Gauss abscissae S_q in {-a, 0, a} with the weights (5, 8, 5) / 18 of the
+// Lagrange values / derivatives L_j(S) = 2S^2 - S, 1 - 4S^2, 2S^2 + S (by sums and differences):
+//   val: out_j = sum_q w_q L_j(S_q) f_q,   der: out_j = sum_q w_q L_j'(S_q) f_q
+__device__ __forceinline__ void lag_val3(double f0, double f1, double f2, double (&o)[3]) {
+    const double s = f0 + f2, d = f2 - f0;
+    const double P = (5.0 / 18.0 * 2.0 * kA * kA) * s, Q = (5.0 / 18.0 * kA) * d;
+    o[0] = P - Q; o[2] = P + Q; o[1] = fma(5.0 / 18.0 * (1.0 - 4.0 * kA * kA), s, (8.0 / 18.0) * f1);
+}
+__device__ __forceinline__ void lag_der3(double f0, double f1, double f2, double (&o)[3]) {
+    const double s = f0 + f2, d = f2 - f0;
+    const double u = (5.0 / 18.0 * 4.0 * kA) * d, t = fma(5.0 / 18.0, s, (8.0 / 18.0) * f1);
+    o[0] = u - t; o[2] = u + t; o[1] = -2.0 * u;
+}
 
 // Sparse LDL^T of M_K = c0 D + d1 M_S + d2 M_T (general_quads.cuh): its off-diagonal pattern is (1,0), (2,0),
 // (3,1), (5,1), (4,2), (5,2); eliminated in the order 3, 4, 0, 1, 2, 5 it fills only (2,1), so a solve
@@ -283,36 +288,45 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                     const int g = gy * 3 + gx;
                     double xs, xt, ys, yt;
                     jac(gx, gy, xs, xt, ys, yt);
-                    e11[g] = fma(yt, Dsx[g], -ys * Dtx[g]);                                   // |J| d vx / dx
-                    e22[g] = fma(xs, Dty[g], -xt * Dsy[g]);                                   // |J| d vy / dy
-                    e12[g] = 0.5 * (fma(xs, Dtx[g], -xt * Dsx[g]) + fma(yt, Dsy[g], -ys * Dty[g]));
+                    const double x = fma(yt, Dsx[g], -ys * Dtx[g]);                           // |J| d vx / dx
+                    const double y = fma(xs, Dty[g], -xt * Dsy[g]);                           // |J| d vy / dy
+                    e11[g] = x + y;                                                           // |J| u (trace)
+                    e22[g] = x - y;                                                           // |J| w, x 1/2 below
+                    e12[g] = fma(xs, Dtx[g], -xt * Dsx[g]) + fma(yt, Dsy[g], -ys * Dty[g]);     // x 1/2 below
                 }
             double E11[6], E12[6], E22[6], q[6];
             proj_raw(e11, q); ldl6_solve(F, q, 1.0, E11);
-            proj_raw(e12, q); ldl6_solve(F, q, 1.0, E12);
-            proj_raw(e22, q); ldl6_solve(F, q, 1.0, E22);
+            proj_raw(e12, q); ldl6_solve(F, q, 0.5, E12);
+            proj_raw(e22, q); ldl6_solve(F, q, 0.5, E22);
             eval_gp<true, true>(E11, e11); eval_gp<true, true>(E12, e12); eval_gp<true, true>(E22, e22);
         }
-        // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in as in the box kernel
+        // ---- VP stress at the Gauss points (Listing 2), alpha^{-1} folded in as in the box kernel,
+        // on the projected trace u = eps11 + eps22 (e11), half difference w = (eps11 - eps22) / 2 (e22) and
+        // eps12 (e12): Delta^2 = u^2 + w^2 + eps12^2 and g11, g22 = a +- b with a = p u - P/2, b = p w / 2
+        // (the box kernel's form), so S11 and S22 come from the projections of a and b.
+        // |J_g| = c0 + d1 S_g + d2 T_g, separably; it multiplies p / Delta and the pressure term
+        const double Jx[3] = {fma(d1, -kA, c0), c0, fma(d1, kA, c0)};
 #pragma unroll
         for (int g = 0; g < 9; ++g) {
-            const double x = e11[g], y = e22[g], z = e12[g];
-            const double draw2 = fma(z, z, fma(1.5 * x, y, 1.25 * fma(x, x, y * y)));
+            const double u = e11[g], w = e22[g], z = e12[g];
+            const double draw2 = fma(u, u, fma(w, w, z * z));
             const double rD = rsqrt_nr(draw2 + a.dmin2);
             const double ph = t.b.Pg[g][eo + lane] * hA;
-            const double pr = ph * rD;
-            const double sub = REPL ? pr * (draw2 > 0.0 ? draw2 * rsqrt_nr(draw2) : 0.0) : ph;
-            const double jd = fma(d1, (g % 3 - 1) * kA, fma(d2, (g / 3 - 1) * kA, c0));   // |J_g|
-            e11[g] = jd * fma(pr, fma(1.25, x, 0.75 * y), -sub);
-            e22[g] = jd * fma(pr, fma(1.25, y, 0.75 * x), -sub);
-            e12[g] = jd * (pr * z);
+            const double jd = g / 3 == 1 ? Jx[g % 3] : fma(d2, (g / 3 - 1) * kA, Jx[g % 3]);   // |J_g|
+            const double pr = ph * rD, prj = jd * pr;
+            const double subj = REPL ? prj * (draw2 > 0.0 ? draw2 * rsqrt_nr(draw2) : 0.0) : jd * ph;
+            e11[g] = fma(prj, u, -subj);      // |J| a
+            e22[g] = prj * w;                 // |J| 2 b
+            e12[g] = prj * z;
         }
         double S11[6], S12[6], S22[6];
         {
-            double q[6];
-            proj_raw(e11, q); ldl6_solve(F, q, 1.0, S11);
+            double q[6], Sa[6], Sb[6];
+            proj_raw(e11, q); ldl6_solve(F, q, 1.0, Sa);
+            proj_raw(e22, q); ldl6_solve(F, q, 0.5, Sb);
             proj_raw(e12, q); ldl6_solve(F, q, 0.5, S12);
-            proj_raw(e22, q); ldl6_solve(F, q, 1.0, S22);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) { S11[k] = Sa[k] + Sb[k]; S22[k] = Sa[k] - Sb[k]; }
         }
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
@@ -347,7 +361,6 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
             double s11[9], s12[9], s22[9];
             eval_gp<true, true>(S11, s11); eval_gp<true, true>(S12, s12); eval_gp<true, true>(S22, s22);
             double AX[9], BX[9], AY[9], BY[9];
-            const double w1[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
 #pragma unroll
             for (int gy = 0; gy < 3; ++gy)
 #pragma unroll
@@ -360,31 +373,27 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                     AY[g] = fma(s12[g], yt, -s22[g] * xt);
                     BY[g] = fma(s22[g], xs, -s12[g] * ys);
                 }
+            // r(jx, jy) = sum_gy [ (sum_gx w L'_jx AX) w L_jy + (sum_gx w L_jx BX) w L'_jy ] (and Y): 1D
+            // contractions over gx for each gy, then over gy
+            double uAX[3][3], uBX[3][3], uAY[3][3], uBY[3][3];   // [gy][jx]
+#pragma unroll
+            for (int gy = 0; gy < 3; ++gy) {
+                lag_der3(AX[gy * 3], AX[gy * 3 + 1], AX[gy * 3 + 2], uAX[gy]);
+                lag_val3(BX[gy * 3], BX[gy * 3 + 1], BX[gy * 3 + 2], uBX[gy]);
+                lag_der3(AY[gy * 3], AY[gy * 3 + 1], AY[gy * 3 + 2], uAY[gy]);
+                lag_val3(BY[gy * 3], BY[gy * 3 + 1], BY[gy * 3 + 2], uBY[gy]);
+            }
 #pragma unroll
             for (int jx = 0; jx < 3; ++jx) {
-                double uAX[3], uBX[3], uAY[3], uBY[3];   // per gy: sum over gx
-#pragma unroll
-                for (int gy = 0; gy < 3; ++gy) {
-                    double pax = 0.0, pbx = 0.0, pay = 0.0, pby = 0.0;
-#pragma unroll
-                    for (int gx = 0; gx < 3; ++gx) {
-                        const double dl = w1[gx] * lag_d(jx, gx), lv = w1[gx] * lag_v(jx, gx);   // constants
-                        pax = fma(AX[gy * 3 + gx], dl, pax); pbx = fma(BX[gy * 3 + gx], lv, pbx);
-                        pay = fma(AY[gy * 3 + gx], dl, pay); pby = fma(BY[gy * 3 + gx], lv, pby);
-                    }
-                    uAX[gy] = pax; uBX[gy] = pbx; uAY[gy] = pay; uBY[gy] = pby;
-                }
+                double vA[3], dB[3], vAy[3], dBy[3];
+                lag_val3(uAX[0][jx], uAX[1][jx], uAX[2][jx], vA);
+                lag_der3(uBX[0][jx], uBX[1][jx], uBX[2][jx], dB);
+                lag_val3(uAY[0][jx], uAY[1][jx], uAY[2][jx], vAy);
+                lag_der3(uBY[0][jx], uBY[1][jx], uBY[2][jx], dBy);
 #pragma unroll
                 for (int jy = 0; jy < 3; ++jy) {
-                    double sx = 0.0, sy = 0.0;
-#pragma unroll
-                    for (int gy = 0; gy < 3; ++gy) {
-                        const double lv = w1[gy] * lag_v(jy, gy), dl = w1[gy] * lag_d(jy, gy);
-                        sx = fma(uAX[gy], lv, fma(uBX[gy], dl, sx));
-                        sy = fma(uAY[gy], lv, fma(uBY[gy], dl, sy));
-                    }
-                    rX[jx][jy] = evalid ? sx : 0.0;
-                    rY[jx][jy] = evalid ? sy : 0.0;
+                    rX[jx][jy] = evalid ? vA[jy] + dB[jy] : 0.0;
+                    rY[jx][jy] = evalid ? vAy[jy] + dBy[jy] : 0.0;
                 }
             }
         }
@@ -420,8 +429,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_gen(const __grid_
                 for (int q = 0; q < 2; ++q) {
                     const int I = 2 * ix + q;
                     const int cc = 2 * lane - 2 + q;
-                    const double mass = t.M[jy][cc];
-                    const double im = mass > 0.0 ? -rcp_nr(mass) : 0.0;       // F = -r / m
+                    const double im = t.M[jy][cc];                            // F = -r / m (-1 / m staged)
                     const double fx = sumx[jy][q] * im, fy = sumy[jy][q] * im;
                     const double vxo = Vx[jy][q], vyo = Vy[jy][q];
                     const double c1 = CC[0][jy][cc], r0x = CC[1][jy][cc], r0y = CC[2][jy][cc];
