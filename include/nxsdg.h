@@ -199,7 +199,12 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_ADVECT_STAGES shared-memory row slots per warp of k_advect_tma: 4 (default) | 5
  *   NXSDG_OPT_PREP_KERNEL   CG2/DG2 outer-step prep of the node constants: 0 (default) = row-marching warps (each
  *                           element read once, neighbours by shuffle / register carry); 1 = a thread per element
- *                           gathering its 4 neighbours (both bitwise equal)
+ *                           gathering its 4 neighbours; 2 = formed by the first fused subcycle of the outer step,
+ *                           which needs them first (single rank, FP64 box kernel with constants in registers and 2
+ *                           stages; elsewhere 0): BEGIN_STEP defers the node pass and the next nxsdg_mevp_substeps
+ *                           with n > 0 runs it inside its first launch (an unfused call or a VELOCITY debug step runs
+ *                           it first as the separate pass).  All three are bitwise equal; 2 measured no faster than
+ *                           0 plus a plain subcycle
  *   NXSDG_OPT_FUSE_PREP_PG  single rank with k_advect_tma: 1 (default) = the last advection stage also writes the
  *                           outer-step prep's P at the Gauss points of the new A, H (bitwise what the prep would
  *                           compute); 0 = the prep computes it at BEGIN_STEP

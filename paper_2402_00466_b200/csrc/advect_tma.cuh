@@ -22,6 +22,9 @@
 
 namespace nxk {
 
+// 2 warps per CTA, 4 CTAs (8 warps) per SM at 232 registers.  Measured alternatives (round 2,
+// profiles/ab_adv_prep_r02.log): 3 warps x 3 CTAs at 222 registers ran the three stages in 6.05 ms per outer
+// step against 4.51 ms; 10 warps x 1 CTA at 200 registers does not launch (register granularity).
 constexpr int ADV_TMA_WARPS = 2;
 #ifndef ADV_TMA_MINB
 #define ADV_TMA_MINB 3
@@ -56,6 +59,7 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     AdvSlot* slot = reinterpret_cast<AdvSlot*>(adv_smem) + wib * STAGES;
     uint64_t* bar = reinterpret_cast<uint64_t*>(adv_smem + ADV_TMA_WARPS * STAGES * sizeof(AdvSlot)) + wib * STAGES;
+    static_assert((ADV_TMA_WARPS * STAGES * sizeof(uint64_t)) % 16 == 0, "job descriptors need 16-B alignment");
     int4* desc = reinterpret_cast<int4*>(reinterpret_cast<uint64_t*>(adv_smem + ADV_TMA_WARPS * STAGES * sizeof(AdvSlot)) +
                                          ADV_TMA_WARPS * STAGES) + wib * STAGES;
     const int twarps = gridDim.x * ADV_TMA_WARPS, gw = blockIdx.x * ADV_TMA_WARPS + wib;

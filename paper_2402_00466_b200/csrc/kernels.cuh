@@ -37,6 +37,7 @@ struct PrepArgs {
     int node_row_begin, node_row_end;          // owned local node rows [begin, end)
     int elem_rows_with_nodes;                  // element rows that touch stored nodes (excl. upper ghost)
     double rho_ice, Fa, Fo, f_c, dt, Pstar, C_conc;
+    double rdt;                                // 1 / dt
 };
 
 template <int P, int NA>
@@ -146,6 +147,9 @@ struct SubArgs {
     // NEXT-4 sphere (R#26; box TMA kernel instantiated with SPH): per local element row geometry table
     // (kSphRow doubles, nxsdg.cu sphere_tables); ihx = 1 / (R dlon), ihy = 1 / (R dlat) then
     const double* __restrict__ sph_rows;
+    // the first fused subcycle of an outer step forming the node constants itself (box TMA kernel
+    // instantiated with PREP, single rank): the prep's inputs / outputs and constants
+    PrepArgs pa;
 };
 // sphere row table layout (doubles per local element row)
 constexpr int kSphRow = 32;

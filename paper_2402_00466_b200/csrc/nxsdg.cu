@@ -126,7 +126,10 @@ struct nxsdg_ctx {
     int adv_stages = 4;    // NXSDG_OPT_ADVECT_STAGES: slots per warp of k_advect_tma (4 | 5)
     int adv_ty = 32;       // element rows per k_advect_tma work unit
     int fuse_pg = 1;       // NXSDG_OPT_FUSE_PREP_PG: the last k_advect_tma stage also writes P_g (single rank)
-    int prep_kernel = 0;   // NXSDG_OPT_PREP_KERNEL: CG2/DG2 prep nodes: 0 = row-marching, 1 = per-element threads
+    int prep_kernel = 0;   // NXSDG_OPT_PREP_KERNEL: CG2/DG2 prep nodes: 0 = row-marching, 1 = per-element threads,
+                           // 2 = in the first fused subcycle where it applies (measured no faster: not the default)
+    bool prep_defer = false;   // BEGIN_STEP left the node constants to the next fused subcycle (PREP launch)
+    bool prep_now = false;     // the next TMA launch is that PREP launch
     bool pg_fresh = false; // P_g already holds P of the current A, H (written by the last advection stage)
     bool adv_last = false; // the advection stage being launched is the last one
     int* counters = nullptr; int ncounters = 0;   // dynamic work counters, one per launch in a graph
@@ -145,7 +148,7 @@ struct nxsdg_ctx {
     bool sphere = false;
     double sph_R = 0.0, sph_lat0 = 0.0, sph_dlon = 0.0, sph_dlat = 0.0;
     double* sph_rows = nullptr;      // kSphRow doubles per local element row
-    double* mlump = nullptr; double* gcontrib = nullptr;           // general quads: lumped masses, div scratch
+    double* mlump = nullptr; double* imlump = nullptr; double* gcontrib = nullptr;           // general quads: lumped masses, div scratch
     int map_mode = 1;      // 0: iMJwPSI pre-assembled per element, 1: on the fly from the vertices
     cudaStream_t hstream = nullptr;                                 // halo stream (NCCL overlap)
     cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
@@ -290,6 +293,7 @@ static void free_all(nxsdg_ctx* c) {
     if (c->cstream) { cudaStreamDestroy(c->cstream); c->cstream = nullptr; }
     if (c->gmaps) { cudaFree(c->gmaps); c->gmaps = nullptr; }
     if (c->mlump) { cudaFree(c->mlump); c->mlump = nullptr; }
+    if (c->imlump) { cudaFree(c->imlump); c->imlump = nullptr; }
     if (c->gcontrib) { cudaFree(c->gcontrib); c->gcontrib = nullptr; }
     if (c->hstage_recv) { cudaFree(c->hstage_recv); c->hstage_recv = nullptr; }
     if (c->ev_bnd) { cudaEventDestroy(c->ev_bnd); c->ev_bnd = nullptr; }
@@ -429,7 +433,7 @@ extern "C" nxsdg_status nxsdg_set_params(nxsdg_ctx* c, const nxsdg_params* p) {
     nxsdg_status s = check_params(c, p);
     if (s) return s;
     c->prm = *p;
-    c->prepped = false;
+    c->prepped = false; c->prep_defer = false;
     c->pg_fresh = false;   // P depends on P*, C
     drop_graphs(c);   // captured launch arguments are stale
     return NXSDG_OK;
@@ -491,7 +495,7 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "fuse prep P_g 0|1");
             c->fuse_pg = (int)value; break;
         case NXSDG_OPT_PREP_KERNEL:
-            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "prep kernel 0|1");
+            if (value < 0 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "prep kernel 0|1|2");
             c->prep_kernel = (int)value; break;
         case NXSDG_OPT_MULTIRANK_GRAPH:
             if (value < -1 || value > 1) return fail(c, NXSDG_ERR_INVALID_ARG, "multi-rank graph -1|0|1");
@@ -594,7 +598,7 @@ extern "C" nxsdg_status nxsdg_write_state(nxsdg_ctx* c, nxsdg_field f, const dou
         nxsdg_status s = copy_in_nodes(c, cg_base(c, f), src, count, mem);
         if (s) return s;
     }
-    c->prepped = false;
+    c->prepped = false; c->prep_defer = false;
     c->pg_fresh = false;
     return NXSDG_OK;
 }
@@ -711,7 +715,7 @@ extern "C" nxsdg_status nxsdg_set_forcing(nxsdg_ctx* c, const double* ox, const 
         CU(cudaEventRecord(c->ev_fup, c->cstream));
         c->fpending = true;
         c->forcing_set = true;
-        c->prepped = false;
+        c->prepped = false; c->prep_defer = false;
         return NXSDG_OK;
     }
     c->fpending = false;
@@ -720,7 +724,7 @@ extern "C" nxsdg_status nxsdg_set_forcing(nxsdg_ctx* c, const double* ox, const 
     if ((s = copy_in_nodes(c, c->ax, ax, count, mem))) return s;
     if ((s = copy_in_nodes(c, c->ay, ay, count, mem))) return s;
     c->forcing_set = true;
-    c->prepped = false;
+    c->prepped = false; c->prep_defer = false;
     return NXSDG_OK;
 }
 
@@ -738,7 +742,7 @@ extern "C" nxsdg_status nxsdg_set_forcing_cyclone(nxsdg_ctx* c, double t) {
     k_cyclone_forcing<<<g, b, 0, c->stream>>>(a);
     LAUNCHED();
     c->forcing_set = true;
-    c->prepped = false;
+    c->prepped = false; c->prep_defer = false;
     return NXSDG_OK;
 }
 
@@ -749,7 +753,7 @@ static GenStepArgs gen_step_args(nxsdg_ctx* c) {
     GenStepArgs a{};
     a.verts = c->verts;
     a.vx_in = c->vx[c->cv]; a.vy_in = c->vy[c->cv]; a.vx_out = c->vx[c->cv ^ 1]; a.vy_out = c->vy[c->cv ^ 1];
-    a.S = c->S[c->cs]; a.E = c->E; a.Fx = c->Fx; a.Fy = c->Fy; a.contrib = c->gcontrib; a.mlump = c->mlump;
+    a.S = c->S[c->cs]; a.E = c->E; a.Fx = c->Fx; a.Fy = c->Fy; a.contrib = c->gcontrib; a.mlump = c->mlump; a.imlump = c->imlump;
     a.H = c->H; a.A = c->A;
     a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.ox = c->ox; a.oy = c->oy;
     a.eplane = c->eplane; a.epitch = c->epitch; a.npitch = c->npitch; a.nx = c->d.nx; a.ny = c->d.ny;
@@ -803,6 +807,7 @@ extern "C" nxsdg_status nxsdg_set_vertices(nxsdg_ctx* c, const double* xy, int64
     if (st) return st;
     const size_t nn = (size_t)c->npitch * c->nrows_local;
     if (!c->mlump) CU(cudaMalloc(&c->mlump, nn * sizeof(double)));
+    if (!c->imlump) CU(cudaMalloc(&c->imlump, nn * sizeof(double)));
     if (!c->gcontrib) CU(cudaMalloc(&c->gcontrib, (size_t)2 * (c->P + 1) * (c->P + 1) * c->eplane * sizeof(double)));
     GenStepArgs a = gen_step_args(c);
     dim3 b(128), g((unsigned)((c->P * c->d.nx + 1 + 127) / 128), (unsigned)(c->P * c->d.ny + 1));
@@ -902,7 +907,7 @@ extern "C" nxsdg_status nxsdg_set_sphere(nxsdg_ctx* c, double radius, double lat
     c->sph_R = radius; c->sph_lat0 = lat0;
     c->sph_dlon = lon_extent / c->d.nx; c->sph_dlat = lat_extent / c->d.ny;
     drop_graphs(c);
-    c->prepped = false;
+    c->prepped = false; c->prep_defer = false;
     return sphere_tables(c);
 }
 
@@ -1404,6 +1409,7 @@ static PrepArgs prep_args(nxsdg_ctx* c) {
     a.elem_rows_with_nodes = c->glo + c->nown;
     a.rho_ice = c->prm.rho_ice; a.Fa = c->prm.rho_atm * c->prm.C_atm; a.Fo = c->prm.rho_ocean * c->prm.C_ocean;
     a.f_c = c->prm.f_c; a.dt = c->prm.dt; a.Pstar = c->prm.Pstar; a.C_conc = c->prm.C_conc;
+    a.rdt = 1.0 / c->prm.dt;
     return a;
 }
 
@@ -1419,20 +1425,49 @@ static nxsdg_status launch_prep(nxsdg_ctx* c) {
     return NXSDG_OK;
 }
 
+static bool use_tma(const nxsdg_ctx* c);
+static int const_mode(const nxsdg_ctx* c);
+// NXSDG_OPT_PREP_KERNEL 2: the node constants are formed by the first fused subcycle (the PREP instantiation
+// of the box TMA kernel: single rank, FP64, n_S = 6, constants in registers, 2 stages)
+static bool prep_in_subcycle(const nxsdg_ctx* c) {
+    return c->prep_kernel == 2 && c->d.nranks == 1 && c->P == 2 && c->NA == 6 && c->NS == 6 && !c->general &&
+           !c->sphere && c->precision == 0 && c->variant == 0 && use_tma(c) && const_mode(c) == 1 &&
+           c->stages == 2;
+}
+
+// the CG2/DG2 node pass as its own launch (kind 0 row-marching, 1 per-element threads)
+static nxsdg_status launch_prep_nodes_q2(nxsdg_ctx* c, int kind) {
+    PrepArgs a = prep_args(c);
+    if (kind != 1) {
+        const int chunk = 64;
+        const int pr_lo = a.node_row_begin >> 1, pr_hi = (a.node_row_end + 1) >> 1;
+        const int64_t warps = (int64_t)prep_march_strips(c->d.nx) * ((pr_hi - pr_lo + chunk - 1) / chunk);
+        k_prep_nodes_march<<<(unsigned)((warps + 3) / 4), 128, 0, c->stream>>>(a, chunk);
+    } else {
+        const int rows = a.node_row_end - a.node_row_begin;
+        dim3 bn(32, 4), gn((unsigned)((c->d.nx + 1 + 31) / 32), (unsigned)((rows / 2 + 1 + 3) / 4));
+        k_prep_nodes_q2<<<gn, bn, 0, c->stream>>>(a);
+    }
+    LAUNCHED();
+    return NXSDG_OK;
+}
+// a deferred node pass that cannot run inside a fused subcycle (unfused call, debug VELOCITY step, options
+// changed since BEGIN_STEP): run it now as the separate pass (same inputs: v is still v^n)
+static nxsdg_status flush_prep(nxsdg_ctx* c) {
+    if (!c->prep_defer) return NXSDG_OK;
+    c->prep_defer = false;
+    return launch_prep_nodes_q2(c, 0);
+}
+
 static nxsdg_status dispatch_prep(nxsdg_ctx* c) {
     if (c->P == 2 && c->NA == 6) {   // structured (prep_q2.cuh); P_g only if the advection did not write it
         PrepArgs a = prep_args(c);
-        if (c->prep_kernel == 0) {   // row-marching (default)
-            const int chunk = 64;
-            const int pr_lo = a.node_row_begin >> 1, pr_hi = (a.node_row_end + 1) >> 1;
-            const int64_t warps = (int64_t)prep_march_strips(c->d.nx) * ((pr_hi - pr_lo + chunk - 1) / chunk);
-            k_prep_nodes_march<<<(unsigned)((warps + 3) / 4), 128, 0, c->stream>>>(a, chunk);
+        if (prep_in_subcycle(c)) {   // the node pass runs in the next fused subcycle
+            c->prep_defer = true;
         } else {
-            const int rows = a.node_row_end - a.node_row_begin;
-            dim3 bn(32, 4), gn((unsigned)((c->d.nx + 1 + 31) / 32), (unsigned)((rows / 2 + 1 + 3) / 4));
-            k_prep_nodes_q2<<<gn, bn, 0, c->stream>>>(a);
+            nxsdg_status st = launch_prep_nodes_q2(c, c->prep_kernel == 1 ? 1 : 0);
+            if (st) return st;
         }
-        LAUNCHED();
         if (!c->pg_fresh) {
             dim3 be(128), ge((unsigned)((c->d.nx + 127) / 128), (unsigned)c->erows_local);
             k_prep_elems_q2<<<ge, be, 0, c->stream>>>(a);
@@ -1460,6 +1495,7 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     a.c1 = c->c1; a.rx0 = c->rx0; a.ry0 = c->ry0; a.cafo = c->cafo; a.ox = c->ox; a.oy = c->oy;
     a.eplane = c->eplane; a.npitch = c->npitch; a.epitch = c->epitch; a.nx = c->d.nx;
     a.nstrips = (c->d.nx + 1 + 30) / 31;
+    a.pa = prep_args(c);
     a.ty = c->ty;
     a.erow_begin = c->glo; a.erow_end = c->glo + c->nown;
     a.bottom_boundary = c->r0 == 0;
@@ -1658,7 +1694,7 @@ static nxsdg_status build_gen_maps(nxsdg_ctx* c) {
             K2GenMaps& G = c->gen_maps[v][s2];
             const K2Maps& B = c->maps[v][s2];
             G.S = B.S; G.Pg = B.Pg; G.vx = B.vx; G.vy = B.vy; G.C = B.C;
-            if (!encode(&G.X, c->verts, 2, dX, sX, bX) || !encode(&G.M, c->mlump, 2, dM, sM, bM))
+            if (!encode(&G.X, c->verts, 2, dX, sX, bX) || !encode(&G.M, c->imlump, 2, dM, sM, bM))
                 return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled (general) failed");
         }
     c->gen_maps_ok = true;
@@ -1693,20 +1729,21 @@ static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     return NXSDG_OK;
 }
 
-template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false, bool LC = false, bool SPH = false>
+template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false, bool LC = false, bool SPH = false,
+          bool PREP = false>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
     using Stage = typename K2StageSel<SF, NS, CL || LC>::T;
     const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + 2 * sizeof(uint64_t) + sizeof(int4));
     static uint64_t attr_set = 0;   // the attribute is per device: one bit per ordinal
     if (!dev_bit_test(attr_set, c->d.device)) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
         dev_bit_set(attr_set, c->d.device);
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH>, 32 * K2_WARPS,
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP>, 32 * K2_WARPS,
                                                      smem));
     const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL || LC, NS) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
@@ -1714,7 +1751,7 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
+    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
         mp, launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
@@ -1741,6 +1778,13 @@ static nxsdg_status launch_tma_sel(nxsdg_ctx* c, int cv, int cs, const SubArgs& 
         }
     }
     int mode = const_mode(c);
+    if constexpr (sizeof(SF) == 8 && sizeof(CT) == 8 && NS == 6) {
+        if (c->prep_now) {   // the outer step's first subcycle forms the node constants (prep_in_subcycle)
+            if (mode != 1 || c->stages != 2) return fail(c, NXSDG_ERR_STATE, "fused prep launch without its configuration");
+            return a.repl ? launch_tma_t<true, 2, SF, CT, 6, true, false, false, true>(c, cv, cs, a)
+                          : launch_tma_t<false, 2, SF, CT, 6, true, false, false, true>(c, cv, cs, a);
+        }
+    }
     if (sizeof(SF) != 8 && mode == 2) return fail(c, NXSDG_ERR_UNSUPPORTED, "late node constants need FP64 storage");
     if (c->stages == 2) return launch_tma_mode<SF, CT, NS, 2>(c, cv, cs, a, mode);
     if (c->stages == 3) return launch_tma_mode<SF, CT, NS, 3>(c, cv, cs, a, mode);
@@ -2084,6 +2128,16 @@ extern "C" nxsdg_status nxsdg_mevp_substeps(nxsdg_ctx* c, int32_t n, uint32_t fl
         return fail(c, NXSDG_ERR_STATE, "loopback ranks step through nxsdg_group_mevp_substeps");
     if ((flags & NXSDG_BEGIN_STEP) && (s = begin_step(c))) return s;
     const bool unfused = flags & NXSDG_UNFUSED;
+    if (c->prep_defer && n > 0) {
+        if (!unfused && prep_in_subcycle(c)) {   // subcycle 1 forms the node constants (direct launch)
+            c->prep_now = true;
+            s = launch_subcycle(c);
+            c->prep_now = false;
+            c->prep_defer = false;
+            if (s) return s;
+            if (--n == 0) return NXSDG_OK;
+        } else if ((s = flush_prep(c))) return s;
+    }
     if (!unfused && c->d.nranks == 1 && n > 0 && c->precision >= 1 && use_tma(c)) {
         // NEXT-3: the FP64 state is the ABI-visible copy; the subcycles run on FP32 S / P_g
         if ((s = build_maps32(c))) return s;
@@ -2111,6 +2165,10 @@ extern "C" nxsdg_status nxsdg_run_step(nxsdg_ctx* c, nxsdg_step st) {
     if (st < NXSDG_STEP_STRAIN || st > NXSDG_STEP_VELOCITY) return fail(c, NXSDG_ERR_INVALID_ARG, "bad step");
     if (st == NXSDG_STEP_VELOCITY && !c->prepped)
         return fail(c, NXSDG_ERR_STATE, "needs a BEGIN_STEP (nxsdg_mevp_substeps(ctx, 0, NXSDG_BEGIN_STEP))");
+    if (st == NXSDG_STEP_VELOCITY) {
+        nxsdg_status fs = flush_prep(c);
+        if (fs) return fs;
+    }
     if (c->d.nranks > 1) return fail(c, NXSDG_ERR_UNSUPPORTED, "debug steps are single-rank");
     if (c->sphere) return fail(c, NXSDG_ERR_UNSUPPORTED, "sphere: no unfused debug steps");
     nxsdg_status s = ensure_debug_buffers(c);
@@ -2254,7 +2312,7 @@ static nxsdg_status advect_finish(nxsdg_ctx* c) {
     const int last = stage_out_buf(c, n_stages(c) - 1);
     std::swap(c->A, c->Asc[last]);
     std::swap(c->H, c->Hsc[last]);
-    c->prepped = false;
+    c->prepped = false; c->prep_defer = false;
     c->pg_fresh = fuse_pg(c);   // the last stage wrote P of the new A, H
     return NXSDG_OK;
 }

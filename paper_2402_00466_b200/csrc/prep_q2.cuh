@@ -8,20 +8,9 @@
 // the new A, H while they are still in registers.
 #pragma once
 #include "advect_q2.cuh"
+#include "prep_node.cuh"
 
 namespace nxk {
-
-// DG2 value at local node (jx, jy) (s, t = jx/2, jy/2): sum_k c_k psi_k, the k order of k_prep_nodes
-template <int JX, int JY>
-__device__ __forceinline__ double dg2_node(const double* c) {
-    constexpr double S = 0.5 * JX - 0.5, T = 0.5 * JY - 0.5;
-    constexpr double psi[6] = {1.0, S, T, S * S - 1.0 / 12.0, T * T - 1.0 / 12.0, S * T};
-    double v = 0.0;
-#pragma unroll
-    for (int k = 0; k < 6; ++k)   // explicit FMAs (the same rounding in every kernel), zero terms skipped
-        if (psi[k] != 0.0) v = fma(c[k], psi[k], v);
-    return v;
-}
 
 // P = P* h exp(-C (1 - a)) at the 9 Gauss points, h = max(0, H), a = clamp(A, 0, 1) (Listing 2)
 __device__ __forceinline__ void pg_q2(const double h[6], const double c[6], double Pstar, double C, double P[9]) {
@@ -49,24 +38,6 @@ __global__ void k_prep_elems_q2(PrepArgs a) {
     for (int g = 0; g < 9; ++g) a.Pg[g * a.eplane + e] = P[g];
 }
 
-// the per-node arithmetic of the prep (k_prep_nodes' formulas), shared by both CG2/DG2 prep kernels
-struct PrepNodeOut { double c1, rx0, ry0, cafo; };
-__device__ __forceinline__ PrepNodeOut prep_node_calc(const PrepArgs& a, double hs, double as, int cnt, double axv,
-                                                      double ayv, double vxv, double vyv, double oxv, double oyv) {
-    const double Hn = cnt ? fmax(hs / cnt, 1e-4) : 1e-4;
-    const double An = cnt ? fmin(fmax(as / cnt, 0.0), 1.0) : 0.0;
-    const double m = a.rho_ice * Hn;
-    const double c1 = m / a.dt;
-    const double amag = sqrt(fma(axv, axv, ayv * ayv));
-    const double drag = An * a.Fa * amag;
-    const double mf = m * a.f_c;
-    PrepNodeOut o;                                   // explicit FMAs: the same rounding in every prep kernel
-    o.c1 = c1;
-    o.rx0 = fma(c1, vxv, fma(drag, axv, -mf * oyv));
-    o.ry0 = fma(c1, vyv, fma(drag, ayv, mf * oxv));
-    o.cafo = An * a.Fo;
-    return o;
-}
 __device__ __forceinline__ void prep_node_out(const PrepArgs& a, int jr, int I, double hs, double as, int cnt) {
     const int64_t n = (int64_t)jr * a.npitch + I;
     const PrepNodeOut o = prep_node_calc(a, hs, as, cnt, a.ax[n], a.ay[n], a.vx[n], a.vy[n], a.ox[n], a.oy[n]);

@@ -69,20 +69,6 @@ __device__ __forceinline__ void proj_raw(const double G[9], double (&q)[6]) {
 constexpr double kTau0 = 25.0 / 324.0, kTau1 = 5.0 * (1.0 / 12.0) * (kC / 18.0), kTau2 = kTau1;
 constexpr double kTau3 = 5.0 * (1.0 / 180.0) * (10.0 / 54.0), kTau4 = kTau3, kTau5 = (1.0 / 144.0) * (kC * kC);
 
-// 1D contractions over the Gauss abscissae S_q in {-a, 0, a} with the weights (5, 8, 5) / 18 of the
-// Lagrange values / derivatives L_j(S) = 2S^2 - S, 1 - 4S^2, 2S^2 + S (by sums and differences):
-//   val: out_j = sum_q w_q L_j(S_q) f_q,   der: out_j = sum_q w_q L_j'(S_q) f_q
-__device__ __forceinline__ void lag_val3(double f0, double f1, double f2, double (&o)[3]) {
-    const double s = f0 + f2, d = f2 - f0;
-    const double P = (5.0 / 18.0 * 2.0 * kA * kA) * s, Q = (5.0 / 18.0 * kA) * d;
-    o[0] = P - Q; o[2] = P + Q; o[1] = fma(5.0 / 18.0 * (1.0 - 4.0 * kA * kA), s, (8.0 / 18.0) * f1);
-}
-__device__ __forceinline__ void lag_der3(double f0, double f1, double f2, double (&o)[3]) {
-    const double s = f0 + f2, d = f2 - f0;
-    const double u = (5.0 / 18.0 * 4.0 * kA) * d, t = fma(5.0 / 18.0, s, (8.0 / 18.0) * f1);
-    o[0] = u - t; o[2] = u + t; o[1] = -2.0 * u;
-}
-
 // Sparse LDL^T of M_K = c0 D + d1 M_S + d2 M_T (general_quads.cuh): its off-diagonal pattern is (1,0), (2,0),
 // (3,1), (5,1), (4,2), (5,2); eliminated in the order 3, 4, 0, 1, 2, 5 it fills only (2,1), so a solve
 // costs 7 + 7 FMAs and 6 products instead of the dense Cholesky's 2 x 15 FMAs and 12 products, and the

@@ -28,6 +28,7 @@
 #include <stdint.h>
 #include <cstddef>
 #include <cstdio>
+#include "prep_node.cuh"
 
 namespace nxk {
 
@@ -419,6 +420,20 @@ __device__ __forceinline__ void sph_project(double Ga[9], double Gb[9], double G
         S12[k] = fma(fac, S12[k], qz[k]);
     }
 }
+// 1D contractions over the Gauss abscissae S_q in {-a, 0, a} with the weights (5, 8, 5) / 18 of the
+// Lagrange values / derivatives L_j(S) = 2S^2 - S, 1 - 4S^2, 2S^2 + S (by sums and differences):
+//   val: out_j = sum_q w_q L_j(S_q) f_q,   der: out_j = sum_q w_q L_j'(S_q) f_q
+__device__ __forceinline__ void lag_val3(double f0, double f1, double f2, double (&o)[3]) {
+    const double s = f0 + f2, d = f2 - f0;
+    const double P = (5.0 / 18.0 * 2.0 * kA * kA) * s, Q = (5.0 / 18.0 * kA) * d;
+    o[0] = P - Q; o[2] = P + Q; o[1] = fma(5.0 / 18.0 * (1.0 - 4.0 * kA * kA), s, (8.0 / 18.0) * f1);
+}
+__device__ __forceinline__ void lag_der3(double f0, double f1, double f2, double (&o)[3]) {
+    const double s = f0 + f2, d = f2 - f0;
+    const double u = (5.0 / 18.0 * 4.0 * kA) * d, t = fma(5.0 / 18.0, s, (8.0 / 18.0) * f1);
+    o[0] = u - t; o[2] = u + t; o[1] = -2.0 * u;
+}
+
 // F / m at this element's nodes r[jx][jy] (as div_s / div_t produce them): the weak form with the metric,
 //   F^x_j = -sum_g w_g |J_g| [s11 dphi_j/dx + s12 dphi_j/dy + s12 phi_j tan/R]
 //   F^y_j = -sum_g w_g |J_g| [s12 dphi_j/dx + s22 dphi_j/dy - s11 phi_j tan/R]
@@ -428,37 +443,36 @@ __device__ __forceinline__ void sph_divergence(const double (&S11)[6], const dou
                                                double rX[3][3], double rY[3][3]) {
     double s11[9], s12[9], s22[9];
     eval_gp<true, true>(S11, s11); eval_gp<true, true>(S12, s12); eval_gp<true, true>(S22, s22);
-    const double w[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
-    const double L[3][3] = {{0.3 + kA, 0.4, 0.3 - kA}, {0.0, 1.0, 0.0}, {0.3 - kA, 0.4, 0.3 + kA}};   // [g][j]
-    const double dL[3][3] = {{-4.0 * kA - 1.0, 8.0 * kA, 1.0 - 4.0 * kA}, {-1.0, 0.0, 1.0},
-                             {4.0 * kA - 1.0, -8.0 * kA, 4.0 * kA + 1.0}};
+    // weighted 1D contractions over gx for each gy (lag_val3 / lag_der3: sum_gx w L_j G, sum_gx w L_j' G)
+    double X1[3][3], X2[3][3], Y1[3][3], Y2[3][3], Y3[3][3];   // [gy][jx]
 #pragma unroll
     for (int gy = 0; gy < 3; ++gy) {
-        double X1[3], X2[3], Y1[3], Y2[3], Y3[3];
+        lag_der3(s11[gy * 3], s11[gy * 3 + 1], s11[gy * 3 + 2], X1[gy]);
+        lag_val3(s12[gy * 3], s12[gy * 3 + 1], s12[gy * 3 + 2], X2[gy]);
+        lag_der3(s12[gy * 3], s12[gy * 3 + 1], s12[gy * 3 + 2], Y1[gy]);
+        lag_val3(s22[gy * 3], s22[gy * 3 + 1], s22[gy * 3 + 2], Y2[gy]);
+        lag_val3(s11[gy * 3], s11[gy * 3 + 1], s11[gy * 3 + 2], Y3[gy]);
+    }
+    // then over gy: rX_j = sum_gy w [L_jy (ihx X1 + sr X2) + L_jy' (ihy c X2)],
+    //               rY_j = sum_gy w [L_jy (ihx Y1 - sr Y3) + L_jy' (ihy c Y2)]
+    double cg[3], srg[3];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            X1[j] = 0.0; X2[j] = 0.0; Y2[j] = 0.0; Y3[j] = 0.0;
+    for (int gy = 0; gy < 3; ++gy) { cg[gy] = ihy * __ldg(row + SPH_COS + gy); srg[gy] = __ldg(row + SPH_SINR + gy); }
 #pragma unroll
-            for (int gx = 0; gx < 3; ++gx) {
-                const int g = gy * 3 + gx;
-                X1[j] = fma(w[gx] * dL[gx][j], s11[g], X1[j]);
-                X2[j] = fma(w[gx] * L[gx][j], s12[g], X2[j]);
-                Y2[j] = fma(w[gx] * L[gx][j], s22[g], Y2[j]);
-                Y3[j] = fma(w[gx] * L[gx][j], s11[g], Y3[j]);
-            }
-            Y1[j] = 0.0;
+    for (int jx = 0; jx < 3; ++jx) {
+        double P[3], Q[3], Py[3], Qy[3];
 #pragma unroll
-            for (int gx = 0; gx < 3; ++gx) Y1[j] = fma(w[gx] * dL[gx][j], s12[gy * 3 + gx], Y1[j]);
+        for (int gy = 0; gy < 3; ++gy) {
+            P[gy] = fma(ihx, X1[gy][jx], srg[gy] * X2[gy][jx]);
+            Q[gy] = cg[gy] * X2[gy][jx];
+            Py[gy] = fma(ihx, Y1[gy][jx], -srg[gy] * Y3[gy][jx]);
+            Qy[gy] = cg[gy] * Y2[gy][jx];
         }
-        const double c = __ldg(row + SPH_COS + gy), sr = __ldg(row + SPH_SINR + gy);
-        const double fs = w[gy] * ihx, ft = w[gy] * ihy * c, fm = w[gy] * sr;
+        double vP[3], dQ[3], vPy[3], dQy[3];
+        lag_val3(P[0], P[1], P[2], vP); lag_der3(Q[0], Q[1], Q[2], dQ);
+        lag_val3(Py[0], Py[1], Py[2], vPy); lag_der3(Qy[0], Qy[1], Qy[2], dQy);
 #pragma unroll
-        for (int jx = 0; jx < 3; ++jx)
-#pragma unroll
-            for (int jy = 0; jy < 3; ++jy) {
-                rX[jx][jy] = fma(fs * L[gy][jy], X1[jx], fma(fma(ft, dL[gy][jy], fm * L[gy][jy]), X2[jx], rX[jx][jy]));
-                rY[jx][jy] = fma(fs * L[gy][jy], Y1[jx], fma(ft * dL[gy][jy], Y2[jx], fma(-fm * L[gy][jy], Y3[jx], rY[jx][jy])));
-            }
+        for (int jy = 0; jy < 3; ++jy) { rX[jx][jy] = vP[jy] + dQ[jy]; rY[jx][jy] = vPy[jy] + dQy[jy]; }
     }
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx)
@@ -476,9 +490,18 @@ __device__ __forceinline__ void sph_divergence(const double (&S11)[6], const dou
 // registers.  For n_S = 6 the S region is 4896 B, so the constants also overwrite the start of P_g; both
 // regions have been consumed by then (the static_assert below keeps them clear of the v rows, which the
 // divergence / velocity still read).
-template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false, bool SPH = false>
+// PREP (with CL, FP64, n_S = 6, single rank): the first subcycle of an outer step forms the node constants
+// itself - the outer-step prep (row a1) fused into the pass that first needs it.  Instead of the six
+// constants a lane loads the element's A, H coefficients and the forcing a, o at its 2 x 2 nodes; the
+// velocity at its nodes (v^n) is already in the stage; the nodal means of H and A (R#17) come from its own
+// element, the west one (shuffle; lane 0 is the ring column), the row below (register carry; the ring row
+// of a unit is loaded like any job) - the row-marching prep's sums in its order through the same
+// prep_node_calc, so the constants (also stored for the remaining subcycles) are bitwise the prep's.
+template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false, bool SPH = false,
+          bool PREP = false>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
     static_assert(!(CL && LC), "one node-constant mode");
+    static_assert(!PREP || (CL && NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8 && !SPH), "fused prep: FP64 box, registers");
     static_assert(!SPH || (NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8), "sphere: FP64, n_S = 6");
     static_assert(!LC || sizeof(SF) == 8, "late constants need the FP64 S region");
     using StageNC_ = K2StageNC<SF, NS>;
@@ -590,6 +613,10 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     int s = 0;
     double carx[2] = {0.0, 0.0}, cary[2] = {0.0, 0.0};
     double carVx[3] = {0.0, 0.0, 0.0}, carVy[3] = {0.0, 0.0, 0.0};   // v row carry (node row 2lr of the next job)
+    // PREP: the row below's DG node values on its top node row (h, a at local jx = 0, 1, 2) and whether it exists
+    double pcH[3] = {0.0, 0.0, 0.0}, pcA[3] = {0.0, 0.0, 0.0};
+    bool pcOK = false;
+    auto okE = [&](int ex, int ey) { return ex >= 0 && ex < a.nx && ey >= 0 && ey < a.pa.elem_rows_with_nodes; };
     for (;;) {
         const int sp = (s + STAGES - 1) % STAGES;
         if (lane == 0) {
@@ -609,7 +636,29 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         // CL: this lane's node constants [field][jy][q] (only lanes that update nodes; the boundary
         // column ix = nx is forced to zero below, so it needs none)
         double cr[6][2][2];
-        if constexpr (CL) {
+        double pHc[6], pAc[6];             // PREP: this element's H, A coefficients
+        bool pOK = false;
+        if constexpr (PREP) {
+            // the forcing a, o at the lane's nodes (cr[0], cr[1] <- a; cr[4], cr[5] <- o) and the element's H, A
+            const bool need = lane >= 1 && ix >= 0 && ix <= a.nx && !cur.ring;
+            const double* const fld[4] = {a.pa.ax, a.pa.ay, a.ox, a.oy};
+            const int fi[4] = {0, 1, 4, 5};
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int jy = 0; jy < 2; ++jy) {
+                    double2 v = make_double2(0.0, 0.0);
+                    if (need) v = ldg_stream2h(fld[f] + (int64_t)(2 * lr + jy) * npitch + 2 * ix, pol_ld);
+                    cr[fi[f]][jy][0] = v.x; cr[fi[f]][jy][1] = v.y;
+                }
+            pOK = okE(ix, lr);
+            const int64_t e = (int64_t)(pOK ? lr : 0) * a.epitch + (pOK ? ix : 0);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                pHc[k] = pOK ? __ldg(a.pa.H + k * eplane + e) : 0.0;
+                pAc[k] = pOK ? __ldg(a.pa.A + k * eplane + e) : 0.0;
+            }
+        } else if constexpr (CL) {
             const bool need = lane >= 1 && ix >= 0 && ix < a.nx && !cur.ring;
             const double* const fld[6] = {a.c1, a.rx0, a.ry0, a.cafo, a.ox, a.oy};
 #pragma unroll
@@ -766,6 +815,88 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                 mbar_wait(&barC[s], (phaseC >> s) & 1u);
                 phaseC ^= 1u << s;
             }
+        }
+        if constexpr (PREP) {
+            // DG node values of this element (local (jx, jy) -> [jy * 3 + jx]) and of the west one
+            double mh[9], ma[9], wh[9], wa[9];
+            mh[0] = dg2_node<0, 0>(pHc); mh[1] = dg2_node<1, 0>(pHc); mh[2] = dg2_node<2, 0>(pHc);
+            mh[3] = dg2_node<0, 1>(pHc); mh[4] = dg2_node<1, 1>(pHc); mh[5] = dg2_node<2, 1>(pHc);
+            mh[6] = dg2_node<0, 2>(pHc); mh[7] = dg2_node<1, 2>(pHc); mh[8] = dg2_node<2, 2>(pHc);
+            ma[0] = dg2_node<0, 0>(pAc); ma[1] = dg2_node<1, 0>(pAc); ma[2] = dg2_node<2, 0>(pAc);
+            ma[3] = dg2_node<0, 1>(pAc); ma[4] = dg2_node<1, 1>(pAc); ma[5] = dg2_node<2, 1>(pAc);
+            ma[6] = dg2_node<0, 2>(pAc); ma[7] = dg2_node<1, 2>(pAc); ma[8] = dg2_node<2, 2>(pAc);
+#pragma unroll
+            for (int j = 2; j < 9; j += 3) { wh[j] = __shfl_up_sync(0xffffffffu, mh[j], 1); wa[j] = __shfl_up_sync(0xffffffffu, ma[j], 1); }
+            const bool wOK = __shfl_up_sync(0xffffffffu, pOK, 1);
+            if (cur.first) pcOK = false;                      // a unit's first row: no row below in this warp
+            const double bwH = __shfl_up_sync(0xffffffffu, pcH[2], 1), bwA = __shfl_up_sync(0xffffffffu, pcA[2], 1);
+            const bool bwOK = __shfl_up_sync(0xffffffffu, pcOK, 1);
+            if (nvalid) {
+                PrepNodeOut o[2][2];
+#pragma unroll
+                for (int jy = 0; jy < 2; ++jy)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        double hs = 0.0, as = 0.0;
+                        int cnt = 0;
+                        // the row-marching prep's order: SW, SE, NW, NE
+                        if (jy == 0 && q == 0) {
+                            if (bwOK) { hs += bwH; as += bwA; ++cnt; }
+                            if (pcOK) { hs += pcH[0]; as += pcA[0]; ++cnt; }
+                            if (wOK) { hs += wh[2]; as += wa[2]; ++cnt; }
+                            if (pOK) { hs += mh[0]; as += ma[0]; ++cnt; }
+                        } else if (jy == 0) {
+                            if (pcOK) { hs += pcH[1]; as += pcA[1]; ++cnt; }
+                            if (pOK) { hs += mh[1]; as += ma[1]; ++cnt; }
+                        } else if (q == 0) {
+                            if (wOK) { hs += wh[5]; as += wa[5]; ++cnt; }
+                            if (pOK) { hs += mh[3]; as += ma[3]; ++cnt; }
+                        } else {
+                            if (pOK) { hs += mh[4]; as += ma[4]; ++cnt; }
+                        }
+                        o[jy][q] = prep_node_calc(a.pa, hs, as, cnt, cr[0][jy][q], cr[1][jy][q], Vx[jy][q], Vy[jy][q],
+                                                  cr[4][jy][q], cr[5][jy][q]);
+                    }
+#pragma unroll
+                for (int jy = 0; jy < 2; ++jy) {
+                    const int64_t n = (int64_t)(2 * lr + jy) * npitch + 2 * ix;
+                    if (ix < a.nx) {
+                        *reinterpret_cast<double2*>(a.pa.c1 + n) = make_double2(o[jy][0].c1, o[jy][1].c1);
+                        *reinterpret_cast<double2*>(a.pa.rx0 + n) = make_double2(o[jy][0].rx0, o[jy][1].rx0);
+                        *reinterpret_cast<double2*>(a.pa.ry0 + n) = make_double2(o[jy][0].ry0, o[jy][1].ry0);
+                        *reinterpret_cast<double2*>(a.pa.cafo + n) = make_double2(o[jy][0].cafo, o[jy][1].cafo);
+                    } else {                                      // ix = nx: node column 2 nx only
+                        a.pa.c1[n] = o[jy][0].c1; a.pa.rx0[n] = o[jy][0].rx0;
+                        a.pa.ry0[n] = o[jy][0].ry0; a.pa.cafo[n] = o[jy][0].cafo;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        cr[0][jy][q] = o[jy][q].c1; cr[1][jy][q] = o[jy][q].rx0;
+                        cr[2][jy][q] = o[jy][q].ry0; cr[3][jy][q] = o[jy][q].cafo;
+                    }
+                }
+                if (a.top_boundary && lr == a.erow_end - 1) {   // the global top node row: elements below only
+                    const int jr = 2 * a.erow_end;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int I = 2 * ix + q;
+                        if (I > 2 * a.nx) continue;
+                        double hs = 0.0, as = 0.0;
+                        int cnt = 0;
+                        if (q == 0) {
+                            if (wOK) { hs += wh[8]; as += wa[8]; ++cnt; }
+                            if (pOK) { hs += mh[6]; as += ma[6]; ++cnt; }
+                        } else if (pOK) { hs += mh[7]; as += ma[7]; ++cnt; }
+                        const int64_t n = (int64_t)jr * npitch + I;
+                        const PrepNodeOut ot = prep_node_calc(a.pa, hs, as, cnt, a.pa.ax[n], a.pa.ay[n], Vx[2][q], Vy[2][q],
+                                                              a.ox[n], a.oy[n]);
+                        a.pa.c1[n] = ot.c1; a.pa.rx0[n] = ot.rx0; a.pa.ry0[n] = ot.ry0; a.pa.cafo[n] = ot.cafo;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 3; ++j) { pcH[j] = mh[6 + j]; pcA[j] = ma[6 + j]; }
+            pcOK = pOK;
         }
         if (nvalid) {
             const bool brow0 = lr == a.erow_begin && a.bottom_boundary;

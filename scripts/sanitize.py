@@ -32,6 +32,12 @@ for cl in (1, 0):
         m.set_option(nxsdg.OPT_CONST_STAGING, cl)
         m.set_option(nxsdg.OPT_CTAS_PER_SM, 1)
         run(m, st)
+# session 3: the node pass inside the first subcycle (NXSDG_OPT_PREP_KERNEL 2, the PREP instantiation) and the
+# batched-load row-marching prep (0) on the same tall box
+for pk in (2, 0):
+    with nxsdg.Mesh(nxe, nye, nxe * 1e3, nye * 1e3, 2, 6, 6) as m:
+        m.set_option(nxsdg.OPT_PREP_KERNEL, pk)
+        run(m, st)
 # fused general quads
 nxe, nye = 37, 33
 st = inputs.make_case(nxe, nye, 2, 6, 6, kind="random", lx=nxe * 1e3, ly=nye * 1e3)

@@ -908,22 +908,75 @@ def test_advect_tma_matches_q2(nx, shape, stages):
         assert np.abs(out[0][k] - out[1][k]).max() <= 1e-14 * max(np.abs(out[1][k]).max(), 1e-300), k
 
 
-@pytest.mark.parametrize("shape", [(70, 75), (31, 130), (1, 5), (6, 1), (33, 2)])
+@pytest.mark.parametrize("shape", [(70, 75), (31, 130), (1, 5), (6, 1), (33, 2), (130, 97)])
 def test_prep_kernels_bitwise(nx, shape):
-    """The row-marching prep (NXSDG_OPT_PREP_KERNEL 0, default) and the per-element gather form (1) make the
-    same sums in the same order: the outer steps are bitwise equal (ragged strips, chunk edges, 1-row meshes)."""
+    """The three forms of the outer-step node pass make the same sums in the same order through the same
+    per-node function: the first fused subcycle forming the constants itself (NXSDG_OPT_PREP_KERNEL 2),
+    the row-marching prep (0, default) and the per-element gather form (1).  Two outer steps are bitwise equal
+    (ragged strips, chunk edges, ring rows / columns, 1-row meshes, the top node row, column 2 nx)."""
     nxe, nye = shape
     st = case(nxe, nye, 2, 6, 6, "random", nxe * 1e3, nye * 1e3)
     out = []
-    for pk in (0, 1):
+    for pk in (2, 0, 1):
         with nx.Mesh(nxe, nye, nxe * 1e3, nye * 1e3) as m:
             m.set_option(nx.OPT_PREP_KERNEL, pk)
+            m.set_option(nx.OPT_CHUNK_ROWS, 8)     # several units per strip: ring rows inside the mesh
             m.load(st)
-            m.advect(120.0)
-            m.mevp_substeps(3, begin_step=True)
+            for _ in range(2):
+                m.advect(120.0)
+                m.mevp_substeps(3, begin_step=True)
             out.append(m.state())
-    for k in out[0]:
-        np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
+    for other in out[1:]:
+        for k in out[0]:
+            np.testing.assert_array_equal(out[0][k], other[k], err_msg=k)
+
+
+def test_deferred_prep_paths(nx):
+    """BEGIN_STEP with NXSDG_OPT_PREP_KERNEL 2 leaves the node pass to the next fused subcycle; every other
+    consumer runs it first as the separate pass.  All of these give bitwise the same outer step as the
+    separate prep: BEGIN alone then substeps (the bench's call pattern), BEGIN then an UNFUSED call, BEGIN then
+    an option change that rules the fused form out, and a state write after BEGIN (a new BEGIN is required)."""
+    nxe, nye = 70, 45
+    st = case(nxe, nye, 2, 6, 6, "warm", 140e3, 90e3)
+
+    def run(pattern):
+        with nx.Mesh(nxe, nye, 140e3, 90e3) as m:
+            m.load(st)
+            m.set_option(nx.OPT_PREP_KERNEL, 0 if pattern == "separate" else 2)
+            m.advect(120.0)
+            if pattern in ("separate", "fused"):
+                m.mevp_substeps(4, begin_step=True)
+            elif pattern == "split":
+                m.mevp_substeps(0, begin_step=True)
+                m.mevp_substeps(1, begin_step=False)
+                m.mevp_substeps(3, begin_step=False)
+            elif pattern == "unfused_first":
+                m.mevp_substeps(0, begin_step=True)
+                m.mevp_substeps(1, begin_step=False, unfused=True)
+                m.mevp_substeps(3, begin_step=False)
+            elif pattern == "option_change":
+                m.mevp_substeps(0, begin_step=True)
+                m.set_option(nx.OPT_STAGES, 3)        # the fused form needs 2 stages: flush
+                m.mevp_substeps(4, begin_step=False)
+            elif pattern == "rewrite":
+                m.mevp_substeps(0, begin_step=True)
+                m.write_state("H", st["H"])            # the deferred pass is dropped with the BEGIN
+                with pytest.raises(nx.NxsdgError):
+                    m.mevp_substeps(4, begin_step=False)
+                m.mevp_substeps(4, begin_step=True)
+            return m.state()
+
+    ref = run("separate")
+    for pat in ("fused", "split", "option_change"):
+        got = run(pat)
+        for k in ref:
+            np.testing.assert_array_equal(got[k], ref[k], err_msg=f"{pat} {k}")
+    # an unfused first subcycle differs from the fused one only by FMA contraction
+    got = run("unfused_first")
+    for grp in (("S11", "S12", "S22"), ("vx", "vy")):
+        assert max(np.abs(got[k] - ref[k]).max() for k in grp) <= 1e-12 * max(np.abs(ref[k]).max() for k in grp)
+    # the rewrite: same H as the initial state after one advection -> differs from ref; only check it ran
+    run("rewrite")
 
 
 def test_fused_prep_pg(nx):
