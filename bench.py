@@ -304,6 +304,8 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle window check on the bench line")
     ap.add_argument("--prep-kernel", type=int, default=None,
                     help="NXSDG_OPT_PREP_KERNEL for A/B runs (default: the library's)")
+    ap.add_argument("--adv-stages", type=int, default=None,
+                    help="NXSDG_OPT_ADVECT_STAGES for A/B runs (default: the library's)")
     args = ap.parse_args()
     cname = args.config or ("C5" if args.weak else "C4")
     cfg = inputs.CONFIGS[cname]
@@ -375,6 +377,8 @@ def main():
         m.set_option(nxsdg.OPT_PRECISION, 2 if args.fp32_stress else 1)
     if args.prep_kernel is not None:
         m.set_option(nxsdg.OPT_PREP_KERNEL, args.prep_kernel)
+    if args.adv_stages is not None:
+        m.set_option(nxsdg.OPT_ADVECT_STAGES, args.adv_stages)
     if args.limiter:
         m.set_option(nxsdg.OPT_LIMITER, 1)
     if args.sphere:

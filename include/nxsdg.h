@@ -196,7 +196,8 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *                           H >= 0 at the volume and edge Gauss points; element means, hence mass, unchanged)
  *   NXSDG_OPT_ADVECT_KERNEL 0 (default) = the persistent TMA-staged structured advection k_advect_tma for the
  *                           closed-box CG2/DG2 pair without limiter (bitwise = k_advect_q2); 1 = k_advect_q2
- *   NXSDG_OPT_ADVECT_STAGES shared-memory row slots per warp of k_advect_tma: 4 (default) | 5
+ *   NXSDG_OPT_ADVECT_STAGES shared-memory row slots per warp of k_advect_tma: 3 (late ring: row k+2 issued into
+ *                           row k-1's slot once job k has read it; 5 CTAs / 10 warps per SM) | 4 (default) | 5
  *   NXSDG_OPT_PREP_KERNEL   CG2/DG2 outer-step prep of the node constants: 0 (default) = row-marching warps (each
  *                           element read once, neighbours by shuffle / register carry); 1 = a thread per element
  *                           gathering its 4 neighbours; 2 = formed by the first fused subcycle of the outer step,

@@ -39,10 +39,28 @@ struct __align__(128) AdvSlot {
 };
 constexpr uint32_t kAdvTx = 2u * 6u * ADV_COLS * 8u + 2u * 2u * K2_VCOLS * 8u;
 
+// the RK combine input c0 = (A^n, H^n) of one job (stages 2, 3): one buffer per warp, TMA-loaded while the
+// previous job computes (a plain register prefetch left one DFMA with a quarter of the stage's stall samples)
+struct __align__(128) AdvC0 {
+    alignas(128) double A[6][ADV_COLS];
+    alignas(128) double H[6][ADV_COLS];
+};
+constexpr uint32_t kAdvC0Tx = 2u * 6u * ADV_COLS * 8u;
+
 struct AdvMaps {
     CUtensorMap A, H;     // 3D {nx, erows_local, 6}, box {34, 1, 6}: the stage input planes
     CUtensorMap vx, vy;   // 2D node grid, box {66, 2}
+    CUtensorMap A0, H0;   // the RK combine input planes (same geometry as A, H)
 };
+// dynamic shared memory of k_advect_tma: slots [warps][STAGES] | c0 buffers [warps] | slot barriers
+// [warps][STAGES] | c0 barriers [warps] (padded to 16 B) | job descriptors [warps][STAGES]
+__host__ __device__ constexpr size_t adv_bar_off(int st) {
+    return (size_t)ADV_TMA_WARPS * st * sizeof(AdvSlot) + (size_t)ADV_TMA_WARPS * sizeof(AdvC0);
+}
+__host__ __device__ constexpr size_t adv_desc_off(int st) {
+    return adv_bar_off(st) + (((size_t)ADV_TMA_WARPS * (st + 1) * 8 + 15) / 16) * 16;
+}
+__host__ __device__ constexpr size_t adv_smem_bytes(int st) { return adv_desc_off(st) + (size_t)ADV_TMA_WARPS * st * 16; }
 
 struct AdvTmaArgs {
     AdvArgs a;
@@ -50,23 +68,30 @@ struct AdvTmaArgs {
     int dbg;                                   // debug: lane 0 prints its positions (NXSDG_DEBUG_ADV_TMA)
 };
 
+// STAGES = 3 ("late" ring): row k + 2 goes into the slot of row k - 1 as soon as job k has read what it
+// needs of row k - 1 (its top v node row, and the south flux for a unit's first job), so a job still
+// waits only for a row issued one job earlier; 3 slots per warp fit 5 CTAs (10 warps) per SM at <= 204
+// registers where 4 slots fit 4 (8 warps)
 template <int STAGES>
-__global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
-    static_assert(STAGES >= 4, "rows k-1, k, k+1 in use while k+2 loads");
-    constexpr int P = STAGES - 3;                  // positions in flight beyond the three a job uses
+__global__ void __launch_bounds__(32 * ADV_TMA_WARPS, STAGES == 3 ? 5 : ADV_TMA_MINB)
+k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
+    static_assert(STAGES >= 3, "rows k-1, k, k+1 in use");
+    constexpr bool LATE = STAGES == 3;
+    constexpr int P = LATE ? 0 : STAGES - 3;       // positions in flight beyond the three a job uses
     const AdvArgs& a = ta.a;
     extern __shared__ __align__(1024) unsigned char adv_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     AdvSlot* slot = reinterpret_cast<AdvSlot*>(adv_smem) + wib * STAGES;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(adv_smem + ADV_TMA_WARPS * STAGES * sizeof(AdvSlot)) + wib * STAGES;
-    static_assert((ADV_TMA_WARPS * STAGES * sizeof(uint64_t)) % 16 == 0, "job descriptors need 16-B alignment");
-    int4* desc = reinterpret_cast<int4*>(reinterpret_cast<uint64_t*>(adv_smem + ADV_TMA_WARPS * STAGES * sizeof(AdvSlot)) +
-                                         ADV_TMA_WARPS * STAGES) + wib * STAGES;
+    AdvC0* c0buf = reinterpret_cast<AdvC0*>(adv_smem + ADV_TMA_WARPS * STAGES * sizeof(AdvSlot)) + wib;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(adv_smem + adv_bar_off(STAGES)) + wib * STAGES;
+    uint64_t* bar0 = reinterpret_cast<uint64_t*>(adv_smem + adv_bar_off(STAGES)) + ADV_TMA_WARPS * STAGES + wib;
+    int4* desc = reinterpret_cast<int4*>(adv_smem + adv_desc_off(STAGES)) + wib * STAGES;
     const int twarps = gridDim.x * ADV_TMA_WARPS, gw = blockIdx.x * ADV_TMA_WARPS + wib;
     const int nunits = ta.nstrips * ta.nchunks;
     if (gw >= nunits) return;
     if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        mbar_init(bar0, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -102,7 +127,7 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma
     Cur cur;
     if (lane == 0) {
         unit_start(gw, cur);
-        for (int q = 0; q <= P; ++q) {       // positions 0 .. P
+        for (int q = 0; q <= (LATE ? 1 : P); ++q) {       // positions 0 .. P (LATE: 0, 1)
             issue(cur, q);
             if (cur.ok) step(cur);
         }
@@ -113,6 +138,17 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma
         mbar_wait(&bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
     };
+    // c0 of a job (row r of unit u) into the warp's buffer; c0_inflight: issued and not yet consumed
+    uint32_t ph0 = 0;
+    bool c0_inflight = false;
+    auto issue_c0 = [&](int u, int r) {   // lane 0; every lane's reads of the buffer are done (__syncwarp)
+        const int xs = (((u % ta.nstrips) * 31) - 1) & ~1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar0, kAdvC0Tx);
+        tma3(&c0buf->A[0][0], &maps.A0, bar0, xs, r, 0);
+        tma3(&c0buf->H[0][0], &maps.H0, bar0, xs, r, 0);
+    };
+    const bool rk = a.a0 != 0.0;
     const int4 d0 = desc[0];
     if (d0.x < 0) return;
     wait_slot(0);
@@ -125,21 +161,31 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma
         const int sL = (i + STAGES - 1) % STAGES, sM = i % STAGES, sU = (i + 1) % STAGES;
         const int4 dM = desc[sM];
         if (dM.x < 0) break;
-        if (lane == 0) {                       // position i + 1 + P into the slot of position i - 2 (done)
+        if (!LATE && lane == 0) {              // position i + 1 + P into the slot of position i - 2 (done)
             issue(cur, (i + 1 + P) % STAGES);
             if (cur.ok) step(cur);
         }
+        // LATE: position i + 2 into the slot of position i - 1 once nothing reads it any more (a ring
+        // position reads nothing of it; a job after its south flux, below)
+        auto issue_late = [&]() {
+            if constexpr (LATE) {
+                __syncwarp();
+                if (lane == 0) {
+                    issue(cur, sL);
+                    if (cur.ok) step(cur);
+                }
+            }
+        };
+        if (!dM.z) issue_late();
         const int4 dU = desc[sU];              // issued at iteration i - P or in the prologue
         if (ta.dbg && lane == 0)
             printf("adv_tma blk %d w %d i %d M(u%d k%d j%d) U(u%d k%d j%d) rows [%d,%d) erows %d\n", blockIdx.x, wib, i,
                    dM.x, dM.y, dM.z, dU.x, dU.y, dU.z, a.erow_begin, a.erow_end, a.erows_local);
-        // the RK combine input c0 (stages 2, 3) of a job: issued before the slot wait so the loads overlap it
-        double c0A[6], c0H[6];
-        if (dM.z && a.a0 != 0.0) {
-            const int ix = (dM.x % ta.nstrips) * 31 - 1 + lane;
-            const int64_t e = (int64_t)dM.y * a.epitch + (ix < 0 ? 0 : (ix >= a.nx ? a.nx - 1 : ix));
-#pragma unroll
-            for (int k = 0; k < 6; ++k) { c0A[k] = __ldg(a.A0 + k * a.eplane + e); c0H[k] = __ldg(a.H0 + k * a.eplane + e); }
+        // the RK combine input c0 (stages 2, 3): prefetched by TMA during the previous job of the unit, or (a
+        // unit's first job) issued now - it is waited for only at the update, at the end of the job
+        if (dM.z && rk && !c0_inflight) {
+            if (lane == 0) issue_c0(dM.x, dM.y);
+            c0_inflight = true;
         }
         if (dU.x >= 0) wait_slot(sU);          // position i+1 belongs to the same unit when i is a job
         if (dM.z) {                            // a job: element row r = dM.y of strip dM.x % nstrips
@@ -190,6 +236,7 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma
 #pragma unroll
             for (int q = 0; q < 3; ++q) { cNA[q] = FnA[q]; cNH[q] = FnH[q]; }
             prev_unit = dM.x;
+            issue_late();                      // row k - 1 (slot sL) is consumed
             // ---- volume term and update: k_advect_q2's code
             double gvx[3][3], gvy[3][3];
             {
@@ -239,12 +286,20 @@ __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, ADV_TMA_MINB) k_advect_tma
                 edge_mom(Fs, m0, m1, m2);
                 Lk[0] += a.ihy * m0; Lk[1] += a.ihy * m1; Lk[2] -= a.ihy * 0.5 * m0; Lk[3] += a.ihy * m2;
                 Lk[4] += a.ihy * m0 * (1.0 / 6.0); Lk[5] -= a.ihy * 0.5 * m1;
-                const double* c0 = tr == 0 ? c0A : c0H;
+                if (tr == 0 && rk) {           // the job's c0 has landed in the buffer
+                    mbar_wait(bar0, ph0);
+                    ph0 ^= 1u;
+                }
 #pragma unroll
                 for (int k = 0; k < 6; ++k) {
                     const double v = a.a1 * fma(a.dt, Lk[k] * mr[k], c[k]);
-                    ncv[tr][k] = (a.a0 != 0.0) ? fma(a.a0, c0[k], v) : v;
+                    ncv[tr][k] = rk ? fma(a.a0, tr == 0 ? c0buf->A[k][eo + lane] : c0buf->H[k][eo + lane], v) : v;
                 }
+            }
+            if (rk) {                          // every lane has read c0: the next job of this unit prefetches its own
+                __syncwarp();
+                c0_inflight = dU.x == dM.x && dU.z;
+                if (lane == 0 && c0_inflight) issue_c0(dU.x, dU.y);
             }
             if (valid) {
 #pragma unroll

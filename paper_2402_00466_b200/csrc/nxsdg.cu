@@ -489,7 +489,7 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "advect kernel 0|1");
             c->adv_kernel = (int)value; break;
         case NXSDG_OPT_ADVECT_STAGES:
-            if (value != 4 && value != 5) return fail(c, NXSDG_ERR_INVALID_ARG, "advect stages 4|5");
+            if (value < 3 || value > 5) return fail(c, NXSDG_ERR_INVALID_ARG, "advect stages 3|4|5");
             c->adv_stages = (int)value; break;
         case NXSDG_OPT_FUSE_PREP_PG:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "fuse prep P_g 0|1");
@@ -2192,7 +2192,7 @@ static bool fuse_pg(const nxsdg_ctx* c) { return c->fuse_pg && c->d.nranks == 1 
 
 template <int ST>
 static nxsdg_status launch_adv_tma_t(nxsdg_ctx* c, const AdvMaps& mp, const AdvTmaArgs& ta) {
-    const size_t smem = (size_t)ADV_TMA_WARPS * ST * (sizeof(AdvSlot) + sizeof(uint64_t) + sizeof(int4));
+    const size_t smem = adv_smem_bytes(ST);
     static uint64_t attr_set = 0;
     if (!dev_bit_test(attr_set, c->d.device)) {
         CU(cudaFuncSetAttribute(k_advect_tma<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -2216,7 +2216,8 @@ static nxsdg_status launch_adv_tma(nxsdg_ctx* c, const AdvArgs& a) {
     const cuuint64_t dA[3] = {nx, er, 6}, dV[2] = {ncols, nr};
     const cuuint32_t bA[3] = {ADV_COLS, 1, 6}, bV[2] = {K2_VCOLS, 2};
     if (!encode(&mp.A, a.Ain, 3, dA, es, bA) || !encode(&mp.H, a.Hin, 3, dA, es, bA) ||
-        !encode(&mp.vx, a.vx, 2, dV, ns, bV) || !encode(&mp.vy, a.vy, 2, dV, ns, bV))
+        !encode(&mp.vx, a.vx, 2, dV, ns, bV) || !encode(&mp.vy, a.vy, 2, dV, ns, bV) ||
+        !encode(&mp.A0, a.A0, 3, dA, es, bA) || !encode(&mp.H0, a.H0, 3, dA, es, bA))
         return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled (advection) failed");
     AdvTmaArgs ta{};
     ta.a = a;
@@ -2224,6 +2225,7 @@ static nxsdg_status launch_adv_tma(nxsdg_ctx* c, const AdvArgs& a) {
     ta.ty = c->adv_ty;
     ta.nchunks = (c->nown + ta.ty - 1) / ta.ty;
     ta.dbg = getenv("NXSDG_DEBUG_ADV_TMA") != nullptr;
+    if (c->adv_stages == 3) return launch_adv_tma_t<3>(c, mp, ta);
     return c->adv_stages == 5 ? launch_adv_tma_t<5>(c, mp, ta) : launch_adv_tma_t<4>(c, mp, ta);
 }
 

@@ -392,23 +392,19 @@ __device__ __forceinline__ void sph_strain(const double Vx[3][3], const double V
         const double g11 = fma(ihx, dsx[g], -sr * vyg[g]);
         const double g22 = ct * dty[g];
         Gu[g] = g11 + g22;
-        Gw[g] = 0.5 * (g11 - g22);
-        Gz[g] = 0.5 * fma(ct, dtx[g], fma(ihx, dsy[g], sr * vxg[g]));
+        Gw[g] = g11 - g22;                                            // x 1/2 in the projection scale
+        Gz[g] = fma(ct, dtx[g], fma(ihx, dsy[g], sr * vxg[g]));     // x 1/2 likewise
     }
     double p[6], E[6];
     proj_coeffs(Gu, 1.0, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, eu);
-    proj_coeffs(Gw, 1.0, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, ew);
-    proj_coeffs(Gz, 1.0, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, e12);
+    proj_coeffs(Gw, 0.5, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, ew);
+    proj_coeffs(Gz, 0.5, p); sph_apply_q(row, p, E); eval_gp<true, true>(E, e12);
 }
 // S11 <- fac S11 + Q (Ra + Rb), S22 <- fac S22 + Q (Ra - Rb), S12 <- fac S12 + Q Rz, with the Gauss-point
 // values weighted by cos(lat) (|J_g| / (R^2 dlon dlat)); b's and z's factor 1/2 in the moments' scale
+// (Ga, Gb, Gz arrive already weighted by cos(lat): the kernel folds it into p / Delta and P / 2)
 __device__ __forceinline__ void sph_project(double Ga[9], double Gb[9], double Gz[9], const double* __restrict__ row,
                                             double fac, double (&S11)[6], double (&S12)[6], double (&S22)[6]) {
-#pragma unroll
-    for (int g = 0; g < 9; ++g) {
-        const double c = __ldg(row + SPH_COS + g / 3);
-        Ga[g] *= c; Gb[g] *= c; Gz[g] *= c;
-    }
     double p[6], qa[6], qb[6], qz[6];
     proj_coeffs(Ga, 1.0, p); sph_apply_q(row, p, qa);
     proj_coeffs(Gb, 0.5, p); sph_apply_q(row, p, qb);
@@ -731,9 +727,16 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             const CT pr = ph * rD;
             // replacement pressure (R#4): P_r/2 = (P/2) Draw/Delta, Draw = draw2 * rsqrt(draw2)
             const CT sub = REPL ? pr * (draw2 > CT(0) ? draw2 * rsqrt_t(draw2) : CT(0)) : ph;
-            eu[g] = fma(pr, u, -sub);
-            ew[g] = pr * w;
-            e12[g] = pr * z;
+            if constexpr (SPH) {   // the sphere projection weights the Gauss values by cos(lat): fold it here
+                const CT c = (CT)__ldg(srow + SPH_COS + g / 3), cpr = c * pr;
+                eu[g] = fma(cpr, u, -(c * sub));
+                ew[g] = cpr * w;
+                e12[g] = cpr * z;
+            } else {
+                eu[g] = fma(pr, u, -sub);
+                ew[g] = pr * w;
+                e12[g] = pr * z;
+            }
         }
         CT C11[NS], C12[NS], C22[NS];
 #pragma unroll

@@ -887,7 +887,7 @@ def test_graph_replay_matches_eager_chunks(nx):
 
 
 @pytest.mark.parametrize("shape", [(70, 75), (31, 33), (1, 5), (6, 1), (130, 97), (32, 64)])
-@pytest.mark.parametrize("stages", [4, 5])
+@pytest.mark.parametrize("stages", [3, 4, 5])
 def test_advect_tma_matches_q2(nx, shape, stages):
     """The persistent TMA-staged advection (k_advect_tma, the default for the closed-box CG2/DG2 pair) does
     k_advect_q2's arithmetic call for call (the compiler may contract a few products into FMAs differently
