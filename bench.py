@@ -235,11 +235,31 @@ def window_parity(m, cfg, rank, world, nsub, dist=None, core=12):
 
     S, V = ("S11", "S12", "S22"), ("vx", "vy")
     e = {"S": err(S), "dS": err(S, True), "v": err(V), "dv": err(V, True), "A": err(("A",)), "H": err(("H",))}
+    bar, floor = 1e-10, None
+    if max(e["S"], e["dS"], e["v"], e["dv"]) > bar:
+        # the window's own rounding floor (R#13 / R#27): the oracle's plain and FMA builds differ
+        # by ~1e-10 at C5's 62.5 m in the increments; the bar is then 4 x that floor, as in the full-size test
+        fm = oracle.Oracle("fma").outer_step(om, oracle.Params(alpha=cfg.alpha, beta=cfg.alpha), nsub, sub, do_advect=True)
+        fc = {}
+        for k, a in fm.items():
+            if k in ("vx", "vy"):
+                fc[k] = a[p * ey:p * (ey + core) + 1, p * ex:p * (ex + core) + 1]
+            elif k in g:
+                fc[k] = a.reshape(h, w, -1)[ey:ey + core, ex:ex + core].reshape(-1, a.shape[1])
+
+        def ferr(keys, inc=False):
+            num = max(float(np.abs((fc[k] - init[k] if inc else fc[k]) - (rc[k] - init[k] if inc else rc[k])).max())
+                      for k in keys)
+            den = max(float(np.abs(rc[k] - init[k] if inc else rc[k]).max()) for k in keys)
+            return num / den if den > 0 else num
+        floor = max(ferr(S), ferr(S, True), ferr(V), ferr(V, True))
+        bar = max(bar, 4.0 * floor)
     return {"window": f"{core}x{core} elements at ({cx},{cy})" +
                       (f", centred on the interface of ranks {world // 2 - 1}/{world // 2}" if world > 1 else
                        ", domain centre"),
             "after": f"advect + prep + {nsub} fused subcycles from the initial state",
-            "errors": e, "pass": max(e["S"], e["dS"], e["v"], e["dv"]) <= 1e-10 and max(e["A"], e["H"]) <= 1e-12,
+            "errors": e, "bar": bar, "oracle_fma_floor": floor,
+            "pass": max(e["S"], e["dS"], e["v"], e["dv"]) <= bar and max(e["A"], e["H"]) <= 1e-12,
             "oracle_s": time.perf_counter() - t0}
 
 

@@ -159,7 +159,10 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
 /* Tuning / A-B options (take effect at the next compute call):
  *   NXSDG_OPT_FUSED_KERNEL  0 (default): TMA-staged structured kernel for p = 2 (table-driven for p = 1);
  *                           1: table-driven register kernel k_subcycle<p> (reference-table variant)
- *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (default 32; one ring row each)
+ *   NXSDG_OPT_CHUNK_ROWS    element rows per warp work unit (one ring row each); 0 (default) = automatic: 32,
+ *                           halved down to 4 while the mesh would give fewer (strip, chunk) units than the
+ *                           device's resident warps (8 per SM) - small single-rank meshes such as C2 (256^2);
+ *                           row strips keep 32; every height gives bitwise the same result
  *   NXSDG_OPT_CTAS_PER_SM   cap on resident CTAs per SM for the persistent TMA kernel (0 = occupancy;
  *                           -1 (default) = tuned: 4 with the node constants in registers or loaded late,
  *                           3 (n_S = 6) / 2 (n_S = 8) with them TMA-staged in FP64, 4 with FP32 storage,

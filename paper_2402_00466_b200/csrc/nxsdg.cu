@@ -114,7 +114,9 @@ struct nxsdg_ctx {
     cudaStream_t stream = nullptr; bool own_stream = false;
     std::string err;
     int64_t launches = 0;
-    int ty = 32;       // fused kernel chunk rows
+    int ty = 0;        // fused kernel chunk rows (NXSDG_OPT_CHUNK_ROWS; 0 = automatic: 32, halved down to 4
+                       // while the strips x chunks work units are fewer than the resident warps)
+    int nsm = 0;       // SM count of the device (cached for the automatic chunk height)
     int variant = 0;   // fused kernel: 0 = TMA-staged structured (p = 2), 1 = table-driven k_subcycle<P>
     int ctas_per_sm = -1;  // -1 = tuned default on C4: 2 (FP64 S, P_g), 4 (FP32 storage)
     int stages = 2;        // TMA pipeline depth 2..4
@@ -334,6 +336,7 @@ extern "C" nxsdg_status nxsdg_create_mesh(const nxsdg_mesh_desc* d, const nxsdg_
     c->epitch = c->geom.epitch; c->eplane = c->geom.eplane; c->npitch = c->geom.npitch;
     auto bail = [&](nxsdg_status s) { nxsdg_status r = s; free_all(c); if (c->own_stream) cudaStreamDestroy(c->stream); delete c; return r; };
     if (cudaSetDevice(d->device) != cudaSuccess) { cudaGetLastError(); return bail(NXSDG_ERR_CUDA); }
+    cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, d->device);
     if (d->stream) c->stream = (cudaStream_t)d->stream;
     else {
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(NXSDG_ERR_CUDA);
@@ -446,7 +449,7 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "fused kernel variant 0|1");
             c->variant = (int)value; break;
         case NXSDG_OPT_CHUNK_ROWS:
-            if (value < 1 || value > (1 << 20)) return fail(c, NXSDG_ERR_INVALID_ARG, "chunk rows >= 1");
+            if (value < 0 || value > (1 << 20)) return fail(c, NXSDG_ERR_INVALID_ARG, "chunk rows >= 1 (0 = automatic)");
             c->ty = (int)value; break;
         case NXSDG_OPT_CTAS_PER_SM:
             if (value < -1 || value > 32) return fail(c, NXSDG_ERR_INVALID_ARG, "ctas per SM -1..32");
@@ -1439,8 +1442,12 @@ static bool prep_in_subcycle(const nxsdg_ctx* c) {
 static nxsdg_status launch_prep_nodes_q2(nxsdg_ctx* c, int kind) {
     PrepArgs a = prep_args(c);
     if (kind != 1) {
-        const int chunk = 64;
         const int pr_lo = a.node_row_begin >> 1, pr_hi = (a.node_row_end + 1) >> 1;
+        // 64 element rows per warp; shorter on small meshes so the warps fill the device (16 resident per SM)
+        int chunk = 64;
+        while (chunk > 4 && (int64_t)prep_march_strips(c->d.nx) * ((pr_hi - pr_lo + chunk - 1) / chunk) <
+                                (int64_t)(c->nsm > 0 ? c->nsm : 148) * 16)
+            chunk /= 2;
         const int64_t warps = (int64_t)prep_march_strips(c->d.nx) * ((pr_hi - pr_lo + chunk - 1) / chunk);
         k_prep_nodes_march<<<(unsigned)((warps + 3) / 4), 128, 0, c->stream>>>(a, chunk);
     } else {
@@ -1488,6 +1495,20 @@ static bool p2p_fused_stores(const nxsdg_ctx* c) {
            !c->general && c->precision == 0;
 }
 
+// Chunk height of the subcycle kernels' work units.  32 rows (tuned on C4 and its 8-GPU strips)
+// unless a small mesh would then give fewer (strip, chunk) units than the 8 resident warps per SM can run at
+// once: C2 (256^2) has 9 strips x 8 chunks = 72 units for 1184 warps, so each warp would march 33 rows while
+// the others idle; halving down to 4 rows (one ring row each) spreads the rows over more warps.  Single rank
+// only; every partition gives bitwise the same result (ring recomputation, fixed-order node sums).
+static int chunk_rows(const nxsdg_ctx* c) {
+    if (c->ty > 0) return c->ty;
+    if (c->d.nranks > 1) return 32;   // row strips keep the tuned height (their boundary / interior split)
+    const int64_t nstrips = (c->d.nx + 1 + 30) / 31, resident = (int64_t)(c->nsm > 0 ? c->nsm : 148) * 8;
+    int ty = 32;
+    while (ty > 4 && nstrips * ((c->nown + ty - 1) / ty) < resident) ty /= 2;
+    return ty;
+}
+
 static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     SubArgs a{};
     a.S_in = c->S[cs]; a.S_out = c->S[cs ^ 1]; a.Pg = c->Pg;
@@ -1496,7 +1517,7 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
     a.eplane = c->eplane; a.npitch = c->npitch; a.epitch = c->epitch; a.nx = c->d.nx;
     a.nstrips = (c->d.nx + 1 + 30) / 31;
     a.pa = prep_args(c);
-    a.ty = c->ty;
+    a.ty = chunk_rows(c);
     a.erow_begin = c->glo; a.erow_end = c->glo + c->nown;
     a.bottom_boundary = c->r0 == 0;
     a.top_boundary = c->r1 == c->d.ny;
@@ -1530,7 +1551,7 @@ static SubArgs sub_args(nxsdg_ctx* c, int cv, int cs) {
 
 // chunk selections for the overlapped multi-rank subcycle
 enum { SEL_ALL = 0, SEL_BOUNDARY = 1, SEL_INTERIOR = 2 };
-static int n_chunks(const nxsdg_ctx* c) { return (c->nown + c->ty - 1) / c->ty; }
+static int n_chunks(const nxsdg_ctx* c) { const int ty = chunk_rows(c); return (c->nown + ty - 1) / ty; }
 static void select_chunks(const nxsdg_ctx* c, int sel, SubArgs& a) {
     const int nc = n_chunks(c);
     if (sel == SEL_BOUNDARY) { a.chunk0 = 0; a.chunk_step = nc > 1 ? nc - 1 : 1; a.nsel = nc > 1 ? 2 : 1; }
@@ -2223,6 +2244,9 @@ static nxsdg_status launch_adv_tma(nxsdg_ctx* c, const AdvArgs& a) {
     ta.a = a;
     ta.nstrips = (c->d.nx + 1 + 30) / 31;
     ta.ty = c->adv_ty;
+    if (c->d.nranks == 1 && c->ty == 0)   // small meshes: as chunk_rows, enough units for the resident warps
+        while (ta.ty > 4 && (int64_t)ta.nstrips * ((c->nown + ta.ty - 1) / ta.ty) < (int64_t)(c->nsm > 0 ? c->nsm : 148) * 8)
+            ta.ty /= 2;
     ta.nchunks = (c->nown + ta.ty - 1) / ta.ty;
     ta.dbg = getenv("NXSDG_DEBUG_ADV_TMA") != nullptr;
     if (c->adv_stages == 3) return launch_adv_tma_t<3>(c, mp, ta);

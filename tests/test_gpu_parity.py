@@ -1176,3 +1176,22 @@ def test_bytes_model_of_the_roofline(nx, p, ns, na, bpe):
     assert count == bpe
     with nx.Mesh(20, 20, 20e3, 20e3, p, ns, na) as m:
         assert m.bytes_per_element_subcycle == bpe
+
+
+@pytest.mark.parametrize("shape", [(256, 256), (96, 40), (7, 130)])
+def test_auto_chunk_rows_bitwise(nx, shape):
+    """NXSDG_OPT_CHUNK_ROWS 0 (default) picks a shorter chunk height on small single-rank meshes so there are
+    enough (strip, chunk) units for the resident warps (C2: 32 -> 4 rows); the fused subcycles and the TMA
+    advection give bitwise the result of the fixed 32-row partition."""
+    nxe, nye = shape
+    st = case(nxe, nye, 2, 6, 6, "warm", nxe * 1e3, nye * 1e3)
+    out = []
+    for ty in (0, 32):
+        with nx.Mesh(nxe, nye, nxe * 1e3, nye * 1e3) as m:
+            m.set_option(nx.OPT_CHUNK_ROWS, ty)
+            m.load(st)
+            m.advect(120.0)
+            m.mevp_substeps(5, begin_step=True)
+            out.append(m.state())
+    for k in out[0]:
+        np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
