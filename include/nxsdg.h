@@ -212,6 +212,10 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_FUSE_PREP_PG  single rank with k_advect_tma: 1 (default) = the last advection stage also writes the
  *                           outer-step prep's P at the Gauss points of the new A, H (bitwise what the prep would
  *                           compute); 0 = the prep computes it at BEGIN_STEP
+ *   NXSDG_OPT_PAIR_SUBCYCLES 1 = two subcycles per launch of the box TMA kernel (temporal blocking: a unit runs
+ *                           subcycle p over a 2-row / 2-column wider halo into scratch buffers, then subcycle
+ *                           p + 1 from them; single rank, FP64, n_S = 6, node constants in registers; an odd
+ *                           count ends with a one-subcycle launch; bitwise equal); 0 (default) = one per launch
  *   NXSDG_OPT_MULTIRANK_GRAPH  row-strip ranks (P2P or NCCL transport): 1 = nxsdg_mevp_substeps captures its
  *                           n fused subcycles - boundary chunks, exchange (peer stores + flag handshake, or
  *                           NCCL send/recv) on the halo stream, interior chunks, join - in one CUDA graph per
@@ -226,7 +230,8 @@ enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_
        NXSDG_OPT_DYNAMIC = 4, NXSDG_OPT_MAP_MODE = 5, NXSDG_OPT_PRECISION = 6, NXSDG_OPT_P2P_FUSED_STORES = 7,
        NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11,
        NXSDG_OPT_V_ROW_CARRY = 12, NXSDG_OPT_MULTIRANK_GRAPH = 13, NXSDG_OPT_ADVECT_KERNEL = 14,
-       NXSDG_OPT_ADVECT_STAGES = 15, NXSDG_OPT_FUSE_PREP_PG = 16, NXSDG_OPT_PREP_KERNEL = 18 };
+       NXSDG_OPT_ADVECT_STAGES = 15, NXSDG_OPT_FUSE_PREP_PG = 16, NXSDG_OPT_PREP_KERNEL = 18,
+       NXSDG_OPT_PAIR_SUBCYCLES = 19 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

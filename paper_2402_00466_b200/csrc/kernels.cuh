@@ -150,6 +150,8 @@ struct SubArgs {
     // the first fused subcycle of an outer step forming the node constants itself (box TMA kernel
     // instantiated with PREP, single rank): the prep's inputs / outputs and constants
     PrepArgs pa;
+    // two subcycles per launch (box TMA kernel instantiated with PAIR): pass A's outputs S^{p+1}, v^{p+1}
+    double* Sx; double* vxx; double* vyx;
 };
 // sphere row table layout (doubles per local element row)
 constexpr int kSphRow = 32;

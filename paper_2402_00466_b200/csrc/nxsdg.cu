@@ -131,6 +131,11 @@ struct nxsdg_ctx {
     int prep_kernel = 0;   // NXSDG_OPT_PREP_KERNEL: CG2/DG2 prep nodes: 0 = row-marching, 1 = per-element threads,
                            // 2 = in the first fused subcycle where it applies (measured no faster: not the default)
     bool prep_defer = false;   // BEGIN_STEP left the node constants to the next fused subcycle (PREP launch)
+    int pair = 0;              // NXSDG_OPT_PAIR_SUBCYCLES: two subcycles per launch (PAIR instantiation)
+    bool pair_now = false;     // the next TMA launch is a PAIR launch
+    double* Sx = nullptr; double* vxx = nullptr; double* vyx = nullptr;   // PAIR scratch (S^{p+1}, v^{p+1})
+    K2Maps mapsP{};            // PAIR pass-B maps over the scratch
+    bool mapsP_ok = false;
     bool prep_now = false;     // the next TMA launch is that PREP launch
     bool pg_fresh = false; // P_g already holds P of the current A, H (written by the last advection stage)
     bool adv_last = false; // the advection stage being launched is the last one
@@ -296,6 +301,9 @@ static void free_all(nxsdg_ctx* c) {
     if (c->gmaps) { cudaFree(c->gmaps); c->gmaps = nullptr; }
     if (c->mlump) { cudaFree(c->mlump); c->mlump = nullptr; }
     if (c->imlump) { cudaFree(c->imlump); c->imlump = nullptr; }
+    if (c->Sx) { cudaFree(c->Sx); c->Sx = nullptr; }
+    if (c->vxx) { cudaFree(c->vxx); c->vxx = nullptr; }
+    if (c->vyx) { cudaFree(c->vyx); c->vyx = nullptr; }
     if (c->gcontrib) { cudaFree(c->gcontrib); c->gcontrib = nullptr; }
     if (c->hstage_recv) { cudaFree(c->hstage_recv); c->hstage_recv = nullptr; }
     if (c->ev_bnd) { cudaEventDestroy(c->ev_bnd); c->ev_bnd = nullptr; }
@@ -408,8 +416,11 @@ extern "C" const char* nxsdg_last_error(const nxsdg_ctx* c) { return c ? c->err.
 extern "C" int64_t nxsdg_kernel_launches(const nxsdg_ctx* c) { return c ? c->launches : -1; }
 extern "C" void* nxsdg_stream(const nxsdg_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
+static bool pair_ok(const nxsdg_ctx* c);
 extern "C" double nxsdg_bytes_per_element_subcycle(const nxsdg_ctx* c) {
     if (!c) return 0.0;
+    // NXSDG_OPT_PAIR_SUBCYCLES: one DRAM pass (the same bytes) per two subcycles
+    if (c->pair && pair_ok(c)) return 4.0 * (2 * c->P * c->P + 6.0 * c->NS + c->NG + 8.0 * c->P * c->P);
     // one fused pass: v gather P^2*2, S read+write 2*3NS, P_g NG,
     // per node (P^2 per element): 6 constants + v write 2
     const double p2 = (double)c->P * c->P;
@@ -500,6 +511,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_PREP_KERNEL:
             if (value < 0 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "prep kernel 0|1|2");
             c->prep_kernel = (int)value; break;
+        case NXSDG_OPT_PAIR_SUBCYCLES:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "pair subcycles 0|1");
+            c->pair = (int)value; break;
         case NXSDG_OPT_MULTIRANK_GRAPH:
             if (value < -1 || value > 1) return fail(c, NXSDG_ERR_INVALID_ARG, "multi-rank graph -1|0|1");
             c->mr_graph = (int)value; break;
@@ -1667,6 +1681,32 @@ static nxsdg_status cvt(nxsdg_ctx* c, const float* src, double* dst, int64_t n) 
 }
 
 static bool use_tma(const nxsdg_ctx* c) { return c->P == 2 && c->variant == 0 && (!c->general || c->NS == 6); }
+// NXSDG_OPT_PAIR_SUBCYCLES: the PAIR instantiation (single rank, FP64 box, n_S = 6, constants in registers)
+static bool pair_ok(const nxsdg_ctx* c) {
+    return c->pair && c->d.nranks == 1 && use_tma(c) && !c->general && !c->sphere && c->NS == 6 && c->precision == 0 &&
+           const_mode(c) == 1 && c->stages <= 3;
+}
+// scratch state of pass A and the pass-B tensor maps over it (same geometry as S and v)
+static nxsdg_status build_pair_maps(nxsdg_ctx* c) {
+    if (c->mapsP_ok) return NXSDG_OK;
+    const size_t ne = (size_t)c->eplane, nn = (size_t)c->npitch * c->nrows_local;
+    if (!c->Sx) { CU(cudaMalloc(&c->Sx, 3 * (size_t)c->NS * ne * sizeof(double))); CU(cudaMemset(c->Sx, 0, 3 * (size_t)c->NS * ne * sizeof(double))); }
+    if (!c->vxx) { CU(cudaMalloc(&c->vxx, nn * sizeof(double))); CU(cudaMemset(c->vxx, 0, nn * sizeof(double))); }
+    if (!c->vyx) { CU(cudaMalloc(&c->vyx, nn * sizeof(double))); CU(cudaMemset(c->vyx, 0, nn * sizeof(double))); }
+    const cuuint64_t nx = c->d.nx, er = c->erows_local, ncols = 2 * (cuuint64_t)c->d.nx + 1, nr = c->nrows_local;
+    const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 8, (cuuint64_t)c->eplane * 8};
+    const cuuint64_t ns[2] = {(cuuint64_t)c->npitch * 8, (cuuint64_t)c->nn * 8};
+    const cuuint64_t nS = 3 * (cuuint64_t)c->NS;
+    const cuuint64_t dS[3] = {nx, er, nS}, dV[2] = {ncols, nr};
+    const cuuint32_t bS[3] = {K2Cols<double>::E, 1, (cuuint32_t)nS}, bV[2] = {K2_VCOLS, 3}, bV2[2] = {K2_VCOLS, 2};
+    K2Maps& M = c->mapsP;
+    M = c->maps[0][0];   // P_g and the constants maps are the same; S and v point at the scratch
+    if (!(encode(&M.S, c->Sx, 3, dS, es, bS) && encode(&M.vx, c->vxx, 2, dV, ns, bV) && encode(&M.vy, c->vyx, 2, dV, ns, bV) &&
+          encode(&M.vx2, c->vxx, 2, dV, ns, bV2) && encode(&M.vy2, c->vyx, 2, dV, ns, bV2)))
+        return fail(c, NXSDG_ERR_CUDA, "cuTensorMapEncodeTiled (pair scratch) failed");
+    c->mapsP_ok = true;
+    return NXSDG_OK;
+}
 // Tail split of a persistent launch with twarps warps: the last chunks become ~8-row sub-units, enough of
 // them (2 x twarps) that every warp's final unit is short, so the warps finish within ~8 jobs of each
 // other instead of ~ty (the idle tail of a launch is half a unit on average)
@@ -1751,20 +1791,20 @@ static nxsdg_status launch_gen_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
 }
 
 template <bool R, int ST, typename SF, typename CT = double, int NS = 6, bool CL = false, bool LC = false, bool SPH = false,
-          bool PREP = false>
+          bool PREP = false, bool PAIR = false>
 static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a) {
     // a.work_counter must be zero when the kernel starts (memset by the caller / graph)
     using Stage = typename K2StageSel<SF, NS, CL || LC>::T;
     const size_t smem = (size_t)K2_WARPS * ST * (sizeof(Stage) + 2 * sizeof(uint64_t) + sizeof(int4));
     static uint64_t attr_set = 0;   // the attribute is per device: one bit per ordinal
     if (!dev_bit_test(attr_set, c->d.device)) {
-        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
         dev_bit_set(attr_set, c->d.device);
     }
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->d.device);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP>, 32 * K2_WARPS,
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP, PAIR>, 32 * K2_WARPS,
                                                      smem));
     const int cap = c->ctas_per_sm < 0 ? default_ctas(sizeof(SF), CL || LC, NS) : c->ctas_per_sm;
     if (cap > 0) occ = std::min(occ, cap);
@@ -1772,8 +1812,8 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
-    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
-        mp, launch_args(c, a, (int64_t)blocks * K2_WARPS));
+    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP, PAIR><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
+        mp, PAIR ? c->mapsP : mp, launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
 // stages x replacement pressure x node-constant staging (TMA box | registers)
@@ -1800,6 +1840,15 @@ static nxsdg_status launch_tma_sel(nxsdg_ctx* c, int cv, int cs, const SubArgs& 
     }
     int mode = const_mode(c);
     if constexpr (sizeof(SF) == 8 && sizeof(CT) == 8 && NS == 6) {
+        if (c->pair_now) {   // two subcycles in one launch (pair_ok): 29-column strips, scratch outputs of pass A
+            SubArgs b = a;
+            b.nstrips = c->d.nx / 29 + 1;
+            b.Sx = c->Sx; b.vxx = c->vxx; b.vyx = c->vyx;
+            if (c->stages >= 3) return b.repl ? launch_tma_t<true, 3, SF, CT, 6, true, false, false, false, true>(c, cv, cs, b)
+                                              : launch_tma_t<false, 3, SF, CT, 6, true, false, false, false, true>(c, cv, cs, b);
+            return b.repl ? launch_tma_t<true, 2, SF, CT, 6, true, false, false, false, true>(c, cv, cs, b)
+                          : launch_tma_t<false, 2, SF, CT, 6, true, false, false, false, true>(c, cv, cs, b);
+        }
         if (c->prep_now) {   // the outer step's first subcycle forms the node constants (prep_in_subcycle)
             if (mode != 1 || c->stages != 2) return fail(c, NXSDG_ERR_STATE, "fused prep launch without its configuration");
             return a.repl ? launch_tma_t<true, 2, SF, CT, 6, true, false, false, true>(c, cv, cs, a)
@@ -2023,12 +2072,15 @@ static nxsdg_status one_subcycle(nxsdg_ctx* c, bool unfused) {
 
 // Capture n fused subcycles into a CUDA graph (nranks == 1) and replay it.
 static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
-    auto key = std::make_tuple(n, c->cv, c->cs + 2 * c->precision);
+    const bool pr = n >= 2 && pair_ok(c);   // two subcycles per launch, an odd count ends with a single one
+    const int nl = pr ? n / 2 + (n & 1) : n;
+    auto key = std::make_tuple(n, c->cv, c->cs + 2 * c->precision + (pr ? 16 : 0));
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
         if (use_tma(c)) {   // descriptors and counters are created outside the capture
             nxsdg_status st = build_maps(c);
+            if (!st && pr) st = build_pair_maps(c);
             if (!st) st = ensure_counters(c, n);
             if (st) return st;
         }
@@ -2044,11 +2096,15 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
                 return fail(c, NXSDG_ERR_CUDA, "graph capture memset: %s", cudaGetErrorString(me));
             }
         }
-        for (int i = 0; i < n; ++i) {
+        for (int i = 0, slot = 0; i < n; ++slot) {
             if (use_tma(c)) {
-                nxsdg_status st = launch_tma(c, cv, cs, i);
+                c->pair_now = pr && n - i >= 2;
+                nxsdg_status st = launch_tma(c, cv, cs, slot);
+                i += c->pair_now ? 2 : 1;
+                c->pair_now = false;
                 if (st) { cudaGraph_t junk; cudaStreamEndCapture(c->stream, &junk); if (junk) cudaGraphDestroy(junk); return st; }
             } else {
+                ++i;
                 SubArgs a = sub_args(c, cv, cs);
                 const int nchunks = (c->nown + a.ty - 1) / a.ty;
                 const unsigned blocks = (unsigned)(((int64_t)a.nstrips * nchunks + 3) / 4);
@@ -2064,11 +2120,11 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
         e = cudaGraphInstantiate(&ge, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return fail(c, NXSDG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-        it = c->graphs.emplace(key, nxsdg_ctx::Graph{ge, n}).first;
+        it = c->graphs.emplace(key, nxsdg_ctx::Graph{ge, nl}).first;
     }
     CU(cudaGraphLaunch(it->second.exec, c->stream));
     c->launches += it->second.launches;
-    if (n & 1) { c->cv ^= 1; c->cs ^= 1; }
+    if (nl & 1) { c->cv ^= 1; c->cs ^= 1; }   // one ping-pong flip per launch (a pair flips once)
     return NXSDG_OK;
 }
 

@@ -493,10 +493,22 @@ __device__ __forceinline__ void sph_divergence(const double (&S11)[6], const dou
 // element, the west one (shuffle; lane 0 is the ring column), the row below (register carry; the ring row
 // of a unit is loaded like any job) - the row-marching prep's sums in its order through the same
 // prep_node_calc, so the constants (also stored for the remaining subcycles) are bitwise the prep's.
+// PAIR (with CL, FP64, n_S = 6, single rank): two subcycles per launch (temporal blocking).  A unit (strip
+// of 29 element columns, chunk [lr0, lr1)) is processed twice: pass A runs subcycle p on rows lr0 - 2 ..
+// lr1 over the columns 29 s - 2 .. 29 s + 29 (lane = column - 29 s + 2) and writes S^{p+1}, v^{p+1} to the
+// scratch buffers (a.Sx, a.vxx, a.vyx; what the unit's pass B reads is all written by the same warp); pass B
+// runs subcycle p + 1 on rows lr0 - 1 .. lr1 - 1 from the scratch (mapsB) and stores S^{p+2}, v^{p+2} of the
+// owned columns (lanes 2 .. 30).  Lanes whose inputs come from outside the warp (pass A lane 0's west node,
+// pass B lanes 0, 1, 31) compute values nobody stores.  Overlapping units write bitwise identical values
+// to the scratch (the arithmetic is the one-subcycle kernel's, partition-invariant).  The new state and
+// the node constants / P_g of a pass-B row were read by pass A moments before: L2 hits, so a launch reads
+// S, P_g, v, the constants once from DRAM and writes S, v once for two subcycles.
 template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false, bool SPH = false,
-          bool PREP = false>
-__global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps, SubArgs a) {
+          bool PREP = false, bool PAIR = false>
+__global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps,
+                                                                   const __grid_constant__ K2Maps mapsB, SubArgs a) {
     static_assert(!(CL && LC), "one node-constant mode");
+    static_assert(!PAIR || (CL && NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8 && !SPH && !PREP), "pair: FP64 box, registers");
     static_assert(!PREP || (CL && NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8 && !SPH), "fused prep: FP64 box, registers");
     static_assert(!SPH || (NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8), "sphere: FP64, n_S = 6");
     static_assert(!LC || sizeof(SF) == 8, "late constants need the FP64 S region");
@@ -525,6 +537,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     // displacing the lines that are: the neighbouring strips' overlap and the shared v row
     const uint64_t pol_ld = l2_policy(a.l2_hints & 1 ? 1 : 0), pol_st = l2_policy(a.l2_hints & 2 ? 1 : 0);
     const uint64_t pol_v = l2_policy(a.l2_hints & 4 ? 2 : 0);
+    const uint64_t pol_keep = l2_policy(2);                      // PAIR: pass-A scratch stores (evict_last)
     // LC: one more mbarrier per stage for the late constants, after the job descriptors
     uint64_t* barC = reinterpret_cast<uint64_t*>(reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) +
                                                  K2_WARPS * STAGES) + wib * STAGES;
@@ -541,9 +554,17 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     // from a global counter (dynamic balancing; a.work_counter is zeroed before each launch),
     // or round-robin (gw + k * twarps) when no counter is given.  Lane 0 runs the prefetch
     // cursor and records each job in the stage's descriptor slot; all lanes read it back.
-    struct Cur { int u, lr, lr1, ix0; bool ring, first, ok; };
+    // PAIR: a unit is pass A (rows end = min(lr1 + 1, erow_end) exclusive, ring lr0 - 2) then pass B (rows up
+    // to lr1, ring lr0 - 1); lr1 holds the current pass's end row, ulr0 / ulr1 the unit's own rows
+    // Between the passes the cursor inserts STAGES - 1 empty positions ("gap"), so pass B's first TMA load is
+    // issued only after the unit's last pass-A job has stored (and fenced) what it reads
+    struct Cur { int u, lr, lr1, ix0, ulr0, ulr1, pass, gap; bool ring, first, ok; };
     auto claim = [&](int u) -> int {      // lane 0: the next unit after u
         return a.work_counter ? twarps + atomicAdd(a.work_counter, 1) : u + twarps;
+    };
+    auto start_pass_b = [&](Cur& c) {
+        c.pass = 1; c.lr1 = c.ulr1; c.gap = 0;
+        c.ring = c.ulr0 > a.erow_begin; c.lr = c.ring ? c.ulr0 - 1 : c.ulr0; c.first = true;
     };
     auto start_unit = [&](int u, Cur& c) {
         for (;;) {                        // skip empty sub-units (ragged last chunk)
@@ -552,38 +573,55 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             int strip, lr0, lr1;
             unit_rows(a, u, strip, lr0, lr1);
             if (lr0 < lr1) {
-                c.u = u; c.lr1 = lr1; c.ix0 = strip * 31;
+                c.u = u; c.lr1 = lr1; c.ix0 = PAIR ? strip * 29 - 1 : strip * 31;
                 c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
+                c.pass = 0; c.ulr0 = lr0; c.ulr1 = lr1; c.gap = 0;
+                if constexpr (PAIR) {
+                    c.lr1 = min(lr1 + 1, a.erow_end);
+                    c.ring = lr0 - 2 >= a.erow_begin;
+                    c.lr = c.ring ? lr0 - 2 : max(lr0 - 1, a.erow_begin);
+                }
                 return;
             }
             u = claim(u);
         }
     };
     auto advance = [&](Cur& c) {          // lane 0 only
+        if (PAIR && c.gap > 0) {              // inside the gap between the passes
+            if (--c.gap == 0) start_pass_b(c);
+            return;
+        }
         ++c.lr; c.ring = false; c.first = false;
-        if (c.lr >= c.lr1) start_unit(claim(c.u), c);
+        if (c.lr >= c.lr1) {
+            if (PAIR && c.pass == 0) c.gap = STAGES - 1;
+            else start_unit(claim(c.u), c);
+        }
     };
     int4* jobs = reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) + wib * STAGES;
     auto record = [&](const Cur& c, int st) {   // lane 0
-        jobs[st] = make_int4(c.ok ? c.u : -1, c.lr, c.lr1, (c.ring ? 1 : 0) | (c.first ? 2 : 0));
+        jobs[st] = make_int4(c.ok ? c.u : -1, c.lr, c.lr1,
+                             (c.ring ? 1 : 0) | (c.first ? 2 : 0) | (c.pass ? 4 : 0) | (c.gap > 0 ? 8 : 0));
     };
     // v row carry: a continuing job (not the first of its unit) loads node rows 2lr+1, 2lr+2 into smem
     // rows 0, 1 and takes row 2lr (the previous job's top row, same lane columns) from registers
     const bool vcarry = a.vcarry != 0;
     auto issue = [&](const Cur& c, int s) {
+        if (PAIR && c.gap > 0) return;       // an empty position: nothing to load
         Stage* t = stg + s;
         const bool cont = vcarry && !c.first;
+        const K2Maps& M = (PAIR && c.pass) ? mapsB : maps;   // pass B reads the pass-A scratch
+        if (PAIR && c.pass) asm volatile("fence.proxy.async.global;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, NOBOX>() - (cont ? 2u * K2_VCOLS * 8u : 0u));
         const int xs = (c.ix0 - 1) & ~(AL - 1);   // 16-B aligned start column (arithmetic: -1 -> -2 / -4)
-        tma3h(&t->S[0][0], &maps.S, &bar[s], xs, c.lr, 0, pol_ld);
+        tma3h(&t->S[0][0], &M.S, &bar[s], xs, c.lr, 0, pol_ld);
         tma3h(&t->Pg[0][0], &maps.Pg, &bar[s], xs, c.lr, 0, pol_ld);
         if (cont) {
-            tma2h(&t->vx[0][0], &maps.vx2, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr + 1, pol_v);
-            tma2h(&t->vy[0][0], &maps.vy2, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr + 1, pol_v);
+            tma2h(&t->vx[0][0], &M.vx2, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr + 1, pol_v);
+            tma2h(&t->vy[0][0], &M.vy2, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr + 1, pol_v);
         } else {
-            tma2h(&t->vx[0][0], &maps.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
-            tma2h(&t->vy[0][0], &maps.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
+            tma2h(&t->vx[0][0], &M.vx, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
+            tma2h(&t->vy[0][0], &M.vy, &bar[s], 2 * (c.ix0 - 1), 2 * c.lr, pol_v);
         }
         if constexpr (!NOBOX) tma3h(&t->C[0][0][0], &maps.C, &bar[s], 2 * c.ix0, 2 * c.lr, 0, pol_ld);
     };
@@ -626,8 +664,22 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             cur.ok = jd.x >= 0;
             if (!cur.ok) break;
             cur.u = jd.x; cur.lr = jd.y; cur.lr1 = jd.z; cur.ring = jd.w & 1; cur.first = (jd.w & 2) != 0;
-            cur.ix0 = (cur.u % a.nstrips) * 31;
+            cur.pass = (jd.w >> 2) & 1;
+            cur.ix0 = PAIR ? (cur.u % a.nstrips) * 29 - 1 : (cur.u % a.nstrips) * 31;
         }
+        if (PAIR && (jobs[s].w & 8)) {       // the gap between a unit's passes: no job
+            __syncwarp();
+            s = (s + 1) % STAGES;
+            continue;
+        }
+        // PAIR: pass A writes the scratch state for every lane whose value is valid (1 .. 31), pass B the
+        // owned lanes 2 .. 30; the one-subcycle kernel stores lanes >= 1
+        const bool passA = PAIR && cur.pass == 0;
+        const bool lane_out = PAIR ? (passA ? lane >= 1 : (lane >= 2 && lane <= 30)) : lane >= 1;
+        SF* const So = passA ? reinterpret_cast<SF*>(a.Sx) : S_out;
+        double* const vxo = passA ? a.vxx : a.vx_out;
+        double* const vyo = passA ? a.vyx : a.vy_out;
+        const uint64_t pst = passA ? pol_keep : pol_st;  // scratch: kept in L2 for pass B (evict_last hint)
         const int ix = cur.ix0 - 1 + lane, lr = cur.lr;
         // CL: this lane's node constants [field][jy][q] (only lanes that update nodes; the boundary
         // column ix = nx is forced to zero below, so it needs none)
@@ -766,13 +818,13 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
 #pragma unroll
         for (int k = 0; k < NS; ++k) { S11[k] = (double)C11[k]; S12[k] = (double)C12[k]; S22[k] = (double)C22[k]; }
         const bool evalid = ix >= 0 && ix < a.nx;
-        if (!cur.ring && evalid && lane >= 1) {
+        if (!cur.ring && evalid && lane_out) {
             const int64_t e = (int64_t)lr * a.epitch + ix;
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
-                st_hint(S_out + k * eplane + e, (SF)S11[k], pol_st);
-                st_hint(S_out + (NS + k) * eplane + e, (SF)S12[k], pol_st);
-                st_hint(S_out + (2 * NS + k) * eplane + e, (SF)S22[k], pol_st);
+                st_hint(So + k * eplane + e, (SF)S11[k], pst);
+                st_hint(So + (NS + k) * eplane + e, (SF)S12[k], pst);
+                st_hint(So + (2 * NS + k) * eplane + e, (SF)S22[k], pst);
             }
             if (a.peer_S_up != nullptr && lr == a.up_elem_row) {   // P2P: the neighbour's ghost element row 0
                 const int64_t pe = a.peer_up_eplane;
@@ -798,7 +850,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         }
         // ---- per-node gather (row below, W, E) + velocity update (R#11), branch-free:
         //      all four owned nodes are updated, boundary nodes select 0, stores are predicated
-        const bool nvalid = lane >= 1 && ix >= 0 && ix <= a.nx && !cur.ring;
+        const bool nvalid = lane_out && ix >= 0 && ix <= a.nx && !cur.ring;
         double sumx[2][2], sumy[2][2];                 // [jy][q]
 #pragma unroll
         for (int jy = 0; jy < 3; ++jy) {
@@ -939,11 +991,11 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                 const int jr = 2 * lr + jy;
                 const int64_t n = (int64_t)jr * npitch + 2 * ix;
                 if (ix < a.nx) {
-                    st_hint2(a.vx_out + n, nvx[0], nvx[1], pol_st);
-                    st_hint2(a.vy_out + n, nvy[0], nvy[1], pol_st);
+                    st_hint2(vxo + n, nvx[0], nvx[1], pst);
+                    st_hint2(vyo + n, nvy[0], nvy[1], pst);
                 } else {                                  // ix == nx: only the boundary column 2 nx
-                    a.vx_out[n] = 0.0;
-                    a.vy_out[n] = 0.0;
+                    vxo[n] = 0.0;
+                    vyo[n] = 0.0;
                 }
                 // P2P fused peer stores: the same values into the neighbours' ghost node rows (a strip
                 // of one element row sends its bottom node row both ways)
@@ -970,10 +1022,11 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             for (int q = 0; q < 2; ++q) {
                 const int I = 2 * ix + q;
                 if (I > 2 * a.nx) continue;
-                a.vx_out[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
-                a.vy_out[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+                vxo[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+                vyo[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
             }
         }
+        if (passA) asm volatile("fence.proxy.async.global;" ::: "memory");   // the scratch feeds pass B's TMA
         __syncwarp();
         s = (s + 1) % STAGES;
     }

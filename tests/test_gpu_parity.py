@@ -1195,3 +1195,27 @@ def test_auto_chunk_rows_bitwise(nx, shape):
             out.append(m.state())
     for k in out[0]:
         np.testing.assert_array_equal(out[0][k], out[1][k], err_msg=k)
+
+
+@pytest.mark.parametrize("shape", [(70, 75), (130, 97), (31, 33), (1, 5), (6, 1), (29, 64), (58, 3), (256, 40)])
+@pytest.mark.parametrize("ty", [0, 4, 32])
+def test_pair_subcycles_bitwise(nx, shape, ty):
+    """NXSDG_OPT_PAIR_SUBCYCLES 1 runs two subcycles per launch (pass A into scratch over a 2-row / 2-column
+    wider halo, pass B from it over 29-column strips); it is the one-subcycle kernel's arithmetic on the same
+    inputs, so 1, 2, 5 and 6 subcycles (odd counts end with a single launch) are bitwise equal to one subcycle
+    per launch: ragged strips, 1-row / 1-column meshes, ring rows at chunk edges and the domain boundary."""
+    nxe, nye = shape
+    st = case(nxe, nye, 2, 6, 6, "random", nxe * 1e3, nye * 1e3)
+    for n in (1, 2, 5, 6):
+        out = []
+        for pair in (0, 1):
+            with nx.Mesh(nxe, nye, nxe * 1e3, nye * 1e3) as m:
+                m.set_option(nx.OPT_PAIR_SUBCYCLES, pair)
+                m.set_option(nx.OPT_CHUNK_ROWS, ty)
+                m.load(st)
+                m.advect(120.0)
+                m.mevp_substeps(n, begin_step=True)
+                m.mevp_substeps(n, begin_step=False)
+                out.append(m.state())
+        for k in out[0]:
+            np.testing.assert_array_equal(out[1][k], out[0][k], err_msg=f"n={n} {k}")
