@@ -1812,8 +1812,10 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const int64_t want = (units + K2_WARPS - 1) / K2_WARPS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
+    typename K2PassB<PAIR>::T mb{};
+    if constexpr (PAIR) mb = c->mapsP;
     k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP, PAIR><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
-        mp, PAIR ? c->mapsP : mp, launch_args(c, a, (int64_t)blocks * K2_WARPS));
+        mp, mb, launch_args(c, a, (int64_t)blocks * K2_WARPS));
     return NXSDG_OK;
 }
 // stages x replacement pressure x node-constant staging (TMA box | registers)

@@ -503,10 +503,16 @@ __device__ __forceinline__ void sph_divergence(const double (&S11)[6], const dou
 // to the scratch (the arithmetic is the one-subcycle kernel's, partition-invariant).  The new state and
 // the node constants / P_g of a pass-B row were read by pass A moments before: L2 hits, so a launch reads
 // S, P_g, v, the constants once from DRAM and writes S, v once for two subcycles.
+// the pass-B maps exist only in the PAIR instantiation (the default kernel keeps its one-map parameter block)
+struct K2NoMaps {};
+template <bool PAIR> struct K2PassB { using T = K2NoMaps; };
+template <> struct K2PassB<true> { using T = K2Maps; };
+
 template <bool REPL, int STAGES, typename SF, typename CT, int NS = 6, bool CL = false, bool LC = false, bool SPH = false,
           bool PREP = false, bool PAIR = false>
 __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_constant__ K2Maps maps,
-                                                                   const __grid_constant__ K2Maps mapsB, SubArgs a) {
+                                                                   const __grid_constant__ typename K2PassB<PAIR>::T mapsB,
+                                                                   SubArgs a) {
     static_assert(!(CL && LC), "one node-constant mode");
     static_assert(!PAIR || (CL && NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8 && !SPH && !PREP), "pair: FP64 box, registers");
     static_assert(!PREP || (CL && NS == 6 && sizeof(SF) == 8 && sizeof(CT) == 8 && !SPH), "fused prep: FP64 box, registers");
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     // displacing the lines that are: the neighbouring strips' overlap and the shared v row
     const uint64_t pol_ld = l2_policy(a.l2_hints & 1 ? 1 : 0), pol_st = l2_policy(a.l2_hints & 2 ? 1 : 0);
     const uint64_t pol_v = l2_policy(a.l2_hints & 4 ? 2 : 0);
-    const uint64_t pol_keep = l2_policy(2);                      // PAIR: pass-A scratch stores (evict_last)
+    const uint64_t pol_keep = PAIR ? l2_policy(2) : 0;           // PAIR: pass-A scratch stores (evict_last)
     // LC: one more mbarrier per stage for the late constants, after the job descriptors
     uint64_t* barC = reinterpret_cast<uint64_t*>(reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) +
                                                  K2_WARPS * STAGES) + wib * STAGES;
@@ -575,8 +581,9 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             if (lr0 < lr1) {
                 c.u = u; c.lr1 = lr1; c.ix0 = PAIR ? strip * 29 - 1 : strip * 31;
                 c.ring = lr0 > 0; c.lr = c.ring ? lr0 - 1 : lr0; c.first = true;
-                c.pass = 0; c.ulr0 = lr0; c.ulr1 = lr1; c.gap = 0;
+                c.pass = 0; c.gap = 0;
                 if constexpr (PAIR) {
+                    c.ulr0 = lr0; c.ulr1 = lr1;
                     c.lr1 = min(lr1 + 1, a.erow_end);
                     c.ring = lr0 - 2 >= a.erow_begin;
                     c.lr = c.ring ? lr0 - 2 : max(lr0 - 1, a.erow_begin);
@@ -600,7 +607,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     int4* jobs = reinterpret_cast<int4*>(bar + K2_WARPS * STAGES - wib * STAGES) + wib * STAGES;
     auto record = [&](const Cur& c, int st) {   // lane 0
         jobs[st] = make_int4(c.ok ? c.u : -1, c.lr, c.lr1,
-                             (c.ring ? 1 : 0) | (c.first ? 2 : 0) | (c.pass ? 4 : 0) | (c.gap > 0 ? 8 : 0));
+                             (c.ring ? 1 : 0) | (c.first ? 2 : 0) | (PAIR ? ((c.pass ? 4 : 0) | (c.gap > 0 ? 8 : 0)) : 0));
     };
     // v row carry: a continuing job (not the first of its unit) loads node rows 2lr+1, 2lr+2 into smem
     // rows 0, 1 and takes row 2lr (the previous job's top row, same lane columns) from registers
@@ -609,7 +616,9 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         if (PAIR && c.gap > 0) return;       // an empty position: nothing to load
         Stage* t = stg + s;
         const bool cont = vcarry && !c.first;
-        const K2Maps& M = (PAIR && c.pass) ? mapsB : maps;   // pass B reads the pass-A scratch
+        const K2Maps* Mp = &maps;
+        if constexpr (PAIR) { if (c.pass) Mp = &mapsB; }       // pass B reads the pass-A scratch
+        const K2Maps& M = *Mp;
         if (PAIR && c.pass) asm volatile("fence.proxy.async.global;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], k2_tx_bytes<SF, NS, NOBOX>() - (cont ? 2u * K2_VCOLS * 8u : 0u));
@@ -664,7 +673,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             cur.ok = jd.x >= 0;
             if (!cur.ok) break;
             cur.u = jd.x; cur.lr = jd.y; cur.lr1 = jd.z; cur.ring = jd.w & 1; cur.first = (jd.w & 2) != 0;
-            cur.pass = (jd.w >> 2) & 1;
+            cur.pass = PAIR ? (jd.w >> 2) & 1 : 0;
             cur.ix0 = PAIR ? (cur.u % a.nstrips) * 29 - 1 : (cur.u % a.nstrips) * 31;
         }
         if (PAIR && (jobs[s].w & 8)) {       // the gap between a unit's passes: no job
@@ -676,10 +685,11 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         // owned lanes 2 .. 30; the one-subcycle kernel stores lanes >= 1
         const bool passA = PAIR && cur.pass == 0;
         const bool lane_out = PAIR ? (passA ? lane >= 1 : (lane >= 2 && lane <= 30)) : lane >= 1;
-        SF* const So = passA ? reinterpret_cast<SF*>(a.Sx) : S_out;
-        double* const vxo = passA ? a.vxx : a.vx_out;
-        double* const vyo = passA ? a.vyx : a.vy_out;
-        const uint64_t pst = passA ? pol_keep : pol_st;  // scratch: kept in L2 for pass B (evict_last hint)
+        // (the one-subcycle kernel addresses its outputs from the parameter block as before: no live registers)
+#define K2_SO (PAIR ? (passA ? reinterpret_cast<SF*>(a.Sx) : S_out) : S_out)
+#define K2_VXO (PAIR ? (passA ? a.vxx : a.vx_out) : a.vx_out)
+#define K2_VYO (PAIR ? (passA ? a.vyx : a.vy_out) : a.vy_out)
+        const uint64_t pst = PAIR && passA ? pol_keep : pol_st;  // scratch: kept in L2 for pass B (evict_last hint)
         const int ix = cur.ix0 - 1 + lane, lr = cur.lr;
         // CL: this lane's node constants [field][jy][q] (only lanes that update nodes; the boundary
         // column ix = nx is forced to zero below, so it needs none)
@@ -822,9 +832,9 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             const int64_t e = (int64_t)lr * a.epitch + ix;
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
-                st_hint(So + k * eplane + e, (SF)S11[k], pst);
-                st_hint(So + (NS + k) * eplane + e, (SF)S12[k], pst);
-                st_hint(So + (2 * NS + k) * eplane + e, (SF)S22[k], pst);
+                st_hint(K2_SO + k * eplane + e, (SF)S11[k], pst);
+                st_hint(K2_SO + (NS + k) * eplane + e, (SF)S12[k], pst);
+                st_hint(K2_SO + (2 * NS + k) * eplane + e, (SF)S22[k], pst);
             }
             if (a.peer_S_up != nullptr && lr == a.up_elem_row) {   // P2P: the neighbour's ghost element row 0
                 const int64_t pe = a.peer_up_eplane;
@@ -991,11 +1001,11 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
                 const int jr = 2 * lr + jy;
                 const int64_t n = (int64_t)jr * npitch + 2 * ix;
                 if (ix < a.nx) {
-                    st_hint2(vxo + n, nvx[0], nvx[1], pst);
-                    st_hint2(vyo + n, nvy[0], nvy[1], pst);
+                    st_hint2(K2_VXO + n, nvx[0], nvx[1], pst);
+                    st_hint2(K2_VYO + n, nvy[0], nvy[1], pst);
                 } else {                                  // ix == nx: only the boundary column 2 nx
-                    vxo[n] = 0.0;
-                    vyo[n] = 0.0;
+                    K2_VXO[n] = 0.0;
+                    K2_VYO[n] = 0.0;
                 }
                 // P2P fused peer stores: the same values into the neighbours' ghost node rows (a strip
                 // of one element row sends its bottom node row both ways)
@@ -1022,14 +1032,17 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
             for (int q = 0; q < 2; ++q) {
                 const int I = 2 * ix + q;
                 if (I > 2 * a.nx) continue;
-                vxo[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
-                vyo[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+                K2_VXO[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
+                K2_VYO[(int64_t)(2 * a.erow_end) * npitch + I] = 0.0;
             }
         }
         if (passA) asm volatile("fence.proxy.async.global;" ::: "memory");   // the scratch feeds pass B's TMA
         __syncwarp();
         s = (s + 1) % STAGES;
     }
+#undef K2_SO
+#undef K2_VXO
+#undef K2_VYO
 }
 
 }  // namespace nxk
