@@ -109,3 +109,16 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
                 assert "oracle.h" not in txt, f
+
+
+def test_binding_option_ids_match_header():
+    """The binding's OPT_* ids are the header's NXSDG_OPT_* enum values (no drift between the two)."""
+    from paper_2402_00466_b200 import nxsdg
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    hdr = {m.group(1): int(m.group(2)) for m in re.finditer(r"NXSDG_OPT_([A-Z0-9_]+)\s*=\s*(\d+)", txt)}
+    assert hdr, "no NXSDG_OPT_* enum in the header"
+    for name, val in hdr.items():
+        assert getattr(nxsdg, "OPT_" + name) == val, name
+    py = {k[4:] for k in dir(nxsdg) if k.startswith("OPT_")}
+    assert py == set(hdr), sorted(py ^ set(hdr))
