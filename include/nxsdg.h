@@ -65,7 +65,8 @@ typedef enum {
     NXSDG_ERR_OOM = 6          /* device allocation failed                           */
 } nxsdg_status;
 
-/* HOST_ASYNC: pinned host memory, copied on the context's copy stream; the call returns at once and
+/* HOST_ASYNC: pinned host memory, copied on the context's copy streams (one for uploads, one for read-backs,
+ * so the two directions overlap on the full-duplex link); the call returns at once and
  * the caller keeps the buffer unchanged until nxsdg_synchronize.  Accepted by nxsdg_set_forcing (the
  * forcing is staged and takes effect at the next BEGIN_STEP, so the upload of step k+1's forcing
  * overlaps step k) and by nxsdg_read_state for NXSDG_VX / NXSDG_VY (a snapshot of v at that point in
@@ -283,7 +284,7 @@ nxsdg_status nxsdg_advect(nxsdg_ctx* ctx, double dt);
 /* Debug: one unfused step on the current state (needs BEGIN_STEP for STRESS/VELOCITY). */
 nxsdg_status nxsdg_run_step(nxsdg_ctx* ctx, nxsdg_step step);
 
-nxsdg_status nxsdg_synchronize(nxsdg_ctx* ctx);   /* waits for the context stream and the copy stream */
+nxsdg_status nxsdg_synchronize(nxsdg_ctx* ctx);   /* waits for the context stream and the copy streams */
 /* Make the context stream wait for every HOST_ASYNC copy issued so far (stream-ordered join). */
 nxsdg_status nxsdg_stream_join(nxsdg_ctx* ctx);
 

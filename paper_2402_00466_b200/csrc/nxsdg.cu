@@ -144,9 +144,11 @@ struct nxsdg_ctx {
     double* hstage_send = nullptr; double* hstage_recv = nullptr;   // packed halo messages
     double* verts = nullptr; double* gmaps = nullptr;               // NEXT-1 general quads (stress step)
     // NXSDG_MEM_HOST_ASYNC: copies on a copy stream, forcing staged until the next BEGIN_STEP
-    cudaStream_t cstream = nullptr;
+    cudaStream_t cstream = nullptr;    // HOST_ASYNC host -> device copies (forcing uploads)
+    cudaStream_t dstream = nullptr;    // HOST_ASYNC device -> host copies (velocity read-back): PCIe is full
+                                       // duplex, so a step's upload and the previous step's read-back overlap
     cudaEvent_t ev_fup = nullptr, ev_fcons = nullptr, ev_vsnap[2] = {nullptr, nullptr}, ev_vdone[2] = {nullptr, nullptr};
-    cudaEvent_t ev_cjoin = nullptr;
+    cudaEvent_t ev_cjoin = nullptr, ev_djoin = nullptr;
     double* fstage[4] = {nullptr, nullptr, nullptr, nullptr};
     double* vsnap[2] = {nullptr, nullptr};
     bool fpending = false;
@@ -297,7 +299,9 @@ static void free_all(nxsdg_ctx* c) {
     if (c->ev_fup) { cudaEventDestroy(c->ev_fup); c->ev_fup = nullptr; }
     if (c->ev_fcons) { cudaEventDestroy(c->ev_fcons); c->ev_fcons = nullptr; }
     if (c->ev_cjoin) { cudaEventDestroy(c->ev_cjoin); c->ev_cjoin = nullptr; }
+    if (c->ev_djoin) { cudaEventDestroy(c->ev_djoin); c->ev_djoin = nullptr; }
     if (c->cstream) { cudaStreamDestroy(c->cstream); c->cstream = nullptr; }
+    if (c->dstream) { cudaStreamDestroy(c->dstream); c->dstream = nullptr; }
     if (c->gmaps) { cudaFree(c->gmaps); c->gmaps = nullptr; }
     if (c->mlump) { cudaFree(c->mlump); c->mlump = nullptr; }
     if (c->imlump) { cudaFree(c->imlump); c->imlump = nullptr; }
@@ -637,10 +641,10 @@ extern "C" nxsdg_status nxsdg_read_state(nxsdg_ctx* c, nxsdg_field f, double* ds
         CU(cudaStreamWaitEvent(c->stream, c->ev_vdone[k], 0));
         CU(cudaMemcpyAsync(c->vsnap[k], cg_base(c, f), nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
         CU(cudaEventRecord(c->ev_vsnap[k], c->stream));
-        CU(cudaStreamWaitEvent(c->cstream, c->ev_vsnap[k], 0));
+        CU(cudaStreamWaitEvent(c->dstream, c->ev_vsnap[k], 0));
         CU(cudaMemcpy2DAsync(dst, cols * sizeof(double), c->vsnap[k] + (size_t)c->P * c->glo * c->npitch,
-                             c->npitch * sizeof(double), cols * sizeof(double), rows, cudaMemcpyDeviceToHost, c->cstream));
-        CU(cudaEventRecord(c->ev_vdone[k], c->cstream));
+                             c->npitch * sizeof(double), cols * sizeof(double), rows, cudaMemcpyDeviceToHost, c->dstream));
+        CU(cudaEventRecord(c->ev_vdone[k], c->dstream));
         return NXSDG_OK;
     }
     if (!dst || (mem != NXSDG_MEM_HOST && mem != NXSDG_MEM_DEVICE) || f < 0 || f >= NXSDG_NFIELDS)
@@ -681,7 +685,9 @@ extern "C" nxsdg_status nxsdg_read_state(nxsdg_ctx* c, nxsdg_field f, double* ds
 static nxsdg_status ensure_async(nxsdg_ctx* c) {
     if (c->cstream) return NXSDG_OK;
     CU(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
-    cudaEvent_t* evs[] = {&c->ev_fup, &c->ev_fcons, &c->ev_vsnap[0], &c->ev_vsnap[1], &c->ev_vdone[0], &c->ev_vdone[1], &c->ev_cjoin};
+    CU(cudaStreamCreateWithFlags(&c->dstream, cudaStreamNonBlocking));
+    cudaEvent_t* evs[] = {&c->ev_fup, &c->ev_fcons, &c->ev_vsnap[0], &c->ev_vsnap[1], &c->ev_vdone[0], &c->ev_vdone[1],
+                          &c->ev_cjoin, &c->ev_djoin};
     for (auto e : evs) CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     return NXSDG_OK;
 }
@@ -705,6 +711,8 @@ extern "C" nxsdg_status nxsdg_stream_join(nxsdg_ctx* c) {
     if (!c->cstream) return NXSDG_OK;
     CU(cudaEventRecord(c->ev_cjoin, c->cstream));
     CU(cudaStreamWaitEvent(c->stream, c->ev_cjoin, 0));
+    CU(cudaEventRecord(c->ev_djoin, c->dstream));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_djoin, 0));
     return NXSDG_OK;
 }
 
@@ -2427,6 +2435,7 @@ extern "C" nxsdg_status nxsdg_synchronize(nxsdg_ctx* c) {
             return fail(c, NXSDG_ERR_NCCL, "NCCL async error %d", (int)ar);
     }
     if (c->cstream) CU(cudaStreamSynchronize(c->cstream));
+    if (c->dstream) CU(cudaStreamSynchronize(c->dstream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaGetLastError());
     return NXSDG_OK;
