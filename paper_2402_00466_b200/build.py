@@ -13,7 +13,7 @@ SOURCES = ["nxsdg.cu"]
 DEPS = ["nxsdg.cu", "kernels.cuh", "tables.cuh", "subcycle_tma.cuh", "subcycle_gen.cuh", "advect_q2.cuh", "general_quads.cuh", "general_steps.cuh",
         "advect_tma.cuh", "prep_q2.cuh", "prep_node.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
+              "-Xcompiler", "-fPIC", "-shared"]
 
 
 def _stale() -> bool:

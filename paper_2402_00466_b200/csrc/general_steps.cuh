@@ -252,7 +252,7 @@ struct GenAdvArgs {
 
 template <int P, int NA>
 __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect_gen(GenAdvArgs ga) {
-    constexpr int NGP = P + 1, NG = NGP * NGP, NCG = (P + 1) * (P + 1);
+    constexpr int NGP = P + 1;
     const RefTab& T = c_tab[P - 1];
     const AdvArgs& a = ga.b;
     __shared__ double sFA[ADV_ROWS][32][NGP], sFH[ADV_ROWS][32][NGP];

@@ -591,7 +591,7 @@ constexpr int ADV_ROWS = 4;   // block = 32 x ADV_ROWS elements
 
 template <int P, int NA>
 __global__ void __launch_bounds__(32 * ADV_ROWS, 3) k_advect(AdvArgs a) {
-    constexpr int NGP = P + 1, NG = NGP * NGP, NCG = (P + 1) * (P + 1);
+    constexpr int NGP = P + 1, NG = NGP * NGP;
     const RefTab& T = c_tab[P - 1];
     __shared__ double sFA[ADV_ROWS][32][NGP], sFH[ADV_ROWS][32][NGP];
     const int tx = threadIdx.x, ty = threadIdx.y;
