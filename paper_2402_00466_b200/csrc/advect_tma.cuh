@@ -72,6 +72,31 @@ struct AdvTmaArgs {
 // needs of row k - 1 (its top v node row, and the south flux for a unit's first job), so a job still
 // waits only for a row issued one job earlier; 3 slots per warp fit 5 CTAs (10 warps) per SM at <= 204
 // registers where 4 slots fit 4 (8 warps)
+// Raw moments (session 3).  k_advect_q2 forms the edge moments m0 = sum w F, m1 = sum w T F, m2 = sum w q(T) F
+// and the volume moments, scales them, accumulates L_k with the 1 / h factors and then applies dt mr_k a1.  Here
+// the moments stay raw (1D Gauss sums with the weights (5, 8, 5) taken as (1, 1.6, 1)) and every scale -
+// 5/18, 5a/18, 1/54, 1/6, 1/2, 1/h, dt, mr_k, a1 - is folded on the host into 18 coefficients per stage
+// (AdvArgs::kc, adv_coeffs in nxsdg.cu), so a tracer's update costs ~70 FP64 operations instead of ~150
+// (the stage is bound by FP64 dependency latency).  Same quantities, another rounding order (~1e-16).
+__device__ __forceinline__ void edge_raw(const double F[3], double& r0, double& r1, double& r2) {
+    const double s = F[0] + F[2];
+    r0 = fma(1.6, F[1], s);      // m0 = 5/18 r0
+    r1 = F[2] - F[0];            // m1 = 5a/18 r1
+    r2 = fma(-2.0, F[1], s);     // m2 = r2 / 54
+}
+// raw volume moments of G[gy][gx]: M00 = (5/18)^2 R00, M10 = (5/18)(5a/18) R10, M01 = (5/18)(5a/18) R01
+__device__ __forceinline__ void vol_raw(const double G[3][3], double& R00, double& R10, double& R01) {
+    double x0[3], x1[3];
+#pragma unroll
+    for (int gy = 0; gy < 3; ++gy) {
+        x0[gy] = fma(1.6, G[gy][1], G[gy][0] + G[gy][2]);
+        x1[gy] = G[gy][2] - G[gy][0];
+    }
+    R00 = fma(1.6, x0[1], x0[0] + x0[2]);
+    R10 = fma(1.6, x1[1], x1[0] + x1[2]);
+    R01 = x0[2] - x0[0];
+}
+
 template <int STAGES>
 __global__ void __launch_bounds__(32 * ADV_TMA_WARPS, STAGES == 3 ? 5 : ADV_TMA_MINB)
 k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
@@ -152,11 +177,10 @@ k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
     const int4 d0 = desc[0];
     if (d0.x < 0) return;
     wait_slot(0);
-    const double mr[6] = {1.0, 12.0, 12.0, 180.0, 180.0, 144.0};
     // the north flux of a job is the south flux of the unit's next job (same edge, same function, same
     // inputs): carried in registers instead of evaluated twice; the unit's first job evaluates its own
     int prev_unit = -1;
-    double cNA[3] = {0.0, 0.0, 0.0}, cNH[3] = {0.0, 0.0, 0.0};
+    double cNA[3] = {0.0, 0.0, 0.0}, cNH[3] = {0.0, 0.0, 0.0};   // raw moments (r0, r1, r2) of the north edge
     for (int i = 0;; ++i) {
         const int sL = (i + STAGES - 1) % STAGES, sM = i % STAGES, sU = (i + 1) % STAGES;
         const int4 dM = desc[sM];
@@ -206,7 +230,7 @@ k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
                 ux[1][jx] = M.vx[0][2 * lane + jx]; uy[1][jx] = M.vy[0][2 * lane + jx];
                 ux[2][jx] = M.vx[1][2 * lane + jx]; uy[2][jx] = M.vy[1][2 * lane + jx];
             }
-            double FeA[3], FeH[3], FnA[3], FnH[3], FwA[3], FwH[3], FsA[3], FsH[3];
+            double FeA[3], FeH[3], FnA[3], FnH[3], FsA[3], FsH[3];
             {   // east edge (closed box: no flux through x = Lx)
 #pragma unroll
                 for (int k = 0; k < 6; ++k) { nb.A[k] = M.A[k][eo + lane + 1]; nb.H[k] = M.H[k][eo + lane + 1]; }
@@ -219,22 +243,27 @@ k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
                 double vn[3]; q2_interp3(uy[2][0], uy[2][1], uy[2][2], vn);
                 q2_edge(false, me, nb, vn, r + 1 < a.erow_end || a.has_north, FnA, FnH);
             }
+            // raw edge moments (east, north here; west by shuffle of the east ones, south carried or evaluated)
+            double rE[2][3], rN[2][3], rW[2][3], rS[2][3];
+            edge_raw(FeA, rE[0][0], rE[0][1], rE[0][2]); edge_raw(FeH, rE[1][0], rE[1][1], rE[1][2]);
+            edge_raw(FnA, rN[0][0], rN[0][1], rN[0][2]); edge_raw(FnH, rN[1][0], rN[1][1], rN[1][2]);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                FwA[q] = __shfl_up_sync(0xffffffffu, FeA[q], 1);
-                FwH[q] = __shfl_up_sync(0xffffffffu, FeH[q], 1);
+                rW[0][q] = __shfl_up_sync(0xffffffffu, rE[0][q], 1);
+                rW[1][q] = __shfl_up_sync(0xffffffffu, rE[1][q], 1);
             }
-            if (prev_unit == dM.x) {   // the previous job was the row below in this unit: its north flux
+            if (prev_unit == dM.x) {   // the previous job was the row below in this unit: its north moments
 #pragma unroll
-                for (int q = 0; q < 3; ++q) { FsA[q] = cNA[q]; FsH[q] = cNH[q]; }
+                for (int q = 0; q < 3; ++q) { rS[0][q] = cNA[q]; rS[1][q] = cNH[q]; }
             } else {   // south edge: the row below (ring row of the unit)
 #pragma unroll
                 for (int k = 0; k < 6; ++k) { nb.A[k] = L.A[k][eo + lane]; nb.H[k] = L.H[k][eo + lane]; }
                 double vn[3]; q2_interp3(uy[0][0], uy[0][1], uy[0][2], vn);
                 q2_edge(false, nb, me, vn, r > a.erow_begin || a.has_south, FsA, FsH);
+                edge_raw(FsA, rS[0][0], rS[0][1], rS[0][2]); edge_raw(FsH, rS[1][0], rS[1][1], rS[1][2]);
             }
 #pragma unroll
-            for (int q = 0; q < 3; ++q) { cNA[q] = FnA[q]; cNH[q] = FnH[q]; }
+            for (int q = 0; q < 3; ++q) { cNA[q] = rN[0][q]; cNH[q] = rN[1][q]; }
             prev_unit = dM.x;
             issue_late();                      // row k - 1 (slot sL) is consumed
             // ---- volume term and update: k_advect_q2's code
@@ -255,44 +284,33 @@ k_advect_tma(const __grid_constant__ AdvMaps maps, AdvTmaArgs ta) {
 #pragma unroll
             for (int tr = 0; tr < 2; ++tr) {
                 const double* c = tr == 0 ? me.A : me.H;
-                const double* Fe = tr == 0 ? FeA : FeH; const double* Fw = tr == 0 ? FwA : FwH;
-                const double* Fn = tr == 0 ? FnA : FnH; const double* Fs = tr == 0 ? FsA : FsH;
                 double cg[3][3], Gx[3][3], Gy[3][3];
                 gp_vals(c, cg);
 #pragma unroll
                 for (int gy = 0; gy < 3; ++gy)
 #pragma unroll
                     for (int g = 0; g < 3; ++g) { Gx[gy][g] = cg[gy][g] * gvx[gy][g]; Gy[gy][g] = cg[gy][g] * gvy[gy][g]; }
-                double x00, x10, x01, y00, y10, y01;
-                vol_mom(Gx, x00, x10, x01);
-                vol_mom(Gy, y00, y10, y01);
+                double X00, X10, X01, Y00, Y10, Y01;
+                vol_raw(Gx, X00, X10, X01);
+                vol_raw(Gy, Y00, Y10, Y01);
+                const double* e = rE[tr]; const double* w = rW[tr]; const double* n = rN[tr]; const double* so = rS[tr];
+                const double d0x = w[0] - e[0], s0x = e[0] + w[0], d1x = w[1] - e[1], s1x = e[1] + w[1], d2x = w[2] - e[2];
+                const double d0y = so[0] - n[0], s0y = n[0] + so[0], d1y = so[1] - n[1], s1y = n[1] + so[1], d2y = so[2] - n[2];
+                // dt a1 mr_k L_k (k_advect_q2's L_k, every scale in a.kc)
                 double Lk[6];
-                Lk[0] = 0.0;
-                Lk[1] = a.ihx * x00;
-                Lk[2] = a.ihy * y00;
-                Lk[3] = 2.0 * a.ihx * x10;
-                Lk[4] = 2.0 * a.ihy * y01;
-                Lk[5] = fma(a.ihx, x01, a.ihy * y10);
-                double m0, m1, m2;
-                edge_mom(Fe, m0, m1, m2);
-                Lk[0] -= a.ihx * m0; Lk[1] -= a.ihx * 0.5 * m0; Lk[2] -= a.ihx * m1; Lk[3] -= a.ihx * m0 * (1.0 / 6.0);
-                Lk[4] -= a.ihx * m2; Lk[5] -= a.ihx * 0.5 * m1;
-                edge_mom(Fw, m0, m1, m2);
-                Lk[0] += a.ihx * m0; Lk[1] -= a.ihx * 0.5 * m0; Lk[2] += a.ihx * m1; Lk[3] += a.ihx * m0 * (1.0 / 6.0);
-                Lk[4] += a.ihx * m2; Lk[5] -= a.ihx * 0.5 * m1;
-                edge_mom(Fn, m0, m1, m2);
-                Lk[0] -= a.ihy * m0; Lk[1] -= a.ihy * m1; Lk[2] -= a.ihy * 0.5 * m0; Lk[3] -= a.ihy * m2;
-                Lk[4] -= a.ihy * m0 * (1.0 / 6.0); Lk[5] -= a.ihy * 0.5 * m1;
-                edge_mom(Fs, m0, m1, m2);
-                Lk[0] += a.ihy * m0; Lk[1] += a.ihy * m1; Lk[2] -= a.ihy * 0.5 * m0; Lk[3] += a.ihy * m2;
-                Lk[4] += a.ihy * m0 * (1.0 / 6.0); Lk[5] -= a.ihy * 0.5 * m1;
+                Lk[0] = fma(a.kc[0], d0x, a.kc[1] * d0y);
+                Lk[1] = fma(a.kc[2], X00, fma(a.kc[3], s0x, a.kc[4] * d1y));
+                Lk[2] = fma(a.kc[5], Y00, fma(a.kc[6], d1x, a.kc[7] * s0y));
+                Lk[3] = fma(a.kc[8], X10, fma(a.kc[9], d0x, a.kc[10] * d2y));
+                Lk[4] = fma(a.kc[11], Y01, fma(a.kc[12], d2x, a.kc[13] * d0y));
+                Lk[5] = fma(a.kc[14], X01, fma(a.kc[15], Y10, fma(a.kc[16], s1x, a.kc[17] * s1y)));
                 if (tr == 0 && rk) {           // the job's c0 has landed in the buffer
                     mbar_wait(bar0, ph0);
                     ph0 ^= 1u;
                 }
 #pragma unroll
                 for (int k = 0; k < 6; ++k) {
-                    const double v = a.a1 * fma(a.dt, Lk[k] * mr[k], c[k]);
+                    const double v = fma(a.a1, c[k], Lk[k]);
                     ncv[tr][k] = rk ? fma(a.a0, tr == 0 ? c0buf->A[k][eo + lane] : c0buf->H[k][eo + lane], v) : v;
                 }
             }

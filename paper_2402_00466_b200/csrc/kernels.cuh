@@ -550,6 +550,7 @@ struct AdvArgs {
     int limit;                                // k_advect_q2: fused R#25 limiter on the stage output
     const double* sph_rows;                   // k_advect_q2<true>: sphere row tables (R#26), ihx = 1/(R dlon)
     double* Pg; double Pstar, C_conc;         // k_advect_tma, last stage: also write P at the Gauss points
+    double kc[18];                            // k_advect_tma: the stage's folded moment coefficients (adv_coeffs)
 };
 
 template <int NA> struct Cf { double A[NA], H[NA]; };

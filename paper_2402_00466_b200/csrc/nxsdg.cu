@@ -2295,7 +2295,25 @@ static nxsdg_status launch_adv_tma_t(nxsdg_ctx* c, const AdvMaps& mp, const AdvT
     return NXSDG_OK;
 }
 
-static nxsdg_status launch_adv_tma(nxsdg_ctx* c, const AdvArgs& a) {
+// k_advect_tma's folded coefficients: every scale between its raw Gauss sums and dt a1 mr_k L_k (advect_tma.cuh)
+static void adv_coeffs(AdvArgs& a) {
+    const double ka = 0.38729833462074170, f = 5.0 / 18.0, g = 5.0 * ka / 18.0;
+    const double mr[6] = {1.0, 12.0, 12.0, 180.0, 180.0, 144.0};
+    double U[6];
+    for (int k = 0; k < 6; ++k) U[k] = a.a1 * a.dt * mr[k];
+    const double hx = a.ihx, hy = a.ihy;
+    const double kc[18] = {U[0] * f * hx, U[0] * f * hy,
+                           U[1] * hx * f * f, -U[1] * hx * (5.0 / 36.0), U[1] * hy * g,
+                           U[2] * hy * f * f, U[2] * hx * g, -U[2] * hy * (5.0 / 36.0),
+                           U[3] * 2.0 * hx * f * g, U[3] * (hx / 6.0) * f, U[3] * hy / 54.0,
+                           U[4] * 2.0 * hy * f * g, U[4] * hx / 54.0, U[4] * (hy / 6.0) * f,
+                           U[5] * hx * f * g, U[5] * hy * f * g, -U[5] * hx * (5.0 * ka / 36.0), -U[5] * hy * (5.0 * ka / 36.0)};
+    for (int k = 0; k < 18; ++k) a.kc[k] = kc[k];
+}
+
+static nxsdg_status launch_adv_tma(nxsdg_ctx* c, const AdvArgs& a0) {
+    AdvArgs a = a0;
+    adv_coeffs(a);
     AdvMaps mp;
     const cuuint64_t nx = c->d.nx, er = c->erows_local, ncols = 2 * (cuuint64_t)c->d.nx + 1, nr = c->nrows_local;
     const cuuint64_t es[2] = {(cuuint64_t)c->epitch * 8, (cuuint64_t)c->eplane * 8};
