@@ -1593,14 +1593,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// L2 sector promotion of the TMA loads: 128 B.  A box row of the S / P_g boxes is 272 B at a 16-B
+// L2 sector promotion of the TMA loads: 64 B.  A box row of the S / P_g boxes is 272 B at a 16-B
 // offset, so 256-B promotion fetches up to 768 B for it and relies on the neighbour strip to use the
 // rest while it is still in L2; at 8 warps/SM that often fails: C4 launch DRAM reads 8.97 GB (256 B)
-// vs 8.53 GB (128 B), sustained 1.910 vs 1.905 ms (profiles/tune_promo_r01.log).  Experiment hook:
-// NXSDG_TMA_L2_PROMOTION = 0 none, 1 64 B, 2 128 B (default), 3 256 B
+// vs 8.53 GB (128 B), sustained 1.910 vs 1.905 ms (profiles/tune_promo_r01.log).  Round 2: 64 B reads
+// less again - DRAM traffic 1.046-1.054 x algorithmic against 1.054-1.097 x at 128 B over four ncu
+// launches, sustained time and the advection / general-quad kernels unchanged
+// (profiles/ab_l2_promotion_r02.log).  Experiment hook: NXSDG_TMA_L2_PROMOTION = 0 none, 1 64 B
+// (default), 2 128 B, 3 256 B
 static CUtensorMapL2promotion l2_promotion() {
     const char* e = getenv("NXSDG_TMA_L2_PROMOTION");
-    const int v = e ? atoi(e) : 2;
+    const int v = e ? atoi(e) : 1;
     return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
          : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
 }
