@@ -326,6 +326,7 @@ def main():
                     help="NXSDG_OPT_PREP_KERNEL for A/B runs (default: the library's)")
     ap.add_argument("--adv-stages", type=int, default=None,
                     help="NXSDG_OPT_ADVECT_STAGES for A/B runs (default: the library's)")
+    ap.add_argument("--pdl", type=int, default=None, help="NXSDG_OPT_PDL for A/B runs (default: the library's)")
     args = ap.parse_args()
     cname = args.config or ("C5" if args.weak else "C4")
     cfg = inputs.CONFIGS[cname]
@@ -399,6 +400,8 @@ def main():
         m.set_option(nxsdg.OPT_PREP_KERNEL, args.prep_kernel)
     if args.adv_stages is not None:
         m.set_option(nxsdg.OPT_ADVECT_STAGES, args.adv_stages)
+    if args.pdl is not None:
+        m.set_option(nxsdg.OPT_PDL, args.pdl)
     if args.limiter:
         m.set_option(nxsdg.OPT_LIMITER, 1)
     if args.sphere:

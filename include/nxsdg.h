@@ -213,6 +213,9 @@ nxsdg_status nxsdg_partition(int32_t ny, int32_t cg_degree, int32_t nranks, int3
  *   NXSDG_OPT_FUSE_PREP_PG  single rank with k_advect_tma: 1 (default) = the last advection stage also writes the
  *                           outer-step prep's P at the Gauss points of the new A, H (bitwise what the prep would
  *                           compute); 0 = the prep computes it at BEGIN_STEP
+ *   NXSDG_OPT_PDL           1 = the subcycle launches of a single-rank graph use programmatic dependent launch:
+ *                           a launch's CTAs set up while the previous subcycle's last CTAs finish and wait
+ *                           (griddepcontrol.wait) before touching S or v; 0 (default: measured no faster) = plain
  *   NXSDG_OPT_PAIR_SUBCYCLES 1 = two subcycles per launch of the box TMA kernel (temporal blocking: a unit runs
  *                           subcycle p over a 2-row / 2-column wider halo into scratch buffers, then subcycle
  *                           p + 1 from them; single rank, FP64, n_S = 6, node constants in registers; an odd
@@ -232,7 +235,7 @@ enum { NXSDG_OPT_FUSED_KERNEL = 0, NXSDG_OPT_CHUNK_ROWS = 1, NXSDG_OPT_CTAS_PER_
        NXSDG_OPT_LIMITER = 8, NXSDG_OPT_CONST_STAGING = 9, NXSDG_OPT_TAIL_SPLIT = 10, NXSDG_OPT_L2_POLICY = 11,
        NXSDG_OPT_V_ROW_CARRY = 12, NXSDG_OPT_MULTIRANK_GRAPH = 13, NXSDG_OPT_ADVECT_KERNEL = 14,
        NXSDG_OPT_ADVECT_STAGES = 15, NXSDG_OPT_FUSE_PREP_PG = 16, NXSDG_OPT_PREP_KERNEL = 18,
-       NXSDG_OPT_PAIR_SUBCYCLES = 19 };
+       NXSDG_OPT_PAIR_SUBCYCLES = 19, NXSDG_OPT_PDL = 20 };
 nxsdg_status nxsdg_set_option(nxsdg_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- state ----------------------------------------------------------------- */

@@ -133,6 +133,9 @@ struct nxsdg_ctx {
     bool prep_defer = false;   // BEGIN_STEP left the node constants to the next fused subcycle (PREP launch)
     int pair = 0;              // NXSDG_OPT_PAIR_SUBCYCLES: two subcycles per launch (PAIR instantiation)
     bool pair_now = false;     // the next TMA launch is a PAIR launch
+    int pdl = 0;               // NXSDG_OPT_PDL: single-rank subcycle graphs launch with programmatic dependence
+                               // (measured no faster: profiles/ab_pdl_r02.log)
+    bool pdl_now = false;      // the next TMA subcycle launch carries the PDL attribute
     double* Sx = nullptr; double* vxx = nullptr; double* vyx = nullptr;   // PAIR scratch (S^{p+1}, v^{p+1})
     K2Maps mapsP{};            // PAIR pass-B maps over the scratch
     bool mapsP_ok = false;
@@ -515,6 +518,9 @@ extern "C" nxsdg_status nxsdg_set_option(nxsdg_ctx* c, int32_t opt, int64_t valu
         case NXSDG_OPT_PREP_KERNEL:
             if (value < 0 || value > 2) return fail(c, NXSDG_ERR_INVALID_ARG, "prep kernel 0|1|2");
             c->prep_kernel = (int)value; break;
+        case NXSDG_OPT_PDL:
+            if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "pdl 0|1");
+            c->pdl = (int)value; break;
         case NXSDG_OPT_PAIR_SUBCYCLES:
             if (value != 0 && value != 1) return fail(c, NXSDG_ERR_INVALID_ARG, "pair subcycles 0|1");
             c->pair = (int)value; break;
@@ -1825,8 +1831,18 @@ static nxsdg_status launch_tma_t(nxsdg_ctx* c, int cv, int cs, const SubArgs& a)
     const K2Maps& mp = sizeof(SF) == 8 ? c->maps[cv][cs] : c->maps32[cv][cs];
     typename K2PassB<PAIR>::T mb{};
     if constexpr (PAIR) mb = c->mapsP;
-    k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP, PAIR><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(
-        mp, mb, launch_args(c, a, (int64_t)blocks * K2_WARPS));
+    const SubArgs la = launch_args(c, a, (int64_t)blocks * K2_WARPS);
+    if (c->pdl_now) {   // programmatic dependent launch: may overlap the previous subcycle's tail (run_graph)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(blocks); cfg.blockDim = dim3(32 * K2_WARPS); cfg.dynamicSmemBytes = smem; cfg.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        CU(cudaLaunchKernelEx(&cfg, k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP, PAIR>, mp, mb, la));
+    } else {
+        k_subcycle_tma<R, ST, SF, CT, NS, CL, LC, SPH, PREP, PAIR><<<blocks, 32 * K2_WARPS, smem, c->stream>>>(mp, mb, la);
+    }
     return NXSDG_OK;
 }
 // stages x replacement pressure x node-constant staging (TMA box | registers)
@@ -2112,9 +2128,11 @@ static nxsdg_status run_graph(nxsdg_ctx* c, int n) {
         for (int i = 0, slot = 0; i < n; ++slot) {
             if (use_tma(c)) {
                 c->pair_now = pr && n - i >= 2;
+                c->pdl_now = c->pdl && slot > 0;   // the previous node is a subcycle launch
                 nxsdg_status st = launch_tma(c, cv, cs, slot);
                 i += c->pair_now ? 2 : 1;
                 c->pair_now = false;
+                c->pdl_now = false;
                 if (st) { cudaGraph_t junk; cudaStreamEndCapture(c->stream, &junk); if (junk) cudaGraphDestroy(junk); return st; }
             } else {
                 ++i;

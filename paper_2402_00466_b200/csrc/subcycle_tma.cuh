@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the next subcycle may be scheduled
 
     // Work list: (strip, chunk) units.  A warp's first unit is gw; further units are claimed
     // from a global counter (dynamic balancing; a.work_counter is zeroed before each launch),
@@ -638,6 +639,11 @@ __global__ void __launch_bounds__(32 * K2_WARPS, 2) k_subcycle_tma(const __grid_
     const double ihx = a.ihx, ihy = a.ihy, fac = a.fac, hA = 0.5 * a.ainv;
     const double mhx = -9.0 * ihx, mhy = -9.0 * ihy;   // -1 / (corner lumped mass / |K|) = -9
     const int64_t npitch = a.npitch, eplane = a.eplane;
+    // Programmatic dependent launch (single-rank subcycle graphs, NXSDG_OPT_PDL): this grid may start while the
+    // previous subcycle's last CTAs finish; everything above (barrier setup) overlaps that tail, and no thread
+    // reads or writes S / v before the previous grid has completed and flushed (griddepcontrol.wait is a no-op
+    // for a launch without the attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // prologue: jobs 0 .. STAGES-2 in flight; job j lives in stage j % STAGES
     Cur pre;
     if (lane == 0) {

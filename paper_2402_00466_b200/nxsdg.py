@@ -35,7 +35,7 @@ TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_P2P = 0, 1, 2, 3
 (OPT_FUSED_KERNEL, OPT_CHUNK_ROWS, OPT_CTAS_PER_SM, OPT_STAGES, OPT_DYNAMIC, OPT_MAP_MODE, OPT_PRECISION,
  OPT_P2P_FUSED_STORES, OPT_LIMITER, OPT_CONST_STAGING, OPT_TAIL_SPLIT, OPT_L2_POLICY, OPT_V_ROW_CARRY,
  OPT_MULTIRANK_GRAPH, OPT_ADVECT_KERNEL, OPT_ADVECT_STAGES, OPT_FUSE_PREP_PG, _OPT_17_UNUSED,
- OPT_PREP_KERNEL, OPT_PAIR_SUBCYCLES) = range(20)
+ OPT_PREP_KERNEL, OPT_PAIR_SUBCYCLES, OPT_PDL) = range(21)
 
 
 class NxsdgError(RuntimeError):
